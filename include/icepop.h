@@ -1,0 +1,216 @@
+/*
+ * icepop.h -- C ABI of the B200-native (sm_100a) IcePop policy-gradient objective.
+ *
+ * This library replaces the reference's hot path, mismatchlab's
+ *   objective_and_grad(groups, theta, theta_old, ref, cfg, bounds, temperature)
+ *   (/root/reference/pkg/src/mismatchlab/objective.py:172-298)
+ * together with the numerics it calls,
+ *   batched_train_logits  (policy.py:279-289)   -> the lm_head contraction Z = H.W / T
+ *   batched_log_softmax   (policy.py:350-355)   -> online log-sum-exp, gather, entropy
+ *   group_advantages      (objective.py:153-159)
+ * The reference has no FFI of its own (it is pure numpy); the Python host layer
+ * (paper_2510_18855_b200.objective / .loss) binds these entry points with ctypes,
+ * exactly as INTEGRATION.md shows for a maintainer wiring it into mismatchlab.
+ *
+ * Conventions
+ *   - Plain pointers and sizes; every pointer is DEVICE memory unless stated.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as void*).
+ *     Nothing synchronises the host except icepop_*_finish, which reads the
+ *     device error word once.
+ *   - Gradients are the reference's ASCENT gradient dJ/dW (objective.py:250-266)
+ *     multiplied by `grad_scale`; a torch loss = -J passes grad_scale = -dL/dloss.
+ *   - Reductions are fixed-order (no floating-point atomics): results are
+ *     bit-stable run to run for a fixed shape and device count.
+ *   - Return codes mirror the reference's exceptions:
+ *       ICEPOP_OK       0
+ *       ICEPOP_EINVAL   1  -> ValueError  (objective.py:190-193, 205-213)
+ *       ICEPOP_ENUMERIC 2  -> NumericError (objective.py:228-229, 241-242, 279-280)
+ *       ICEPOP_ECUDA    3  -> RuntimeError (CUDA launch / runtime failure)
+ *       ICEPOP_EARCH    4  -> RuntimeError (device is not sm_100)
+ *     icepop_last_error() returns a per-thread message for the last failure.
+ */
+#ifndef ICEPOP_B200_H_
+#define ICEPOP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ICEPOP_ABI_VERSION 1
+
+enum icepop_status {
+  ICEPOP_OK = 0,
+  ICEPOP_EINVAL = 1,
+  ICEPOP_ENUMERIC = 2,
+  ICEPOP_ECUDA = 3,
+  ICEPOP_EARCH = 4
+};
+
+/* objective.py:41-44 (Algo) */
+enum icepop_algo { ICEPOP_ALGO_ICEPOP = 0, ICEPOP_ALGO_GRPO = 1, ICEPOP_ALGO_TIS = 2 };
+
+/* Weight layouts. [d,V] is the reference PolicyParams layout (policy.py:132-155,
+ * weights[n_features, vocab]); [V,d] is the usual lm_head (nn.Linear) layout. */
+enum icepop_weight_layout { ICEPOP_W_DV = 0, ICEPOP_W_VD = 1 };
+
+/* Device error word bits (read by icepop_*_finish). */
+#define ICEPOP_ERR_CALIB_OVERFLOW 1u  /* objective.py:228-229 */
+#define ICEPOP_ERR_RATIO_OVERFLOW 2u  /* objective.py:241-242 */
+#define ICEPOP_ERR_NONFINITE      4u  /* objective.py:279-280, policy.py:287-288 */
+
+/* Layout of the per-rank fp64 statistics vector (summed across ranks by the caller). */
+enum icepop_stat {
+  ICEPOP_STAT_OBJECTIVE = 0,        /* sum_t w_t * (s_t - gamma*kl_t)            objective.py:268-278 */
+  ICEPOP_STAT_N_POPPED = 1,         /* #(not kept)                               objective.py:284     */
+  ICEPOP_STAT_TOKENS = 2,           /* token count                               objective.py:291     */
+  ICEPOP_STAT_SUM_ENTROPY = 3,      /* sum_t entropy_t                           objective.py:293     */
+  ICEPOP_STAT_SUM_ENTROPY_POPPED = 4,/* sum over popped tokens of entropy_t      objective.py:294     */
+  ICEPOP_STAT_SUM_LOGP = 5,         /* sum_t lp_cur_t                            objective.py:292     */
+  ICEPOP_STAT_SUM_KL = 6,           /* sum_t kl_t                                objective.py:290     */
+  ICEPOP_STAT_ERRORS = 7,           /* OR of ICEPOP_ERR_* (as a double)                               */
+  ICEPOP_NSTATS = 8
+};
+
+/* objective.py:47-82 (MaskingBounds, ObjectiveConfig) + the temperature argument. */
+typedef struct icepop_config {
+  double alpha;        /* inclusive lower calibration bound  (default 0.5) */
+  double beta;         /* inclusive upper calibration bound  (default 5.0) */
+  double clip_eps;     /* PPO clip epsilon                   (default 0.2) */
+  double tis_cap;      /* TIS truncation cap                 (default 2.0) */
+  double temperature;  /* logits are divided by it           (default 1.0) */
+  double kl_coeff;     /* gamma of the KL-to-ref penalty     (default 0.0) */
+  int32_t algo;        /* enum icepop_algo */
+  int32_t _pad;
+} icepop_config;
+
+/* Batch geometry. Tokens are packed sequence-major in the reference's order
+ * (group-major, then rollout, then token: objective.py:271-276). A rank owns the
+ * contiguous global token range [token_offset, token_offset + n_tokens). */
+typedef struct icepop_shape {
+  int64_t n_tokens;      /* local tokens on this rank (rows of hidden)         */
+  int64_t token_offset;  /* global index of the first local token              */
+  int64_t hidden;        /* d  (n_features in the reference)                   */
+  int64_t vocab;         /* V                                                  */
+  int32_t n_seqs;        /* S, sequences (rollouts) in the GLOBAL batch        */
+  int32_t n_groups;      /* prompt groups in the GLOBAL batch                  */
+  int32_t weight_layout; /* enum icepop_weight_layout                          */
+  int32_t _pad;
+} icepop_shape;
+
+/* Per-sequence metadata, replicated on every rank (device pointers). */
+typedef struct icepop_batch {
+  const int32_t* tokens;        /* [n_tokens]     sampled token id y_t (local)          */
+  const double* lp_train_old;   /* [n_tokens]     TokenRecord.logp_train_old (local)    */
+  const double* lp_infer_old;   /* [n_tokens]     TokenRecord.logp_infer_old (local)    */
+  const int32_t* cu_seqlens;    /* [n_seqs+1]     global token offsets of sequences     */
+  const int32_t* group_offsets; /* [n_groups+1]   sequence offsets of prompt groups     */
+  const double* advantages;     /* [n_seqs]       PromptGroup.advantages, or NULL       */
+  const double* rewards;        /* [n_seqs]       used (with group_advantages) if advantages == NULL */
+} icepop_batch;
+
+/* ---- library ---------------------------------------------------------------------- */
+int icepop_abi_version(void);
+const char* icepop_last_error(void);
+/* 0 on an sm_100 device with the kernels loadable; ICEPOP_EARCH otherwise. */
+int icepop_device_check(int device);
+
+/* ---- K0: group advantages (objective.py:153-159) ---------------------------------- */
+/* adv[i] = (R_i - mean_g R) / max(std_pop,g(R), 1e-6) for every sequence i of group g.
+ * Groups of fewer than 2 sequences are rejected (ICEPOP_EINVAL), as in the reference. */
+int icepop_group_advantages(const double* rewards, const int32_t* group_offsets, int32_t n_groups,
+                            int32_t n_seqs, double* advantages, void* stream);
+
+/* ---- bf16 tensor-core path (production) ------------------------------------------- */
+/* hidden: [n_tokens, d] bf16 row-major. weight: bf16 in `weight_layout`.
+ * Workspace sizes (bytes) for icepop_fwd_bf16 / icepop_bwd_bf16. The backward
+ * materialises bf16 dZ chunks of at most `max_chunk_tokens` rows (0 = all rows);
+ * passing a smaller workspace than recommended shrinks the chunk (>= 128 rows). */
+int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens,
+                           size_t* fwd_bytes, size_t* bwd_bytes);
+
+typedef struct icepop_fwd_out {
+  float* lse;          /* [n_tokens] log-sum-exp of z = H.W/T (saved for backward)      */
+  double* lp_cur;      /* [n_tokens] log pi_theta(y_t)  (objective.py:223-225)           */
+  float* entropy;      /* [n_tokens] -sum p log p       (objective.py:274)               */
+  uint8_t* kept;       /* [n_tokens] IcePop mask        (objective.py:230-238)           */
+  double* calib;       /* [n_tokens] c_t                (objective.py:227)               */
+  double* surrogate;   /* [n_tokens] s_t                (objective.py:246)               */
+  float* coeff;        /* [n_tokens] dJ/dlogit scale    (objective.py:250)  (for bwd)     */
+  double* stats;       /* [ICEPOP_NSTATS] this rank's partial sums                        */
+} icepop_fwd_out;
+
+/* Forward: fused lm_head GEMM + online log-softmax/gather/entropy (tcgen05), then the
+ * IcePop epilogue. Logits are never written to HBM. */
+int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
+                    const void* weight, const icepop_batch* batch, const icepop_fwd_out* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Log-prob only (no IcePop epilogue): lse, lp = z[y]-lse, entropy. Used to record
+ * lp_train_old (scheduler.py:296-311) with the same kernel. Any output may be NULL. */
+int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const void* hidden,
+                        const void* weight, const int32_t* tokens, float* lse, double* lp,
+                        float* entropy, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward: recompute logits tile by tile, dZ = grad_scale*coeff_t*(e_y - softmax(z_t))
+ * (bf16 chunk), then grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05.
+ * grad_hidden: [n_tokens, d], bf16 if grad_hidden_f32 == 0 else f32; may be NULL.
+ * grad_weight: f32 in the weight's layout; accumulate != 0 adds into it; may be NULL. */
+int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
+                    const void* weight, const int32_t* tokens, const float* lse,
+                    const float* coeff, double grad_scale, void* grad_hidden,
+                    int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- fp64 SIMT validation path ----------------------------------------------------- */
+/* Same semantics in fp64 on CUDA cores (still CUDA, no CPU fallback), so the
+ * reference's exact-identity and finite-difference tests run unchanged on the GPU.
+ * Supports the KL-to-ref term (objective.py:254-263) when weight_ref != NULL.
+ * hidden [n_tokens, d] f64; weight / weight_ref f64 in `weight_layout`. */
+int icepop_workspace_bytes_f64(const icepop_shape* shape, int32_t with_ref, size_t* bytes);
+
+typedef struct icepop_f64_out {
+  double* lse;         /* [n_tokens]                                                     */
+  double* lp_cur;      /* [n_tokens]                                                     */
+  double* entropy;     /* [n_tokens]                                                     */
+  double* kl;          /* [n_tokens] kl_t (0 when weight_ref == NULL)                    */
+  double* lse_ref;     /* [n_tokens] (written when weight_ref != NULL)                   */
+  uint8_t* kept;
+  double* calib;
+  double* surrogate;
+  double* coeff;       /* [n_tokens] objective.py:250                                   */
+  double* stats;       /* [ICEPOP_NSTATS]                                                */
+} icepop_f64_out;
+
+int icepop_fwd_f64(const icepop_shape* shape, const icepop_config* cfg, const double* hidden,
+                   const double* weight, const double* weight_ref, const icepop_batch* batch,
+                   const icepop_f64_out* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* grad_hidden [n_tokens,d] f64 (may be NULL); grad_weight f64 in weight layout (may be NULL).
+ * kl/lse_ref/coeff/lse come from icepop_fwd_f64. */
+int icepop_bwd_f64(const icepop_shape* shape, const icepop_config* cfg, const double* hidden,
+                   const double* weight, const double* weight_ref, const icepop_batch* batch,
+                   const icepop_f64_out* fwd, double grad_scale, double* grad_hidden,
+                   double* grad_weight, int32_t accumulate, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* ---- completion --------------------------------------------------------------------- */
+/* Synchronises `stream` once, reads stats[ICEPOP_STAT_ERRORS] and maps it to
+ * ICEPOP_ENUMERIC with the reference's message; `stats` may be a host or device pointer
+ * to the (already all-reduced) statistics vector. */
+int icepop_finish(const double* stats, void* stream);
+
+/* ---- building blocks exposed for tests / benchmarks --------------------------------- */
+/* C[M,N] = A.B with bf16 operands on tcgen05, f32 accumulate, f32 or bf16 output.
+ * a_mn_major: A stored [K,M] (M contiguous) instead of [M,K]; b_mn_major: B stored
+ * [K,N] instead of [N,K]. ldc in elements. accumulate adds into C (f32 only). */
+int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                     int32_t a_mn_major, int32_t b_mn_major, int32_t c_f32, int32_t accumulate,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ICEPOP_B200_H_ */

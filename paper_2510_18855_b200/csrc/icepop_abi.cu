@@ -1,0 +1,690 @@
+// icepop_abi.cu -- extern "C" entry points of libicepop_b200.so (include/icepop.h).
+//
+// Host-side orchestration only: argument validation with the reference's error
+// semantics, workspace carving, TMA descriptor encoding and kernel launches. All
+// arithmetic runs in the kernels of umma_gemm.cuh / token_kernels.cuh / f64_kernels.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/icepop.h"
+#include "f64_kernels.cuh"
+#include "token_kernels.cuh"
+#include "umma_gemm.cuh"
+
+using namespace icp;
+
+namespace {
+
+constexpr uint32_t ERR_BAD_TOKEN = 8u;
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define ICP_CUDA(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(ICEPOP_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),  \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+#define ICP_TRY(expr)            \
+  do {                           \
+    int _r = (expr);             \
+    if (_r != ICEPOP_OK) return _r; \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+int encode_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+              uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(ICEPOP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0)
+    return fail(ICEPOP_EINVAL, "TMA operand base must be 16-byte aligned");
+  if ((ld_elems * 2) % 16 != 0)
+    return fail(ICEPOP_EINVAL, "TMA operand row stride must be a multiple of 8 bf16 elements");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ICEPOP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ICEPOP_OK;
+}
+
+// Operand X of C = X_A . X_B^T viewed as [mn, k]:
+//   K-major : stored [mn rows, k cols] with row stride ld   -> box {64, tile_mn}
+//   MN-major: stored [k rows, mn cols] with row stride ld   -> box {64, 64}
+int operand_map(CUtensorMap* map, const void* ptr, int64_t mn, int64_t k, int64_t ld, bool mn_major,
+                int tile_mn) {
+  if (!mn_major) return encode_2d(map, ptr, (uint64_t)k, (uint64_t)mn, (uint64_t)ld, 64, tile_mn);
+  return encode_2d(map, ptr, (uint64_t)mn, (uint64_t)k, (uint64_t)ld, 64, 64);
+}
+
+constexpr int BN_ = 256;
+
+template <bool A_MN, bool B_MN, int EPI>
+int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
+                cudaStream_t st) {
+  auto kern = umma_gemm_kernel<BN_, A_MN, B_MN, EPI>;
+  constexpr size_t smem = GemmCfg<BN_>::SMEM;
+  static bool attr_done = false;
+  if (!attr_done) {
+    ICP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done = true;
+  }
+  const int grid = std::min(sh.num_tiles, num_sms());
+  kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, sh, ep);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+// C[M,N] = A . B^T with the given operand majors; epilogue `epi`.
+int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
+             int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
+  if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
+    return fail(ICEPOP_EINVAL, "GEMM extent too large");
+  CUtensorMap ta, tb;
+  ICP_TRY(operand_map(&ta, A, M, K, lda, a_mn, BM));
+  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, BN_));
+  GemmShape sh;
+  sh.M = (int)M;
+  sh.N = (int)N;
+  sh.K = (int)K;
+  sh.m_tiles = (int)((M + BM - 1) / BM);
+  sh.n_tiles = (int)((N + BN_ - 1) / BN_);
+  sh.k_blocks = (int)((K + BK - 1) / BK);
+  if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
+  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+  sh.group_m = 16;
+  if (epi == EPI_STORE) {
+    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st);
+    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st);
+    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, sh, ep, st);
+    return launch_umma<true, true, EPI_STORE>(ta, tb, sh, ep, st);
+  }
+  if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
+  if (epi == EPI_LSE) {
+    if (!b_mn) return launch_umma<false, false, EPI_LSE>(ta, tb, sh, ep, st);
+    return launch_umma<false, true, EPI_LSE>(ta, tb, sh, ep, st);
+  }
+  if (!b_mn) return launch_umma<false, false, EPI_DZ>(ta, tb, sh, ep, st);
+  return launch_umma<false, true, EPI_DZ>(ta, tb, sh, ep, st);
+}
+
+// ------------------------------------------------------------------ validation helpers
+int check_config(const icepop_config* c) {
+  if (!c) return fail(ICEPOP_EINVAL, "null config");
+  // MaskingBounds.__post_init__ (objective.py:54-56), ObjectiveConfig (objective.py:74-82)
+  if (!(0.0 < c->alpha && c->alpha <= 1.0 && 1.0 <= c->beta))
+    return fail(ICEPOP_EINVAL, "bounds must satisfy 0 < alpha <= 1 <= beta, got [%g, %g]", c->alpha, c->beta);
+  if (!(0.0 < c->clip_eps && c->clip_eps < 1.0)) return fail(ICEPOP_EINVAL, "clip_eps must be in (0, 1)");
+  if (!(c->kl_coeff >= 0.0)) return fail(ICEPOP_EINVAL, "kl_coeff must be nonnegative");
+  if (!(c->tis_cap > 0.0)) return fail(ICEPOP_EINVAL, "tis_cap must be positive");
+  if (!(c->temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
+  if (c->algo < 0 || c->algo > 2) return fail(ICEPOP_EINVAL, "unknown algo %d", c->algo);
+  return ICEPOP_OK;
+}
+
+int check_shape(const icepop_shape* s, bool bf16) {
+  if (!s) return fail(ICEPOP_EINVAL, "null shape");
+  if (s->n_tokens < 0 || s->token_offset < 0) return fail(ICEPOP_EINVAL, "negative token range");
+  if (s->hidden <= 0 || s->vocab <= 0) return fail(ICEPOP_EINVAL, "hidden and vocab must be positive");
+  if (s->n_seqs <= 0 || s->n_groups <= 0)
+    return fail(ICEPOP_EINVAL, "objective needs at least one prompt group");
+  if (s->weight_layout != ICEPOP_W_DV && s->weight_layout != ICEPOP_W_VD)
+    return fail(ICEPOP_EINVAL, "unknown weight layout");
+  if (bf16 && (s->hidden % 8 != 0 || s->vocab % 8 != 0))
+    return fail(ICEPOP_EINVAL, "bf16 path needs hidden and vocab multiples of 8 (got %lld, %lld)",
+                (long long)s->hidden, (long long)s->vocab);
+  return ICEPOP_OK;
+}
+
+// Per-sequence advantages: given, or K0 from rewards (objective.py:153-159).
+int prepare_advantages(const icepop_shape* s, const icepop_batch* b, double* ws_adv, const double** adv,
+                       cudaStream_t st) {
+  if (b->advantages) {
+    *adv = b->advantages;
+    return ICEPOP_OK;
+  }
+  if (!b->rewards) return fail(ICEPOP_EINVAL, "either advantages or rewards must be given");
+  const int nb = (s->n_groups + 127) / 128;
+  k0_group_advantages<<<nb, 128, 0, st>>>(b->rewards, b->group_offsets, s->n_groups, ws_adv);
+  ICP_CUDA(cudaGetLastError());
+  *adv = ws_adv;
+  return ICEPOP_OK;
+}
+
+int token_grid(int64_t n) {
+  int64_t g = (n + TOK_THREADS - 1) / TOK_THREADS;
+  g = std::min<int64_t>(g, (int64_t)num_sms() * 8);
+  return (int)std::max<int64_t>(g, 1);
+}
+
+void fill_token_args(TokenArgs& a, const icepop_shape* s, const icepop_config* c, const icepop_batch* b,
+                     const double* adv) {
+  memset(&a, 0, sizeof(a));
+  a.n_tokens = s->n_tokens;
+  a.token_offset = s->token_offset;
+  a.n_seqs = s->n_seqs;
+  a.n_groups = s->n_groups;
+  a.tokens = b->tokens;
+  a.lp_old = b->lp_train_old;
+  a.lp_inf = b->lp_infer_old;
+  a.cu_seqlens = b->cu_seqlens;
+  a.group_offsets = b->group_offsets;
+  a.adv = adv;
+  a.alpha = c->alpha;
+  a.beta = c->beta;
+  a.clip_eps = c->clip_eps;
+  a.tis_cap = c->tis_cap;
+  a.temperature = c->temperature;
+  a.kl_coeff = c->kl_coeff;
+  a.algo = c->algo;
+}
+
+__global__ void k_check_tokens(const int32_t* tokens, int64_t n, int64_t V, unsigned* err) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int y = tokens[t];
+    if (y < 0 || y >= V) atomicOr(err, ERR_BAD_TOKEN);
+  }
+}
+
+__global__ void k_merge_err(const unsigned* err, double* stats) {
+  const unsigned e = (unsigned)stats[ICEPOP_STAT_ERRORS] | *err;
+  stats[ICEPOP_STAT_ERRORS] = (double)e;
+}
+
+__global__ void k_scale_f64(double* z, int64_t n, double temperature) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = z[i] / temperature;
+}
+
+int gemm_f64(const double* A, int64_t sam, int64_t sak, const double* B, int64_t sbk, int64_t sbn, double* C,
+             int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return ICEPOP_OK;
+  if ((M + F64_TM - 1) / F64_TM > 65535) return fail(ICEPOP_EINVAL, "fp64 validation path: too many rows");
+  dim3 grid((unsigned)((N + F64_TN - 1) / F64_TN), (unsigned)((M + F64_TM - 1) / F64_TM));
+  k_gemm_f64<<<grid, 256, 0, st>>>(A, sam, sak, B, sbk, sbn, C, ldc, (int)M, (int)N, (int)K, accumulate);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+// Z[N,V] = H[N,d] . W  (W in layout)
+int logits_f64(const icepop_shape* s, const double* H, const double* W, double* Z, cudaStream_t st) {
+  const int64_t N = s->n_tokens, d = s->hidden, V = s->vocab;
+  if (s->weight_layout == ICEPOP_W_DV) return gemm_f64(H, d, 1, W, V, 1, Z, V, N, V, d, 0, st);
+  return gemm_f64(H, d, 1, W, 1, d, Z, V, N, V, d, 0, st);
+}
+
+struct BF16Workspace {
+  float* part;
+  float* ztok;
+  double* adv;
+  double* block_stats;
+  unsigned* err;
+  __nv_bfloat16* dz;
+  int64_t chunk;
+  size_t bytes;
+};
+
+BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk) {
+  Carver c(base);
+  BF16Workspace w;
+  const int64_t n_tiles = (s->vocab + BN_ - 1) / BN_;
+  w.part = c.take<float>((size_t)n_tiles * 3 * std::max<int64_t>(s->n_tokens, 1));
+  w.ztok = c.take<float>((size_t)std::max<int64_t>(s->n_tokens, 1));
+  w.adv = c.take<double>((size_t)s->n_seqs);
+  w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
+  w.err = c.take<unsigned>(4);
+  w.dz = c.take<__nv_bfloat16>((size_t)chunk * (size_t)s->vocab);
+  w.chunk = chunk;
+  w.bytes = align_up(c.off, 256);
+  return w;
+}
+
+int64_t fwd_part_bytes(const icepop_shape* s) {
+  BF16Workspace w = carve_bf16(s, nullptr, 0);
+  return (int64_t)w.bytes;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int icepop_abi_version(void) { return ICEPOP_ABI_VERSION; }
+
+const char* icepop_last_error(void) { return g_last_error.c_str(); }
+
+int icepop_device_check(int device) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return fail(ICEPOP_ECUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  if (p.major != 10 || p.minor != 0)
+    return fail(ICEPOP_EARCH, "libicepop_b200 is built for sm_100a; device %d is sm_%d%d", device, p.major, p.minor);
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, umma_gemm_kernel<BN_, false, false, EPI_LSE>);
+  if (e != cudaSuccess) return fail(ICEPOP_EARCH, "sm_100a kernels not loadable: %s", cudaGetErrorString(e));
+  return ICEPOP_OK;
+}
+
+int icepop_group_advantages(const double* rewards, const int32_t* group_offsets, int32_t n_groups, int32_t n_seqs,
+                            double* advantages, void* stream) {
+  if (!rewards || !group_offsets || !advantages || n_groups <= 0 || n_seqs <= 0)
+    return fail(ICEPOP_EINVAL, "invalid group_advantages arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k0_group_advantages<<<(n_groups + 127) / 128, 128, 0, st>>>(rewards, group_offsets, n_groups, advantages);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, size_t* fwd_bytes,
+                           size_t* bwd_bytes) {
+  ICP_TRY(check_shape(shape, true));
+  int64_t chunk = shape->n_tokens;
+  if (max_chunk_tokens > 0) chunk = std::min<int64_t>(chunk, max_chunk_tokens);
+  chunk = std::max<int64_t>(chunk, 1);
+  if (fwd_bytes) *fwd_bytes = (size_t)fwd_part_bytes(shape);
+  if (bwd_bytes) *bwd_bytes = carve_bf16(shape, nullptr, chunk).bytes;
+  return ICEPOP_OK;
+}
+
+int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                        const int32_t* tokens, float* lse, double* lp, float* entropy, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
+                    const icepop_batch* batch, const icepop_fwd_out* out, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  ICP_TRY(check_config(cfg));
+  if (!batch || !out || !out->stats) return fail(ICEPOP_EINVAL, "null batch/out/stats");
+  if (cfg->kl_coeff > 0.0)
+    return fail(ICEPOP_EINVAL, "kl_coeff > 0 is only available in the fp64 path in this build");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BF16Workspace w = carve_bf16(shape, workspace, 0);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  const double* adv = nullptr;
+  ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
+  ICP_CUDA(cudaMemsetAsync(w.err, 0, sizeof(unsigned), st));
+  if (N > 0) {
+    k_check_tokens<<<token_grid(N), TOK_THREADS, 0, st>>>(batch->tokens, N, V, w.err);
+    ICP_CUDA(cudaGetLastError());
+    // K1: fused lm_head GEMM + online softmax statistics (logits stay in TMEM)
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.scale_log2 = (float)(1.4426950408889634 / cfg->temperature);
+    ep.inv_t = (float)(1.0 / cfg->temperature);
+    ep.targets = batch->tokens;
+    ep.part = w.part;
+    ep.ztok = w.ztok;
+    const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
+    ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
+  }
+  // K2: merge + IcePop epilogue
+  TokenArgs a;
+  fill_token_args(a, shape, cfg, batch, adv);
+  a.part = w.part;
+  a.n_parts = (int32_t)((V + BN_ - 1) / BN_);
+  a.ztok = w.ztok;
+  a.lse_f = out->lse;
+  a.lp_cur = out->lp_cur;
+  a.entropy_f = out->entropy;
+  a.kept = out->kept;
+  a.calib = out->calib;
+  a.surrogate = out->surrogate;
+  a.coeff_f = out->coeff;
+  a.block_stats = w.block_stats;
+  const int grid = token_grid(N);
+  k2_icepop_tokens<0><<<grid, TOK_THREADS, 0, st>>>(a);
+  ICP_CUDA(cudaGetLastError());
+  k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
+  k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+__global__ void k_logprob_finish(const float* part, int n_parts, const float* ztok, int64_t n, float* lse,
+                                 double* lp, float* entropy) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    float M = -1e30f;
+    for (int j = 0; j < n_parts; ++j) M = fmaxf(M, part[(int64_t)j * 3 * n + t]);
+    float S = 0.f, Q = 0.f;
+    for (int j = 0; j < n_parts; ++j) {
+      const float* p = part + (int64_t)j * 3 * n + t;
+      const float sc = exp2f(p[0] - M);
+      S = fmaf(p[n], sc, S);
+      Q = fmaf(sc, fmaf(p[0] - M, p[n], p[2 * n]), Q);
+    }
+    const float l2s = log2f(S);
+    const float l = (M + l2s) * LN2_F;
+    if (lse) lse[t] = l;
+    if (lp) lp[t] = (double)(ztok[t] - l);
+    if (entropy) entropy[t] = (l2s - Q / S) * LN2_F;
+  }
+}
+
+int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                        const int32_t* tokens, float* lse, double* lp, float* entropy, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BF16Workspace w = carve_bf16(shape, workspace, 0);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  if (N == 0) return ICEPOP_OK;
+  EpiParams ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.scale_log2 = (float)(1.4426950408889634 / temperature);
+  ep.inv_t = (float)(1.0 / temperature);
+  ep.targets = tokens;
+  ep.part = w.part;
+  ep.ztok = w.ztok;
+  const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
+  ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
+  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)((V + BN_ - 1) / BN_), w.ztok, N, lse, lp,
+                                                          entropy);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
+                    const int32_t* tokens, const float* lse, const float* coeff, double grad_scale, void* grad_hidden,
+                    int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  ICP_TRY(check_config(cfg));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  if (N == 0) {
+    if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
+    return ICEPOP_OK;
+  }
+  // chunk = as many dZ rows as the workspace holds (multiple of 128, >= 128)
+  const size_t fixed = carve_bf16(shape, nullptr, 0).bytes + 256;
+  if (!workspace || workspace_bytes < fixed + (size_t)128 * V * 2)
+    return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", fixed + (size_t)128 * V * 2);
+  int64_t chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
+  chunk = std::min<int64_t>(chunk, N);
+  if (chunk < N) chunk = chunk / BM * BM;
+  BF16Workspace w = carve_bf16(shape, workspace, chunk);
+  if (w.bytes > workspace_bytes) return fail(ICEPOP_EINVAL, "backward workspace carve overflow");
+
+  for (int64_t c0 = 0; c0 < N; c0 += chunk) {
+    const int64_t nc = std::min<int64_t>(chunk, N - c0);
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hidden) + c0 * d;
+    // K3: recompute logits, dZ chunk (bf16)
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.scale_log2 = (float)(1.4426950408889634 / cfg->temperature);
+    ep.inv_t = (float)(1.0 / cfg->temperature);
+    ep.targets = tokens + c0;
+    ep.lse = lse + c0;
+    ep.coeff = coeff + c0;
+    ep.coeff_scale = (float)grad_scale;
+    ep.dz = w.dz;
+    ep.ldz = V;
+    ep.vec_ok = (V % 8 == 0) && ((reinterpret_cast<uintptr_t>(w.dz) & 15u) == 0);
+    ICP_TRY(run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, nc, V, d, ep, st));
+    // K4: grad_hidden = dZ . W^T   (M = nc, N = d, K = V)
+    if (grad_hidden) {
+      EpiParams eh;
+      memset(&eh, 0, sizeof(eh));
+      const size_t esz = grad_hidden_f32 ? 4 : 2;
+      eh.out = static_cast<uint8_t*>(grad_hidden) + (size_t)c0 * d * esz;
+      eh.ldo = d;
+      eh.out_f32 = grad_hidden_f32 ? 1 : 0;
+      eh.vec_ok = ((reinterpret_cast<uintptr_t>(eh.out) & 15u) == 0) && (d % 8 == 0);
+      // B operand viewed [N = d, K = V]: W[d,V] is K-major, W[V,d] is MN-major
+      ICP_TRY(run_umma(EPI_STORE, w.dz, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st));
+    }
+    // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
+    if (grad_weight) {
+      EpiParams ew;
+      memset(&ew, 0, sizeof(ew));
+      ew.out = grad_weight;
+      ew.out_f32 = 1;
+      ew.accumulate = (accumulate || c0 > 0) ? 1 : 0;
+      ew.vec_ok = ((reinterpret_cast<uintptr_t>(grad_weight) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
+      if (dv) {
+        ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
+        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st));
+      } else {
+        ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
+        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st));
+      }
+    }
+  }
+  return ICEPOP_OK;
+}
+
+// ------------------------------------------------------------------ fp64 validation path
+int icepop_workspace_bytes_f64(const icepop_shape* shape, int32_t with_ref, size_t* bytes) {
+  ICP_TRY(check_shape(shape, false));
+  Carver c(nullptr);
+  c.take<double>((size_t)shape->n_tokens * shape->vocab);
+  if (with_ref) c.take<double>((size_t)shape->n_tokens * shape->vocab);
+  c.take<double>((size_t)shape->n_seqs);
+  c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
+  c.take<unsigned>(4);
+  c.take<double>((size_t)std::max<int64_t>(shape->n_tokens, 1));
+  *bytes = align_up(c.off, 256);
+  return ICEPOP_OK;
+}
+
+struct F64Workspace {
+  double* Z;
+  double* Zref;
+  double* adv;
+  double* block_stats;
+  unsigned* err;
+  double* kw;
+  size_t bytes;
+};
+
+static F64Workspace carve_f64(const icepop_shape* s, void* base, bool with_ref) {
+  Carver c(base);
+  F64Workspace w;
+  w.Z = c.take<double>((size_t)s->n_tokens * s->vocab);
+  w.Zref = with_ref ? c.take<double>((size_t)s->n_tokens * s->vocab) : nullptr;
+  w.adv = c.take<double>((size_t)s->n_seqs);
+  w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
+  w.err = c.take<unsigned>(4);
+  w.kw = c.take<double>((size_t)std::max<int64_t>(s->n_tokens, 1));
+  w.bytes = align_up(c.off, 256);
+  return w;
+}
+
+int icepop_fwd_f64(const icepop_shape* shape, const icepop_config* cfg, const double* hidden, const double* weight,
+                   const double* weight_ref, const icepop_batch* batch, const icepop_f64_out* out, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, false));
+  ICP_TRY(check_config(cfg));
+  if (!batch || !out || !out->stats || !out->lse || !out->lp_cur || !out->entropy)
+    return fail(ICEPOP_EINVAL, "null batch/out");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool with_ref = weight_ref != nullptr;
+  F64Workspace w = carve_f64(shape, workspace, with_ref);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "fp64 workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, V = shape->vocab;
+  const double* adv = nullptr;
+  ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
+  ICP_CUDA(cudaMemsetAsync(w.err, 0, sizeof(unsigned), st));
+  if (N > 0) {
+    k_check_tokens<<<token_grid(N), TOK_THREADS, 0, st>>>(batch->tokens, N, V, w.err);
+    ICP_TRY(logits_f64(shape, hidden, weight, w.Z, st));
+    if (with_ref) ICP_TRY(logits_f64(shape, hidden, weight_ref, w.Zref, st));
+    k_rowstats_f64<<<(unsigned)N, F64_ROW_THREADS, 0, st>>>(w.Z, w.Zref, V, cfg->temperature, batch->tokens,
+                                                            out->lse, out->lp_cur, out->entropy,
+                                                            with_ref ? out->kl : nullptr,
+                                                            with_ref ? out->lse_ref : nullptr, w.err);
+    ICP_CUDA(cudaGetLastError());
+    if (!with_ref && out->kl) ICP_CUDA(cudaMemsetAsync(out->kl, 0, sizeof(double) * N, st));
+  }
+  TokenArgs a;
+  fill_token_args(a, shape, cfg, batch, adv);
+  a.lp_cur_in = out->lp_cur;
+  a.entropy_in = out->entropy;
+  a.kl_in = with_ref ? out->kl : nullptr;
+  a.kept = out->kept;
+  a.calib = out->calib;
+  a.surrogate = out->surrogate;
+  a.coeff_d = out->coeff;
+  a.block_stats = w.block_stats;
+  const int grid = token_grid(N);
+  k2_icepop_tokens<1><<<grid, TOK_THREADS, 0, st>>>(a);
+  ICP_CUDA(cudaGetLastError());
+  k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
+  k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_bwd_f64(const icepop_shape* shape, const icepop_config* cfg, const double* hidden, const double* weight,
+                   const double* weight_ref, const icepop_batch* batch, const icepop_f64_out* fwd, double grad_scale,
+                   double* grad_hidden, double* grad_weight, int32_t accumulate, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, false));
+  ICP_TRY(check_config(cfg));
+  if (!fwd || !fwd->lse || !fwd->coeff) return fail(ICEPOP_EINVAL, "null forward outputs");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool kl_grad = weight_ref != nullptr && cfg->kl_coeff > 0.0;
+  if (kl_grad && (!fwd->kl || !fwd->lse_ref || !batch))
+    return fail(ICEPOP_EINVAL, "KL gradient needs kl, lse_ref and the batch geometry");
+  F64Workspace w = carve_f64(shape, workspace, kl_grad);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "fp64 workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  if (N == 0) {
+    if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(double) * d * V, st));
+    return ICEPOP_OK;
+  }
+  const int sg = std::min<int64_t>((N * V + 255) / 256, (int64_t)num_sms() * 16);
+  ICP_TRY(logits_f64(shape, hidden, weight, w.Z, st));
+  if (cfg->temperature != 1.0) k_scale_f64<<<sg, 256, 0, st>>>(w.Z, N * V, cfg->temperature);
+  if (kl_grad) {
+    ICP_TRY(logits_f64(shape, hidden, weight_ref, w.Zref, st));
+    if (cfg->temperature != 1.0) k_scale_f64<<<sg, 256, 0, st>>>(w.Zref, N * V, cfg->temperature);
+    k_kl_weight_f64<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(batch->cu_seqlens, shape->n_seqs,
+                                                                 batch->group_offsets, shape->n_groups,
+                                                                 shape->token_offset, N, cfg->kl_coeff,
+                                                                 cfg->temperature, w.kw);
+  }
+  k_dz_f64<<<(unsigned)N, F64_ROW_THREADS, 0, st>>>(w.Z, kl_grad ? w.Zref : nullptr, V, batch ? batch->tokens : nullptr,
+                                                    fwd->lse, kl_grad ? fwd->lse_ref : nullptr,
+                                                    kl_grad ? fwd->kl : nullptr, fwd->coeff, kl_grad ? w.kw : nullptr,
+                                                    grad_scale);
+  ICP_CUDA(cudaGetLastError());
+  if (grad_hidden) {
+    // dH[t,f] = sum_v dZ[t,v] W(f,v)
+    if (dv) ICP_TRY(gemm_f64(w.Z, V, 1, weight, 1, V, grad_hidden, d, N, d, V, 0, st));
+    else ICP_TRY(gemm_f64(w.Z, V, 1, weight, d, 1, grad_hidden, d, N, d, V, 0, st));
+  }
+  if (grad_weight) {
+    if (dv) ICP_TRY(gemm_f64(hidden, 1, d, w.Z, V, 1, grad_weight, V, d, V, N, accumulate, st));
+    else ICP_TRY(gemm_f64(w.Z, 1, V, hidden, d, 1, grad_weight, d, V, d, N, accumulate, st));
+  }
+  return ICEPOP_OK;
+}
+
+int icepop_finish(const double* stats, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ICP_CUDA(cudaStreamSynchronize(st));
+  double host_err = 0.0;
+  ICP_CUDA(cudaMemcpy(&host_err, stats + ICEPOP_STAT_ERRORS, sizeof(double), cudaMemcpyDefault));
+  const unsigned e = (unsigned)host_err;
+  if (e & ERR_BAD_TOKEN) return fail(ICEPOP_EINVAL, "token id outside the vocabulary");
+  if (e & ICEPOP_ERR_CALIB_OVERFLOW) return fail(ICEPOP_ENUMERIC, "calibration ratio overflow");
+  if (e & ICEPOP_ERR_RATIO_OVERFLOW) return fail(ICEPOP_ENUMERIC, "importance ratio overflow");
+  if (e & ICEPOP_ERR_NONFINITE) return fail(ICEPOP_ENUMERIC, "objective or gradient is not finite");
+  return ICEPOP_OK;
+}
+
+int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K, int32_t a_mn_major,
+                     int32_t b_mn_major, int32_t c_f32, int32_t accumulate, void* stream) {
+  if (!A || !B || !C) return fail(ICEPOP_EINVAL, "null operand");
+  if (accumulate && !c_f32) return fail(ICEPOP_EINVAL, "accumulate needs an f32 output");
+  EpiParams ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.out = C;
+  ep.ldo = N;
+  ep.out_f32 = c_f32 ? 1 : 0;
+  ep.accumulate = accumulate ? 1 : 0;
+  ep.vec_ok = ((reinterpret_cast<uintptr_t>(C) & 15u) == 0) && (N % 8 == 0);
+  // A: [M,K] (K-major) or [K,M]; B: [N,K] or [K,N]
+  const int64_t lda = a_mn_major ? M : K;
+  const int64_t ldb = b_mn_major ? N : K;
+  return run_umma(EPI_STORE, A, lda, a_mn_major != 0, B, ldb, b_mn_major != 0, M, N, K, ep,
+                  static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

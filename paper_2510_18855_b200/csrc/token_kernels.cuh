@@ -1,0 +1,262 @@
+// token_kernels.cuh -- per-token, bandwidth-bound kernels of the IcePop path.
+//
+//   k0_group_advantages : objective.py:153-159 (numpy pairwise-sum order reproduced, so
+//                         the advantages are bit-identical to the reference's).
+//   k2_icepop_tokens    : merge of the K1 split-V partials (lse, lp_cur, entropy) and the
+//                         IcePop mask / ratio / clipped surrogate / gradient coefficient,
+//                         objective.py:215-252, with the reference's fp64 arithmetic order.
+//   k_finalize_stats    : fixed-order reduction of per-block fp64 partials (no atomics).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/icepop.h"
+
+namespace icp {
+
+constexpr int TOK_THREADS = 256;
+constexpr float LN2_F = 0.69314718055994531f;
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum)
+// for contiguous data, over f(i) for i in [0, n). Reproducing its association order
+// makes the group advantages bit-identical to numpy's r.mean() / r.std().
+template <class F>
+__device__ double np_pairwise_sum(F f, int lo, int n) {
+  if (n < 8) {
+    double res = 0.;
+    for (int i = 0; i < n; ++i) res += f(lo + i);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += f(lo + i + j);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += f(lo + i);
+    return res;
+  }
+  // n > 128: split in two halves with the first a multiple of 8 (iterative on the left)
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(f, lo, n2) + np_pairwise_sum(f, lo + n2, n - n2);
+}
+
+// One thread per group: A_i = (R_i - mean) / max(std_pop, 1e-6)  (objective.py:153-159).
+// Groups with fewer than 2 sequences yield NaN (the host layer raises ValueError first).
+__global__ void k0_group_advantages(const double* __restrict__ rewards,
+                                    const int32_t* __restrict__ group_offsets, int32_t n_groups,
+                                    double* __restrict__ adv) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const int s0 = group_offsets[g], s1 = group_offsets[g + 1];
+  const int n = s1 - s0;
+  const double* r = rewards + s0;
+  if (n < 2) {
+    for (int i = 0; i < n; ++i) adv[s0 + i] = nan("");
+    return;
+  }
+  const double mean = np_pairwise_sum([&](int i) { return r[i]; }, 0, n) / (double)n;
+  const double var = np_pairwise_sum([&](int i) { const double x = r[i] - mean; return x * x; }, 0, n) / (double)n;
+  const double std = sqrt(var);
+  const double den = std > 1e-6 ? std : 1e-6;  // max(std, 1e-6)
+  for (int i = 0; i < n; ++i) adv[s0 + i] = (r[i] - mean) / den;
+}
+
+struct TokenArgs {
+  int64_t n_tokens;
+  int64_t token_offset;
+  int32_t n_seqs;
+  int32_t n_groups;
+  const int32_t* tokens;
+  const double* lp_old;
+  const double* lp_inf;
+  const int32_t* cu_seqlens;
+  const int32_t* group_offsets;
+  const double* adv;
+  // bf16 mode inputs: K1 partials
+  const float* part;  // [n_parts][3][n_tokens]
+  int32_t n_parts;
+  const float* ztok;  // [n_tokens]
+  // f64 mode inputs (already computed per token by the f64 row kernel)
+  const double* lp_cur_in;
+  const double* entropy_in;
+  const double* kl_in;
+  // config
+  double alpha, beta, clip_eps, tis_cap, temperature, kl_coeff;
+  int32_t algo;
+  // outputs (any may be null unless noted)
+  float* lse_f;
+  double* lp_cur;
+  float* entropy_f;
+  uint8_t* kept;
+  double* calib;
+  double* surrogate;
+  float* coeff_f;
+  double* coeff_d;
+  double* block_stats;  // [gridDim.x][ICEPOP_NSTATS] (required)
+};
+
+__device__ __forceinline__ int upper_bound_i32(const int32_t* a, int n, int64_t x) {
+  // first index i in [0, n) with a[i] > x (a non-decreasing)
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Per-token weight w_t = 1 / (n_groups * G_g * n_i)  (objective.py:215)
+__device__ __forceinline__ void seq_of_token(const TokenArgs& a, int64_t t_global, int& seq, double& w) {
+  seq = upper_bound_i32(a.cu_seqlens, a.n_seqs + 1, t_global) - 1;
+  const int g = upper_bound_i32(a.group_offsets, a.n_groups + 1, seq) - 1;
+  const int64_t n_i = (int64_t)a.cu_seqlens[seq + 1] - a.cu_seqlens[seq];
+  const int64_t G = (int64_t)a.group_offsets[g + 1] - a.group_offsets[g];
+  w = 1.0 / (double)((int64_t)a.n_groups * G * n_i);
+}
+
+template <int NW>
+__device__ __forceinline__ void block_reduce_stats(double (&st)[ICEPOP_NSTATS], unsigned err,
+                                                   double* out) {
+  __shared__ double sh[NW][ICEPOP_NSTATS];
+  __shared__ unsigned sherr[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < ICEPOP_NSTATS - 1; ++k) {
+    double v = st[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    st[k] = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) err |= __shfl_xor_sync(0xffffffffu, err, o);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < ICEPOP_NSTATS - 1; ++k) sh[warp][k] = st[k];
+    sherr[warp] = err;
+  }
+  __syncthreads();
+  if (threadIdx.x < ICEPOP_NSTATS) {
+    const int k = threadIdx.x;
+    double v = 0.0;
+    unsigned e = 0;
+    for (int w = 0; w < NW; ++w) {
+      if (k < ICEPOP_NSTATS - 1) v += sh[w][k]; else e |= sherr[w];
+    }
+    out[(int64_t)blockIdx.x * ICEPOP_NSTATS + k] = (k < ICEPOP_NSTATS - 1) ? v : (double)e;
+  }
+}
+
+// MODE 0: bf16 path (merge K1 partials), MODE 1: fp64 path (lp_cur/entropy/kl given).
+template <int MODE>
+__global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs a) {
+  double st[ICEPOP_NSTATS] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned err = 0;
+  const double clip_lo = 1.0 - a.clip_eps, clip_hi = 1.0 + a.clip_eps;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.n_tokens;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double lp_cur, ent, kl = 0.0;
+    if (MODE == 0) {
+      // merge split-V partials (log2 units) -> lse, entropy; lp = z[y] - lse
+      float M = -1e30f;
+      for (int j = 0; j < a.n_parts; ++j) M = fmaxf(M, a.part[(int64_t)j * 3 * a.n_tokens + t]);
+      float S = 0.f, Q = 0.f;
+      for (int j = 0; j < a.n_parts; ++j) {
+        const float* p = a.part + (int64_t)j * 3 * a.n_tokens + t;
+        const float mj = p[0], sj = p[a.n_tokens], qj = p[2 * a.n_tokens];
+        const float sc = exp2f(mj - M);
+        S = fmaf(sj, sc, S);
+        Q = fmaf(sc, fmaf(mj - M, sj, qj), Q);
+      }
+      const float l2s = log2f(S);
+      const float lse = (M + l2s) * LN2_F;
+      const float entf = (l2s - Q / S) * LN2_F;
+      lp_cur = (double)(a.ztok[t] - lse);
+      ent = (double)entf;
+      if (a.lse_f) a.lse_f[t] = lse;
+      if (a.entropy_f) a.entropy_f[t] = entf;
+      if (!isfinite(lse) || !isfinite(entf) || !isfinite(a.ztok[t])) err |= ICEPOP_ERR_NONFINITE;
+    } else {
+      lp_cur = a.lp_cur_in[t];
+      ent = a.entropy_in[t];
+      kl = a.kl_in ? a.kl_in[t] : 0.0;
+    }
+    if (a.lp_cur && MODE == 0) a.lp_cur[t] = lp_cur;
+
+    int seq;
+    double w;
+    seq_of_token(a, a.token_offset + t, seq, w);
+    const double A = a.adv[seq];
+    const double lpo = a.lp_old[t];
+    // calibration and mask (objective.py:227-238)
+    const double c = exp(lpo - a.lp_inf[t]);
+    if (!isfinite(c)) err |= ICEPOP_ERR_CALIB_OVERFLOW;
+    bool kept;
+    double factor;
+    if (a.algo == ICEPOP_ALGO_ICEPOP) {
+      kept = (c >= a.alpha) && (c <= a.beta);
+      factor = kept ? c : 0.0;
+    } else if (a.algo == ICEPOP_ALGO_GRPO) {
+      kept = true;
+      factor = c;
+    } else {
+      kept = true;
+      factor = fmin(c, a.tis_cap);
+    }
+    // ratio / clip / surrogate (objective.py:240-246)
+    const double r = exp(lp_cur - lpo);
+    if (!isfinite(r)) err |= ICEPOP_ERR_RATIO_OVERFLOW;
+    const double unclipped = r * A;
+    const double clipped = fmin(fmax(r, clip_lo), clip_hi) * A;
+    const bool active = unclipped <= clipped;
+    const double pg = factor * (active ? unclipped : clipped);
+    // gradient coefficient (objective.py:250)
+    const double coeff = active ? w * factor * r * A / a.temperature : 0.0;
+    const double value = pg - a.kl_coeff * kl;
+
+    if (a.kept) a.kept[t] = kept ? 1 : 0;
+    if (a.calib) a.calib[t] = c;
+    if (a.surrogate) a.surrogate[t] = pg;
+    if (a.coeff_f) a.coeff_f[t] = (float)coeff;
+    if (a.coeff_d) a.coeff_d[t] = coeff;
+
+    st[ICEPOP_STAT_OBJECTIVE] += w * value;
+    st[ICEPOP_STAT_N_POPPED] += kept ? 0.0 : 1.0;
+    st[ICEPOP_STAT_TOKENS] += 1.0;
+    st[ICEPOP_STAT_SUM_ENTROPY] += ent;
+    st[ICEPOP_STAT_SUM_ENTROPY_POPPED] += kept ? 0.0 : ent;
+    st[ICEPOP_STAT_SUM_LOGP] += lp_cur;
+    st[ICEPOP_STAT_SUM_KL] += kl;
+  }
+  if (!isfinite(st[ICEPOP_STAT_OBJECTIVE])) err |= ICEPOP_ERR_NONFINITE;
+  block_reduce_stats<TOK_THREADS / 32>(st, err, a.block_stats);
+}
+
+// Single block: stats[k] = sum over blocks (fixed order); errors OR-ed.
+__global__ void k_finalize_stats(const double* __restrict__ block_stats, int n_blocks,
+                                 double* __restrict__ stats) {
+  __shared__ double sh[ICEPOP_NSTATS][33];
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;  // 8 warps x 32 lanes
+  double v = 0.0;
+  unsigned e = 0;
+  for (int b = lane; b < n_blocks; b += 32) {
+    const double x = block_stats[(int64_t)b * ICEPOP_NSTATS + k];
+    if (k == ICEPOP_STAT_ERRORS) e |= (unsigned)x; else v += x;
+  }
+  sh[k][lane] = (k == ICEPOP_STAT_ERRORS) ? (double)e : v;
+  __syncthreads();
+  if (lane == 0) {
+    double acc = 0.0;
+    unsigned ee = 0;
+    for (int i = 0; i < 32; ++i) {
+      if (k == ICEPOP_STAT_ERRORS) ee |= (unsigned)sh[k][i]; else acc += sh[k][i];
+    }
+    stats[k] = (k == ICEPOP_STAT_ERRORS) ? (double)ee : acc;
+  }
+}
+
+}  // namespace icp

@@ -1,0 +1,367 @@
+// umma_gemm.cuh -- persistent, warp-specialised tcgen05 GEMM for sm_100a with the
+// three epilogues the IcePop path needs:
+//
+//   EPI_STORE : C (+)= A.B^T   -> f32 / bf16 (grad_hidden K4, grad_weight K5)
+//   EPI_LSE   : Z = A.B^T / T  -> per-(row, n-tile) online (max, sum-exp, sum p*z) partials
+//               plus the gathered logit of the sampled token; Z never leaves TMEM (K1).
+//               Replaces batched_train_logits + batched_log_softmax (policy.py:279-289,
+//               350-355) and the gather lp_cur = log_probs[pos, tok] (objective.py:223).
+//   EPI_DZ    : recompute Z tile, dZ = c_t * (e_{y_t} - softmax(z_t)) -> bf16 (K3),
+//               objective.py:250-252.
+//
+// Tile: BM = 128 rows (one TMEM lane per row), BN = 256 columns, BK = 64 (one 128-byte
+// swizzle atom of bf16). Roles (192 threads, 1 CTA / SM):
+//   warp 0      : TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane), 2 TMEM accumulators
+//   warps 2..5  : epilogue; thread i of warp w owns TMEM lane 32*(w%4)+i == tile row.
+// The accumulator is double-buffered in TMEM (2 x 256 of the 512 columns) so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#pragma once
+
+#include "sm100.cuh"
+
+namespace icp {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int GEMM_THREADS = 192;
+constexpr float LOG2E_F = 1.4426950408889634f;
+
+enum EpiKind { EPI_STORE = 0, EPI_LSE = 1, EPI_DZ = 2 };
+
+struct GemmShape {
+  int32_t M, N, K;
+  int32_t m_tiles, n_tiles, k_blocks;
+  int32_t num_tiles;
+  int32_t group_m;  // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
+};
+
+struct EpiParams {
+  // EPI_STORE
+  void* out;
+  int64_t ldo;
+  int32_t out_f32;
+  int32_t accumulate;
+  int32_t vec_ok;  // 16-byte aligned rows -> vector stores
+  // EPI_LSE / EPI_DZ
+  float scale_log2;        // log2(e) / T
+  float inv_t;             // 1 / T
+  const int32_t* targets;  // [M] sampled token ids
+  float* part;             // EPI_LSE: [n_tiles][3][M] (max2, sum, q) in log2 units
+  float* ztok;             // EPI_LSE: [M] z[y] (natural units), written by the owning tile
+  const float* lse;        // EPI_DZ: [M] natural units
+  const float* coeff;      // EPI_DZ: [M]
+  float coeff_scale;       // EPI_DZ: grad_scale
+  __nv_bfloat16* dz;       // EPI_DZ: [M, ldz]
+  int64_t ldz;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& m_blk, int& n_blk) {
+  const int group = sh.group_m * sh.n_tiles;
+  const int g = tile / group;
+  const int first_m = g * sh.group_m;
+  const int gm = min(sh.m_tiles - first_m, sh.group_m);
+  const int r = tile - g * group;
+  m_blk = first_m + r % gm;
+  n_blk = r / gm;
+}
+
+// ------------------------------------------------------------------ epilogues
+template <int BN>
+__device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
+                                          int row, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool row_ok = m < sh.M;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);  // warp-collective: never inside a per-thread branch
+    const int col0 = n0 + c * 32;
+    if (!row_ok || col0 >= sh.N) continue;
+    const bool full = (col0 + 32 <= sh.N) && ep.vec_ok;
+    if (ep.out_f32) {
+      float* dst = reinterpret_cast<float*>(ep.out) + (int64_t)m * ep.ldo + col0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          if (ep.accumulate) {
+            const float4 p = *reinterpret_cast<const float4*>(dst + j);
+            o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+          }
+          *reinterpret_cast<float4*>(dst + j) = o;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < sh.N) dst[j] = ep.accumulate ? dst[j] + v[j] : v[j];
+      }
+    } else {
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + (int64_t)m * ep.ldo + col0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 o;
+          o.x = pack_bf16x2(v[j], v[j + 1]);
+          o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+          o.z = pack_bf16x2(v[j + 4], v[j + 5]);
+          o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+          *reinterpret_cast<uint4*>(dst + j) = o;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < sh.N) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+    }
+  }
+}
+
+// Online log-sum-exp over this tile's BN columns for one row, in log2 units:
+//   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z*log2(e)
+// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge.
+template <int BN>
+__device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
+                                        int n_blk, int row, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool row_ok = m < sh.M;
+  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    const int col0 = n0 + c * 32;
+    if (col0 >= sh.N) continue;  // warp-uniform
+    const int rel = y - col0;
+    if ((unsigned)rel < 32u) {  // the sampled token's logit lives in this chunk
+      float zt = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) zt = (j == rel) ? v[j] : zt;
+      if (row_ok) ep.ztok[m] = zt * ep.inv_t;
+    }
+    float cm = -1e30f;
+    if (col0 + 32 <= sh.N) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        v[j] *= ep.scale_log2;
+        cm = fmaxf(cm, v[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        v[j] = (col0 + j < sh.N) ? v[j] * ep.scale_log2 : -1e30f;
+        cm = fmaxf(cm, v[j]);
+      }
+    }
+    const float nm = fmaxf(run_m, cm);
+    const float a = fast_exp2(run_m - nm);
+    run_q = a * (run_q + (run_m - nm) * run_s);
+    run_s = a * run_s;
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float d = v[j] - nm;
+      const float e = fast_exp2(d);
+      s += e;
+      q = fmaf(e, d, q);
+    }
+    run_s += s;
+    run_q += q;
+    run_m = nm;
+  }
+  if (row_ok) {
+    float* p = ep.part + (int64_t)n_blk * 3 * sh.M + m;
+    p[0] = run_m;
+    p[sh.M] = run_s;
+    p[2 * (int64_t)sh.M] = run_q;
+  }
+}
+
+// dZ = coeff_scale * c_t * (e_{y_t} - softmax(z_t)) for this tile -> bf16.
+template <int BN>
+__device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
+                                       int row, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool row_ok = m < sh.M;
+  const float lse2 = row_ok ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
+  const float cf = row_ok ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
+  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    const int col0 = n0 + c * 32;
+    if (!row_ok || col0 >= sh.N) continue;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float p0 = fast_exp2(fmaf(v[2 * j], ep.scale_log2, -lse2));
+      const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
+      const float d0 = fmaf(-cf, p0, (col0 + 2 * j == y) ? cf : 0.f);
+      const float d1 = fmaf(-cf, p1, (col0 + 2 * j + 1 == y) ? cf : 0.f);
+      pk[j] = pack_bf16x2(d0, d1);
+    }
+    __nv_bfloat16* dst = ep.dz + (int64_t)m * ep.ldz + col0;
+    if (col0 + 32 <= sh.N && ep.vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+        if (col0 + 2 * j < sh.N) dst[2 * j] = h.x;
+        if (col0 + 2 * j + 1 < sh.N) dst[2 * j + 1] = h.y;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ mainloop
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmShape sh, const EpiParams ep) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES);
+  const uint32_t tempty0 = smem_u32(bars + 2 * STAGES + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull0 + 8 * s, 1);
+      mbar_init(tempty0 + 8 * s, 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+        int m_blk, n_blk;
+        tile_coords(sh, tile, m_blk, n_blk);
+        const int m0 = m_blk * BM, n0 = n_blk * BN;
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+          const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
+          if (!A_MN) {
+            tma_load_2d(a_dst, &tmA, fb, kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * (BK * 128), &tmA, fb, m0 + 64 * j, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_dst, &tmB, fb, kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * (BK * 128), &tmB, fb, n0 + 64 * j, kb * BK);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
+                                     : sdesc_sw128(a_base + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
+                                     : sdesc_sw128(b_base + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs finish
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+      int m_blk, n_blk;
+      tile_coords(sh, tile, m_blk, n_blk);
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m_blk * BM, n_blk * BN, row, taddr);
+      if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m_blk * BM, n_blk * BN, n_blk, row, taddr);
+      if (EPI == EPI_DZ) epi_dz<BN>(sh, ep, m_blk * BM, n_blk * BN, row, taddr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+}  // namespace icp

@@ -1,0 +1,473 @@
+"""Tensor-level IcePop objective on B200: the torch face of ``libicepop_b200.so``.
+
+Three layers, all on device, none with a CPU fallback:
+
+* :func:`icepop_fwd` / :func:`icepop_bwd` -- functional forward (K1 fused lm_head GEMM +
+  online log-softmax, K2 IcePop epilogue) and backward (K3 recompute -> bf16 dZ chunk,
+  K4 dHidden, K5 dW), dispatched on dtype: bfloat16 -> tcgen05 path, float64 -> SIMT
+  validation path.
+* :func:`icepop_loss` -- a ``torch.library`` custom op with autograd (loss = -J), for
+  training code that wants ``loss.backward()``.
+* :class:`PackedBatch` -- the packed per-token / per-sequence metadata the kernels read
+  (the reference's ``PromptGroup``/``TokenRecord`` objects flattened in its own
+  group-major order, objective.py:204-276).
+
+Semantics follow objective.py:172-298; ``stats`` holds this
+rank's partial sums (include/icepop.h ``enum icepop_stat``) -- sum them across ranks
+(``paper_2510_18855_b200.distributed``) before deriving the global diagnostics.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+
+ALGOS = {"icepop": _lib.ALGO_ICEPOP, "grpo": _lib.ALGO_GRPO, "tis": _lib.ALGO_TIS}
+LAYOUTS = {"dv": _lib.W_DV, "vd": _lib.W_VD}
+
+# Largest bf16 dZ chunk the backward materialises (bytes); the rest of the batch is
+# processed in further chunks with dW accumulated in place.
+DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(32 << 30)))
+
+
+@dataclass(frozen=True)
+class IcePopConfig:
+    """objective.py:47-82 (MaskingBounds + ObjectiveConfig) and the temperature."""
+
+    alpha: float = 0.5
+    beta: float = 5.0
+    clip_eps: float = 0.2
+    tis_cap: float = 2.0
+    temperature: float = 1.0
+    kl_coeff: float = 0.0
+    algo: str = "icepop"
+
+    def to_c(self) -> _lib.Config:
+        if self.algo not in ALGOS:
+            raise ValueError(f"unknown algorithm {self.algo!r}")
+        return _lib.Config(
+            alpha=self.alpha,
+            beta=self.beta,
+            clip_eps=self.clip_eps,
+            tis_cap=self.tis_cap,
+            temperature=self.temperature,
+            kl_coeff=self.kl_coeff,
+            algo=ALGOS[self.algo],
+        )
+
+
+@dataclass
+class PackedBatch:
+    """Packed rollout batch, device tensors.
+
+    tokens / lp_train_old / lp_infer_old cover this rank's contiguous token range
+    [token_offset, token_offset + n_local); cu_seqlens, group_offsets and advantages
+    (or rewards) describe the GLOBAL batch and are replicated on every rank.
+    """
+
+    tokens: torch.Tensor  # int32 [n_local]
+    lp_train_old: torch.Tensor  # float64 [n_local]
+    lp_infer_old: torch.Tensor  # float64 [n_local]
+    cu_seqlens: torch.Tensor  # int32 [S+1]
+    group_offsets: torch.Tensor  # int32 [n_groups+1]
+    advantages: torch.Tensor | None = None  # float64 [S]
+    rewards: torch.Tensor | None = None  # float64 [S] (advantages computed by K0 if None)
+    token_offset: int = 0
+
+    @property
+    def n_seqs(self) -> int:
+        return int(self.cu_seqlens.numel()) - 1
+
+    @property
+    def n_groups(self) -> int:
+        return int(self.group_offsets.numel()) - 1
+
+    def to_c(self) -> _lib.Batch:
+        return _lib.Batch(
+            tokens=_lib.ptr(self.tokens),
+            lp_train_old=_lib.ptr(self.lp_train_old),
+            lp_infer_old=_lib.ptr(self.lp_infer_old),
+            cu_seqlens=_lib.ptr(self.cu_seqlens),
+            group_offsets=_lib.ptr(self.group_offsets),
+            advantages=_lib.ptr(self.advantages),
+            rewards=_lib.ptr(self.rewards),
+        )
+
+    def validate(self) -> None:
+        for name in ("tokens", "cu_seqlens", "group_offsets"):
+            if getattr(self, name).dtype != torch.int32:
+                raise ValueError(f"{name} must be int32")
+        for name in ("lp_train_old", "lp_infer_old"):
+            if getattr(self, name).dtype != torch.float64:
+                raise ValueError(f"{name} must be float64 (the mask is computed bit-exactly in fp64)")
+        if self.advantages is None and self.rewards is None:
+            raise ValueError("either advantages or rewards must be given")
+        if self.n_groups < 1:
+            raise ValueError("objective needs at least one prompt group")
+
+
+@dataclass
+class IcePopForward:
+    """Per-token outputs (this rank) and the fp64 partial statistics vector."""
+
+    lse: torch.Tensor
+    lp_cur: torch.Tensor
+    entropy: torch.Tensor
+    kept: torch.Tensor
+    calib: torch.Tensor
+    surrogate: torch.Tensor
+    coeff: torch.Tensor
+    stats: torch.Tensor  # float64 [8] on device
+    kl: torch.Tensor | None = None
+    lse_ref: torch.Tensor | None = None
+    extras: dict = field(default_factory=dict)
+
+
+def _shape(hidden: torch.Tensor, weight: torch.Tensor, layout: str, batch: PackedBatch) -> _lib.Shape:
+    if layout not in LAYOUTS:
+        raise ValueError(f"weight layout must be 'dv' ([d,V]) or 'vd' ([V,d]), got {layout!r}")
+    if hidden.dim() != 2 or weight.dim() != 2:
+        raise ValueError("hidden and weight must be 2-D")
+    n, d = hidden.shape
+    if layout == "dv":
+        dw, v = weight.shape
+    else:
+        v, dw = weight.shape
+    if dw != d:
+        raise ValueError(f"hidden dim {d} does not match weight {tuple(weight.shape)} ({layout})")
+    if batch.tokens.numel() != n or batch.lp_train_old.numel() != n or batch.lp_infer_old.numel() != n:
+        raise ValueError("per-token tensors must have one entry per hidden row")
+    return _lib.Shape(
+        n_tokens=n,
+        token_offset=batch.token_offset,
+        hidden=d,
+        vocab=v,
+        n_seqs=batch.n_seqs,
+        n_groups=batch.n_groups,
+        weight_layout=LAYOUTS[layout],
+    )
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _lib_for(t: torch.Tensor):
+    if t.device.type != "cuda":
+        raise RuntimeError("libicepop_b200 runs on CUDA tensors only (no CPU fallback)")
+    return _lib.ensure_device(t.device.index if t.device.index is not None else torch.cuda.current_device())
+
+
+def icepop_fwd(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    batch: PackedBatch,
+    cfg: IcePopConfig = IcePopConfig(),
+    layout: str = "vd",
+    weight_ref: torch.Tensor | None = None,
+) -> IcePopForward:
+    """Forward of the IcePop objective on this rank's tokens (objective.py:215-278)."""
+    lib = _lib_for(hidden)
+    batch.validate()
+    hidden = hidden.contiguous()
+    weight = weight.contiguous()
+    shape = _shape(hidden, weight, layout, batch)
+    dev = hidden.device
+    n = shape.n_tokens
+    st = _stream(dev)
+    stats = torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev)
+    kept = torch.empty(n, dtype=torch.uint8, device=dev)
+    calib = torch.empty(n, dtype=torch.float64, device=dev)
+    surrogate = torch.empty(n, dtype=torch.float64, device=dev)
+    lp_cur = torch.empty(n, dtype=torch.float64, device=dev)
+    c_cfg = cfg.to_c()
+    c_batch = batch.to_c()
+    if hidden.dtype == torch.bfloat16:
+        if weight.dtype != torch.bfloat16:
+            raise ValueError("bf16 hidden needs a bf16 weight")
+        if weight_ref is not None:
+            raise ValueError("weight_ref (KL-to-ref) is only available in the fp64 path in this build")
+        lse = torch.empty(n, dtype=torch.float32, device=dev)
+        entropy = torch.empty(n, dtype=torch.float32, device=dev)
+        coeff = torch.empty(n, dtype=torch.float32, device=dev)
+        fwd_b = _lib._sz()
+        _lib.check(lib.icepop_workspace_bytes(shape, 0, fwd_b, None))
+        ws = torch.empty(max(fwd_b.value, 1), dtype=torch.uint8, device=dev)
+        out = _lib.FwdOut(
+            lse=lse.data_ptr(),
+            lp_cur=lp_cur.data_ptr(),
+            entropy=entropy.data_ptr(),
+            kept=kept.data_ptr(),
+            calib=calib.data_ptr(),
+            surrogate=surrogate.data_ptr(),
+            coeff=coeff.data_ptr(),
+            stats=stats.data_ptr(),
+        )
+        _lib.check(lib.icepop_fwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), c_batch, out,
+                                       ws.data_ptr(), ws.numel(), st))
+        return IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats)
+    if hidden.dtype == torch.float64:
+        if weight.dtype != torch.float64:
+            raise ValueError("fp64 hidden needs an fp64 weight")
+        wr = None
+        if weight_ref is not None:
+            wr = weight_ref.contiguous()
+            if wr.shape != weight.shape or wr.dtype != torch.float64:
+                raise ValueError("weight_ref must match weight's shape and dtype")
+        lse = torch.empty(n, dtype=torch.float64, device=dev)
+        entropy = torch.empty(n, dtype=torch.float64, device=dev)
+        coeff = torch.empty(n, dtype=torch.float64, device=dev)
+        kl = torch.zeros(n, dtype=torch.float64, device=dev)
+        lse_ref = torch.zeros(n, dtype=torch.float64, device=dev)
+        nb = _lib._sz()
+        _lib.check(lib.icepop_workspace_bytes_f64(shape, 1 if wr is not None else 0, nb))
+        ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=dev)
+        out = _lib.F64Out(
+            lse=lse.data_ptr(),
+            lp_cur=lp_cur.data_ptr(),
+            entropy=entropy.data_ptr(),
+            kl=kl.data_ptr(),
+            lse_ref=lse_ref.data_ptr(),
+            kept=kept.data_ptr(),
+            calib=calib.data_ptr(),
+            surrogate=surrogate.data_ptr(),
+            coeff=coeff.data_ptr(),
+            stats=stats.data_ptr(),
+        )
+        _lib.check(lib.icepop_fwd_f64(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), c_batch,
+                                      out, ws.data_ptr(), ws.numel(), st))
+        return IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats, kl=kl, lse_ref=lse_ref)
+    raise ValueError(f"unsupported dtype {hidden.dtype}: use bfloat16 (tensor cores) or float64 (validation)")
+
+
+def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int) -> int:
+    """Backward workspace for a dZ chunk of at most DZ_CHUNK_BYTES."""
+    lib = _lib.load()
+    shape = _lib.Shape(n_tokens=n_tokens, token_offset=0, hidden=hidden, vocab=vocab, n_seqs=max(n_seqs, 1),
+                       n_groups=1, weight_layout=_lib.W_VD)
+    chunk = max(128, min(n_tokens, DZ_CHUNK_BYTES // (2 * vocab)) // 128 * 128)
+    bwd_b = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, chunk, None, bwd_b))
+    return bwd_b.value
+
+
+def icepop_bwd(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    batch: PackedBatch,
+    fwd: IcePopForward,
+    cfg: IcePopConfig = IcePopConfig(),
+    layout: str = "vd",
+    grad_scale: float = 1.0,
+    need_hidden: bool = True,
+    need_weight: bool = True,
+    grad_weight: torch.Tensor | None = None,
+    weight_ref: torch.Tensor | None = None,
+    grad_hidden_dtype: torch.dtype | None = None,
+) -> tuple[torch.Tensor | None, torch.Tensor | None]:
+    """Gradients of grad_scale * J: (d/dhidden, d/dweight), objective.py:250-266.
+
+    ``grad_weight`` (f32 for bf16 inputs, f64 for fp64), if given, is accumulated into.
+    """
+    lib = _lib_for(hidden)
+    hidden = hidden.contiguous()
+    weight = weight.contiguous()
+    shape = _shape(hidden, weight, layout, batch)
+    dev = hidden.device
+    st = _stream(dev)
+    n, d, v = shape.n_tokens, shape.hidden, shape.vocab
+    c_cfg = cfg.to_c()
+    wshape = tuple(weight.shape)
+    if hidden.dtype == torch.bfloat16:
+        gh_dtype = grad_hidden_dtype or torch.bfloat16
+        if gh_dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("grad_hidden_dtype must be bfloat16 or float32")
+        gh = torch.empty((n, d), dtype=gh_dtype, device=dev) if need_hidden else None
+        accumulate = grad_weight is not None
+        gw = grad_weight if accumulate else (torch.empty(wshape, dtype=torch.float32, device=dev) if need_weight else None)
+        if gw is not None and (gw.dtype != torch.float32 or tuple(gw.shape) != wshape or not gw.is_contiguous()):
+            raise ValueError("grad_weight must be a contiguous float32 tensor shaped like weight")
+        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs), dtype=torch.uint8, device=dev)
+        _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), batch.tokens.data_ptr(),
+                                       fwd.lse.data_ptr(), fwd.coeff.data_ptr(), float(grad_scale), _lib.ptr(gh),
+                                       1 if gh_dtype == torch.float32 else 0, _lib.ptr(gw), 1 if accumulate else 0,
+                                       ws.data_ptr(), ws.numel(), st))
+        return gh, gw
+    if hidden.dtype == torch.float64:
+        gh = torch.empty((n, d), dtype=torch.float64, device=dev) if need_hidden else None
+        accumulate = grad_weight is not None
+        gw = grad_weight if accumulate else (torch.empty(wshape, dtype=torch.float64, device=dev) if need_weight else None)
+        wr = weight_ref.contiguous() if weight_ref is not None else None
+        nb = _lib._sz()
+        kl_grad = wr is not None and cfg.kl_coeff > 0.0
+        _lib.check(lib.icepop_workspace_bytes_f64(shape, 1 if kl_grad else 0, nb))
+        ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=dev)
+        f = _lib.F64Out(
+            lse=fwd.lse.data_ptr(),
+            lp_cur=fwd.lp_cur.data_ptr(),
+            entropy=fwd.entropy.data_ptr(),
+            kl=_lib.ptr(fwd.kl),
+            lse_ref=_lib.ptr(fwd.lse_ref),
+            kept=None,
+            calib=None,
+            surrogate=None,
+            coeff=fwd.coeff.data_ptr(),
+            stats=fwd.stats.data_ptr(),
+        )
+        _lib.check(lib.icepop_bwd_f64(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr),
+                                      batch.to_c(), f, float(grad_scale), _lib.ptr(gh), _lib.ptr(gw),
+                                      1 if accumulate else 0, ws.data_ptr(), ws.numel(), st))
+        return gh, gw
+    raise ValueError(f"unsupported dtype {hidden.dtype}")
+
+
+def finish(stats: torch.Tensor) -> None:
+    """One host sync; raise NumericError/ValueError from the device error word."""
+    lib = _lib.load()
+    _lib.check(lib.icepop_finish(stats.data_ptr(), _stream(stats.device)))
+
+
+@dataclass
+class Diagnostics:
+    """Global diagnostics derived from the all-reduced stats (objective.py:282-298)."""
+
+    objective_value: float
+    clipped_fraction: float
+    token_count: int
+    mean_logp: float
+    entropy_all: float
+    entropy_clipped: float
+    kl_to_ref: float
+
+    @classmethod
+    def from_stats(cls, stats) -> "Diagnostics":
+        s = [float(x) for x in (stats.tolist() if hasattr(stats, "tolist") else stats)]
+        n = s[_lib.STAT_TOKENS]
+        popped = s[_lib.STAT_N_POPPED]
+        return cls(
+            objective_value=s[_lib.STAT_OBJECTIVE],
+            clipped_fraction=popped / n if n else 0.0,
+            token_count=int(round(n)),
+            mean_logp=s[_lib.STAT_SUM_LOGP] / n if n else math.nan,
+            entropy_all=s[_lib.STAT_SUM_ENTROPY] / n if n else math.nan,
+            entropy_clipped=s[_lib.STAT_SUM_ENTROPY_POPPED] / popped if popped else math.nan,
+            kl_to_ref=s[_lib.STAT_SUM_KL] / n if n else math.nan,
+        )
+
+
+# --------------------------------------------------------------------------- custom op
+@torch.library.custom_op("icepop_b200::icepop_loss", mutates_args=())
+def _icepop_loss_op(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    tokens: torch.Tensor,
+    lp_train_old: torch.Tensor,
+    lp_infer_old: torch.Tensor,
+    cu_seqlens: torch.Tensor,
+    group_offsets: torch.Tensor,
+    advantages: torch.Tensor,
+    alpha: float,
+    beta: float,
+    clip_eps: float,
+    tis_cap: float,
+    temperature: float,
+    algo: int,
+    layout: int,
+    token_offset: int,
+) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
+    batch = PackedBatch(tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages,
+                        token_offset=token_offset)
+    f = icepop_fwd(hidden, weight, batch, cfg, "dv" if layout == _lib.W_DV else "vd")
+    loss = -f.stats[_lib.STAT_OBJECTIVE]
+    return loss, f.stats, f.lse, f.lp_cur, f.entropy, f.kept, f.coeff.to(torch.float64)
+
+
+@_icepop_loss_op.register_fake
+def _(hidden, weight, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages, alpha, beta,
+      clip_eps, tis_cap, temperature, algo, layout, token_offset):
+    n = hidden.shape[0]
+    f64 = dict(dtype=torch.float64, device=hidden.device)
+    # lse / entropy are f32 on the bf16 path and f64 on the validation path
+    f32 = dict(dtype=torch.float64 if hidden.dtype == torch.float64 else torch.float32, device=hidden.device)
+    return (hidden.new_empty((), dtype=torch.float64), hidden.new_empty((_lib.NSTATS,), **{"dtype": torch.float64}),
+            torch.empty(n, **f32), torch.empty(n, **f64), torch.empty(n, **f32),
+            torch.empty(n, dtype=torch.uint8, device=hidden.device), torch.empty(n, **f64))
+
+
+def _setup_context(ctx, inputs, output):
+    (hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, alpha, beta, clip_eps, tis_cap, temperature, algo, layout,
+     token_offset) = inputs
+    loss, stats, lse, lp_cur, entropy, kept, coeff = output
+    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff)
+    ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset)
+
+
+def _backward(ctx, grad_loss, *unused):
+    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff = ctx.saved_tensors
+    alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset = ctx.cfg
+    cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
+    batch = PackedBatch(tokens, lp_old, lp_inf, cu, go, adv, token_offset=token_offset)
+    # loss = -J: scale the per-token coefficients on device (no host sync for grad_loss)
+    scale = -grad_loss.to(torch.float64)
+    if hidden.dtype == torch.bfloat16:
+        c = (coeff * scale).to(torch.float32)
+        fwd = IcePopForward(lse, None, None, None, None, None, c, None)
+    else:
+        fwd = IcePopForward(lse, torch.empty_like(lse, dtype=torch.float64),
+                            torch.empty_like(lse, dtype=torch.float64), None, None, None, coeff * scale,
+                            torch.zeros(_lib.NSTATS, dtype=torch.float64, device=lse.device))
+    lay = "dv" if layout == _lib.W_DV else "vd"
+    gh, gw = icepop_bwd(hidden, weight, batch, fwd, cfg, lay, 1.0, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+    if gw is not None:
+        gw = gw.to(weight.dtype)
+    if gh is not None:
+        gh = gh.to(hidden.dtype)
+    return (gh, gw) + (None,) * 14
+
+
+_icepop_loss_op.register_autograd(_backward, setup_context=_setup_context)
+
+
+def icepop_loss(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    batch: PackedBatch,
+    cfg: IcePopConfig = IcePopConfig(),
+    layout: str = "vd",
+):
+    """Differentiable IcePop loss (= -J on this rank's tokens) and per-token aux.
+
+    Returns ``(loss, aux)`` with aux = dict(stats, lse, lp_cur, entropy, kept, coeff).
+    ``batch.advantages`` must be given (compute them with K0 via
+    :func:`group_advantages` when starting from rewards).
+    """
+    if batch.advantages is None:
+        raise ValueError("icepop_loss needs batch.advantages (see group_advantages)")
+    if cfg.kl_coeff != 0.0:
+        raise ValueError("icepop_loss: kl_coeff must be 0 (KL-to-ref is the fp64 functional path)")
+    loss, stats, lse, lp_cur, entropy, kept, coeff = _icepop_loss_op(
+        hidden, weight, batch.tokens, batch.lp_train_old, batch.lp_infer_old, batch.cu_seqlens,
+        batch.group_offsets, batch.advantages, cfg.alpha, cfg.beta, cfg.clip_eps, cfg.tis_cap, cfg.temperature,
+        ALGOS[cfg.algo], LAYOUTS[layout], batch.token_offset)
+    return loss, dict(stats=stats, lse=lse, lp_cur=lp_cur, entropy=entropy, kept=kept, coeff=coeff)
+
+
+def group_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor) -> torch.Tensor:
+    """K0 on device: per-group z-scored rewards (objective.py:153-159), bit-identical to numpy."""
+    lib = _lib_for(rewards)
+    if rewards.dtype != torch.float64 or group_offsets.dtype != torch.int32:
+        raise ValueError("rewards must be float64 and group_offsets int32")
+    if group_offsets.device.type == "cpu":  # host offsets: validate, then move
+        if bool((torch.diff(group_offsets) < 2).any()):
+            raise ValueError("advantage normalization needs a group of >= 2 rewards")
+        group_offsets = group_offsets.to(rewards.device)
+    out = torch.empty_like(rewards)
+    _lib.check(lib.icepop_group_advantages(rewards.data_ptr(), group_offsets.data_ptr(), group_offsets.numel() - 1,
+                                           rewards.numel(), out.data_ptr(), _stream(rewards.device)))
+    return out

@@ -1,0 +1,57 @@
+"""Shared fixtures. `-m gpu` tests need a B200 and the built libicepop_b200.so;
+everything else runs on the CPU build container."""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and libicepop_b200.so")
+
+
+def golden_cases() -> list[str]:
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "advantages")
+
+
+def load_golden(name: str) -> dict:
+    with np.load(GOLDEN / f"{name}.npz") as z:
+        d = {k: z[k] for k in z.files}
+    for k in ("alpha", "beta", "clip_eps", "tis_cap", "temperature", "kl_coeff", "out_objective",
+              "out_clipped_fraction", "out_kl_to_ref", "out_mean_logp", "out_entropy_all", "out_entropy_clipped"):
+        d[k] = float(d[k])
+    d["algo"] = str(d["algo"])
+    d["has_ref"] = bool(d["has_ref"])
+    d["out_token_count"] = int(d["out_token_count"])
+    return d
+
+
+def golden_hidden(d: dict) -> np.ndarray:
+    """H = multihot(feats): the reference's 4-hot contraction as a dense matrix."""
+    from paper_2510_18855_b200.features import multihot
+
+    return multihot(d["feats"], d["weight"].shape[0])
+
+
+def oracle_kwargs(d: dict) -> dict:
+    return dict(alpha=d["alpha"], beta=d["beta"], clip_eps=d["clip_eps"], tis_cap=d["tis_cap"],
+                temperature=d["temperature"], kl_coeff=d["kl_coeff"], algo=d["algo"], layout="dv",
+                weight_ref=d["weight_ref"] if d["has_ref"] else None)
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)

@@ -1,0 +1,46 @@
+"""tcgen05 GEMM core (K4/K5 building block) vs torch fp32 matmul, all operand majors."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, M, N, K, a_mn, b_mn, c_f32=True, accumulate=False, C=None):
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    A_st = A.t().contiguous() if a_mn else A.contiguous()
+    B_st = B.t().contiguous() if b_mn else B.contiguous()
+    if C is None:
+        C = torch.zeros(M, N, dtype=torch.float32 if c_f32 else torch.bfloat16, device=A.device)
+    _lib.check(lib.icepop_gemm_bf16(A_st.data_ptr(), B_st.data_ptr(), C.data_ptr(), M, N, K, int(a_mn), int(b_mn),
+                                    int(c_f32), int(accumulate), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return C
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1024, 2048, 512), (136, 264, 1000)])
+def test_gemm_majors(cuda_device, a_mn, b_mn, M, N, K):
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).to(cuda_device)
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16).to(cuda_device)
+    C = _gemm(A, B, M, N, K, a_mn, b_mn)
+    ref = A.double() @ B.double().T
+    err = (C.double() - ref).abs().max().item()
+    assert err <= 1e-3 * (K ** 0.5), f"max abs err {err}"
+
+
+def test_gemm_bf16_out_and_accumulate(cuda_device):
+    M, N, K = 256, 512, 320
+    A = torch.randn(M, K, device=cuda_device).to(torch.bfloat16)
+    B = torch.randn(N, K, device=cuda_device).to(torch.bfloat16)
+    ref = A.double() @ B.double().T
+    Cb = _gemm(A, B, M, N, K, 0, 0, c_f32=False)
+    assert (Cb.double() - ref).abs().max().item() < 0.02 * ref.abs().max().item()
+    C0 = torch.ones(M, N, device=cuda_device)
+    C1 = _gemm(A, B, M, N, K, 1, 1, accumulate=True, C=C0)
+    assert torch.allclose(C1.double(), ref + 1.0, atol=1e-2, rtol=1e-4)
