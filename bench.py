@@ -1,0 +1,461 @@
+"""IcePop fwd+bwd throughput on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (token-sharded, weak scaling)
+
+A step = one IcePop forward (K0 advantages, K1 fused lm_head GEMM + online softmax, K2
+epilogue) + backward (K3 recompute -> bf16 dZ chunks, K4 dHidden, K5 dW) over one batch
+of synthetic inputs of the named config, plus (N>1) the NCCL all-reduce of the fp64
+statistics and of dW. `value` is measured with inputs resident in HBM; `e2e` goes
+through the public API from pinned host buffers with the H2D copies of the step's
+inputs and the D2H read of its loss inside the timed region.
+
+--impl reference times the reference's algorithm on the host cores (the numpy oracle
+port of objective.py:172-298; the reference itself is pure numpy and has no GPU path)
+on a bounded token sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "IcePop fwd+bwd tokens/sec at 1/2/4/8 B200; % tensor-pipe peak; CPU-ref speedup"
+UNIT = "tokens/s"
+
+# SURVEY.md section 8 configs (per rank for the weak-scaling sweep)
+CONFIGS = {
+    "c1": dict(name="C1 CPU-reference shape: 8 seqs x 512 tok, d=1024, V=32768, G=8", seqs=8, seq_len=512,
+               hidden=1024, vocab=32768, group=8, seed=0, sigma_inf=0.233),
+    "c2": dict(name="C2 single B200: 64 seqs x 4096 tok, d=4096, V=157184 (Ling-2.0), G=8", seqs=64, seq_len=4096,
+               hidden=4096, vocab=157184, group=8, seed=1, sigma_inf=0.233),
+    "c3": dict(name="C3 Ling-1T lm_head shard: 8 seqs x 4096 tok/GPU, d=8192, V=157184, G=8", seqs=8, seq_len=4096,
+               hidden=8192, vocab=157184, group=8, seed=2, sigma_inf=0.233),
+    "c5": dict(name="C5 scaling point: 32 seqs x 4096 tok/GPU, d=8192, V=157184, G=8", seqs=32, seq_len=4096,
+               hidden=8192, vocab=157184, group=8, seed=4, sigma_inf=0.233),
+}
+
+FLOP_PER_TOKEN = lambda d, v: 6.0 * d * v  # noqa: E731  algorithmic (fwd + dH + dW), SURVEY 8d
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return dict(tflops=float(j["bf16_tflops"]), tflops_sustained=float(j.get("bf16_tflops_sustained", 0) or 0),
+                    hbm=float(j["hbm_gbs"]), source="measured")
+    return dict(tflops=1590.0, tflops_sustained=1400.0, hbm=6650.0, source="fallback")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def pump():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+        self.thread = threading.Thread(target=pump, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- inputs
+def make_batch_host(cfg: dict, rank: int, world: int):
+    """Seeded synthetic rollout batch for this rank: rewards ~ Bernoulli(0.5),
+    groups of `group` sequences, this rank owns `seqs` whole sequences."""
+    rng = np.random.default_rng(cfg["seed"])
+    S_global = cfg["seqs"] * world
+    T = cfg["seq_len"]
+    cu = (np.arange(S_global + 1, dtype=np.int64) * T).astype(np.int32)
+    go = np.arange(0, S_global + 1, cfg["group"], dtype=np.int32)
+    rewards = rng.integers(0, 2, S_global).astype(np.float64)
+    n_local = cfg["seqs"] * T
+    return dict(cu=cu, go=go, rewards=rewards, n_local=n_local, token_offset=rank * n_local)
+
+
+def build_device_inputs(cfg, meta, dev, rank):
+    import torch
+
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import PackedBatch, icepop_fwd  # noqa: F401
+
+    g = torch.Generator(device=dev).manual_seed(1000 * cfg["seed"] + rank)
+    N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
+    H = torch.randn(N, d, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+    W = (torch.randn(V, d, device=dev, generator=g, dtype=torch.float32) * (2.0 / np.sqrt(d))).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (N,), device=dev, generator=g, dtype=torch.int32)
+    # setup forward (untimed): lp_theta(y) -> lp_old = lp + N(0, 0.1) exercises the clip
+    # branch; lp_inf = lp_old - N(0, sigma) pops ~1.5 permille
+    lib = _lib.ensure_device(dev.index)
+    shape = _lib.Shape(n_tokens=N, token_offset=meta["token_offset"], hidden=d, vocab=V,
+                       n_seqs=len(meta["cu"]) - 1, n_groups=len(meta["go"]) - 1, weight_layout=_lib.W_VD)
+    fb = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, fb, None))
+    ws = torch.empty(fb.value, dtype=torch.uint8, device=dev)
+    lp = torch.empty(N, dtype=torch.float64, device=dev)
+    _lib.check(lib.icepop_logprob_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), None,
+                                       lp.data_ptr(), None, ws.data_ptr(), ws.numel(),
+                                       torch.cuda.current_stream(dev).cuda_stream))
+    del ws
+    lp_old = lp + 0.1 * torch.randn(N, device=dev, dtype=torch.float64, generator=g)
+    lp_inf = lp_old - cfg["sigma_inf"] * torch.randn(N, device=dev, dtype=torch.float64, generator=g)
+    batch = PackedBatch(tokens=tokens, lp_train_old=lp_old, lp_infer_old=lp_inf,
+                        cu_seqlens=torch.from_numpy(meta["cu"]).to(dev), group_offsets=torch.from_numpy(meta["go"]).to(dev),
+                        advantages=None, rewards=torch.from_numpy(meta["rewards"]).to(dev),
+                        token_offset=meta["token_offset"])
+    return H, W, batch
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import (DZ_CHUNK_BYTES, Diagnostics, IcePopConfig, PackedBatch, finish,
+                                            icepop_bwd, icepop_fwd)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    meta = make_batch_host(cfg, rank, world)
+    H, W, batch = build_device_inputs(cfg, meta, dev, rank)
+    icfg = IcePopConfig()
+    N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
+    chunk = max(128, min(N, DZ_CHUNK_BYTES // (2 * V)) // 128 * 128)
+    n_chunks = -(-N // chunk)
+    launches_per_step = 6 + 3 * n_chunks  # K0, token check, K1, K2, finalize, err-merge + (K3,K4,K5)/chunk
+
+    def step_into():
+        # loss = -J: grad_scale -1 gives d(loss)/d(hidden), d(loss)/d(W)
+        f = icepop_fwd(H, W, batch, icfg, layout="vd")
+        gh, g = icepop_bwd(H, W, batch, f, icfg, layout="vd", grad_scale=-1.0)
+        if world > 1:
+            dist.all_reduce(f.stats)
+            dist.all_reduce(g)
+        return f
+
+    # warm-up (also validates the error word once)
+    for _ in range(args.warmup):
+        f = step_into()
+    finish(f.stats)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: inputs resident (H 2.1 GB, W 1.3 GB > 126 MB L2)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        f = step_into()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    diag = Diagnostics.from_stats(f.stats.cpu())
+
+    # ---------------- per-kernel timing pass (same work, events between launches)
+    kern = kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev) if not args.no_kernel_timing else {}
+
+    # ---------------- end-to-end through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(H, W, batch, icfg, args, dev, world)
+
+    tokens_total = N * world
+    value = tokens_total / (ms / 1e3)
+    pk = peaks()
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; random-init lm_head weights)",
+        "config": {"workload": cfg["name"], "global_batch": tokens_total, "seq_len": cfg["seq_len"],
+                   "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
+                   "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
+                   "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
+                   "popped_fraction": round(diag.clipped_fraction, 6)},
+        "gpu_launches": launches_per_step * args.steps,
+        "step_tflops_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12, 1),
+        "step_frac_of_peak_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12 / pk["tflops"], 4),
+        "peak_source": pk["source"],
+    }
+    if kern:
+        line["kernels_ms"] = {k: round(v["ms"], 3) for k, v in kern.items()}
+        dom = max(kern, key=lambda k: kern[k]["ms"] * kern[k]["count"])
+        ach = kern[dom]["flop"] / (kern[dom]["ms"] / 1e3) / 1e12
+        line["roofline"] = {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": pk["tflops"],
+                            "unit": "TFLOP/s", "frac": round(ach / pk["tflops"], 4), "traffic": None,
+                            "peak_kind": "burst (%s)" % pk["source"]}
+    if e2e:
+        line["e2e"] = e2e
+    if clocks:
+        line["clocks"] = clocks
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, H, W, batch, meta, args.cpu_tokens)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev):
+    """Average device time of K1(+K2), K3, K4, K5 launched one by one on the torch stream."""
+    import torch
+
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import icepop_fwd
+
+    lib = _lib.ensure_device(dev.index)
+    st = torch.cuda.current_stream(dev)
+    N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
+    res = {}
+
+    def timed(name, fn, flop, reps=2):
+        fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        res[name] = {"ms": a.elapsed_time(b) / reps, "flop": flop, "count": 1}
+
+    holder = {}
+
+    def fwd():
+        holder["f"] = icepop_fwd(H, W, batch, icfg, layout="vd")
+
+    timed("K1_fwd_lse+K2", fwd, 2.0 * N * d * V)
+    f = holder["f"]
+    nc = min(chunk, N)
+    dz = torch.empty((nc, V), dtype=torch.bfloat16, device=dev)
+    gh = torch.empty((nc, d), dtype=torch.bfloat16, device=dev)
+    gw = torch.zeros((V, d), dtype=torch.float32, device=dev)
+    shape = _lib.Shape(n_tokens=nc, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs, n_groups=batch.n_groups,
+                       weight_layout=_lib.W_VD)
+    s = st.cuda_stream
+    timed("K3_dz", lambda: _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(),
+                                                         batch.tokens.data_ptr(), f.lse.data_ptr(),
+                                                         f.coeff.data_ptr(), -1.0, dz.data_ptr(), V, s)),
+          2.0 * nc * d * V)
+    timed("K4_dhidden", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), nc, d, V,
+                                                                0, 1, 0, 0, s)), 2.0 * nc * d * V)
+    timed("K5_dweight", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, nc,
+                                                                1, 1, 1, 1, s)), 2.0 * nc * d * V)
+    del dz, gh, gw
+    return res
+
+
+def run_e2e(H, W, batch, icfg, args, dev, world):
+    """Public API from pinned host inputs: H2D of the step's inputs + D2H of its loss."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_18855_b200.loss import PackedBatch, icepop_bwd, icepop_fwd
+
+    host = {k: v.cpu().pin_memory() for k, v in dict(H=H, tokens=batch.tokens, lp_old=batch.lp_train_old,
+                                                     lp_inf=batch.lp_infer_old, cu=batch.cu_seqlens,
+                                                     go=batch.group_offsets, rewards=batch.rewards).items()}
+    dbuf = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    out_host = torch.empty(8, dtype=torch.float64).pin_memory()
+    steps = max(1, min(args.steps, 3))
+
+    def one():
+        for k in host:
+            dbuf[k].copy_(host[k], non_blocking=True)
+        b = PackedBatch(dbuf["tokens"], dbuf["lp_old"], dbuf["lp_inf"], dbuf["cu"], dbuf["go"], None, dbuf["rewards"],
+                        batch.token_offset)
+        f = icepop_fwd(dbuf["H"], W, b, icfg, layout="vd")
+        _, g = icepop_bwd(dbuf["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
+        if world > 1:
+            dist.all_reduce(f.stats)
+            dist.all_reduce(g)
+        out_host.copy_(f.stats, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        one()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": round(H.shape[0] * world / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": 64, "ms_per_step": round(ms, 3), "steps": steps}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_sample(cfg, n_tokens, seed=0):
+    """A bounded host sample of the same workload: 1 group of 2 sequences."""
+    rng = np.random.default_rng(seed)
+    d, V = cfg["hidden"], cfg["vocab"]
+    T = max(1, n_tokens // 2)
+    H = rng.standard_normal((2 * T, d), dtype=np.float32).astype(np.float64)
+    tokens = rng.integers(0, V, 2 * T).astype(np.int32)
+    lp_old = rng.normal(-12.0, 0.3, 2 * T)
+    lp_inf = lp_old - rng.normal(0, cfg["sigma_inf"], 2 * T)
+    return H, tokens, lp_old, lp_inf, np.array([0, T, 2 * T], dtype=np.int32), np.array([0, 2], dtype=np.int32), \
+        np.array([1.0, -1.0])
+
+
+def time_oracle(cfg, n_tokens, W64, seed=0):
+    from oracle.icepop_oracle import icepop_dense
+
+    H, tok, lpo, lpi, cu, go, adv = cpu_sample(cfg, n_tokens, seed)
+    t0 = time.perf_counter()
+    icepop_dense(H, W64, tok, lpo, lpi, cu, go, adv, layout="vd")
+    return time.perf_counter() - t0, len(tok)
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def sample_tokens(cfg, W64, target_s: float) -> int:
+    """Tokens per CPU sample so one sample takes about target_s (probe with 4 tokens)."""
+    dt, n = time_oracle(cfg, 4, W64, seed=999)
+    return int(max(4, min(4096, 2 * round(target_s * n / dt / 2))))
+
+
+def cpu_baseline(cfg, H, W, batch, meta, n_tokens):
+    W64 = W.float().cpu().numpy().astype(np.float64)
+    n_tokens = n_tokens or sample_tokens(cfg, W64, 15.0)
+    dt, n = time_oracle(cfg, n_tokens, W64)
+    return {"value": round(n / dt, 3), "unit": UNIT, "cores": blas_threads(), "kind": "port",
+            "sample": f"{n} tokens (1 group x 2 seqs) at d={cfg['hidden']}, V={cfg['vocab']}, fp64 numpy oracle "
+                      f"(objective.py:172-298 restated densely, oracle/icepop_oracle.py), {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's algorithm on host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    rng = np.random.default_rng(123)
+    W64 = (rng.standard_normal((cfg["vocab"], cfg["hidden"]), dtype=np.float32) * (2.0 / np.sqrt(cfg["hidden"]))
+           ).astype(np.float64)
+    n_tok = args.cpu_tokens or sample_tokens(cfg, W64, 6.0)
+    for i in range(args.warmup):
+        time_oracle(cfg, n_tok, W64, seed=i)
+    tot_t, tot_n = 0.0, 0
+    for i in range(args.steps):
+        dt, n = time_oracle(cfg, n_tok, W64, seed=100 + i)
+        tot_t += dt
+        tot_n += n
+    value = tot_n / tot_t
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * tot_t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)", "impl": "reference",
+        "config": {"workload": CONFIGS[args.config]["name"], "hidden": cfg["hidden"], "vocab": cfg["vocab"],
+                   "parallelism": "host cores (numpy/OpenBLAS)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": blas_threads(), "kind": "port",
+                         "sample": f"{n_tok} tokens per step (1 group x 2 seqs), fp64 numpy restatement "
+                                   "of objective.py:172-298 (oracle/icepop_oracle.py)"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0 = size it to a few seconds)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

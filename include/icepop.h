@@ -164,6 +164,14 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
                     int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* K3 alone: dZ[t, v] = grad_scale * coeff_t * (e_{y_t} - softmax(z_t))_v for the
+ * shape->n_tokens rows of `hidden`, written as bf16 to dz[t * ldz + v]. The building
+ * block icepop_bwd_bf16 chains with K4/K5 (icepop_gemm_bf16); exposed so callers can
+ * interleave V-slab dW reductions with it. */
+int icepop_dz_bf16(const icepop_shape* shape, double temperature, const void* hidden,
+                   const void* weight, const int32_t* tokens, const float* lse,
+                   const float* coeff, double grad_scale, void* dz, int64_t ldz, void* stream);
+
 /* ---- fp64 SIMT validation path ----------------------------------------------------- */
 /* Same semantics in fp64 on CUDA cores (still CUDA, no CPU fallback), so the
  * reference's exact-identity and finite-difference tests run unchanged on the GPU.

@@ -309,6 +309,26 @@ int64_t fwd_part_bytes(const icepop_shape* s) {
   return (int64_t)w.bytes;
 }
 
+// K3 for `rows` rows of hidden starting at h (tokens/lse/coeff already offset).
+int launch_dz(const icepop_shape* shape, double temperature, const void* h, const void* weight,
+              const int32_t* tokens, const float* lse, const float* coeff, double grad_scale,
+              __nv_bfloat16* dz, int64_t ldz, int64_t rows, cudaStream_t st) {
+  const int64_t d = shape->hidden, V = shape->vocab;
+  const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  EpiParams ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.scale_log2 = (float)(1.4426950408889634 / temperature);
+  ep.inv_t = (float)(1.0 / temperature);
+  ep.targets = tokens;
+  ep.lse = lse;
+  ep.coeff = coeff;
+  ep.coeff_scale = (float)grad_scale;
+  ep.dz = dz;
+  ep.ldz = ldz;
+  ep.vec_ok = (ldz % 8 == 0) && ((reinterpret_cast<uintptr_t>(dz) & 15u) == 0);
+  return run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, rows, V, d, ep, st);
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -467,13 +487,19 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
     return ICEPOP_OK;
   }
-  // chunk = as many dZ rows as the workspace holds (multiple of 128, >= 128)
-  const size_t fixed = carve_bf16(shape, nullptr, 0).bytes + 256;
-  if (!workspace || workspace_bytes < fixed + (size_t)128 * V * 2)
-    return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", fixed + (size_t)128 * V * 2);
+  // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
+  const int64_t min_rows = std::min<int64_t>(N, BM);
+  const size_t need_min = carve_bf16(shape, nullptr, min_rows).bytes;
+  if (!workspace || workspace_bytes < need_min)
+    return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", need_min);
+  const size_t fixed = carve_bf16(shape, nullptr, 0).bytes;
   int64_t chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
-  chunk = std::min<int64_t>(chunk, N);
-  if (chunk < N) chunk = chunk / BM * BM;
+  if (chunk >= N) {
+    chunk = N;
+  } else {
+    chunk = std::max<int64_t>(chunk / BM * BM, BM);
+  }
+  while (chunk > min_rows && carve_bf16(shape, nullptr, chunk).bytes > workspace_bytes) chunk -= BM;
   BF16Workspace w = carve_bf16(shape, workspace, chunk);
   if (w.bytes > workspace_bytes) return fail(ICEPOP_EINVAL, "backward workspace carve overflow");
 
@@ -481,18 +507,8 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     const int64_t nc = std::min<int64_t>(chunk, N - c0);
     const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hidden) + c0 * d;
     // K3: recompute logits, dZ chunk (bf16)
-    EpiParams ep;
-    memset(&ep, 0, sizeof(ep));
-    ep.scale_log2 = (float)(1.4426950408889634 / cfg->temperature);
-    ep.inv_t = (float)(1.0 / cfg->temperature);
-    ep.targets = tokens + c0;
-    ep.lse = lse + c0;
-    ep.coeff = coeff + c0;
-    ep.coeff_scale = (float)grad_scale;
-    ep.dz = w.dz;
-    ep.ldz = V;
-    ep.vec_ok = (V % 8 == 0) && ((reinterpret_cast<uintptr_t>(w.dz) & 15u) == 0);
-    ICP_TRY(run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, nc, V, d, ep, st));
+    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, tokens + c0, lse + c0, coeff + c0, grad_scale, w.dz, V,
+                      nc, st));
     // K4: grad_hidden = dZ . W^T   (M = nc, N = d, K = V)
     if (grad_hidden) {
       EpiParams eh;
@@ -523,6 +539,17 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     }
   }
   return ICEPOP_OK;
+}
+
+int icepop_dz_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                   const int32_t* tokens, const float* lse, const float* coeff, double grad_scale, void* dz,
+                   int64_t ldz, void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
+  if (!hidden || !weight || !tokens || !lse || !coeff || !dz) return fail(ICEPOP_EINVAL, "null argument");
+  if (ldz < shape->vocab) return fail(ICEPOP_EINVAL, "ldz must be >= vocab");
+  return launch_dz(shape, temperature, hidden, weight, tokens, lse, coeff, grad_scale,
+                   static_cast<__nv_bfloat16*>(dz), ldz, shape->n_tokens, static_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------------ fp64 validation path

@@ -21,12 +21,14 @@ constexpr float LN2_F = 0.69314718055994531f;
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum)
 // for contiguous data, over f(i) for i in [0, n). Reproducing its association order
-// makes the group advantages bit-identical to numpy's r.mean() / r.std().
+// makes the group advantages bit-identical to numpy's r.mean() / r.std(). All adds are
+// __dadd_rn and the squares __dmul_rn so nvcc cannot contract them into FMAs (numpy
+// rounds every operation separately).
 template <class F>
 __device__ double np_pairwise_sum(F f, int lo, int n) {
   if (n < 8) {
     double res = 0.;
-    for (int i = 0; i < n; ++i) res += f(lo + i);
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, f(lo + i));
     return res;
   }
   if (n <= 128) {
@@ -34,15 +36,16 @@ __device__ double np_pairwise_sum(F f, int lo, int n) {
     for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
     int i = 8;
     for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += f(lo + i + j);
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += f(lo + i);
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
     return res;
   }
   // n > 128: split in two halves with the first a multiple of 8 (iterative on the left)
   int n2 = n / 2;
   n2 -= n2 % 8;
-  return np_pairwise_sum(f, lo, n2) + np_pairwise_sum(f, lo + n2, n - n2);
+  return __dadd_rn(np_pairwise_sum(f, lo, n2), np_pairwise_sum(f, lo + n2, n - n2));
 }
 
 // One thread per group: A_i = (R_i - mean) / max(std_pop, 1e-6)  (objective.py:153-159).
@@ -60,10 +63,10 @@ __global__ void k0_group_advantages(const double* __restrict__ rewards,
     return;
   }
   const double mean = np_pairwise_sum([&](int i) { return r[i]; }, 0, n) / (double)n;
-  const double var = np_pairwise_sum([&](int i) { const double x = r[i] - mean; return x * x; }, 0, n) / (double)n;
+  const double var = np_pairwise_sum([&](int i) { const double x = __dsub_rn(r[i], mean); return __dmul_rn(x, x); }, 0, n) / (double)n;
   const double std = sqrt(var);
   const double den = std > 1e-6 ? std : 1e-6;  // max(std, 1e-6)
-  for (int i = 0; i < n; ++i) adv[s0 + i] = (r[i] - mean) / den;
+  for (int i = 0; i < n; ++i) adv[s0 + i] = __ddiv_rn(__dsub_rn(r[i], mean), den);
 }
 
 struct TokenArgs {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     const double A = a.adv[seq];
     const double lpo = a.lp_old[t];
     // calibration and mask (objective.py:227-238)
-    const double c = exp(lpo - a.lp_inf[t]);
+    const double c = exp(__dsub_rn(lpo, a.lp_inf[t]));
     if (!isfinite(c)) err |= ICEPOP_ERR_CALIB_OVERFLOW;
     bool kept;
     double factor;
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
       factor = fmin(c, a.tis_cap);
     }
     // ratio / clip / surrogate (objective.py:240-246)
-    const double r = exp(lp_cur - lpo);
+    const double r = exp(__dsub_rn(lp_cur, lpo));
     if (!isfinite(r)) err |= ICEPOP_ERR_RATIO_OVERFLOW;
     const double unclipped = r * A;
     const double clipped = fmin(fmax(r, clip_lo), clip_hi) * A;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     const double pg = factor * (active ? unclipped : clipped);
     // gradient coefficient (objective.py:250)
     const double coeff = active ? w * factor * r * A / a.temperature : 0.0;
-    const double value = pg - a.kl_coeff * kl;
+    const double value = __dsub_rn(pg, __dmul_rn(a.kl_coeff, kl));  // objective.py:268, no FMA
 
     if (a.kept) a.kept[t] = kept ? 1 : 0;
     if (a.calib) a.calib[t] = c;

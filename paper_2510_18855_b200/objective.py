@@ -1,0 +1,331 @@
+"""Drop-in replacement for mismatchlab's ``objective`` module (objective.py:1-326).
+
+``objective_and_grad`` keeps the reference signature, validation order, exceptions,
+``TokenRecord.logp_train_cur`` write-back and ``LossBreakdown`` fields, but runs on the
+B200 through ``libicepop_b200.so``:
+
+* ``precision="fp64"`` (default): the fp64 SIMT CUDA validation path -- the reference's
+  exact-identity and finite-difference tests (test_objective.py) hold unchanged;
+* ``precision="bf16"``: the tcgen05 tensor-core path (weights rounded to bf16, fp32
+  accumulation; tolerances in tests/test_parity_gpu.py).
+
+The reference's 4-hot feature contraction is packed as a dense multi-hot H
+(features.py), so both precisions run the same dense kernels as a real lm_head.
+
+When mismatchlab is importable its data classes are re-exported (so enum identity and
+isinstance checks in the caller keep working); otherwise identical definitions are used.
+:func:`install` rebinds the reference's three bindings of the name (objective.py,
+scheduler.py:38 and __init__.py:33).
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from .errors import NumericError
+
+try:  # pragma: no cover - depends on the host environment
+    from mismatchlab.objective import (  # type: ignore
+        Algo,
+        LossBreakdown,
+        MaskingBounds,
+        ObjectiveConfig,
+        PromptGroup,
+        TokenRecord,
+    )
+
+    _HAVE_REFERENCE = True
+except Exception:  # noqa: BLE001
+    _HAVE_REFERENCE = False
+
+    class Algo(enum.Enum):  # objective.py:41-44
+        ICEPOP = "icepop"
+        GRPO = "grpo"
+        TIS = "tis"
+
+    @dataclass(frozen=True)
+    class MaskingBounds:  # objective.py:47-56
+        alpha: float = 0.5
+        beta: float = 5.0
+
+        def __post_init__(self) -> None:
+            if not (0.0 < self.alpha <= 1.0 <= self.beta):
+                raise ValueError(f"bounds must satisfy 0 < alpha <= 1 <= beta, got [{self.alpha}, {self.beta}]")
+
+    @dataclass(frozen=True)
+    class ObjectiveConfig:  # objective.py:66-82
+        algo: Algo = Algo.ICEPOP
+        clip_eps: float = 0.2
+        kl_coeff: float = 0.0
+        group_size: int = 8
+        tis_cap: float = 2.0
+
+        def __post_init__(self) -> None:
+            if not 0.0 < self.clip_eps < 1.0:
+                raise ValueError("clip_eps must be in (0, 1)")
+            if self.kl_coeff < 0.0:
+                raise ValueError("kl_coeff must be nonnegative")
+            if self.group_size < 2:
+                raise ValueError("group_size must be >= 2")
+            if self.tis_cap <= 0.0:
+                raise ValueError("tis_cap must be positive")
+
+    @dataclass
+    class TokenRecord:  # objective.py:85-103
+        token: int
+        logp_infer_old: float
+        logp_train_old: float
+        logp_train_cur: float
+        gen_version: int
+
+        def __post_init__(self) -> None:
+            for name in ("logp_infer_old", "logp_train_old", "logp_train_cur"):
+                if not math.isfinite(getattr(self, name)):
+                    raise NumericError(f"TokenRecord.{name} is not finite")
+
+    @dataclass
+    class PromptGroup:  # objective.py:106-119
+        task: Any
+        rollouts: list
+        rewards: list
+        advantages: list
+
+        def __post_init__(self) -> None:
+            if not (len(self.rollouts) == len(self.rewards) == len(self.advantages)):
+                raise ValueError("rollouts, rewards, and advantages must have equal length")
+            if not all(math.isfinite(a) for a in self.advantages):
+                raise NumericError("group advantages contain non-finite values")
+
+    @dataclass
+    class LossBreakdown:  # objective.py:122-139
+        objective_value: float
+        per_token_mask_kept: np.ndarray
+        clipped_fraction: float
+        grad: np.ndarray
+        kl_to_ref: float
+        token_count: int = 0
+        mean_logp: float = 0.0
+        entropy_all: float = 0.0
+        entropy_clipped: float = math.nan
+        per_token_surrogate: np.ndarray = field(default_factory=lambda: np.zeros(0))
+        per_token_calibration: np.ndarray = field(default_factory=lambda: np.zeros(0))
+        per_token_entropy: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+        @property
+        def grad_norm(self) -> float:
+            return float(np.linalg.norm(self.grad))
+
+
+_DEFAULT_PRECISION = "fp64"
+
+
+def set_default_precision(precision: str) -> None:
+    """Select the path used when objective_and_grad is called without ``precision``."""
+    global _DEFAULT_PRECISION
+    if precision not in ("fp64", "bf16"):
+        raise ValueError("precision must be 'fp64' or 'bf16'")
+    _DEFAULT_PRECISION = precision
+
+
+def mask(k: float, bounds: MaskingBounds) -> float:
+    """objective.py:59-63 -- k if alpha <= k <= beta (inclusive), else 0."""
+    if not math.isfinite(k) or k <= 0.0:
+        raise ValueError(f"mask argument must be a finite positive ratio, got {k}")
+    return k if bounds.alpha <= k <= bounds.beta else 0.0
+
+
+def group_advantages(rewards) -> np.ndarray:
+    """objective.py:153-159 on the device (K0; bit-identical to numpy's mean/std)."""
+    import torch
+
+    from .loss import group_advantages as _k0
+
+    r = np.asarray(rewards, dtype=np.float64)
+    if r.size < 2:
+        raise ValueError("advantage normalization needs a group of >= 2 rewards")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = _k0(torch.from_numpy(r).to(dev), torch.tensor([0, r.size], dtype=torch.int32, device=dev))
+    return out.cpu().numpy()
+
+
+def empty_breakdown(params) -> LossBreakdown:
+    """objective.py:142-150."""
+    return LossBreakdown(objective_value=0.0, per_token_mask_kept=np.zeros(0, dtype=bool), clipped_fraction=0.0,
+                         grad=np.zeros_like(params.weights), kl_to_ref=0.0)
+
+
+def _algo_name(algo) -> str:
+    return algo.value if hasattr(algo, "value") else str(algo)
+
+
+@dataclass
+class _Packed:
+    tokens: np.ndarray
+    lp_old: np.ndarray
+    lp_inf: np.ndarray
+    cu: np.ndarray
+    go: np.ndarray
+    adv: np.ndarray
+    feats: np.ndarray
+    records: list
+
+
+def _pack(groups, theta, theta_old) -> _Packed:
+    """Validate like objective.py:190-213 and flatten in group-major order (:271-276)."""
+    from .features import rollout_feats
+
+    if not groups:
+        raise ValueError("objective needs at least one prompt group")
+    if theta_old.version_id > theta.version_id:
+        raise ValueError("theta_old must not be newer than theta")
+    tokens, lp_old, lp_inf, cu, go, adv, feats, records = [], [], [], [0], [0], [], [], []
+    for group in groups:
+        if not group.rollouts:
+            raise ValueError("empty prompt group")
+        for rollout, advantage in zip(group.rollouts, group.advantages):
+            toks = rollout.tokens
+            if not toks:
+                raise ValueError("empty rollout in prompt group")
+            if any(rec.gen_version > theta_old.version_id for rec in toks):
+                raise ValueError("token generated by a version newer than theta_old")
+            ids = [rec.token for rec in toks]
+            tokens += ids
+            lp_old += [rec.logp_train_old for rec in toks]
+            lp_inf += [rec.logp_infer_old for rec in toks]
+            records += toks
+            feats.append(rollout_feats(group.task.prompt_id, ids, theta.n_features))
+            cu.append(cu[-1] + len(toks))
+            adv.append(float(advantage))
+        go.append(go[-1] + len(group.rollouts))
+    return _Packed(np.asarray(tokens, dtype=np.int32), np.asarray(lp_old, dtype=np.float64),
+                   np.asarray(lp_inf, dtype=np.float64), np.asarray(cu, dtype=np.int32),
+                   np.asarray(go, dtype=np.int32), np.asarray(adv, dtype=np.float64), np.concatenate(feats), records)
+
+
+def objective_and_grad(
+    groups,
+    theta,
+    theta_old,
+    ref,
+    cfg,
+    bounds,
+    temperature: float = 1.0,
+    *,
+    precision: str | None = None,
+    device=None,
+) -> LossBreakdown:
+    """Objective value and its exact analytic ascent gradient w.r.t. theta, on the GPU.
+
+    Same contract as objective.py:172-298, including the write-back of the recomputed
+    lp_cur into every TokenRecord (objective.py:224-225).
+    """
+    import torch
+
+    from .features import multihot
+    from .loss import Diagnostics, IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd
+
+    if temperature <= 0:
+        raise ValueError("temperature must be positive")
+    precision = precision or _DEFAULT_PRECISION
+    p = _pack(groups, theta, theta_old)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n_features, vocab = theta.weights.shape
+    icfg = IcePopConfig(alpha=bounds.alpha, beta=bounds.beta, clip_eps=cfg.clip_eps, tis_cap=cfg.tis_cap,
+                        temperature=float(temperature), kl_coeff=cfg.kl_coeff, algo=_algo_name(cfg.algo))
+    batch = PackedBatch(
+        tokens=torch.from_numpy(p.tokens).to(dev),
+        lp_train_old=torch.from_numpy(p.lp_old).to(dev),
+        lp_infer_old=torch.from_numpy(p.lp_inf).to(dev),
+        cu_seqlens=torch.from_numpy(p.cu).to(dev),
+        group_offsets=torch.from_numpy(p.go).to(dev),
+        advantages=torch.from_numpy(p.adv).to(dev),
+    )
+    if precision == "fp64":
+        H = torch.from_numpy(multihot(p.feats, n_features)).to(dev)
+        W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
+        Wr = torch.from_numpy(np.ascontiguousarray(ref.weights, dtype=np.float64)).to(dev) if ref is not None else None
+        fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
+        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
+    elif precision == "bf16":
+        if ref is not None:
+            raise ValueError("the bf16 drop-in does not compute the KL-to-ref term yet; use precision='fp64'")
+        if vocab % 8:
+            raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
+        nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
+        H = torch.from_numpy(multihot(p.feats, nf_pad)).to(torch.bfloat16).to(dev)
+        Wn = np.zeros((nf_pad, vocab))
+        Wn[:n_features] = theta.weights
+        W = torch.from_numpy(Wn).to(torch.bfloat16).to(dev)
+        fwd = icepop_fwd(H, W, batch, icfg, layout="dv")
+        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False)
+        gw = gw[:n_features]
+    else:
+        raise ValueError("precision must be 'fp64' or 'bf16'")
+    finish(fwd.stats)
+    diag = Diagnostics.from_stats(fwd.stats.cpu())
+    grad = gw.to(torch.float64).cpu().numpy()
+    lp_cur = fwd.lp_cur.cpu().numpy()
+    for rec, value in zip(p.records, lp_cur):  # objective.py:224-225
+        rec.logp_train_cur = float(value)
+    if not math.isfinite(diag.objective_value) or not np.isfinite(grad).all():
+        raise NumericError("objective or gradient is not finite")
+    kept = fwd.kept.cpu().numpy().astype(bool)
+    return LossBreakdown(
+        objective_value=diag.objective_value,
+        per_token_mask_kept=kept,
+        clipped_fraction=diag.clipped_fraction,
+        grad=grad,
+        kl_to_ref=diag.kl_to_ref if ref is not None else 0.0,
+        token_count=diag.token_count,
+        mean_logp=diag.mean_logp,
+        entropy_all=diag.entropy_all,
+        entropy_clipped=diag.entropy_clipped,
+        per_token_surrogate=fwd.surrogate.cpu().numpy(),
+        per_token_calibration=fwd.calib.cpu().numpy(),
+        per_token_entropy=fwd.entropy.to(torch.float64).cpu().numpy(),
+    )
+
+
+def sgd_update(theta, grad: np.ndarray, lr: float):
+    """objective.py:301-311 (host update; the fused device update is SURVEY 8f-2)."""
+    if lr <= 0:
+        raise ValueError("learning rate must be positive")
+    if grad.shape != theta.weights.shape:
+        raise ValueError("gradient shape does not match parameters")
+    with np.errstate(over="ignore"):
+        weights = theta.weights + lr * grad
+    if not np.isfinite(weights).all():
+        raise NumericError("parameter update produced non-finite weights")
+    return type(theta)(weights=weights, version_id=theta.version_id + 1)
+
+
+def momentum_update(theta, grad, velocity, lr: float, beta: float = 0.9):
+    """objective.py:314-326."""
+    if not 0.0 <= beta < 1.0:
+        raise ValueError("momentum beta must be in [0, 1)")
+    new_velocity = beta * velocity + grad
+    return sgd_update(theta, new_velocity, lr), new_velocity
+
+
+def install(precision: str | None = None) -> None:
+    """Rebind mismatchlab's objective_and_grad to this drop-in."""
+    import mismatchlab  # type: ignore
+    import mismatchlab.objective  # type: ignore
+    import mismatchlab.scheduler  # type: ignore
+
+    if precision is not None:
+        set_default_precision(precision)
+    for mod in (mismatchlab, mismatchlab.objective, mismatchlab.scheduler):
+        mod.objective_and_grad = objective_and_grad
+
+
+__all__ = [
+    "Algo", "LossBreakdown", "MaskingBounds", "ObjectiveConfig", "PromptGroup", "TokenRecord", "empty_breakdown",
+    "group_advantages", "install", "mask", "momentum_update", "objective_and_grad", "set_default_precision",
+    "sgd_update",
+]

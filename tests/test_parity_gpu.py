@@ -70,7 +70,7 @@ def test_fp64_path_matches_reference_golden(cuda_device, name):
     assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
     assert diag.token_count == d["out_token_count"]
     assert diag.clipped_fraction == d["out_clipped_fraction"]
-    np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=1e-15, atol=0)
+    np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=4.5e-16, atol=0)
     np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(f.surrogate.cpu().numpy(), d["out_surrogate"], rtol=1e-10, atol=1e-13)
     np.testing.assert_allclose(f.entropy.cpu().numpy(), d["out_entropy"], rtol=1e-12, atol=1e-13)
@@ -104,7 +104,9 @@ def test_bf16_path_matches_reference_golden(cuda_device, name):
     assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
     assert diag.token_count == d["out_token_count"]
     assert diag.clipped_fraction == d["out_clipped_fraction"]
-    np.testing.assert_array_equal(f.calib.cpu().numpy(), d["out_calibration"])
+    # CUDA's fp64 exp and numpy's may differ by one ulp (the mask is still bit-exact
+    # unless a calibration ratio sits within an ulp of alpha or beta)
+    np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=4.5e-16, atol=0)
     # GEMM-dependent quantities: tolerance
     np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], atol=2e-3, rtol=1e-3)
     np.testing.assert_allclose(f.entropy.cpu().numpy(), d["out_entropy"], atol=2e-3, rtol=1e-3)
