@@ -218,6 +218,11 @@ int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N
                      int32_t a_mn_major, int32_t b_mn_major, int32_t c_f32, int32_t accumulate,
                      void* stream);
 
+/* Tile configuration of the tcgen05 GEMMs: 2 (default) = CTA pairs with cta_group::2
+ * MMAs on 256 x 256 tiles, 1 = single-CTA 128 x 256 tiles. Process-wide; the
+ * ICEPOP_CTA_GROUP environment variable sets the initial value. */
+int icepop_set_cta_group(int32_t cta_group);
+
 #ifdef __cplusplus
 }
 #endif

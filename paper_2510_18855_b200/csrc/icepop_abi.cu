@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -123,20 +124,64 @@ int operand_map(CUtensorMap* map, const void* ptr, int64_t mn, int64_t k, int64_
 
 constexpr int BN_ = 256;
 
-template <bool A_MN, bool B_MN, int EPI>
-int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
-                cudaStream_t st) {
-  auto kern = umma_gemm_kernel<BN_, A_MN, B_MN, EPI>;
-  constexpr size_t smem = GemmCfg<BN_>::SMEM;
+int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
+
+int cta_group() {
+  if (g_cta_group == 0) {
+    const char* e = getenv("ICEPOP_CTA_GROUP");
+    g_cta_group = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  return g_cta_group;
+}
+
+template <bool A_MN, bool B_MN, int EPI, int CG>
+int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
+                   cudaStream_t st) {
+  auto kern = umma_gemm_kernel<BN_, A_MN, B_MN, EPI, CG>;
+  constexpr size_t smem = GemmCfg<BN_, CG>::SMEM;
   static bool attr_done = false;
   if (!attr_done) {
     ICP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done = true;
   }
-  const int grid = std::min(sh.num_tiles, num_sms());
-  kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, sh, ep);
-  ICP_CUDA(cudaGetLastError());
+  const int units = std::min(sh.num_tiles, num_sms() / CG);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(units * CG));
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, ep));
   return ICEPOP_OK;
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
+                cudaStream_t st, int cg) {
+  if (cg == 2) return launch_umma_cg<A_MN, B_MN, EPI, 2>(ta, tb, sh, ep, st);
+  return launch_umma_cg<A_MN, B_MN, EPI, 1>(ta, tb, sh, ep, st);
+}
+
+// Tile raster: `group_m` m-tiles sweep the n dimension together. ICEPOP_GROUP_M overrides
+// (tuning experiments); otherwise 16 tile rows (sustained-power sweep on B200: 16 beat
+// 4, 8 and 32 for every GEMM of the path, see profiles/README.md).
+int group_m_for(int epi, int m_tiles, int n_tiles, int cg) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("ICEPOP_GROUP_M");
+    env = e ? std::max(1, atoi(e)) : 0;
+  }
+  (void)epi;
+  (void)n_tiles;
+  const int g = env > 0 ? env : 16;
+  return std::max(1, std::min(g, m_tiles));
 }
 
 // C[M,N] = A . B^T with the given operand majors; epilogue `epi`.
@@ -145,32 +190,33 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
+  const int cg = cta_group();
   CUtensorMap ta, tb;
   ICP_TRY(operand_map(&ta, A, M, K, lda, a_mn, BM));
-  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, BN_));
+  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, BN_ / cg));
   GemmShape sh;
   sh.M = (int)M;
   sh.N = (int)N;
   sh.K = (int)K;
-  sh.m_tiles = (int)((M + BM - 1) / BM);
+  sh.m_tiles = (int)((M + BM * cg - 1) / (BM * cg));
   sh.n_tiles = (int)((N + BN_ - 1) / BN_);
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
-  sh.group_m = 16;
+  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg);
   if (epi == EPI_STORE) {
-    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st);
-    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st);
-    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, sh, ep, st);
-    return launch_umma<true, true, EPI_STORE>(ta, tb, sh, ep, st);
+    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
+    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st, cg);
+    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
+    return launch_umma<true, true, EPI_STORE>(ta, tb, sh, ep, st, cg);
   }
   if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
   if (epi == EPI_LSE) {
-    if (!b_mn) return launch_umma<false, false, EPI_LSE>(ta, tb, sh, ep, st);
-    return launch_umma<false, true, EPI_LSE>(ta, tb, sh, ep, st);
+    if (!b_mn) return launch_umma<false, false, EPI_LSE>(ta, tb, sh, ep, st, cg);
+    return launch_umma<false, true, EPI_LSE>(ta, tb, sh, ep, st, cg);
   }
-  if (!b_mn) return launch_umma<false, false, EPI_DZ>(ta, tb, sh, ep, st);
-  return launch_umma<false, true, EPI_DZ>(ta, tb, sh, ep, st);
+  if (!b_mn) return launch_umma<false, false, EPI_DZ>(ta, tb, sh, ep, st, cg);
+  return launch_umma<false, true, EPI_DZ>(ta, tb, sh, ep, st, cg);
 }
 
 // ------------------------------------------------------------------ validation helpers
@@ -345,7 +391,7 @@ int icepop_device_check(int device) {
   if (p.major != 10 || p.minor != 0)
     return fail(ICEPOP_EARCH, "libicepop_b200 is built for sm_100a; device %d is sm_%d%d", device, p.major, p.minor);
   cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, umma_gemm_kernel<BN_, false, false, EPI_LSE>);
+  e = cudaFuncGetAttributes(&fa, umma_gemm_kernel<BN_, false, false, EPI_LSE, 2>);
   if (e != cudaSuccess) return fail(ICEPOP_EARCH, "sm_100a kernels not loadable: %s", cudaGetErrorString(e));
   return ICEPOP_OK;
 }
@@ -693,6 +739,12 @@ int icepop_finish(const double* stats, void* stream) {
   if (e & ICEPOP_ERR_CALIB_OVERFLOW) return fail(ICEPOP_ENUMERIC, "calibration ratio overflow");
   if (e & ICEPOP_ERR_RATIO_OVERFLOW) return fail(ICEPOP_ENUMERIC, "importance ratio overflow");
   if (e & ICEPOP_ERR_NONFINITE) return fail(ICEPOP_ENUMERIC, "objective or gradient is not finite");
+  return ICEPOP_OK;
+}
+
+int icepop_set_cta_group(int32_t cta_group) {
+  if (cta_group != 1 && cta_group != 2) return fail(ICEPOP_EINVAL, "cta_group must be 1 or 2");
+  g_cta_group = cta_group;
   return ICEPOP_OK;
 }
 

@@ -56,13 +56,18 @@ struct EpiParams {
   int64_t ldz;
 };
 
-template <int BN>
+// CG = 1: one CTA computes a 128 x BN tile (cta_group::1).
+// CG = 2: a CTA pair computes a 256 x BN tile with cta_group::2 MMAs issued by the leader;
+//         each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so the B operand
+//         is read from L2 once per pair instead of once per CTA.
+template <int BN, int CG>
 struct GemmCfg {
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr int TILE_M = BM * CG;
   static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
 };
 
@@ -229,12 +234,13 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
 }
 
 // ------------------------------------------------------------------ mainloop
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmShape sh, const EpiParams ep) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int B_ROWS = BN / CG;  // rows of B staged by this CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -249,69 +255,98 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int unit = blockIdx.x / CG;     // CTA pair (or CTA) index
+  const int n_units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
+      // Only the pair leader arrives (with expect_tx covering BOTH CTAs' TMA bytes); the peer's
+      // loads just complete_tx on it. A per-k-block remote arrive from the peer would cost a
+      // GPU-scope fence (MEMBAR.ALL.GPU) per stage and halved throughput when measured.
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull0 + 8 * s, 1);
-      mbar_init(tempty0 + 8 * s, 4);  // one arrive per epilogue warp
+      mbar_init(tempty0 + 8 * s, 4 * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
-    tmem_relinquish();
+    if (CG == 2) {
+      tmem_alloc_cg2(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(smem_u32(tmem_holder), Cfg::TMEM_COLS);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs of a pair load their own halves)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
         int m_blk, n_blk;
         tile_coords(sh, tile, m_blk, n_blk);
-        const int m0 = m_blk * BM, n0 = n_blk * BN;
+        const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
+        const int n0 = n_blk * BN + (int)rank * B_ROWS;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          const uint32_t fb = full0 + 8 * stage;
-          mbar_arrive_expect_tx(fb, Cfg::STAGE_BYTES);
+          const uint32_t fb_local = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
-          if (!A_MN) {
-            tma_load_2d(a_dst, &tmA, fb, kb * BK, m0);
-          } else {
+          if (CG == 1) {
+            mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
+            if (!A_MN) {
+              tma_load_2d(a_dst, &tmA, fb_local, kb * BK, m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * (BK * 128), &tmA, fb, m0 + 64 * j, kb * BK);
-          }
-          if (!B_MN) {
-            tma_load_2d(b_dst, &tmB, fb, kb * BK, n0);
-          } else {
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * (BK * 128), &tmA, fb_local, m0 + 64 * j, kb * BK);
+            }
+            if (!B_MN) {
+              tma_load_2d(b_dst, &tmB, fb_local, kb * BK, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * (BK * 128), &tmB, fb, n0 + 64 * j, kb * BK);
+              for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d(b_dst + j * (BK * 128), &tmB, fb_local, n0 + 64 * j, kb * BK);
+            }
+          } else {
+            const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
+            if (rank == 0) mbar_arrive_expect_tx(fb_local, CG * Cfg::STAGE_BYTES);
+            if (!A_MN) {
+              tma_load_2d_cg2(a_dst, &tmA, fb, kb * BK, m0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_cg2(a_dst + j * (BK * 128), &tmA, fb, m0 + 64 * j, kb * BK);
+            }
+            if (!B_MN) {
+              tma_load_2d_cg2(b_dst, &tmB, fb, kb * BK, n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d_cg2(b_dst + j * (BK * 128), &tmB, fb, n0 + 64 * j, kb * BK);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    // ---------------- MMA issuer (the pair leader only)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -326,41 +361,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                      : sdesc_sw128(a_base + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
                                      : sdesc_sw128(b_base + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if (CG == 2) umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs finish
+          // frees the smem slot (in both CTAs) when these MMAs finish
+          if (CG == 2) umma_commit_cg2(empty0 + 8 * stage, 0x3); else umma_commit(empty0 + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue warps (of both CTAs)
+        if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
-    // ---------------- epilogue warps
+    // ---------------- epilogue warps: this CTA's 128 rows of the pair tile
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < sh.num_tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
       int m_blk, n_blk;
       tile_coords(sh, tile, m_blk, n_blk);
+      const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
-      if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m_blk * BM, n_blk * BN, row, taddr);
-      if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m_blk * BM, n_blk * BN, n_blk, row, taddr);
-      if (EPI == EPI_DZ) epi_dz<BN>(sh, ep, m_blk * BM, n_blk * BN, row, taddr);
+      if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
+      if (EPI == EPI_DZ) epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(mapa_shared(tempty0 + 8 * acc, 0));
+        else mbar_arrive(tempty0 + 8 * acc);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (CG == 2) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

@@ -8,6 +8,16 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request):
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    _lib.check(lib.icepop_set_cta_group(request.param))
+    yield request.param
+    _lib.check(lib.icepop_set_cta_group(2))
+
+
 def _gemm(A, B, M, N, K, a_mn, b_mn, c_f32=True, accumulate=False, C=None):
     from paper_2510_18855_b200 import _lib
 
@@ -23,8 +33,9 @@ def _gemm(A, B, M, N, K, a_mn, b_mn, c_f32=True, accumulate=False, C=None):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1024, 2048, 512), (136, 264, 1000)])
-def test_gemm_majors(cuda_device, a_mn, b_mn, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (1024, 2048, 512), (136, 264, 1000),
+                                   (520, 136, 72)])
+def test_gemm_majors(cuda_device, cta_group, a_mn, b_mn, M, N, K):
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
     A = torch.randn(M, K, generator=g).to(torch.bfloat16).to(cuda_device)
     B = torch.randn(N, K, generator=g).to(torch.bfloat16).to(cuda_device)
@@ -34,7 +45,7 @@ def test_gemm_majors(cuda_device, a_mn, b_mn, M, N, K):
     assert err <= 1e-3 * (K ** 0.5), f"max abs err {err}"
 
 
-def test_gemm_bf16_out_and_accumulate(cuda_device):
+def test_gemm_bf16_out_and_accumulate(cuda_device, cta_group):
     M, N, K = 256, 512, 320
     A = torch.randn(M, K, device=cuda_device).to(torch.bfloat16)
     B = torch.randn(N, K, device=cuda_device).to(torch.bfloat16)

@@ -86,8 +86,18 @@ def test_fp64_path_matches_reference_golden(cuda_device, name):
     np.testing.assert_allclose(g, d["out_grad"], rtol=1e-9, atol=1e-13)
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request):
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    _lib.check(lib.icepop_set_cta_group(request.param))
+    yield request.param
+    _lib.check(lib.icepop_set_cta_group(2))
+
+
 @pytest.mark.parametrize("name", [n for n in golden_cases() if "kl" not in n and "refdiag" not in n])
-def test_bf16_path_matches_reference_golden(cuda_device, name):
+def test_bf16_path_matches_reference_golden(cuda_device, cta_group, name):
     from paper_2510_18855_b200.loss import Diagnostics, finish, icepop_bwd, icepop_fwd
 
     d = load_golden(name)
