@@ -1,0 +1,250 @@
+"""Dense (Ling-style) inputs on the bf16 tcgen05 path vs the fp64 oracle on the same
+bf16-rounded inputs: ragged packed sequences, tails that are not tile multiples, both
+weight layouts, both CTA configurations, token shards, error semantics and autograd.
+
+Tolerances: kept mask / popped count bit-exact; lp_cur, entropy abs <= 2e-3 (+1e-3 rel);
+objective rel <= 1e-3; dW, dH relative Frobenius error <= 1e-2.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(n_seqs=6, d=320, V=1000, seed=0, lens=None, group=3, sigma=0.3, layout="vd"):
+    rng = np.random.default_rng(seed)
+    lens = lens or list(rng.integers(40, 400, n_seqs))
+    N = int(sum(lens))
+    H = torch.from_numpy(rng.normal(0, 1, (N, d))).to(torch.bfloat16)
+    shape_w = (V, d) if layout == "vd" else (d, V)
+    W = torch.from_numpy(rng.normal(0, 2 / np.sqrt(d), shape_w)).to(torch.bfloat16)
+    tokens = rng.integers(0, V, N).astype(np.int32)
+    # lp_old near the model's own log-prob so ratios straddle the clip band
+    Hd, Wd = H.double().numpy(), W.double().numpy()
+    z = Hd @ (Wd.T if layout == "vd" else Wd)
+    lse = z.max(1) + np.log(np.exp(z - z.max(1, keepdims=True)).sum(1))
+    lp_old = z[np.arange(N), tokens] - lse + rng.normal(0, 0.15, N)
+    lp_inf = lp_old - rng.normal(0, sigma, N)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    go = np.arange(0, n_seqs + 1, group).astype(np.int32)
+    if go[-1] != n_seqs:
+        go = np.append(go, n_seqs).astype(np.int32)
+    adv = rng.normal(0, 1, n_seqs)
+    return dict(H=H, W=W, tokens=tokens, lp_old=lp_old, lp_inf=lp_inf, cu=cu, go=go, adv=adv, layout=layout)
+
+
+def _batch(c, dev, sl=None):
+    from paper_2510_18855_b200.loss import PackedBatch
+
+    sl = sl or slice(0, len(c["tokens"]))
+    return PackedBatch(torch.from_numpy(c["tokens"][sl]).to(dev), torch.from_numpy(c["lp_old"][sl]).to(dev),
+                       torch.from_numpy(c["lp_inf"][sl]).to(dev), torch.from_numpy(c["cu"]).to(dev),
+                       torch.from_numpy(c["go"]).to(dev), torch.from_numpy(c["adv"]).to(dev),
+                       token_offset=sl.start or 0)
+
+
+def _oracle(c, **kw):
+    from oracle.icepop_oracle import icepop_dense
+
+    return icepop_dense(c["H"].double().numpy(), c["W"].double().numpy(), c["tokens"], c["lp_old"], c["lp_inf"],
+                        c["cu"], c["go"], c["adv"], layout=c["layout"], **kw)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request):
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    _lib.check(lib.icepop_set_cta_group(request.param))
+    yield request.param
+    _lib.check(lib.icepop_set_cta_group(2))
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+@pytest.mark.parametrize("algo", ["icepop", "grpo", "tis"])
+def test_dense_bf16_vs_oracle(cuda_device, cta_group, layout, algo):
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    c = _case(seed=3, layout=layout)
+    cfg = IcePopConfig(algo=algo)
+    b = _batch(c, cuda_device)
+    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), b, cfg, layout=layout)
+    gh, gw = icepop_bwd(c["H"].to(cuda_device), c["W"].to(cuda_device), b, f, cfg, layout=layout,
+                        grad_hidden_dtype=torch.float32)
+    finish(f.stats)
+    o = _oracle(c, algo=algo)
+    diag = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), o["kept"])
+    assert diag.clipped_fraction == o["clipped_fraction"]
+    if algo == "icepop":
+        assert 0 < o["n_clipped"] < len(c["tokens"])  # the case really pops tokens
+    np.testing.assert_allclose(f.lp_cur.cpu().numpy(), o["lp_cur"], atol=2e-3, rtol=1e-3)
+    np.testing.assert_allclose(f.lse.cpu().numpy(), o["lse"], atol=2e-3, rtol=1e-4)
+    np.testing.assert_allclose(f.entropy.cpu().numpy(), o["entropy"], atol=2e-3, rtol=1e-3)
+    assert diag.objective_value == pytest.approx(o["objective"], rel=1e-3, abs=1e-6)
+    assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_shards_sum_to_full_batch(cuda_device):
+    """Token ranges cutting sequences mid-way (token_offset) reproduce the full batch."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=5, seed=7)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    full = icepop_fwd(H, W, _batch(c, cuda_device), cfg)
+    _, gw_full = icepop_bwd(H, W, _batch(c, cuda_device), full, cfg, need_hidden=False)
+    N = len(c["tokens"])
+    cuts = [0, int(c["cu"][1]) + 17, N // 2 + 3, N]
+    stats = torch.zeros(8, dtype=torch.float64, device=cuda_device)
+    gw = torch.zeros_like(gw_full)
+    kept = []
+    for s, e in zip(cuts, cuts[1:]):
+        b = _batch(c, cuda_device, slice(s, e))
+        f = icepop_fwd(H[s:e], W, b, cfg)
+        icepop_bwd(H[s:e], W, b, f, cfg, need_hidden=False, grad_weight=gw)
+        stats[:7] += f.stats[:7]
+        kept.append(f.kept)
+        assert torch.equal(f.calib, full.calib[s:e])
+        assert torch.equal(f.coeff, full.coeff[s:e])
+    assert torch.equal(torch.cat(kept), full.kept)
+    torch.testing.assert_close(stats[:7], full.stats[:7], rtol=1e-9, atol=1e-12)
+    assert _rel(gw.cpu().numpy(), gw_full.cpu().numpy()) < 1e-5
+
+
+def test_backward_chunking_matches_single_chunk(cuda_device, monkeypatch):
+    """A small dZ workspace forces several token chunks with dW accumulated in place."""
+    import paper_2510_18855_b200.loss as L
+
+    c = _case(n_seqs=4, seed=11, lens=[300, 260, 130, 500])
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = L.icepop_fwd(H, W, _batch(c, cuda_device), L.IcePopConfig())
+    gh1, gw1 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
+    monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * 1000 * 2)  # 256-row chunks
+    gh2, gw2 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
+    assert torch.equal(gh1, gh2)
+    assert _rel(gw2.cpu().numpy(), gw1.cpu().numpy()) < 1e-5  # fp32 partial sums per chunk
+
+
+def test_temperature(cuda_device):
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(seed=5)
+    cfg = IcePopConfig(temperature=0.6)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), cfg)
+    gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, grad_hidden_dtype=torch.float32)
+    o = _oracle(c, temperature=0.6)
+    np.testing.assert_allclose(f.lp_cur.cpu().numpy(), o["lp_cur"], atol=3e-3, rtol=1e-3)
+    assert Diagnostics.from_stats(f.stats.cpu()).objective_value == pytest.approx(o["objective"], rel=2e-3)
+    assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_numeric_error_on_calibration_overflow(cuda_device):
+    from paper_2510_18855_b200.errors import NumericError
+    from paper_2510_18855_b200.loss import IcePopConfig, finish, icepop_fwd
+
+    c = _case(seed=2)
+    c["lp_old"] = c["lp_old"].copy()
+    c["lp_old"][5] = 800.0  # exp(800 - lp_inf) overflows (objective.py:228-229)
+    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), _batch(c, cuda_device), IcePopConfig())
+    with pytest.raises(NumericError, match="calibration ratio overflow"):
+        finish(f.stats)
+
+
+def test_token_out_of_vocab_is_value_error(cuda_device):
+    from paper_2510_18855_b200.loss import IcePopConfig, finish, icepop_fwd
+
+    c = _case(seed=2)
+    c["tokens"] = c["tokens"].copy()
+    c["tokens"][3] = 1000  # == V
+    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), _batch(c, cuda_device), IcePopConfig())
+    with pytest.raises(ValueError, match="vocabulary"):
+        finish(f.stats)
+
+
+def test_config_validation_matches_reference():
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=1)
+    dev = torch.device("cuda", 0)
+    for bad in (IcePopConfig(alpha=1.5), IcePopConfig(beta=0.9), IcePopConfig(clip_eps=1.0),
+                IcePopConfig(tis_cap=0.0), IcePopConfig(temperature=0.0)):
+        with pytest.raises(ValueError):
+            icepop_fwd(c["H"].to(dev), c["W"].to(dev), _batch(c, dev), bad)
+    assert _lib.load().icepop_abi_version() == 1
+
+
+def test_custom_op_autograd_matches_functional(cuda_device):
+    """loss = -J through torch.library custom op; grads equal -dJ/dW, -dJ/dH."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd, icepop_loss
+
+    c = _case(seed=9)
+    H = c["H"].to(cuda_device).requires_grad_(True)
+    W = c["W"].to(cuda_device).requires_grad_(True)
+    b = _batch(c, cuda_device)
+    loss, aux = icepop_loss(H, W, b, IcePopConfig(), layout="vd")
+    (2.0 * loss).backward()
+    f = icepop_fwd(H.detach(), W.detach(), b, IcePopConfig())
+    gh, gw = icepop_bwd(H.detach(), W.detach(), b, f, IcePopConfig(), grad_scale=-2.0,
+                        grad_hidden_dtype=torch.float32)
+    assert loss.item() == pytest.approx(-f.stats[0].item(), rel=1e-12)
+    assert _rel(H.grad.float().cpu().numpy(), gh.cpu().numpy()) < 1e-2
+    assert _rel(W.grad.float().cpu().numpy(), gw.cpu().numpy()) < 1e-2
+    assert torch.equal(aux["kept"], f.kept)
+
+
+def test_logprob_entry_matches_forward(cuda_device):
+    """icepop_logprob_bf16 (recording lp_train_old, scheduler.py:296-311) == forward lp."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=4)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig())
+    lib = _lib.ensure_device(0)
+    N = H.shape[0]
+    shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=H.shape[1], vocab=W.shape[0], n_seqs=1, n_groups=1,
+                       weight_layout=_lib.W_VD)
+    fb = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, fb, None))
+    ws = torch.empty(fb.value, dtype=torch.uint8, device=cuda_device)
+    lp = torch.empty(N, dtype=torch.float64, device=cuda_device)
+    lse = torch.empty(N, dtype=torch.float32, device=cuda_device)
+    ent = torch.empty(N, dtype=torch.float32, device=cuda_device)
+    tok = torch.from_numpy(c["tokens"]).to(cuda_device)
+    _lib.check(lib.icepop_logprob_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tok.data_ptr(), lse.data_ptr(),
+                                       lp.data_ptr(), ent.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(lp, f.lp_cur) and torch.equal(lse, f.lse) and torch.equal(ent, f.entropy)
+
+
+def test_long_cot_ragged_high_mask_rate(cuda_device):
+    """C4-shaped (scaled): ragged lognormal lengths, ~5% popped tokens."""
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    rng = np.random.default_rng(42)
+    lens = list(np.clip(rng.lognormal(np.log(600), 0.6, 8), 64, 2048).astype(int))
+    c = _case(n_seqs=8, d=256, V=2048, seed=21, lens=lens, group=4, sigma=0.42)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig())
+    _, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, IcePopConfig(), need_hidden=False)
+    finish(f.stats)
+    o = _oracle(c)
+    d = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), o["kept"])
+    assert 0.02 < d.clipped_fraction < 0.10
+    assert d.objective_value == pytest.approx(o["objective"], rel=1e-3)
+    assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2

@@ -1,0 +1,144 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): token sharding, the fp64 statistics
+all-reduce with OR-ed error bits, bucketed dW all-reduce, and that per-rank partial sums
+of the oracle over token shards (sequences cut mid-way) reproduce the full-batch objective."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import golden_hidden, load_golden, oracle_kwargs
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_ranks(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        if isinstance(v, Exception):
+            raise v
+    return [out[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("n,world,align", [(10, 2, 1), (10, 3, 1), (1000, 8, 128), (5, 8, 1), (0, 2, 1)])
+def test_shard_range_partitions(n, world, align):
+    from paper_2510_18855_b200.distributed import shard_range
+
+    ranges = [shard_range(n, world, r, align) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+        assert a1 == b0 and a0 <= a1
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= align
+
+
+def _stats_fn(rank, world):
+    from paper_2510_18855_b200.distributed import allreduce_stats
+
+    s = torch.tensor([1.5 * (rank + 1), 1.0, 10.0, 2.0, 0.5, -3.0, 0.0, float(1 << rank)], dtype=torch.float64)
+    allreduce_stats(s)
+    return s.tolist()
+
+
+def test_allreduce_stats_sums_and_ors_error_bits():
+    out = run_ranks(_stats_fn)
+    for s in out:
+        assert s[:7] == [4.5, 2.0, 20.0, 4.0, 1.0, -6.0, 0.0]
+        assert s[7] == 3.0  # bit0 | bit1, not 1 + 2 misread
+
+
+def _same_bits_fn(rank, world):
+    from paper_2510_18855_b200.distributed import allreduce_stats
+
+    s = torch.zeros(8, dtype=torch.float64)
+    s[7] = 1.0
+    allreduce_stats(s)
+    return s[7].item()
+
+
+def test_allreduce_stats_same_bit_on_two_ranks_stays_that_bit():
+    assert run_ranks(_same_bits_fn) == [1.0, 1.0]
+
+
+def _grad_fn(rank, world):
+    from paper_2510_18855_b200.distributed import allreduce_grad, wait_grad
+
+    g = torch.arange(1000, dtype=torch.float32).reshape(10, 100) * (rank + 1)
+    wait_grad(allreduce_grad(g, bucket_bytes=256))  # 64-element buckets
+    return g.numpy()
+
+
+def test_allreduce_grad_buckets():
+    out = run_ranks(_grad_fn)
+    ref = np.arange(1000, dtype=np.float32).reshape(10, 100) * 3
+    for g in out:
+        assert np.array_equal(g, ref)
+
+
+def _per_token_oracle(d):
+    """Per-token pieces of J and the diagnostics for the full batch (oracle)."""
+    from oracle.icepop_oracle import icepop_dense, per_token_weights
+
+    o = icepop_dense(golden_hidden(d), d["weight"], d["tokens"], d["lp_train_old"], d["lp_infer_old"],
+                     d["cu_seqlens"], d["group_offsets"], d["advantages"], **oracle_kwargs(d))
+    w = per_token_weights(d["cu_seqlens"], d["group_offsets"])
+    return o, w
+
+
+def _shard_objective_fn(rank, world):
+    from paper_2510_18855_b200.distributed import allreduce_stats, shard_range
+
+    d = load_golden("medium_icepop")
+    o, w = _per_token_oracle(d)
+    s, e = shard_range(len(d["tokens"]), world, rank)
+    kept = o["kept"][s:e]
+    ent = o["entropy"][s:e]
+    stats = torch.tensor([float((w[s:e] * o["surrogate"][s:e]).sum()), float((~kept).sum()), float(e - s),
+                          float(ent.sum()), float(ent[~kept].sum()), float(o["lp_cur"][s:e].sum()), 0.0, 0.0],
+                         dtype=torch.float64)
+    allreduce_stats(stats)
+    return stats.tolist(), o["objective"], o["n_clipped"], o["token_count"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_token_shards_reproduce_full_batch_objective(world):
+    """Ranks cut sequences mid-way; the per-token weights still come out exact."""
+    d = load_golden("medium_icepop")
+    cu = d["cu_seqlens"]
+    from paper_2510_18855_b200.distributed import shard_range
+
+    cuts = [shard_range(len(d["tokens"]), world, r)[0] for r in range(1, world)]
+    assert any(c not in set(cu.tolist()) for c in cuts), "fixture should cut a sequence"
+    out = run_ranks(_shard_objective_fn, world=world)
+    stats, J, n_clipped, n_tok = out[0]
+    assert stats[0] == pytest.approx(J, rel=1e-12, abs=1e-15)
+    assert stats[1] == n_clipped and stats[2] == n_tok
