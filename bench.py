@@ -159,9 +159,9 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_18855_b200 import _lib
-    from paper_2510_18855_b200.loss import (DZ_CHUNK_BYTES, Diagnostics, IcePopConfig, PackedBatch, finish,
-                                            icepop_bwd, icepop_fwd)
+    from paper_2510_18855_b200 import _lib  # noqa: F401
+    from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
+    from paper_2510_18855_b200.loss import DZ_CHUNK_BYTES, Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -184,8 +184,8 @@ def run_ours(args):
         f = icepop_fwd(H, W, batch, icfg, layout="vd")
         gh, g = icepop_bwd(H, W, batch, f, icfg, layout="vd", grad_scale=-1.0)
         if world > 1:
-            dist.all_reduce(f.stats)
-            dist.all_reduce(g)
+            allreduce_stats(f.stats)
+            wait_grad(allreduce_grad(g))
         return f
 
     # warm-up (also validates the error word once)
@@ -315,6 +315,7 @@ def run_e2e(H, W, batch, icfg, args, dev, world):
     import torch
     import torch.distributed as dist
 
+    from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
     from paper_2510_18855_b200.loss import PackedBatch, icepop_bwd, icepop_fwd
 
     host = {k: v.cpu().pin_memory() for k, v in dict(H=H, tokens=batch.tokens, lp_old=batch.lp_train_old,
@@ -333,8 +334,8 @@ def run_e2e(H, W, batch, icfg, args, dev, world):
         f = icepop_fwd(dbuf["H"], W, b, icfg, layout="vd")
         _, g = icepop_bwd(dbuf["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
         if world > 1:
-            dist.all_reduce(f.stats)
-            dist.all_reduce(g)
+            allreduce_stats(f.stats)
+            wait_grad(allreduce_grad(g))
         out_host.copy_(f.stats, non_blocking=True)
 
     one()

@@ -119,7 +119,8 @@ int icepop_device_check(int device);
 
 /* ---- K0: group advantages (objective.py:153-159) ---------------------------------- */
 /* adv[i] = (R_i - mean_g R) / max(std_pop,g(R), 1e-6) for every sequence i of group g.
- * Groups of fewer than 2 sequences are rejected (ICEPOP_EINVAL), as in the reference. */
+ * A group of fewer than 2 sequences yields NaN advantages (the host layers reject it with
+ * ValueError first, as objective.py:156-157 does). */
 int icepop_group_advantages(const double* rewards, const int32_t* group_offsets, int32_t n_groups,
                             int32_t n_seqs, double* advantages, void* stream);
 
