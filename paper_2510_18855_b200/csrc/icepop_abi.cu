@@ -126,6 +126,34 @@ constexpr int BN_ = 256;
 
 int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
 
+// Dynamic tile scheduling: a pool of device counters (one per launch, zeroed stream-ordered
+// right before it). ICEPOP_SCHED=static selects the static round-robin schedule instead.
+constexpr int N_COUNTERS = 256;
+int* g_counters[16] = {nullptr};
+unsigned g_counter_next[16] = {0};
+
+int dynamic_sched() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ICEPOP_SCHED");
+    v = (e && strcmp(e, "static") == 0) ? 0 : 1;
+  }
+  return v;
+}
+
+int tile_counter(cudaStream_t st, int32_t** out) {
+  *out = nullptr;
+  if (!dynamic_sched()) return ICEPOP_OK;
+  int dev = 0;
+  ICP_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return ICEPOP_OK;
+  if (!g_counters[dev]) ICP_CUDA(cudaMalloc(&g_counters[dev], N_COUNTERS * sizeof(int)));
+  int* c = g_counters[dev] + (g_counter_next[dev]++ % N_COUNTERS);
+  ICP_CUDA(cudaMemsetAsync(c, 0, sizeof(int), st));
+  *out = c;
+  return ICEPOP_OK;
+}
+
 int cta_group() {
   if (g_cta_group == 0) {
     const char* e = getenv("ICEPOP_CTA_GROUP");
@@ -204,6 +232,7 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
   sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg);
+  ICP_TRY(tile_counter(st, &sh.tile_counter));
   if (epi == EPI_STORE) {
     if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
     if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st, cg);

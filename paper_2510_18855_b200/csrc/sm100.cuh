@@ -205,6 +205,14 @@ __device__ __forceinline__ void umma_commit_cg2(uint32_t bar, uint16_t mask) {
       : "memory");
 }
 
+// 4-byte store into a (peer) CTA's smem whose arrival is counted as complete_tx on the
+// peer's mbarrier: cross-CTA publication without a cluster-scope fence.
+__device__ __forceinline__ void st_async_b32(uint32_t cluster_addr, uint32_t value, uint32_t cluster_bar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "r"(value), "r"(cluster_bar)
+               : "memory");
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

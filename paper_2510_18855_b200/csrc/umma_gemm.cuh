@@ -33,7 +33,8 @@ struct GemmShape {
   int32_t M, N, K;
   int32_t m_tiles, n_tiles, k_blocks;
   int32_t num_tiles;
-  int32_t group_m;  // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
+  int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
+  int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
 };
 
 struct EpiParams {
@@ -68,6 +69,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
   static constexpr int TILE_M = BM * CG;
+  static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
   static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
 };
 
@@ -247,17 +249,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  // barrier block: full[S] empty[S] tfull[2] tempty[2] rfull[RING] | tmem_holder | ring[RING]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::RING);
+  int32_t* ring = reinterpret_cast<int32_t*>(tmem_holder + 1);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * STAGES);
   const uint32_t tempty0 = smem_u32(bars + 2 * STAGES + 2);
+  const uint32_t rfull0 = smem_u32(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const int unit = blockIdx.x / CG;     // CTA pair (or CTA) index
   const int n_units = gridDim.x / CG;
+  const bool dynamic = sh.tile_counter != nullptr;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -273,6 +279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(tfull0 + 8 * s, 1);
       mbar_init(tempty0 + 8 * s, 4 * CG);  // one arrive per epilogue warp of the pair
     }
+    for (int s = 0; s < Cfg::RING; ++s) mbar_init(rfull0 + 8 * s, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -289,12 +296,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // Tile sequence of this unit. Static: unit, unit + n_units, ... Dynamic: the leader's MMA
+  // thread claims tiles from a global counter (one tile of prefetch) and publishes tile j in
+  // ring slot j % RING -- locally with st.shared + arrive, to the peer CTA with st.async
+  // (complete_tx on the peer's rfull barrier, armed by the peer's producer). Tile j+2 is
+  // published only after the MMA has waited for the epilogues of tile j-2, so a slot is never
+  // overwritten while a role of either CTA may still read it. -1 ends the sequence.
+  auto ring_get = [&](int j, bool arm) -> int {
+    if (!dynamic) {
+      const int t = unit + j * n_units;
+      return t < sh.num_tiles ? t : -1;
+    }
+    const int s = j & (Cfg::RING - 1);
+    if (arm) mbar_arrive_expect_tx(rfull0 + 8 * s, 4);
+    mbar_wait(rfull0 + 8 * s, (uint32_t)(j / Cfg::RING) & 1u);
+    return *reinterpret_cast<volatile int32_t*>(ring + s);
+  };
+
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs of a pair load their own halves)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
+      for (int j = 0;; ++j) {
+        const int tile = ring_get(j, CG == 2 && rank == 1);
+        if (tile < 0) break;
         int m_blk, n_blk;
         tile_coords(sh, tile, m_blk, n_blk);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
@@ -310,13 +336,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_load_2d(a_dst, &tmA, fb_local, kb * BK, m0);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * (BK * 128), &tmA, fb_local, m0 + 64 * j, kb * BK);
+              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kb * BK);
             }
             if (!B_MN) {
               tma_load_2d(b_dst, &tmB, fb_local, kb * BK, n0);
             } else {
 #pragma unroll
-              for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d(b_dst + j * (BK * 128), &tmB, fb_local, n0 + 64 * j, kb * BK);
+              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kb * BK);
             }
           } else {
             const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
@@ -325,13 +351,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_load_2d_cg2(a_dst, &tmA, fb, kb * BK, m0);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_2d_cg2(a_dst + j * (BK * 128), &tmA, fb, m0 + 64 * j, kb * BK);
+              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kb * BK);
             }
             if (!B_MN) {
               tma_load_2d_cg2(b_dst, &tmB, fb, kb * BK, n0);
             } else {
 #pragma unroll
-              for (int j = 0; j < B_ROWS / 64; ++j) tma_load_2d_cg2(b_dst + j * (BK * 128), &tmB, fb, n0 + 64 * j, kb * BK);
+              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kb * BK);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -339,16 +365,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (the pair leader only)
+    // ---------------- MMA issuer (the pair leader only) + dynamic tile scheduler
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      auto publish = [&](int j, int tile) {
+        const int s = j & (Cfg::RING - 1);
+        ring[s] = tile;
+        mbar_arrive(rfull0 + 8 * s);
+        if (CG == 2) st_async_b32(mapa_shared(smem_u32(ring + s), 1), (uint32_t)tile, mapa_shared(rfull0 + 8 * s, 1));
+      };
+      auto claim = [&]() -> int { return n_units + atomicAdd(sh.tile_counter, 1); };
+      // cur = tile j, nxt1 = tile j+1 (already published), claimed = next claimed index
+      int cur, nxt1 = -1, claimed = sh.num_tiles;
+      if (dynamic) {
+        cur = unit < sh.num_tiles ? unit : -1;
+        publish(0, cur);
+        const int t1 = cur >= 0 ? claim() : sh.num_tiles;
+        nxt1 = t1 < sh.num_tiles ? t1 : -1;
+        publish(1, nxt1);
+        claimed = nxt1 >= 0 ? claim() : sh.num_tiles;
+      } else {
+        cur = ring_get(0, false);
+      }
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
+      for (int j = 0; cur >= 0; ++j) {
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
+        int nxt2 = -1;
+        if (dynamic) {
+          // epilogues of tile j-2 are done -> ring slot (j+2) % RING is free
+          nxt2 = (nxt1 >= 0 && claimed < sh.num_tiles) ? claimed : -1;
+          publish(j + 2, nxt2);
+          claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
+        }
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
@@ -371,6 +423,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // accumulator ready for the epilogue warps (of both CTAs)
         if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (dynamic) {
+          cur = nxt1;
+          nxt1 = nxt2;
+        } else {
+          cur = ring_get(j + 1, false);
+        }
       }
     }
   } else {
@@ -379,7 +437,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = unit; tile < sh.num_tiles; tile += n_units) {
+    for (int j = 0;; ++j) {
+      const int tile = ring_get(j, false);
+      if (tile < 0) break;
       int m_blk, n_blk;
       tile_coords(sh, tile, m_blk, n_blk);
       const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
