@@ -141,6 +141,15 @@ int dynamic_sched() {
   return v;
 }
 
+int long_k_blocks() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ICEPOP_LONG_K_BLOCKS");
+    v = e ? std::max(1, atoi(e)) : 256;
+  }
+  return v;
+}
+
 int tile_counter(cudaStream_t st, int32_t** out) {
   *out = nullptr;
   if (!dynamic_sched()) return ICEPOP_OK;
@@ -232,7 +241,15 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
   sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg);
-  ICP_TRY(tile_counter(st, &sh.tile_counter));
+  // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
+  // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
+  sh.wave_counter = nullptr;
+  if (sh.k_blocks >= long_k_blocks()) {
+    ICP_TRY(tile_counter(st, &sh.wave_counter));
+    sh.tile_counter = nullptr;
+  } else {
+    ICP_TRY(tile_counter(st, &sh.tile_counter));
+  }
   if (epi == EPI_STORE) {
     if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
     if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st, cg);

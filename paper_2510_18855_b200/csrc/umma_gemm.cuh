@@ -35,7 +35,14 @@ struct GemmShape {
   int32_t num_tiles;
   int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
+  int32_t* wave_counter;  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 struct EpiParams {
   // EPI_STORE
@@ -264,6 +271,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int unit = blockIdx.x / CG;     // CTA pair (or CTA) index
   const int n_units = gridDim.x / CG;
   const bool dynamic = sh.tile_counter != nullptr;
+  // Long-K GEMMs (K4, K5): static waves of n_units tiles with a grid barrier between waves, so
+  // the pairs sharing A/B slices stay within a few stages of each other in k and the slices
+  // are served from L2 (a dynamic claim order desynchronises k across in-flight tiles).
+  const bool waves = !dynamic && sh.wave_counter != nullptr;
+  const int n_waves = (sh.num_tiles + n_units - 1) / n_units;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -320,7 +332,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int j = 0;; ++j) {
         const int tile = ring_get(j, CG == 2 && rank == 1);
-        if (tile < 0) break;
+        if (tile < 0) {
+          if (waves && rank == 0 && n_waves > j) atomicAdd(sh.wave_counter, n_waves - j);  // pre-pay
+          break;
+        }
+        if (waves && rank == 0 && j > 0) {
+          // all units must have issued every load of wave j-1 before anyone starts wave j
+          // (the grid is sized so every unit is co-resident; the watchdog guards the spin)
+          const int target = n_units * j;
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire_gpu(sh.wave_counter) < target) {
+            __nanosleep(128);
+            if (globaltimer_ns() - t0 > 20000000000ull) {
+              printf("icepop: wave barrier watchdog (block %d)\n", blockIdx.x);
+              __trap();
+            }
+          }
+        }
         int m_blk, n_blk;
         tile_coords(sh, tile, m_blk, n_blk);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
@@ -362,6 +390,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (waves && rank == 0) atomicAdd(sh.wave_counter, 1);
       }
     }
   } else if (warp == 1) {
