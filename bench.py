@@ -177,7 +177,8 @@ def run_ours(args):
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
     chunk = max(128, min(N, DZ_CHUNK_BYTES // (2 * V)) // 128 * 128)
     n_chunks = -(-N // chunk)
-    launches_per_step = 6 + 3 * n_chunks  # K0, token check, K1, K2, finalize, err-merge + (K3,K4,K5)/chunk
+    # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: 4 compaction kernels + (K3, K4, K5) per chunk
+    launches_per_step = 6 + 4 + 3 * n_chunks
 
     def step_into():
         # loss = -J: grad_scale -1 gives d(loss)/d(hidden), d(loss)/d(W)

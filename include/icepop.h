@@ -224,6 +224,12 @@ int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N
  * ICEPOP_CTA_GROUP environment variable sets the initial value. */
 int icepop_set_cta_group(int32_t cta_group);
 
+/* Backward row skipping: rows whose gradient coefficient is exactly zero (popped tokens,
+ * clip-inactive tokens, zero-advantage sequences; objective.py:250) contribute nothing to
+ * dW and get dHidden = 0, so icepop_bwd_bf16 compacts the active rows on the device and
+ * runs K3-K5 on them only (1 = default; ICEPOP_SKIP_INACTIVE=0 sets the initial value 0). */
+int icepop_set_skip_inactive(int32_t enable);
+
 #ifdef __cplusplus
 }
 #endif

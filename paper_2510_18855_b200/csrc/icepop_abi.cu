@@ -209,21 +209,30 @@ int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& s
 // Tile raster: `group_m` m-tiles sweep the n dimension together. ICEPOP_GROUP_M overrides
 // (tuning experiments); otherwise 16 tile rows (sustained-power sweep on B200: 16 beat
 // 4, 8 and 32 for every GEMM of the path, see profiles/README.md).
-int group_m_for(int epi, int m_tiles, int n_tiles, int cg) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("ICEPOP_GROUP_M");
-    env = e ? std::max(1, atoi(e)) : 0;
-  }
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+
+int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k) {
+  static const int g_short = env_int("ICEPOP_GROUP_M", 16);
+  static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 16);
   (void)epi;
   (void)n_tiles;
-  const int g = env > 0 ? env : 16;
+  (void)cg;
+  const int g = long_k ? g_long : g_short;
   return std::max(1, std::min(g, m_tiles));
 }
 
 // C[M,N] = A . B^T with the given operand majors; epilogue `epi`.
+struct Extent {
+  const int32_t* dev = nullptr;  // device-side extent (compacted row count), or null
+  int32_t base = 0;
+  int32_t dim = 0;  // 1: M, 2: K
+};
+
 int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
-             int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st) {
+             int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent()) {
   if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
@@ -240,7 +249,10 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
-  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg);
+  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, sh.k_blocks >= long_k_blocks());
+  sh.ext_dev = ext.dev;
+  sh.ext_base = ext.base;
+  sh.ext_dim = ext.dim;
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;
@@ -376,20 +388,56 @@ struct BF16Workspace {
   double* adv;
   double* block_stats;
   unsigned* err;
+  // backward, active-row compaction (skip mode)
+  int32_t* idx;
+  int32_t* block_counts;
+  int32_t* block_offsets;
+  int32_t* n_active;
+  __nv_bfloat16* hid_act;
+  int32_t* tok_act;
+  float* lse_act;
+  float* coeff_act;
   __nv_bfloat16* dz;
   int64_t chunk;
   size_t bytes;
 };
 
-BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk) {
+// Rows with a zero gradient coefficient are skipped in the backward unless
+// ICEPOP_SKIP_INACTIVE=0.
+int g_skip_inactive = -1;
+
+bool skip_inactive() {
+  if (g_skip_inactive < 0) {
+    const char* e = getenv("ICEPOP_SKIP_INACTIVE");
+    g_skip_inactive = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return g_skip_inactive == 1;
+}
+
+// Forward part (partials, stats) is always carved; `bwd` adds the compaction buffers and
+// `chunk` rows of bf16 dZ.
+BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool bwd = false) {
   Carver c(base);
   BF16Workspace w;
+  memset(&w, 0, sizeof(w));
+  const int64_t n = std::max<int64_t>(s->n_tokens, 1);
   const int64_t n_tiles = (s->vocab + BN_ - 1) / BN_;
-  w.part = c.take<float>((size_t)n_tiles * 3 * std::max<int64_t>(s->n_tokens, 1));
-  w.ztok = c.take<float>((size_t)std::max<int64_t>(s->n_tokens, 1));
+  w.part = c.take<float>((size_t)n_tiles * 3 * n);
+  w.ztok = c.take<float>((size_t)n);
   w.adv = c.take<double>((size_t)s->n_seqs);
   w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
   w.err = c.take<unsigned>(4);
+  if (bwd && skip_inactive()) {
+    const int64_t nb = (n + COMPACT_BLOCK - 1) / COMPACT_BLOCK;
+    w.idx = c.take<int32_t>((size_t)n);
+    w.block_counts = c.take<int32_t>((size_t)nb);
+    w.block_offsets = c.take<int32_t>((size_t)nb);
+    w.n_active = c.take<int32_t>(4);
+    w.hid_act = c.take<__nv_bfloat16>((size_t)n * s->hidden);
+    w.tok_act = c.take<int32_t>((size_t)n);
+    w.lse_act = c.take<float>((size_t)n);
+    w.coeff_act = c.take<float>((size_t)n);
+  }
   w.dz = c.take<__nv_bfloat16>((size_t)chunk * (size_t)s->vocab);
   w.chunk = chunk;
   w.bytes = align_up(c.off, 256);
@@ -404,7 +452,7 @@ int64_t fwd_part_bytes(const icepop_shape* s) {
 // K3 for `rows` rows of hidden starting at h (tokens/lse/coeff already offset).
 int launch_dz(const icepop_shape* shape, double temperature, const void* h, const void* weight,
               const int32_t* tokens, const float* lse, const float* coeff, double grad_scale,
-              __nv_bfloat16* dz, int64_t ldz, int64_t rows, cudaStream_t st) {
+              __nv_bfloat16* dz, int64_t ldz, int64_t rows, cudaStream_t st, Extent ext = Extent()) {
   const int64_t d = shape->hidden, V = shape->vocab;
   const bool dv = shape->weight_layout == ICEPOP_W_DV;
   EpiParams ep;
@@ -418,7 +466,8 @@ int launch_dz(const icepop_shape* shape, double temperature, const void* h, cons
   ep.dz = dz;
   ep.ldz = ldz;
   ep.vec_ok = (ldz % 8 == 0) && ((reinterpret_cast<uintptr_t>(dz) & 15u) == 0);
-  return run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, rows, V, d, ep, st);
+  ep.zero_rows_to = (int32_t)rows;
+  return run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, rows, V, d, ep, st, ext);
 }
 
 }  // namespace
@@ -459,7 +508,7 @@ int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, 
   if (max_chunk_tokens > 0) chunk = std::min<int64_t>(chunk, max_chunk_tokens);
   chunk = std::max<int64_t>(chunk, 1);
   if (fwd_bytes) *fwd_bytes = (size_t)fwd_part_bytes(shape);
-  if (bwd_bytes) *bwd_bytes = carve_bf16(shape, nullptr, chunk).bytes;
+  if (bwd_bytes) *bwd_bytes = carve_bf16(shape, nullptr, chunk, true).bytes;
   return ICEPOP_OK;
 }
 
@@ -580,38 +629,73 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     return ICEPOP_OK;
   }
   // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
+  const bool skip = skip_inactive();
   const int64_t min_rows = std::min<int64_t>(N, BM);
-  const size_t need_min = carve_bf16(shape, nullptr, min_rows).bytes;
+  const size_t need_min = carve_bf16(shape, nullptr, min_rows, true).bytes;
   if (!workspace || workspace_bytes < need_min)
     return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", need_min);
-  const size_t fixed = carve_bf16(shape, nullptr, 0).bytes;
+  const size_t fixed = carve_bf16(shape, nullptr, 0, true).bytes;
   int64_t chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
   if (chunk >= N) {
     chunk = N;
   } else {
     chunk = std::max<int64_t>(chunk / BM * BM, BM);
   }
-  while (chunk > min_rows && carve_bf16(shape, nullptr, chunk).bytes > workspace_bytes) chunk -= BM;
-  BF16Workspace w = carve_bf16(shape, workspace, chunk);
+  while (chunk > min_rows && carve_bf16(shape, nullptr, chunk, true).bytes > workspace_bytes) chunk -= BM;
+  BF16Workspace w = carve_bf16(shape, workspace, chunk, true);
   if (w.bytes > workspace_bytes) return fail(ICEPOP_EINVAL, "backward workspace carve overflow");
+
+  const void* hsrc = hidden;
+  const int32_t* tok_src = tokens;
+  const float* lse_src = lse;
+  const float* coeff_src = coeff;
+  const size_t gh_esz = grad_hidden_f32 ? 4 : 2;
+  if (skip) {
+    // compact the rows with coeff != 0 (device-side count: no host sync)
+    const int nb = (int)((N + COMPACT_BLOCK - 1) / COMPACT_BLOCK);
+    k_active_count<<<nb, COMPACT_BLOCK, 0, st>>>(coeff, N, w.block_counts);
+    k_active_scan<<<1, std::min(1024, nb), 0, st>>>(w.block_counts, nb, w.block_offsets, w.n_active);
+    k_active_scatter<<<nb, COMPACT_BLOCK, 0, st>>>(coeff, N, w.block_offsets, w.idx);
+    const int64_t d8 = d / 8;
+    const int gg = (int)std::min<int64_t>((N * d8 + 255) / 256, (int64_t)num_sms() * 16);
+    k_gather_active<<<gg, 256, 0, st>>>(w.idx, w.n_active, reinterpret_cast<const uint4*>(hidden), d8, tokens, lse,
+                                        coeff, reinterpret_cast<uint4*>(w.hid_act), w.tok_act, w.lse_act,
+                                        w.coeff_act, N);
+    ICP_CUDA(cudaGetLastError());
+    if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));
+    if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
+    hsrc = w.hid_act;
+    tok_src = w.tok_act;
+    lse_src = w.lse_act;
+    coeff_src = w.coeff_act;
+  }
 
   for (int64_t c0 = 0; c0 < N; c0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, N - c0);
-    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hidden) + c0 * d;
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hsrc) + c0 * d;
+    Extent ext_m, ext_k;
+    if (skip) {
+      ext_m.dev = w.n_active;
+      ext_m.base = (int32_t)c0;
+      ext_m.dim = 1;
+      ext_k = ext_m;
+      ext_k.dim = 2;
+    }
     // K3: recompute logits, dZ chunk (bf16)
-    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, tokens + c0, lse + c0, coeff + c0, grad_scale, w.dz, V,
-                      nc, st));
+    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, tok_src + c0, lse_src + c0, coeff_src + c0, grad_scale,
+                      w.dz, V, nc, st, ext_m));
     // K4: grad_hidden = dZ . W^T   (M = nc, N = d, K = V)
     if (grad_hidden) {
       EpiParams eh;
       memset(&eh, 0, sizeof(eh));
-      const size_t esz = grad_hidden_f32 ? 4 : 2;
-      eh.out = static_cast<uint8_t*>(grad_hidden) + (size_t)c0 * d * esz;
+      // skip mode scatters compacted row m back to token idx[c0 + m]
+      eh.out = skip ? grad_hidden : static_cast<uint8_t*>(grad_hidden) + (size_t)c0 * d * gh_esz;
+      eh.row_index = skip ? w.idx + c0 : nullptr;
       eh.ldo = d;
       eh.out_f32 = grad_hidden_f32 ? 1 : 0;
       eh.vec_ok = ((reinterpret_cast<uintptr_t>(eh.out) & 15u) == 0) && (d % 8 == 0);
       // B operand viewed [N = d, K = V]: W[d,V] is K-major, W[V,d] is MN-major
-      ICP_TRY(run_umma(EPI_STORE, w.dz, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st));
+      ICP_TRY(run_umma(EPI_STORE, w.dz, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m));
     }
     // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
     if (grad_weight) {
@@ -619,14 +703,14 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
       memset(&ew, 0, sizeof(ew));
       ew.out = grad_weight;
       ew.out_f32 = 1;
-      ew.accumulate = (accumulate || c0 > 0) ? 1 : 0;
+      ew.accumulate = (skip || accumulate || c0 > 0) ? 1 : 0;
       ew.vec_ok = ((reinterpret_cast<uintptr_t>(grad_weight) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
       if (dv) {
         ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st));
+        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st, ext_k));
       } else {
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st));
+        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st, ext_k));
       }
     }
   }
@@ -791,6 +875,11 @@ int icepop_finish(const double* stats, void* stream) {
 int icepop_set_cta_group(int32_t cta_group) {
   if (cta_group != 1 && cta_group != 2) return fail(ICEPOP_EINVAL, "cta_group must be 1 or 2");
   g_cta_group = cta_group;
+  return ICEPOP_OK;
+}
+
+int icepop_set_skip_inactive(int32_t enable) {
+  g_skip_inactive = enable ? 1 : 0;
   return ICEPOP_OK;
 }
 

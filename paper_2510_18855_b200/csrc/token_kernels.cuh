@@ -262,4 +262,100 @@ __global__ void k_finalize_stats(const double* __restrict__ block_stats, int n_b
   }
 }
 
+// ------------------------------------------------------------------ active-row compaction
+// Rows whose gradient coefficient is exactly zero (popped tokens, clip-inactive tokens,
+// zero-advantage sequences) have dZ == 0 (objective.py:250-252), so the backward GEMMs run
+// on the compacted active rows only. Order-preserving (deterministic) three-pass compaction;
+// the count stays on the device so the backward needs no host sync.
+constexpr int COMPACT_BLOCK = 1024;
+
+__global__ void __launch_bounds__(COMPACT_BLOCK) k_active_count(const float* __restrict__ coeff, int64_t n,
+                                                              int32_t* __restrict__ block_counts) {
+  __shared__ int warp_counts[COMPACT_BLOCK / 32];
+  const int64_t t = (int64_t)blockIdx.x * COMPACT_BLOCK + threadIdx.x;
+  const bool act = t < n && coeff[t] != 0.f;
+  const unsigned b = __ballot_sync(0xffffffffu, act);
+  if ((threadIdx.x & 31) == 0) warp_counts[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < COMPACT_BLOCK / 32; ++w) c += warp_counts[w];
+    block_counts[blockIdx.x] = c;
+  }
+}
+
+// Single block: exclusive scan of block counts (sequential in chunks; nb is small).
+__global__ void k_active_scan(const int32_t* __restrict__ block_counts, int nb, int32_t* __restrict__ block_offsets,
+                              int32_t* __restrict__ n_active) {
+  __shared__ int partial[1024];
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+  int s = 0;
+  for (int b = b0; b < b1; ++b) s += block_counts[b];
+  partial[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int v = partial[i];
+      partial[i] = acc;
+      acc += v;
+    }
+    *n_active = acc;
+  }
+  __syncthreads();
+  int off = partial[threadIdx.x];
+  for (int b = b0; b < b1; ++b) {
+    block_offsets[b] = off;
+    off += block_counts[b];
+  }
+}
+
+__global__ void __launch_bounds__(COMPACT_BLOCK) k_active_scatter(const float* __restrict__ coeff, int64_t n,
+                                                                const int32_t* __restrict__ block_offsets,
+                                                                int32_t* __restrict__ idx) {
+  __shared__ int warp_counts[COMPACT_BLOCK / 32];
+  const int64_t t = (int64_t)blockIdx.x * COMPACT_BLOCK + threadIdx.x;
+  const bool act = t < n && coeff[t] != 0.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, act);
+  if (lane == 0) warp_counts[warp] = __popc(b);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += warp_counts[w];
+  if (act) idx[block_offsets[blockIdx.x] + before + __popc(b & ((1u << lane) - 1u))] = (int32_t)t;
+}
+
+// Gather active rows: hid_act[i] = hid[idx[i]] (bf16 rows of d elements, d % 8 == 0) and the
+// per-row scalars; rows [n_active, rows_cap) are zero-filled up to the next multiple of 256.
+__global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_active,
+                                const uint4* __restrict__ hid, int64_t d8, const int32_t* __restrict__ tok,
+                                const float* __restrict__ lse, const float* __restrict__ coeff,
+                                uint4* __restrict__ hid_act, int32_t* __restrict__ tok_act,
+                                float* __restrict__ lse_act, float* __restrict__ coeff_act, int64_t rows_cap) {
+  const int na = *n_active;
+  const int64_t rows_r = ((int64_t)na + 255) / 256 * 256;
+  const int64_t rows = rows_cap < rows_r ? rows_cap : rows_r;
+  const int64_t total = rows * d8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d8, c = i - r * d8;
+    if (r < na) {
+      const int32_t src = idx[r];
+      hid_act[i] = hid[(int64_t)src * d8 + c];
+      if (c == 0) {
+        tok_act[r] = tok[src];
+        lse_act[r] = lse[src];
+        coeff_act[r] = coeff[src];
+      }
+    } else {
+      hid_act[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (c == 0) {
+        tok_act[r] = 0;
+        lse_act[r] = 0.f;
+        coeff_act[r] = 0.f;
+      }
+    }
+  }
+}
+
 }  // namespace icp

@@ -36,7 +36,28 @@ struct GemmShape {
   int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
   int32_t* wave_counter;  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr
+  // Device-side extent (sync-free compaction): if ext_dev, the M (ext_dim = 1) or K (ext_dim = 2)
+  // extent is clamp(*ext_dev - ext_base, 0, static extent), read at kernel start.
+  const int32_t* ext_dev;
+  int32_t ext_base;
+  int32_t ext_dim;
 };
+
+// Resolve a device-side extent into the shape every role of the kernel uses.
+__device__ __forceinline__ void resolve_extent(GemmShape& sh, int tile_m, int bn) {
+  if (!sh.ext_dev) return;
+  const int e = max(0, min(*sh.ext_dev - sh.ext_base, sh.ext_dim == 1 ? sh.M : sh.K));
+  if (sh.ext_dim == 1) {
+    sh.M = e;
+    sh.m_tiles = (e + tile_m - 1) / tile_m;
+  } else {
+    sh.K = e;
+    sh.k_blocks = (e + 63) / 64;
+    if (sh.k_blocks == 0) sh.m_tiles = 0;  // nothing to accumulate
+  }
+  (void)bn;
+  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+}
 
 __device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
   int v;
@@ -62,6 +83,8 @@ struct EpiParams {
   float coeff_scale;       // EPI_DZ: grad_scale
   __nv_bfloat16* dz;       // EPI_DZ: [M, ldz]
   int64_t ldz;
+  int32_t zero_rows_to;    // EPI_DZ: rows in [M, zero_rows_to) of the last tile are written as 0
+  const int32_t* row_index;  // EPI_STORE: output row of GEMM row m is row_index[m] (scatter), or null
 };
 
 // CG = 1: one CTA computes a 128 x BN tile (cta_group::1).
@@ -94,8 +117,9 @@ __device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& 
 template <int BN>
 __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
                                           int row, uint32_t taddr) {
-  const int m = m0 + row;
-  const bool row_ok = m < sh.M;
+  const int mm = m0 + row;
+  const bool row_ok = mm < sh.M;
+  const int m = (row_ok && ep.row_index) ? __ldg(ep.row_index + mm) : mm;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
@@ -207,10 +231,13 @@ template <int BN>
 __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
                                        int row, uint32_t taddr) {
   const int m = m0 + row;
-  const bool row_ok = m < sh.M;
-  const float lse2 = row_ok ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
-  const float cf = row_ok ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
-  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  // rows past the (device-side) extent but inside the buffer are written as zeros, so a
+  // reduction over rows (K5) never reads stale data in the last k-block
+  const bool row_ok = m < sh.M || m < ep.zero_rows_to;
+  const bool live = m < sh.M;
+  const float lse2 = live ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
+  const float cf = live ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
+  const int y = live ? __ldg(ep.targets + m) : -1;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
@@ -224,7 +251,7 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
       const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
       const float d0 = fmaf(-cf, p0, (col0 + 2 * j == y) ? cf : 0.f);
       const float d1 = fmaf(-cf, p1, (col0 + 2 * j + 1 == y) ? cf : 0.f);
-      pk[j] = pack_bf16x2(d0, d1);
+      pk[j] = live ? pack_bf16x2(d0, d1) : 0u;
     }
     __nv_bfloat16* dst = ep.dz + (int64_t)m * ep.ldz + col0;
     if (col0 + 32 <= sh.N && ep.vec_ok) {
@@ -246,8 +273,10 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmShape sh, const EpiParams ep) {
+                     const GemmShape sh_in, const EpiParams ep) {
   using Cfg = GemmCfg<BN, CG>;
+  GemmShape sh = sh_in;
+  resolve_extent(sh, Cfg::TILE_M, BN);
   constexpr int STAGES = Cfg::STAGES;
   constexpr int B_ROWS = BN / CG;  // rows of B staged by this CTA
   extern __shared__ uint8_t smem_raw[];

@@ -248,3 +248,48 @@ def test_long_cot_ragged_high_mask_rate(cuda_device):
     assert 0.02 < d.clipped_fraction < 0.10
     assert d.objective_value == pytest.approx(o["objective"], rel=1e-3)
     assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_skip_inactive_rows_matches_full_backward(cuda_device, cta_group, layout):
+    """Zero-coefficient rows (zero-advantage sequences, popped and clip-inactive tokens) are
+    compacted away in the backward; dHidden must be identical and dW equal up to fp32 order."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=8, seed=13, group=2, layout=layout, lens=[300, 170, 260, 90, 410, 333, 129, 257])
+    c["adv"] = c["adv"].copy()
+    c["adv"][[0, 1, 4, 5]] = 0.0  # two zero-variance groups
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    b = _batch(c, cuda_device)
+    f = icepop_fwd(H, W, b, cfg, layout=layout)
+    n_zero = int((f.coeff == 0).sum())
+    assert n_zero > len(c["tokens"]) // 3
+    lib = _lib.ensure_device(0)
+    res = {}
+    try:
+        for skip in (0, 1):
+            _lib.check(lib.icepop_set_skip_inactive(skip))
+            res[skip] = icepop_bwd(H, W, b, f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
+    finally:
+        _lib.check(lib.icepop_set_skip_inactive(1))
+    (gh0, gw0), (gh1, gw1) = res[0], res[1]
+    assert torch.equal(gh0, gh1)
+    assert torch.all(gh1[f.coeff == 0] == 0)
+    assert _rel(gw1.cpu().numpy(), gw0.cpu().numpy()) < 1e-5
+    o = _oracle(c)
+    assert _rel(gw1.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh1.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_skip_inactive_all_rows_inactive(cuda_device):
+    """Every coefficient zero: gradients are exactly zero (the GEMMs see an empty extent)."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=4, seed=17, group=2)
+    c["adv"] = np.zeros_like(c["adv"])
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig())
+    gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, IcePopConfig())
+    assert torch.count_nonzero(gh) == 0 and torch.count_nonzero(gw) == 0
