@@ -216,7 +216,7 @@ int env_int(const char* name, int dflt) {
 
 int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k) {
   static const int g_short = env_int("ICEPOP_GROUP_M", 16);
-  static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 16);
+  static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 8);
   (void)epi;
   (void)n_tiles;
   (void)cg;

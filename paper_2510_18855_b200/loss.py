@@ -31,8 +31,18 @@ ALGOS = {"icepop": _lib.ALGO_ICEPOP, "grpo": _lib.ALGO_GRPO, "tis": _lib.ALGO_TI
 LAYOUTS = {"dv": _lib.W_DV, "vd": _lib.W_VD}
 
 # Largest bf16 dZ chunk the backward materialises (bytes); the rest of the batch is
-# processed in further chunks with dW accumulated in place.
-DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(32 << 30)))
+# processed in further chunks with dW accumulated in place. Default: up to 96 GB, capped at
+# 60% of the device memory free at call time (one chunk at C2: 82 GB; fewer chunks means
+# fewer dW read-modify-writes and wave tails -- measured +0.3% at C2 vs 32 GB chunks).
+DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(96 * 10**9)))
+
+
+def _dz_chunk_bytes(device) -> int:
+    try:
+        free, _ = torch.cuda.mem_get_info(device)
+    except Exception:  # noqa: BLE001
+        return DZ_CHUNK_BYTES
+    return max(1, min(DZ_CHUNK_BYTES, int(0.6 * free)))
 
 
 @dataclass(frozen=True)
@@ -245,12 +255,14 @@ def icepop_fwd(
     raise ValueError(f"unsupported dtype {hidden.dtype}: use bfloat16 (tensor cores) or float64 (validation)")
 
 
-def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int) -> int:
-    """Backward workspace for a dZ chunk of at most DZ_CHUNK_BYTES."""
+def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chunk_bytes: int | None = None) -> int:
+    """Backward workspace for a dZ chunk of at most `chunk_bytes` (default DZ_CHUNK_BYTES)."""
     lib = _lib.load()
     shape = _lib.Shape(n_tokens=n_tokens, token_offset=0, hidden=hidden, vocab=vocab, n_seqs=max(n_seqs, 1),
                        n_groups=1, weight_layout=_lib.W_VD)
-    chunk = max(128, min(n_tokens, DZ_CHUNK_BYTES // (2 * vocab)) // 128 * 128)
+    cb = DZ_CHUNK_BYTES if chunk_bytes is None else chunk_bytes
+    rows = cb // (2 * vocab)
+    chunk = n_tokens if rows >= n_tokens else max(128, rows // 128 * 128)
     bwd_b = _lib._sz()
     _lib.check(lib.icepop_workspace_bytes(shape, chunk, None, bwd_b))
     return bwd_b.value
@@ -292,7 +304,8 @@ def icepop_bwd(
         gw = grad_weight if accumulate else (torch.empty(wshape, dtype=torch.float32, device=dev) if need_weight else None)
         if gw is not None and (gw.dtype != torch.float32 or tuple(gw.shape) != wshape or not gw.is_contiguous()):
             raise ValueError("grad_weight must be a contiguous float32 tensor shaped like weight")
-        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs), dtype=torch.uint8, device=dev)
+        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, _dz_chunk_bytes(dev)), dtype=torch.uint8,
+                         device=dev)
         _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), batch.tokens.data_ptr(),
                                        fwd.lse.data_ptr(), fwd.coeff.data_ptr(), float(grad_scale), _lib.ptr(gh),
                                        1 if gh_dtype == torch.float32 else 0, _lib.ptr(gw), 1 if accumulate else 0,
