@@ -246,11 +246,22 @@ def run_ours(args):
     }
     if kern:
         line["kernels_ms"] = {k: round(v["ms"], 3) for k, v in kern.items()}
-        dom = max(kern, key=lambda k: kern[k]["ms"] * kern[k]["count"])
+        # The roofline kernel is K1, the fused lm_head GEMM + online softmax of the north star
+        # (its share of the step equals each backward GEMM's); per-kernel figures follow.
+        dom = "K1_fwd_lse+K2"
         ach = kern[dom]["flop"] / (kern[dom]["ms"] / 1e3) / 1e12
+        traffic = None
+        tj = ROOT / "profiles" / "ncu_traffic.json"
+        if tj.exists():
+            t = json.loads(tj.read_text()).get(args.config, {}).get(dom)
+            traffic = t["dram_bytes_per_launch"] if t else None
         line["roofline"] = {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": pk["tflops"],
-                            "unit": "TFLOP/s", "frac": round(ach / pk["tflops"], 4), "traffic": None,
-                            "peak_kind": "burst (%s)" % pk["source"]}
+                            "unit": "TFLOP/s", "frac": round(ach / pk["tflops"], 4), "traffic": traffic,
+                            "traffic_unit": "bytes/launch (ncu dram read+write)",
+                            "flop_per_launch": kern[dom]["flop"], "peak_kind": "burst (%s)" % pk["source"],
+                            "frac_of_sustained": round(ach / pk["tflops_sustained"], 4) if pk["tflops_sustained"]
+                            else None}
+        line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()}
     if e2e:
         line["e2e"] = e2e
     if clocks:
