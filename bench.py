@@ -138,7 +138,7 @@ def build_device_inputs(cfg, meta, dev, rank):
     shape = _lib.Shape(n_tokens=N, token_offset=meta["token_offset"], hidden=d, vocab=V,
                        n_seqs=len(meta["cu"]) - 1, n_groups=len(meta["go"]) - 1, weight_layout=_lib.W_VD)
     fb = _lib._sz()
-    _lib.check(lib.icepop_workspace_bytes(shape, 0, fb, None))
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
     ws = torch.empty(fb.value, dtype=torch.uint8, device=dev)
     lp = torch.empty(N, dtype=torch.float64, device=dev)
     _lib.check(lib.icepop_logprob_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), None,
@@ -311,9 +311,9 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev):
     shape = _lib.Shape(n_tokens=nc, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs, n_groups=batch.n_groups,
                        weight_layout=_lib.W_VD)
     s = st.cuda_stream
-    timed("K3_dz", lambda: _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(),
-                                                         batch.tokens.data_ptr(), f.lse.data_ptr(),
-                                                         f.coeff.data_ptr(), -1.0, dz.data_ptr(), V, s)),
+    saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr())
+    timed("K3_dz", lambda: _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), None, saved, -1.0,
+                                                         dz.data_ptr(), V, s)),
           2.0 * nc * d * V)
     timed("K4_dhidden", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), nc, d, V,
                                                                 0, 1, 0, 0, s)), 2.0 * nc * d * V)

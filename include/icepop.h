@@ -125,11 +125,11 @@ int icepop_group_advantages(const double* rewards, const int32_t* group_offsets,
                             int32_t n_seqs, double* advantages, void* stream);
 
 /* ---- bf16 tensor-core path (production) ------------------------------------------- */
-/* hidden: [n_tokens, d] bf16 row-major. weight: bf16 in `weight_layout`.
- * Workspace sizes (bytes) for icepop_fwd_bf16 / icepop_bwd_bf16. The backward
- * materialises bf16 dZ chunks of at most `max_chunk_tokens` rows (0 = all rows);
- * passing a smaller workspace than recommended shrinks the chunk (>= 128 rows). */
-int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens,
+/* hidden: [n_tokens, d] bf16 row-major. weight (and weight_ref): bf16 in `weight_layout`.
+ * Workspace sizes (bytes) for icepop_fwd_bf16 / icepop_bwd_bf16 (with_ref: a weight_ref
+ * will be passed). The backward materialises bf16 dZ chunks of at most `max_chunk_tokens`
+ * rows (0 = all rows); a smaller workspace than recommended shrinks the chunk (>= 128 rows). */
+int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, int32_t with_ref,
                            size_t* fwd_bytes, size_t* bwd_bytes);
 
 typedef struct icepop_fwd_out {
@@ -141,13 +141,18 @@ typedef struct icepop_fwd_out {
   double* surrogate;   /* [n_tokens] s_t                (objective.py:246)               */
   float* coeff;        /* [n_tokens] dJ/dlogit scale    (objective.py:250)  (for bwd)     */
   double* stats;       /* [ICEPOP_NSTATS] this rank's partial sums                        */
+  /* KL-to-ref outputs (objective.py:254-263), written when weight_ref != NULL; may be NULL */
+  float* kl;           /* [n_tokens] kl_t = sum_v p (log p - log p_ref)                    */
+  float* lse_ref;      /* [n_tokens] log-sum-exp of z_ref = H.W_ref/T                      */
+  float* kl_w;         /* [n_tokens] w_t * gamma / T (the KL gradient's coefficient)       */
 } icepop_fwd_out;
 
 /* Forward: fused lm_head GEMM + online log-softmax/gather/entropy (tcgen05), then the
- * IcePop epilogue. Logits are never written to HBM. */
+ * IcePop epilogue. Logits are never written to HBM. With weight_ref != NULL a second B
+ * operand shares every hidden tile (dual accumulators) and kl_t enters J as -gamma*kl_t. */
 int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
-                    const void* weight, const icepop_batch* batch, const icepop_fwd_out* out,
-                    void* workspace, size_t workspace_bytes, void* stream);
+                    const void* weight, const void* weight_ref, const icepop_batch* batch,
+                    const icepop_fwd_out* out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Log-prob only (no IcePop epilogue): lse, lp = z[y]-lse, entropy. Used to record
  * lp_train_old (scheduler.py:296-311) with the same kernel. Any output may be NULL. */
@@ -155,23 +160,34 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
                         const void* weight, const int32_t* tokens, float* lse, double* lp,
                         float* entropy, void* workspace, size_t workspace_bytes, void* stream);
 
+/* What the backward reads from the forward (device pointers). */
+typedef struct icepop_saved {
+  const int32_t* tokens;  /* [n_tokens] */
+  const float* lse;       /* [n_tokens] */
+  const float* coeff;     /* [n_tokens] */
+  const float* lse_ref;   /* [n_tokens] KL gradient inputs: used when gamma > 0 and       */
+  const float* kl;        /* [n_tokens] weight_ref != NULL, else may be NULL              */
+  const float* kl_w;      /* [n_tokens]                                                   */
+} icepop_saved;
+
 /* Backward: recompute logits tile by tile, dZ = grad_scale*coeff_t*(e_y - softmax(z_t))
- * (bf16 chunk), then grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05.
+ * [- grad_scale*kl_w_t*p*(log p - log p_ref - kl_t) when gamma > 0] (bf16 chunk), then
+ * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05.
  * grad_hidden: [n_tokens, d], bf16 if grad_hidden_f32 == 0 else f32; may be NULL.
  * grad_weight: f32 in the weight's layout; accumulate != 0 adds into it; may be NULL. */
 int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
-                    const void* weight, const int32_t* tokens, const float* lse,
-                    const float* coeff, double grad_scale, void* grad_hidden,
-                    int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate,
-                    void* workspace, size_t workspace_bytes, void* stream);
+                    const void* weight, const void* weight_ref, const icepop_saved* saved,
+                    double grad_scale, void* grad_hidden, int32_t grad_hidden_f32,
+                    float* grad_weight, int32_t accumulate, void* workspace, size_t workspace_bytes,
+                    void* stream);
 
 /* K3 alone: dZ[t, v] = grad_scale * coeff_t * (e_{y_t} - softmax(z_t))_v for the
  * shape->n_tokens rows of `hidden`, written as bf16 to dz[t * ldz + v]. The building
  * block icepop_bwd_bf16 chains with K4/K5 (icepop_gemm_bf16); exposed so callers can
  * interleave V-slab dW reductions with it. */
 int icepop_dz_bf16(const icepop_shape* shape, double temperature, const void* hidden,
-                   const void* weight, const int32_t* tokens, const float* lse,
-                   const float* coeff, double grad_scale, void* dz, int64_t ldz, void* stream);
+                   const void* weight, const void* weight_ref, const icepop_saved* saved,
+                   double grad_scale, void* dz, int64_t ldz, void* stream);
 
 /* ---- fp64 SIMT validation path ----------------------------------------------------- */
 /* Same semantics in fp64 on CUDA cores (still CUDA, no CPU fallback), so the

@@ -78,6 +78,20 @@ class FwdOut(ctypes.Structure):
         ("surrogate", _c_p),
         ("coeff", _c_p),
         ("stats", _c_p),
+        ("kl", _c_p),
+        ("lse_ref", _c_p),
+        ("kl_w", _c_p),
+    ]
+
+
+class Saved(ctypes.Structure):
+    _fields_ = [
+        ("tokens", _c_p),
+        ("lse", _c_p),
+        ("coeff", _c_p),
+        ("lse_ref", _c_p),
+        ("kl", _c_p),
+        ("kl_w", _c_p),
     ]
 
 
@@ -103,10 +117,10 @@ SIGNATURES: dict[str, tuple] = {
     "icepop_last_error": (ctypes.c_char_p, []),
     "icepop_device_check": (ctypes.c_int, [ctypes.c_int]),
     "icepop_group_advantages": (ctypes.c_int, [_c_p, _c_p, _i32, _i32, _c_p, _c_p]),
-    "icepop_workspace_bytes": (ctypes.c_int, [_P(Shape), _i64, _P(_sz), _P(_sz)]),
+    "icepop_workspace_bytes": (ctypes.c_int, [_P(Shape), _i64, _i32, _P(_sz), _P(_sz)]),
     "icepop_fwd_bf16": (
         ctypes.c_int,
-        [_P(Shape), _P(Config), _c_p, _c_p, _P(Batch), _P(FwdOut), _c_p, _sz, _c_p],
+        [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Batch), _P(FwdOut), _c_p, _sz, _c_p],
     ),
     "icepop_logprob_bf16": (
         ctypes.c_int,
@@ -114,9 +128,9 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "icepop_bwd_bf16": (
         ctypes.c_int,
-        [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _c_p, _c_p, _f64, _c_p, _i32, _c_p, _i32, _c_p, _sz, _c_p],
+        [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i32, _c_p, _i32, _c_p, _sz, _c_p],
     ),
-    "icepop_dz_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _f64, _c_p, _i64, _c_p]),
+    "icepop_dz_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i64, _c_p]),
     "icepop_workspace_bytes_f64": (ctypes.c_int, [_P(Shape), _i32, _P(_sz)]),
     "icepop_fwd_f64": (
         ctypes.c_int,

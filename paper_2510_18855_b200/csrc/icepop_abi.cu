@@ -171,11 +171,11 @@ int cta_group() {
   return g_cta_group;
 }
 
-template <bool A_MN, bool B_MN, int EPI, int CG>
-int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
-                   cudaStream_t st) {
-  auto kern = umma_gemm_kernel<BN_, A_MN, B_MN, EPI, CG>;
-  constexpr size_t smem = GemmCfg<BN_, CG>::SMEM;
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const GemmShape& sh,
+                   const EpiParams& ep, cudaStream_t st) {
+  auto kern = umma_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
+  constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI)>::SMEM;
   static bool attr_done = false;
   if (!attr_done) {
     ICP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -195,15 +195,16 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, sh, ep));
+  ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tb2, sh, ep));
   return ICEPOP_OK;
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const GemmShape& sh, const EpiParams& ep,
-                cudaStream_t st, int cg) {
-  if (cg == 2) return launch_umma_cg<A_MN, B_MN, EPI, 2>(ta, tb, sh, ep, st);
-  return launch_umma_cg<A_MN, B_MN, EPI, 1>(ta, tb, sh, ep, st);
+int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const GemmShape& sh,
+                const EpiParams& ep, cudaStream_t st, int cg) {
+  constexpr int BN = epi_dual(EPI) ? 128 : BN_;
+  if (cg == 2) return launch_umma_cg<BN, A_MN, B_MN, EPI, 2>(ta, tb, tb2, sh, ep, st);
+  return launch_umma_cg<BN, A_MN, B_MN, EPI, 1>(ta, tb, tb2, sh, ep, st);
 }
 
 // Tile raster: `group_m` m-tiles sweep the n dimension together. ICEPOP_GROUP_M overrides
@@ -231,21 +232,29 @@ struct Extent {
   int32_t dim = 0;  // 1: M, 2: K
 };
 
+// BN of a GEMM with epilogue `epi` (the dual-accumulator KL variants use 128-column tiles).
+inline int bn_of(int epi) { return epi_dual(epi) ? 128 : BN_; }
+
 int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
-             int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent()) {
+             int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent(),
+             const void* B2 = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
   const int cg = cta_group();
-  CUtensorMap ta, tb;
+  const int bn = bn_of(epi);
+  if (epi_dual(epi) && !B2) return fail(ICEPOP_EINVAL, "dual-accumulator GEMM needs a second B operand");
+  CUtensorMap ta, tb, tb2;
   ICP_TRY(operand_map(&ta, A, M, K, lda, a_mn, BM));
-  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, BN_ / cg));
+  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, bn / cg));
+  if (B2) ICP_TRY(operand_map(&tb2, B2, N, K, ldb, b_mn, bn / cg));
+  else tb2 = tb;
   GemmShape sh;
   sh.M = (int)M;
   sh.N = (int)N;
   sh.K = (int)K;
   sh.m_tiles = (int)((M + BM * cg - 1) / (BM * cg));
-  sh.n_tiles = (int)((N + BN_ - 1) / BN_);
+  sh.n_tiles = (int)((N + bn - 1) / bn);
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
@@ -263,18 +272,28 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
     ICP_TRY(tile_counter(st, &sh.tile_counter));
   }
   if (epi == EPI_STORE) {
-    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
-    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, sh, ep, st, cg);
-    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, sh, ep, st, cg);
-    return launch_umma<true, true, EPI_STORE>(ta, tb, sh, ep, st, cg);
+    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
+    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
+    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
+    return launch_umma<true, true, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
   }
   if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
-  if (epi == EPI_LSE) {
-    if (!b_mn) return launch_umma<false, false, EPI_LSE>(ta, tb, sh, ep, st, cg);
-    return launch_umma<false, true, EPI_LSE>(ta, tb, sh, ep, st, cg);
+  switch (epi) {
+    case EPI_LSE:
+      return b_mn ? launch_umma<false, true, EPI_LSE>(ta, tb, tb2, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_LSE>(ta, tb, tb2, sh, ep, st, cg);
+    case EPI_DZ:
+      return b_mn ? launch_umma<false, true, EPI_DZ>(ta, tb, tb2, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_DZ>(ta, tb, tb2, sh, ep, st, cg);
+    case EPI_LSE_REF:
+      return b_mn ? launch_umma<false, true, EPI_LSE_REF>(ta, tb, tb2, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_LSE_REF>(ta, tb, tb2, sh, ep, st, cg);
+    case EPI_DZ_REF:
+      return b_mn ? launch_umma<false, true, EPI_DZ_REF>(ta, tb, tb2, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_DZ_REF>(ta, tb, tb2, sh, ep, st, cg);
+    default:
+      return fail(ICEPOP_EINVAL, "unknown epilogue %d", epi);
   }
-  if (!b_mn) return launch_umma<false, false, EPI_DZ>(ta, tb, sh, ep, st, cg);
-  return launch_umma<false, true, EPI_DZ>(ta, tb, sh, ep, st, cg);
 }
 
 // ------------------------------------------------------------------ validation helpers
@@ -415,14 +434,15 @@ bool skip_inactive() {
 }
 
 // Forward part (partials, stats) is always carved; `bwd` adds the compaction buffers and
-// `chunk` rows of bf16 dZ.
-BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool bwd = false) {
+// `chunk` rows of bf16 dZ. `ref`: KL-to-ref partials (6 rows per 128-column vocab tile).
+BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool bwd = false, bool ref = false) {
   Carver c(base);
   BF16Workspace w;
   memset(&w, 0, sizeof(w));
   const int64_t n = std::max<int64_t>(s->n_tokens, 1);
-  const int64_t n_tiles = (s->vocab + BN_ - 1) / BN_;
-  w.part = c.take<float>((size_t)n_tiles * 3 * n);
+  const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
+  const int64_t n_tiles = (s->vocab + bn - 1) / bn;
+  w.part = c.take<float>((size_t)n_tiles * (ref ? 6 : 3) * n);
   w.ztok = c.take<float>((size_t)n);
   w.adv = c.take<double>((size_t)s->n_seqs);
   w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
@@ -444,30 +464,47 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   return w;
 }
 
-int64_t fwd_part_bytes(const icepop_shape* s) {
-  BF16Workspace w = carve_bf16(s, nullptr, 0);
+int64_t fwd_part_bytes(const icepop_shape* s, bool ref) {
+  BF16Workspace w = carve_bf16(s, nullptr, 0, false, ref);
   return (int64_t)w.bytes;
 }
 
-// K3 for `rows` rows of hidden starting at h (tokens/lse/coeff already offset).
+// K3 for `rows` rows of hidden starting at h (saved-tensor pointers already offset). With
+// `weight_ref` and saved->kl set it is the dual-accumulator KL variant (gamma > 0).
 int launch_dz(const icepop_shape* shape, double temperature, const void* h, const void* weight,
-              const int32_t* tokens, const float* lse, const float* coeff, double grad_scale,
-              __nv_bfloat16* dz, int64_t ldz, int64_t rows, cudaStream_t st, Extent ext = Extent()) {
+              const void* weight_ref, const icepop_saved& sv, double grad_scale, __nv_bfloat16* dz, int64_t ldz,
+              int64_t rows, cudaStream_t st, Extent ext = Extent()) {
   const int64_t d = shape->hidden, V = shape->vocab;
   const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  const bool ref = weight_ref && sv.kl && sv.lse_ref && sv.kl_w;
   EpiParams ep;
   memset(&ep, 0, sizeof(ep));
   ep.scale_log2 = (float)(1.4426950408889634 / temperature);
   ep.inv_t = (float)(1.0 / temperature);
-  ep.targets = tokens;
-  ep.lse = lse;
-  ep.coeff = coeff;
+  ep.targets = sv.tokens;
+  ep.lse = sv.lse;
+  ep.coeff = sv.coeff;
+  ep.lse_ref = sv.lse_ref;
+  ep.kl = sv.kl;
+  ep.kl_w = sv.kl_w;
   ep.coeff_scale = (float)grad_scale;
   ep.dz = dz;
   ep.ldz = ldz;
   ep.vec_ok = (ldz % 8 == 0) && ((reinterpret_cast<uintptr_t>(dz) & 15u) == 0);
   ep.zero_rows_to = (int32_t)rows;
-  return run_umma(EPI_DZ, h, d, false, weight, dv ? V : d, dv, rows, V, d, ep, st, ext);
+  return run_umma(ref ? EPI_DZ_REF : EPI_DZ, h, d, false, weight, dv ? V : d, dv, rows, V, d, ep, st, ext,
+                  ref ? weight_ref : nullptr);
+}
+
+icepop_saved offset_saved(const icepop_saved& s, int64_t o) {
+  icepop_saved r = s;
+  r.tokens = s.tokens + o;
+  r.lse = s.lse + o;
+  r.coeff = s.coeff + o;
+  if (s.lse_ref) r.lse_ref = s.lse_ref + o;
+  if (s.kl) r.kl = s.kl + o;
+  if (s.kl_w) r.kl_w = s.kl_w + o;
+  return r;
 }
 
 }  // namespace
@@ -501,31 +538,26 @@ int icepop_group_advantages(const double* rewards, const int32_t* group_offsets,
   return ICEPOP_OK;
 }
 
-int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, size_t* fwd_bytes,
-                           size_t* bwd_bytes) {
+int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, int32_t with_ref,
+                           size_t* fwd_bytes, size_t* bwd_bytes) {
   ICP_TRY(check_shape(shape, true));
   int64_t chunk = shape->n_tokens;
   if (max_chunk_tokens > 0) chunk = std::min<int64_t>(chunk, max_chunk_tokens);
   chunk = std::max<int64_t>(chunk, 1);
-  if (fwd_bytes) *fwd_bytes = (size_t)fwd_part_bytes(shape);
+  if (fwd_bytes) *fwd_bytes = (size_t)fwd_part_bytes(shape, with_ref != 0);
   if (bwd_bytes) *bwd_bytes = carve_bf16(shape, nullptr, chunk, true).bytes;
   return ICEPOP_OK;
 }
 
-int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
-                        const int32_t* tokens, float* lse, double* lp, float* entropy, void* workspace,
-                        size_t workspace_bytes, void* stream);
-
 int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
-                    const icepop_batch* batch, const icepop_fwd_out* out, void* workspace, size_t workspace_bytes,
-                    void* stream) {
+                    const void* weight_ref, const icepop_batch* batch, const icepop_fwd_out* out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
   ICP_TRY(check_shape(shape, true));
   ICP_TRY(check_config(cfg));
   if (!batch || !out || !out->stats) return fail(ICEPOP_EINVAL, "null batch/out/stats");
-  if (cfg->kl_coeff > 0.0)
-    return fail(ICEPOP_EINVAL, "kl_coeff > 0 is only available in the fp64 path in this build");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  BF16Workspace w = carve_bf16(shape, workspace, 0);
+  const bool ref = weight_ref != nullptr;
+  BF16Workspace w = carve_bf16(shape, workspace, 0, false, ref);
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
@@ -544,13 +576,20 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     ep.part = w.part;
     ep.ztok = w.ztok;
     const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
-    ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
+    ICP_TRY(run_umma(ref ? EPI_LSE_REF : EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st,
+                     Extent(), ref ? weight_ref : nullptr));
   }
   // K2: merge + IcePop epilogue
   TokenArgs a;
   fill_token_args(a, shape, cfg, batch, adv);
+  if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
   a.part = w.part;
-  a.n_parts = (int32_t)((V + BN_ - 1) / BN_);
+  const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
+  a.n_parts = (int32_t)((V + bn - 1) / bn);
+  a.part_rows = ref ? 6 : 3;
+  a.kl_f = ref ? out->kl : nullptr;
+  a.lse_ref_f = ref ? out->lse_ref : nullptr;
+  a.kl_w_f = ref ? out->kl_w : nullptr;
   a.ztok = w.ztok;
   a.lse_f = out->lse;
   a.lp_cur = out->lp_cur;
@@ -595,7 +634,7 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   ICP_TRY(check_shape(shape, true));
   if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  BF16Workspace w = carve_bf16(shape, workspace, 0);
+  BF16Workspace w = carve_bf16(shape, workspace, 0, false, false);
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ICEPOP_EINVAL, "workspace too small: need %zu bytes", w.bytes);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
@@ -616,11 +655,21 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
 }
 
 int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
-                    const int32_t* tokens, const float* lse, const float* coeff, double grad_scale, void* grad_hidden,
+                    const void* weight_ref, const icepop_saved* saved, double grad_scale, void* grad_hidden,
                     int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate, void* workspace,
                     size_t workspace_bytes, void* stream) {
   ICP_TRY(check_shape(shape, true));
   ICP_TRY(check_config(cfg));
+  if (!saved || !saved->tokens || !saved->lse || !saved->coeff) return fail(ICEPOP_EINVAL, "null saved tensors");
+  // the KL term only enters the gradient when gamma > 0 (objective.py:259)
+  const bool kl_grad = weight_ref && cfg->kl_coeff > 0.0;
+  if (kl_grad && (!saved->kl || !saved->lse_ref || !saved->kl_w))
+    return fail(ICEPOP_EINVAL, "the KL gradient needs saved kl, lse_ref and kl_w");
+  icepop_saved sv = *saved;
+  if (!kl_grad) sv.kl = sv.lse_ref = sv.kl_w = nullptr;
+  const int32_t* tokens = sv.tokens;
+  const float* lse = sv.lse;
+  const float* coeff = sv.coeff;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
   const bool dv = shape->weight_layout == ICEPOP_W_DV;
@@ -629,7 +678,7 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     return ICEPOP_OK;
   }
   // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
-  const bool skip = skip_inactive();
+  const bool skip = skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
   const int64_t min_rows = std::min<int64_t>(N, BM);
   const size_t need_min = carve_bf16(shape, nullptr, min_rows, true).bytes;
   if (!workspace || workspace_bytes < need_min)
@@ -682,8 +731,14 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
       ext_k.dim = 2;
     }
     // K3: recompute logits, dZ chunk (bf16)
-    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, tok_src + c0, lse_src + c0, coeff_src + c0, grad_scale,
-                      w.dz, V, nc, st, ext_m));
+    icepop_saved cs = offset_saved(sv, c0);
+    if (skip) {
+      cs.tokens = tok_src + c0;
+      cs.lse = lse_src + c0;
+      cs.coeff = coeff_src + c0;
+    }
+    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V, nc,
+                      st, ext_m));
     // K4: grad_hidden = dZ . W^T   (M = nc, N = d, K = V)
     if (grad_hidden) {
       EpiParams eh;
@@ -718,13 +773,14 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
 }
 
 int icepop_dz_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
-                   const int32_t* tokens, const float* lse, const float* coeff, double grad_scale, void* dz,
-                   int64_t ldz, void* stream) {
+                   const void* weight_ref, const icepop_saved* saved, double grad_scale, void* dz, int64_t ldz,
+                   void* stream) {
   ICP_TRY(check_shape(shape, true));
   if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
-  if (!hidden || !weight || !tokens || !lse || !coeff || !dz) return fail(ICEPOP_EINVAL, "null argument");
+  if (!hidden || !weight || !saved || !saved->tokens || !saved->lse || !saved->coeff || !dz)
+    return fail(ICEPOP_EINVAL, "null argument");
   if (ldz < shape->vocab) return fail(ICEPOP_EINVAL, "ldz must be >= vocab");
-  return launch_dz(shape, temperature, hidden, weight, tokens, lse, coeff, grad_scale,
+  return launch_dz(shape, temperature, hidden, weight, weight_ref, *saved, grad_scale,
                    static_cast<__nv_bfloat16*>(dz), ldz, shape->n_tokens, static_cast<cudaStream_t>(stream));
 }
 

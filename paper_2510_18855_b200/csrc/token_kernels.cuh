@@ -81,8 +81,9 @@ struct TokenArgs {
   const int32_t* group_offsets;
   const double* adv;
   // bf16 mode inputs: K1 partials
-  const float* part;  // [n_parts][3][n_tokens]
+  const float* part;  // [n_parts][part_rows][n_tokens]
   int32_t n_parts;
+  int32_t part_rows;  // 3, or 6 with the KL-to-ref terms (epi_lse_ref)
   const float* ztok;  // [n_tokens]
   // f64 mode inputs (already computed per token by the f64 row kernel)
   const double* lp_cur_in;
@@ -100,6 +101,9 @@ struct TokenArgs {
   double* surrogate;
   float* coeff_f;
   double* coeff_d;
+  float* kl_f;       // KL-to-ref outputs (part_rows == 6)
+  float* lse_ref_f;
+  float* kl_w_f;     // w_t * gamma / T (backward coefficient of the KL gradient)
   double* block_stats;  // [gridDim.x][ICEPOP_NSTATS] (required)
 };
 
@@ -165,15 +169,24 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     double lp_cur, ent, kl = 0.0;
     if (MODE == 0) {
       // merge split-V partials (log2 units) -> lse, entropy; lp = z[y] - lse
-      float M = -1e30f;
-      for (int j = 0; j < a.n_parts; ++j) M = fmaxf(M, a.part[(int64_t)j * 3 * a.n_tokens + t]);
-      float S = 0.f, Q = 0.f;
+      const int64_t R = a.part_rows;
+      float M = -1e30f, Mr = -1e30f;
       for (int j = 0; j < a.n_parts; ++j) {
-        const float* p = a.part + (int64_t)j * 3 * a.n_tokens + t;
+        const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
+        M = fmaxf(M, p[0]);
+        if (R == 6) Mr = fmaxf(Mr, p[3 * a.n_tokens]);
+      }
+      float S = 0.f, Q = 0.f, Sr = 0.f, X = 0.f;
+      for (int j = 0; j < a.n_parts; ++j) {
+        const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
         const float mj = p[0], sj = p[a.n_tokens], qj = p[2 * a.n_tokens];
         const float sc = exp2f(mj - M);
         S = fmaf(sj, sc, S);
         Q = fmaf(sc, fmaf(mj - M, sj, qj), Q);
+        if (R == 6) {
+          Sr = fmaf(p[4 * a.n_tokens], exp2f(p[3 * a.n_tokens] - Mr), Sr);
+          X = fmaf(p[5 * a.n_tokens], sc, X);
+        }
       }
       const float l2s = log2f(S);
       const float lse = (M + l2s) * LN2_F;
@@ -183,6 +196,15 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
       if (a.lse_f) a.lse_f[t] = lse;
       if (a.entropy_f) a.entropy_f[t] = entf;
       if (!isfinite(lse) || !isfinite(entf) || !isfinite(a.ztok[t])) err |= ICEPOP_ERR_NONFINITE;
+      if (R == 6) {
+        // kl = sum_v p (logp - logp_ref) = sum_v p (z - z_ref) - lse + lse_ref  (objective.py:257-258)
+        const float lse_r = (Mr + log2f(Sr)) * LN2_F;
+        const float klf = (X / S) * LN2_F - lse + lse_r;
+        kl = (double)klf;
+        if (a.kl_f) a.kl_f[t] = klf;
+        if (a.lse_ref_f) a.lse_ref_f[t] = lse_r;
+        if (!isfinite(klf)) err |= ICEPOP_ERR_NONFINITE;
+      }
     } else {
       lp_cur = a.lp_cur_in[t];
       ent = a.entropy_in[t];
@@ -226,6 +248,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     if (a.surrogate) a.surrogate[t] = pg;
     if (a.coeff_f) a.coeff_f[t] = (float)coeff;
     if (a.coeff_d) a.coeff_d[t] = coeff;
+    if (a.kl_w_f) a.kl_w_f[t] = (float)(w * a.kl_coeff / a.temperature);
 
     st[ICEPOP_STAT_OBJECTIVE] += w * value;
     st[ICEPOP_STAT_N_POPPED] += kept ? 0.0 : 1.0;

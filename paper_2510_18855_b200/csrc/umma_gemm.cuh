@@ -27,7 +27,11 @@ constexpr int BK = 64;
 constexpr int GEMM_THREADS = 192;
 constexpr float LOG2E_F = 1.4426950408889634f;
 
-enum EpiKind { EPI_STORE = 0, EPI_LSE = 1, EPI_DZ = 2 };
+// EPI_LSE_REF / EPI_DZ_REF are the KL-to-ref variants (objective.py:254-263): a second B
+// operand (W_ref) shares every A (hidden) tile and accumulates into a second TMEM accumulator.
+enum EpiKind { EPI_STORE = 0, EPI_LSE = 1, EPI_DZ = 2, EPI_LSE_REF = 3, EPI_DZ_REF = 4 };
+
+__host__ __device__ constexpr bool epi_dual(int epi) { return epi == EPI_LSE_REF || epi == EPI_DZ_REF; }
 
 struct GemmShape {
   int32_t M, N, K;
@@ -85,19 +89,25 @@ struct EpiParams {
   int64_t ldz;
   int32_t zero_rows_to;    // EPI_DZ: rows in [M, zero_rows_to) of the last tile are written as 0
   const int32_t* row_index;  // EPI_STORE: output row of GEMM row m is row_index[m] (scatter), or null
+  // EPI_DZ_REF
+  const float* lse_ref;    // [M] natural units
+  const float* kl;         // [M] kl_t
+  const float* kl_w;       // [M] w_t * gamma / T
 };
 
 // CG = 1: one CTA computes a 128 x BN tile (cta_group::1).
 // CG = 2: a CTA pair computes a 256 x BN tile with cta_group::2 MMAs issued by the leader;
 //         each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so the B operand
 //         is read from L2 once per pair instead of once per CTA.
-template <int BN, int CG>
+template <int BN, int CG, bool DUAL = false>
 struct GemmCfg {
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr int B2_BYTES = DUAL ? B_BYTES : 0;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + B2_BYTES;
+  static constexpr int STAGES = (220 * 1024 / STAGE_BYTES) < 6 ? (220 * 1024 / STAGE_BYTES) : 6;
+  static constexpr int NACC = DUAL ? 2 : 1;              // accumulators per tile
+  static constexpr int TMEM_COLS = 2 * BN * NACC;        // double-buffered
   static constexpr int TILE_M = BM * CG;
   static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
   static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
@@ -269,12 +279,134 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
   }
 }
 
+// KL-to-ref forward epilogue: as epi_lse for z (accumulator 0) plus, for z_ref (accumulator
+// 1 = TMEM column + BN), the ref online (max, sum) and the cross term
+// x = sum_j 2^(u_j - mx) (u_j - ur_j), u = z log2(e): after the merge,
+// sum_v p_v (z_v - zr_v) = ln2 * X / S and kl = that - lse + lse_ref (objective.py:257-258).
+template <int BN>
+__device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
+                                            int n_blk, int row, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool row_ok = m < sh.M;
+  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_x = 0.f;
+  float ref_m = -1e30f, ref_s = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32], w[32];
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld32(taddr + BN + c * 32, w);
+    const int col0 = n0 + c * 32;
+    if (col0 >= sh.N) continue;  // warp-uniform
+    const int rel = y - col0;
+    if ((unsigned)rel < 32u) {
+      float zt = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) zt = (j == rel) ? v[j] : zt;
+      if (row_ok) ep.ztok[m] = zt * ep.inv_t;
+    }
+    float cm = -1e30f, cr = -1e30f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const bool ok = col0 + j < sh.N;
+      v[j] = ok ? v[j] * ep.scale_log2 : -1e30f;
+      w[j] = ok ? w[j] * ep.scale_log2 : -1e30f;
+      cm = fmaxf(cm, v[j]);
+      cr = fmaxf(cr, w[j]);
+    }
+    const float nm = fmaxf(run_m, cm);
+    const float a = fast_exp2(run_m - nm);
+    run_q = a * (run_q + (run_m - nm) * run_s);
+    run_s = a * run_s;
+    run_x = a * run_x;
+    const float nr = fmaxf(ref_m, cr);
+    ref_s *= fast_exp2(ref_m - nr);
+    float s = 0.f, q = 0.f, x = 0.f, sr = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float d = v[j] - nm;
+      const float e = fast_exp2(d);
+      s += e;
+      q = fmaf(e, d, q);
+      x = fmaf(e, v[j] - w[j], x);
+      sr += fast_exp2(w[j] - nr);
+    }
+    run_s += s;
+    run_q += q;
+    run_x += x;
+    run_m = nm;
+    ref_s += sr;
+    ref_m = nr;
+  }
+  if (row_ok) {
+    float* p = ep.part + (int64_t)n_blk * 6 * sh.M + m;
+    p[0] = run_m;
+    p[sh.M] = run_s;
+    p[2 * (int64_t)sh.M] = run_q;
+    p[3 * (int64_t)sh.M] = ref_m;
+    p[4 * (int64_t)sh.M] = ref_s;
+    p[5 * (int64_t)sh.M] = run_x;
+  }
+}
+
+// KL-to-ref backward epilogue (gamma > 0), objective.py:250-263:
+//   dZ = s * [ c (e_y - p) - kw * p * ((logp - logp_ref) - kl) ],  kw = w gamma / T.
+template <int BN>
+__device__ __forceinline__ void epi_dz_ref(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
+                                           int row, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool row_ok = m < sh.M;
+  const float lse2 = row_ok ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
+  const float lser2 = row_ok ? __ldg(ep.lse_ref + m) * LOG2E_F : 0.f;
+  const float cf = row_ok ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
+  const float kw = row_ok ? __ldg(ep.kl_w + m) * ep.coeff_scale : 0.f;
+  const float kl = row_ok ? __ldg(ep.kl + m) : 0.f;
+  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  constexpr float LN2 = 0.69314718055994531f;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32], w[32];
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld32(taddr + BN + c * 32, w);
+    const int col0 = n0 + c * 32;
+    if (!row_ok || col0 >= sh.N) continue;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float d[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float lp2 = fmaf(v[2 * j + h], ep.scale_log2, -lse2);    // log2 p
+        const float lpr2 = fmaf(w[2 * j + h], ep.scale_log2, -lser2);  // log2 p_ref
+        const float p = fast_exp2(lp2);
+        const float diff = (lp2 - lpr2) * LN2 - kl;
+        d[h] = fmaf(-cf, p, (col0 + 2 * j + h == y) ? cf : 0.f) - kw * p * diff;
+      }
+      pk[j] = pack_bf16x2(d[0], d[1]);
+    }
+    __nv_bfloat16* dst = ep.dz + (int64_t)m * ep.ldz + col0;
+    if (col0 + 32 <= sh.N && ep.vec_ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        reinterpret_cast<uint4*>(dst)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const __nv_bfloat162 hh = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+        if (col0 + 2 * j < sh.N) dst[2 * j] = hh.x;
+        if (col0 + 2 * j + 1 < sh.N) dst[2 * j + 1] = hh.y;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ mainloop
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmShape sh_in, const EpiParams ep) {
-  using Cfg = GemmCfg<BN, CG>;
+                     const __grid_constant__ CUtensorMap tmB2, const GemmShape sh_in, const EpiParams ep) {
+  constexpr bool DUAL = epi_dual(EPI);
+  using Cfg = GemmCfg<BN, CG, DUAL>;
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
   constexpr int STAGES = Cfg::STAGES;
@@ -284,6 +416,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sB2 = sB + STAGES * Cfg::B_BYTES;  // DUAL only
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   // barrier block: full[S] empty[S] tfull[2] tempty[2] rfull[RING] | tmem_holder | ring[RING]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::RING);
@@ -309,6 +442,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (DUAL) prefetch_tmap(&tmB2);
     for (int s = 0; s < STAGES; ++s) {
       // Only the pair leader arrives (with expect_tx covering BOTH CTAs' TMA bytes); the peer's
       // loads just complete_tx on it. A per-k-block remote arrive from the peer would cost a
@@ -387,6 +521,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t fb_local = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint32_t b2_dst = smem_u32(sB2 + stage * Cfg::B_BYTES);
+          (void)b2_dst;
           if (CG == 1) {
             mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
             if (!A_MN) {
@@ -397,9 +533,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             if (!B_MN) {
               tma_load_2d(b_dst, &tmB, fb_local, kb * BK, n0);
+              if (DUAL) tma_load_2d(b2_dst, &tmB2, fb_local, kb * BK, n0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kb * BK);
+              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
+                tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kb * BK);
+                if (DUAL) tma_load_2d(b2_dst + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kb * BK);
+              }
             }
           } else {
             const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
@@ -412,9 +552,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             if (!B_MN) {
               tma_load_2d_cg2(b_dst, &tmB, fb, kb * BK, n0);
+              if (DUAL) tma_load_2d_cg2(b2_dst, &tmB2, fb, kb * BK, n0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kb * BK);
+              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
+                tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kb * BK);
+                if (DUAL) tma_load_2d_cg2(b2_dst + j2 * (BK * 128), &tmB2, fb, n0 + 64 * j2, kb * BK);
+              }
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -459,20 +603,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           publish(j + 2, nxt2);
           claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
         }
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BN * Cfg::NACC;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint32_t b2_base = smem_u32(sB2 + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
                                      : sdesc_sw128(a_base + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
                                      : sdesc_sw128(b_base + kk * 32, 16, 1024);
-            if (CG == 2) umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-            else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+            if (CG == 2) umma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
+            else umma_bf16(d_tmem, ad, bd, idesc, accum);
+            if (DUAL) {
+              const uint64_t bd2 = B_MN ? sdesc_sw128(b2_base + kk * 2048, BK * 128, 1024)
+                                        : sdesc_sw128(b2_base + kk * 32, 16, 1024);
+              if (CG == 2) umma_bf16_cg2(d_tmem + BN, ad, bd2, idesc, accum);
+              else umma_bf16(d_tmem + BN, ad, bd2, idesc, accum);
+            }
           }
           // frees the smem slot (in both CTAs) when these MMAs finish
           if (CG == 2) umma_commit_cg2(empty0 + 8 * stage, 0x3); else umma_commit(empty0 + 8 * stage);
@@ -503,10 +655,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
       if (EPI == EPI_DZ) epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      if (EPI == EPI_LSE_REF) epi_lse_ref<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
+      if (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

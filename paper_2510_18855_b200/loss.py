@@ -200,13 +200,21 @@ def icepop_fwd(
     if hidden.dtype == torch.bfloat16:
         if weight.dtype != torch.bfloat16:
             raise ValueError("bf16 hidden needs a bf16 weight")
+        wr = None
         if weight_ref is not None:
-            raise ValueError("weight_ref (KL-to-ref) is only available in the fp64 path in this build")
+            wr = weight_ref.contiguous()
+            if wr.shape != weight.shape or wr.dtype != torch.bfloat16:
+                raise ValueError("weight_ref must match weight's shape and dtype")
         lse = torch.empty(n, dtype=torch.float32, device=dev)
         entropy = torch.empty(n, dtype=torch.float32, device=dev)
         coeff = torch.empty(n, dtype=torch.float32, device=dev)
+        kl = lse_ref = kl_w = None
+        if wr is not None:
+            kl = torch.empty(n, dtype=torch.float32, device=dev)
+            lse_ref = torch.empty(n, dtype=torch.float32, device=dev)
+            kl_w = torch.empty(n, dtype=torch.float32, device=dev)
         fwd_b = _lib._sz()
-        _lib.check(lib.icepop_workspace_bytes(shape, 0, fwd_b, None))
+        _lib.check(lib.icepop_workspace_bytes(shape, 0, 1 if wr is not None else 0, fwd_b, None))
         ws = torch.empty(max(fwd_b.value, 1), dtype=torch.uint8, device=dev)
         out = _lib.FwdOut(
             lse=lse.data_ptr(),
@@ -217,10 +225,15 @@ def icepop_fwd(
             surrogate=surrogate.data_ptr(),
             coeff=coeff.data_ptr(),
             stats=stats.data_ptr(),
+            kl=_lib.ptr(kl),
+            lse_ref=_lib.ptr(lse_ref),
+            kl_w=_lib.ptr(kl_w),
         )
-        _lib.check(lib.icepop_fwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), c_batch, out,
-                                       ws.data_ptr(), ws.numel(), st))
-        return IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats)
+        _lib.check(lib.icepop_fwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), c_batch,
+                                       out, ws.data_ptr(), ws.numel(), st))
+        f = IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats, kl=kl, lse_ref=lse_ref)
+        f.extras["kl_w"] = kl_w
+        return f
     if hidden.dtype == torch.float64:
         if weight.dtype != torch.float64:
             raise ValueError("fp64 hidden needs an fp64 weight")
@@ -264,7 +277,7 @@ def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chu
     rows = cb // (2 * vocab)
     chunk = n_tokens if rows >= n_tokens else max(128, rows // 128 * 128)
     bwd_b = _lib._sz()
-    _lib.check(lib.icepop_workspace_bytes(shape, chunk, None, bwd_b))
+    _lib.check(lib.icepop_workspace_bytes(shape, chunk, 0, None, bwd_b))
     return bwd_b.value
 
 
@@ -306,10 +319,12 @@ def icepop_bwd(
             raise ValueError("grad_weight must be a contiguous float32 tensor shaped like weight")
         ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, _dz_chunk_bytes(dev)), dtype=torch.uint8,
                          device=dev)
-        _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), batch.tokens.data_ptr(),
-                                       fwd.lse.data_ptr(), fwd.coeff.data_ptr(), float(grad_scale), _lib.ptr(gh),
-                                       1 if gh_dtype == torch.float32 else 0, _lib.ptr(gw), 1 if accumulate else 0,
-                                       ws.data_ptr(), ws.numel(), st))
+        wr = weight_ref.contiguous() if weight_ref is not None else None
+        saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
+                           lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")))
+        _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
+                                       float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
+                                       _lib.ptr(gw), 1 if accumulate else 0, ws.data_ptr(), ws.numel(), st))
         return gh, gw
     if hidden.dtype == torch.float64:
         gh = torch.empty((n, d), dtype=torch.float64, device=dev) if need_hidden else None

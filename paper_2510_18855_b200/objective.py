@@ -252,17 +252,20 @@ def objective_and_grad(
         fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
         _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
     elif precision == "bf16":
-        if ref is not None:
-            raise ValueError("the bf16 drop-in does not compute the KL-to-ref term yet; use precision='fp64'")
         if vocab % 8:
             raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
         nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
+
+        def pad_bf16(w):
+            wn = np.zeros((nf_pad, vocab))
+            wn[:n_features] = w
+            return torch.from_numpy(wn).to(torch.bfloat16).to(dev)
+
         H = torch.from_numpy(multihot(p.feats, nf_pad)).to(torch.bfloat16).to(dev)
-        Wn = np.zeros((nf_pad, vocab))
-        Wn[:n_features] = theta.weights
-        W = torch.from_numpy(Wn).to(torch.bfloat16).to(dev)
-        fwd = icepop_fwd(H, W, batch, icfg, layout="dv")
-        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False)
+        W = pad_bf16(theta.weights)
+        Wr = pad_bf16(ref.weights) if ref is not None else None
+        fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
+        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
         gw = gw[:n_features]
     else:
         raise ValueError("precision must be 'fp64' or 'bf16'")

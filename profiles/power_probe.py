@@ -99,8 +99,8 @@ def main():
         f = icepop_fwd(H, W, batch, IcePopConfig(), layout="vd")
         run(f"K1 fwd cta{cg}", lambda: icepop_fwd(H, W, batch, IcePopConfig(), layout="vd"), flop, a.seconds)
         run(f"K3 dz cta{cg}", lambda: _lib.check(lib.icepop_dz_bf16(
-            shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), f.lse.data_ptr(), f.coeff.data_ptr(), -1.0,
-            dz.data_ptr(), V, st)), flop, a.seconds)
+            shape, 1.0, H.data_ptr(), W.data_ptr(), None, _lib.Saved(tokens=tokens.data_ptr(), lse=f.lse.data_ptr(),
+            coeff=f.coeff.data_ptr()), -1.0, dz.data_ptr(), V, st)), flop, a.seconds)
         run(f"K4 dhidden cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
             dz.data_ptr(), W.data_ptr(), gh.data_ptr(), N, d, V, 0, 1, 0, 0, st)), flop, a.seconds)
         run(f"K5 dweight cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(

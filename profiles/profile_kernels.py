@@ -53,8 +53,7 @@ def main():
 
     def k3():
         f = holder["f"]
-        _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), f.lse.data_ptr(),
-                                      f.coeff.data_ptr(), -1.0, dz.data_ptr(), V, st))
+        _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), None, _lib.Saved(tokens=tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr()), -1.0, dz.data_ptr(), V, st))
 
     def k4():
         _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), N, d, V, 0, 1, 0, 0, st))

@@ -218,7 +218,7 @@ def test_logprob_entry_matches_forward(cuda_device):
     shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=H.shape[1], vocab=W.shape[0], n_seqs=1, n_groups=1,
                        weight_layout=_lib.W_VD)
     fb = _lib._sz()
-    _lib.check(lib.icepop_workspace_bytes(shape, 0, fb, None))
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
     ws = torch.empty(fb.value, dtype=torch.uint8, device=cuda_device)
     lp = torch.empty(N, dtype=torch.float64, device=cuda_device)
     lse = torch.empty(N, dtype=torch.float32, device=cuda_device)
@@ -293,3 +293,32 @@ def test_skip_inactive_all_rows_inactive(cuda_device):
     f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig())
     gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, IcePopConfig())
     assert torch.count_nonzero(gh) == 0 and torch.count_nonzero(gw) == 0
+
+
+@pytest.mark.parametrize("kl_coeff", [0.0, 0.4])
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff):
+    """KL-to-ref on tensor cores (objective.py:254-263): dual-accumulator GEMMs; the KL
+    diagnostic always, its gradient when gamma > 0."""
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    c = _case(seed=31, layout=layout, V=1000)
+    rng = np.random.default_rng(7)
+    Wr = torch.from_numpy(c["W"].double().numpy() + rng.normal(0, 0.05, tuple(c["W"].shape))).to(torch.bfloat16)
+    cfg = IcePopConfig(kl_coeff=kl_coeff)
+    H, W, Wrd = c["H"].to(cuda_device), c["W"].to(cuda_device), Wr.to(cuda_device)
+    b = _batch(c, cuda_device)
+    f = icepop_fwd(H, W, b, cfg, layout=layout, weight_ref=Wrd)
+    gh, gw = icepop_bwd(H, W, b, f, cfg, layout=layout, weight_ref=Wrd, grad_hidden_dtype=torch.float32)
+    finish(f.stats)
+    from oracle.icepop_oracle import icepop_dense
+
+    o = icepop_dense(c["H"].double().numpy(), c["W"].double().numpy(), c["tokens"], c["lp_old"], c["lp_inf"],
+                     c["cu"], c["go"], c["adv"], layout=layout, kl_coeff=kl_coeff, weight_ref=Wr.double().numpy())
+    d = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), o["kept"])
+    np.testing.assert_allclose(f.kl.cpu().numpy(), o["kl"], atol=2e-3, rtol=2e-2)
+    assert d.kl_to_ref == pytest.approx(o["kl_to_ref"], rel=1e-2, abs=1e-4)
+    assert d.objective_value == pytest.approx(o["objective"], rel=2e-3, abs=1e-5)
+    assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2

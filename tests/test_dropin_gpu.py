@@ -119,15 +119,18 @@ def test_dropin_fp64_matches_reference_golden(name):
     np.testing.assert_allclose(written, d["out_lp_cur"], rtol=1e-12, atol=1e-13)
 
 
-@pytest.mark.parametrize("name", ["small_icepop", "medium_icepop", "medium_tis", "temp_icepop"])
+@pytest.mark.parametrize("name", ["small_icepop", "medium_icepop", "medium_tis", "temp_icepop", "small_icepop_kl",
+                                  "small_icepop_refdiag"])
 def test_dropin_bf16_matches_reference_golden(name):
     O = _obj()
     d = load_golden(name)
     cfg, bounds = cfg_of(d)
-    out = O.objective_and_grad(groups_from_golden(d), Params(d["weight"], 1), Params(d["weight"], 0), None, cfg,
+    ref = Params(d["weight_ref"], 0) if d["has_ref"] else None
+    out = O.objective_and_grad(groups_from_golden(d), Params(d["weight"], 1), Params(d["weight"], 0), ref, cfg,
                                bounds, d["temperature"], precision="bf16")
     assert np.array_equal(out.per_token_mask_kept, d["out_kept"])
-    assert out.objective_value == pytest.approx(d["out_objective"], rel=1e-3, abs=1e-5)
+    assert out.objective_value == pytest.approx(d["out_objective"], rel=2e-3, abs=1e-5)
+    assert out.kl_to_ref == pytest.approx(d["out_kl_to_ref"], rel=1e-2, abs=1e-4)
     assert np.linalg.norm(out.grad - d["out_grad"]) / np.linalg.norm(d["out_grad"]) < 1e-2
 
 
