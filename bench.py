@@ -141,8 +141,10 @@ def build_device_inputs(cfg, meta, dev, rank):
     _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
     ws = torch.empty(fb.value, dtype=torch.uint8, device=dev)
     lp = torch.empty(N, dtype=torch.float64, device=dev)
-    _lib.check(lib.icepop_logprob_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), None,
-                                       lp.data_ptr(), None, ws.data_ptr(), ws.numel(),
+    lse0 = torch.empty(N, dtype=torch.float32, device=dev)
+    ent0 = torch.empty(N, dtype=torch.float32, device=dev)
+    _lib.check(lib.icepop_logprob_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), tokens.data_ptr(), lse0.data_ptr(),
+                                       lp.data_ptr(), ent0.data_ptr(), ws.data_ptr(), ws.numel(),
                                        torch.cuda.current_stream(dev).cuda_stream))
     del ws
     lp_old = lp + 0.1 * torch.randn(N, device=dev, dtype=torch.float64, generator=g)
@@ -151,7 +153,11 @@ def build_device_inputs(cfg, meta, dev, rank):
                         cu_seqlens=torch.from_numpy(meta["cu"]).to(dev), group_offsets=torch.from_numpy(meta["go"]).to(dev),
                         advantages=None, rewards=torch.from_numpy(meta["rewards"]).to(dev),
                         token_offset=meta["token_offset"])
-    return H, W, batch
+    # on-policy variant (theta == theta_old): lp_train_old is exactly the recorded lp
+    onp = PackedBatch(tokens=tokens, lp_train_old=lp, lp_infer_old=lp - (lp_old - lp_inf),
+                      cu_seqlens=batch.cu_seqlens, group_offsets=batch.group_offsets, advantages=None,
+                      rewards=batch.rewards, token_offset=meta["token_offset"])
+    return H, W, batch, (onp, lse0, ent0)
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -172,7 +178,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     meta = make_batch_host(cfg, rank, world)
-    H, W, batch = build_device_inputs(cfg, meta, dev, rank)
+    H, W, batch, onpolicy = build_device_inputs(cfg, meta, dev, rank)
     icfg = IcePopConfig()
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
     rows = _dz_chunk_bytes(dev) // (2 * V)
@@ -219,6 +225,42 @@ def run_ours(args):
     ms = float(t.item())
     diag = Diagnostics.from_stats(f.stats.cpu())
 
+    # ---------------- on-policy variant (extra line item; the headline is the general case)
+    onp_res = None
+    if not args.no_onpolicy:
+        from paper_2510_18855_b200.loss import icepop_fwd_onpolicy
+
+        ob, lse0, ent0 = onpolicy
+
+        def step_onp():
+            f = icepop_fwd_onpolicy(ob, lse0, ent0, icfg, hidden_dim=d, vocab=V)
+            _, g = icepop_bwd(H, W, ob, f, icfg, layout="vd", grad_scale=-1.0)
+            if world > 1:
+                allreduce_stats(f.stats)
+                wait_grad(allreduce_grad(g))
+            return f
+
+        for _ in range(2):
+            step_onp()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        o0.record()
+        n_onp = max(2, min(args.steps, 4))
+        for _ in range(n_onp):
+            step_onp()
+        o1.record()
+        torch.cuda.synchronize()
+        oms = o0.elapsed_time(o1) / n_onp
+        t2 = torch.tensor([oms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        oms = float(t2.item())
+        onp_res = {"value": round(N * world / (oms / 1e3), 1), "unit": UNIT, "ms_per_step": round(oms, 3),
+                   "steps": n_onp, "note": "theta == theta_old (the reference loop's own case, scheduler.py:540) "
+                   "with lp_train_old recorded by icepop_logprob_bf16: GEMM-free exact forward + full backward"}
+
     # ---------------- per-kernel timing pass (same work, events between launches)
     kern = kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev) if not args.no_kernel_timing else {}
 
@@ -264,6 +306,8 @@ def run_ours(args):
         line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()}
     if e2e:
         line["e2e"] = e2e
+    if onp_res:
+        line["on_policy"] = onp_res
     if clocks:
         line["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -485,6 +529,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--no-onpolicy", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)

@@ -154,6 +154,15 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
                     const void* weight, const void* weight_ref, const icepop_batch* batch,
                     const icepop_fwd_out* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* On-policy forward (theta == theta_old, as in the reference's own loop, scheduler.py:540-541,
+ * with lp_train_old recorded by icepop_logprob_bf16 under the same weights): then
+ * lp_cur == lp_train_old exactly and r == 1 (objective.py:240), so no GEMM runs -- the IcePop
+ * epilogue uses the recorded lse/entropy and out->lse receives lse_old for the backward.
+ * Cuts the loss step from 8.d.V to 6.d.V executed FLOPs per token. No KL-to-ref term. */
+int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch,
+                        const float* lse_old, const float* entropy_old, const icepop_fwd_out* out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* Log-prob only (no IcePop epilogue): lse, lp = z[y]-lse, entropy. Used to record
  * lp_train_old (scheduler.py:296-311) with the same kernel. Any output may be NULL. */
 int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const void* hidden,

@@ -122,6 +122,10 @@ SIGNATURES: dict[str, tuple] = {
         ctypes.c_int,
         [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Batch), _P(FwdOut), _c_p, _sz, _c_p],
     ),
+    "icepop_fwd_onpolicy": (
+        ctypes.c_int,
+        [_P(Shape), _P(Config), _P(Batch), _c_p, _c_p, _P(FwdOut), _c_p, _sz, _c_p],
+    ),
     "icepop_logprob_bf16": (
         ctypes.c_int,
         [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p],

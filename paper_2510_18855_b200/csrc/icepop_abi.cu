@@ -608,6 +608,46 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
   return ICEPOP_OK;
 }
 
+int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch,
+                        const float* lse_old, const float* entropy_old, const icepop_fwd_out* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, false));
+  ICP_TRY(check_config(cfg));
+  if (!batch || !out || !out->stats || !lse_old) return fail(ICEPOP_EINVAL, "null batch/out/stats/lse_old");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BF16Workspace w = carve_bf16(shape, workspace, 0, false, false);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, V = shape->vocab;
+  const double* adv = nullptr;
+  ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
+  ICP_CUDA(cudaMemsetAsync(w.err, 0, sizeof(unsigned), st));
+  if (N > 0) {
+    k_check_tokens<<<token_grid(N), TOK_THREADS, 0, st>>>(batch->tokens, N, V, w.err);
+    ICP_CUDA(cudaGetLastError());
+  }
+  TokenArgs a;
+  fill_token_args(a, shape, cfg, batch, adv);
+  a.kl_coeff = 0.0;
+  a.lse_in = lse_old;
+  a.entropy_in_f = entropy_old;
+  a.lse_f = out->lse;
+  a.lp_cur = out->lp_cur;
+  a.entropy_f = out->entropy;
+  a.kept = out->kept;
+  a.calib = out->calib;
+  a.surrogate = out->surrogate;
+  a.coeff_f = out->coeff;
+  a.block_stats = w.block_stats;
+  const int grid = token_grid(N);
+  k2_icepop_tokens<2><<<grid, TOK_THREADS, 0, st>>>(a);
+  ICP_CUDA(cudaGetLastError());
+  k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
+  k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
 __global__ void k_logprob_finish(const float* part, int n_parts, const float* ztok, int64_t n, float* lse,
                                  double* lp, float* entropy) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {

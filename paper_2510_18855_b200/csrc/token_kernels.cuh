@@ -89,6 +89,9 @@ struct TokenArgs {
   const double* lp_cur_in;
   const double* entropy_in;
   const double* kl_in;
+  // on-policy mode (MODE 2): recorded lse / entropy of lp_train_old's forward
+  const float* lse_in;
+  const float* entropy_in_f;
   // config
   double alpha, beta, clip_eps, tis_cap, temperature, kl_coeff;
   int32_t algo;
@@ -158,7 +161,8 @@ __device__ __forceinline__ void block_reduce_stats(double (&st)[ICEPOP_NSTATS], 
   }
 }
 
-// MODE 0: bf16 path (merge K1 partials), MODE 1: fp64 path (lp_cur/entropy/kl given).
+// MODE 0: bf16 path (merge K1 partials), MODE 1: fp64 path (lp_cur/entropy/kl given),
+// MODE 2: on-policy (theta == theta_old): lp_cur = lp_train_old, lse/entropy recorded.
 template <int MODE>
 __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs a) {
   double st[ICEPOP_NSTATS] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -205,12 +209,18 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
         if (a.lse_ref_f) a.lse_ref_f[t] = lse_r;
         if (!isfinite(klf)) err |= ICEPOP_ERR_NONFINITE;
       }
-    } else {
+    } else if (MODE == 1) {
       lp_cur = a.lp_cur_in[t];
       ent = a.entropy_in[t];
       kl = a.kl_in ? a.kl_in[t] : 0.0;
+    } else {
+      lp_cur = a.lp_old[t];
+      const float ef = a.entropy_in_f ? a.entropy_in_f[t] : 0.f;
+      ent = (double)ef;
+      if (a.lse_f) a.lse_f[t] = a.lse_in[t];
+      if (a.entropy_f) a.entropy_f[t] = ef;
     }
-    if (a.lp_cur && MODE == 0) a.lp_cur[t] = lp_cur;
+    if (a.lp_cur && MODE != 1) a.lp_cur[t] = lp_cur;
 
     int seq;
     double w;

@@ -268,6 +268,58 @@ def icepop_fwd(
     raise ValueError(f"unsupported dtype {hidden.dtype}: use bfloat16 (tensor cores) or float64 (validation)")
 
 
+def icepop_logprob(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor, layout: str = "vd",
+                   temperature: float = 1.0) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """log pi(y_t), lse_t and entropy_t with the K1 kernel (the train engine's lp recording,
+    scheduler.py:296-311 / policy.py:411-442): returns (lp f64, lse f32, entropy f32)."""
+    lib = _lib_for(hidden)
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ValueError("icepop_logprob runs on bf16 hidden/weight")
+    hidden, weight = hidden.contiguous(), weight.contiguous()
+    n, d = hidden.shape
+    v = weight.shape[1] if layout == "dv" else weight.shape[0]
+    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=1, n_groups=1,
+                       weight_layout=LAYOUTS[layout])
+    dev = hidden.device
+    fb = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
+    ws = torch.empty(max(fb.value, 1), dtype=torch.uint8, device=dev)
+    lp = torch.empty(n, dtype=torch.float64, device=dev)
+    lse = torch.empty(n, dtype=torch.float32, device=dev)
+    ent = torch.empty(n, dtype=torch.float32, device=dev)
+    _lib.check(lib.icepop_logprob_bf16(shape, float(temperature), hidden.data_ptr(), weight.data_ptr(),
+                                       tokens.data_ptr(), lse.data_ptr(), lp.data_ptr(), ent.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), _stream(dev)))
+    return lp, lse, ent
+
+
+def icepop_fwd_onpolicy(batch: PackedBatch, lse_old: torch.Tensor, entropy_old: torch.Tensor | None,
+                        cfg: IcePopConfig = IcePopConfig(), hidden_dim: int = 8, vocab: int = 8) -> IcePopForward:
+    """Forward when theta == theta_old and batch.lp_train_old came from :func:`icepop_logprob`
+    with the same weights: lp_cur == lp_train_old exactly, so no GEMM runs (6.d.V per token
+    for the whole loss step instead of 8.d.V). Pair with icepop_bwd as usual."""
+    lib = _lib_for(batch.tokens)
+    batch.validate()
+    n = batch.tokens.numel()
+    dev = batch.tokens.device
+    shape = _lib.Shape(n_tokens=n, token_offset=batch.token_offset, hidden=hidden_dim, vocab=vocab,
+                       n_seqs=batch.n_seqs, n_groups=batch.n_groups, weight_layout=_lib.W_VD)
+    f = IcePopForward(torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                      torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.uint8, device=dev),
+                      torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
+                      torch.empty(n, dtype=torch.float32, device=dev),
+                      torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev))
+    fb = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
+    ws = torch.empty(max(fb.value, 1), dtype=torch.uint8, device=dev)
+    out = _lib.FwdOut(lse=f.lse.data_ptr(), lp_cur=f.lp_cur.data_ptr(), entropy=f.entropy.data_ptr(),
+                      kept=f.kept.data_ptr(), calib=f.calib.data_ptr(), surrogate=f.surrogate.data_ptr(),
+                      coeff=f.coeff.data_ptr(), stats=f.stats.data_ptr())
+    _lib.check(lib.icepop_fwd_onpolicy(shape, cfg.to_c(), batch.to_c(), lse_old.data_ptr(), _lib.ptr(entropy_old),
+                                       out, ws.data_ptr(), ws.numel(), _stream(dev)))
+    return f
+
+
 def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chunk_bytes: int | None = None) -> int:
     """Backward workspace for a dZ chunk of at most `chunk_bytes` (default DZ_CHUNK_BYTES)."""
     lib = _lib.load()

@@ -322,3 +322,26 @@ def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff):
     assert d.objective_value == pytest.approx(o["objective"], rel=2e-3, abs=1e-5)
     assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
     assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_on_policy_forward_equals_full_forward(cuda_device):
+    """theta == theta_old with lp_train_old recorded by icepop_logprob: the GEMM-free
+    forward is bit-identical to the full forward (r == 1 exactly), and so is the backward."""
+    from paper_2510_18855_b200.loss import (IcePopConfig, PackedBatch, icepop_bwd, icepop_fwd, icepop_fwd_onpolicy,
+                                            icepop_logprob)
+
+    c = _case(seed=23)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    tok = torch.from_numpy(c["tokens"]).to(cuda_device)
+    lp, lse, ent = icepop_logprob(H, W, tok)
+    b = _batch(c, cuda_device)
+    b = PackedBatch(b.tokens, lp, lp - torch.from_numpy(np.random.default_rng(0).normal(0, 0.3, len(c["tokens"]))).to(
+        cuda_device), b.cu_seqlens, b.group_offsets, b.advantages)
+    cfg = IcePopConfig()
+    full = icepop_fwd(H, W, b, cfg)
+    onp = icepop_fwd_onpolicy(b, lse, ent, cfg, hidden_dim=H.shape[1], vocab=W.shape[0])
+    for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff", "stats"):
+        assert torch.equal(getattr(full, name), getattr(onp, name)), name
+    gh1, gw1 = icepop_bwd(H, W, b, full, cfg)
+    gh2, gw2 = icepop_bwd(H, W, b, onp, cfg)
+    assert torch.equal(gh1, gh2) and torch.equal(gw1, gw2)
