@@ -198,6 +198,23 @@ int icepop_dz_bf16(const icepop_shape* shape, double temperature, const void* hi
                    const void* weight, const void* weight_ref, const icepop_saved* saved,
                    double grad_scale, void* dz, int64_t ldz, void* stream);
 
+/* ---- discrepancy probe (discrepancy.py:132-161) -------------------------- */
+/* kl[t] = KL(softmax(H.W_p/T)_t || softmax(H.W_q/T)_t) per row (e.g. p = the inference
+ * engine's weights, q = the training weights: delta_t of Theorem 1) with the dual-accumulator
+ * GEMM; *mean_kl (device) = mean over rows. Any output pointer may be NULL. Workspace: the
+ * forward size of icepop_workspace_bytes(with_ref = 1). */
+int icepop_kl_bf16(const icepop_shape* shape, double temperature, const void* hidden,
+                   const void* weight_p, const void* weight_q, float* kl, float* lse_p, float* lse_q,
+                   double* mean_kl, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- optimizer step (objective.py:301-326) --------------------------------- */
+/* Gradient ascent on an fp32 master copy: v = beta v + g (velocity != NULL) or v = g;
+ * w += lr v; weight_bf16 (may be NULL) receives the bf16 copy the GEMMs read. Non-finite
+ * weights set ICEPOP_ERR_NONFINITE in stats[ICEPOP_STAT_ERRORS] (stats may be NULL);
+ * icepop_finish(stats) maps it to NumericError. lr <= 0 or beta outside [0,1) -> EINVAL. */
+int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, void* weight_bf16,
+                          int64_t n, double lr, double beta, double* stats, void* stream);
+
 /* ---- fp64 SIMT validation path ----------------------------------------------------- */
 /* Same semantics in fp64 on CUDA cores (still CUDA, no CPU fallback), so the
  * reference's exact-identity and finite-difference tests run unchanged on the GPU.

@@ -135,6 +135,8 @@ SIGNATURES: dict[str, tuple] = {
         [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i32, _c_p, _i32, _c_p, _sz, _c_p],
     ),
     "icepop_dz_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i64, _c_p]),
+    "icepop_kl_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "icepop_sgd_update_f32": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _f64, _f64, _c_p, _c_p]),
     "icepop_workspace_bytes_f64": (ctypes.c_int, [_P(Shape), _i32, _P(_sz)]),
     "icepop_fwd_f64": (
         ctypes.c_int,

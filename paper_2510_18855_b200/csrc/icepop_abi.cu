@@ -964,7 +964,61 @@ int icepop_finish(const double* stats, void* stream) {
   if (e & ERR_BAD_TOKEN) return fail(ICEPOP_EINVAL, "token id outside the vocabulary");
   if (e & ICEPOP_ERR_CALIB_OVERFLOW) return fail(ICEPOP_ENUMERIC, "calibration ratio overflow");
   if (e & ICEPOP_ERR_RATIO_OVERFLOW) return fail(ICEPOP_ENUMERIC, "importance ratio overflow");
-  if (e & ICEPOP_ERR_NONFINITE) return fail(ICEPOP_ENUMERIC, "objective or gradient is not finite");
+  if (e & ICEPOP_ERR_NONFINITE) return fail(ICEPOP_ENUMERIC, "objective, gradient or update is not finite");
+  return ICEPOP_OK;
+}
+
+int icepop_kl_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight_p,
+                   const void* weight_q, float* kl, float* lse_p, float* lse_q, double* mean_kl, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
+  if (!hidden || !weight_p || !weight_q) return fail(ICEPOP_EINVAL, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BF16Workspace w = carve_bf16(shape, workspace, 0, false, true);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "workspace too small: need %zu bytes", w.bytes);
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  if (N == 0) return fail(ICEPOP_EINVAL, "probe set must be non-empty");  // discrepancy.py:136-137
+  EpiParams ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.scale_log2 = (float)(1.4426950408889634 / temperature);
+  ep.inv_t = (float)(1.0 / temperature);
+  ep.part = w.part;
+  ep.ztok = w.ztok;
+  const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
+  ICP_TRY(run_umma(EPI_LSE_REF, hidden, d, false, weight_p, b_mn ? V : d, b_mn, N, V, d, ep, st, Extent(), weight_q));
+  const int grid = token_grid(N);
+  k_kl_finish<<<grid, TOK_THREADS, 0, st>>>(w.part, (int)((V + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF)), N, kl,
+                                            lse_p, lse_q, w.block_stats);
+  if (mean_kl) k_sum_blocks<<<1, 32, 0, st>>>(w.block_stats, grid, 1.0 / (double)N, mean_kl);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, void* weight_bf16, int64_t n, double lr,
+                          double beta, double* stats, void* stream) {
+  // objective.py:303-306, 320-321
+  if (!(lr > 0.0)) return fail(ICEPOP_EINVAL, "learning rate must be positive");
+  if (velocity && !(beta >= 0.0 && beta < 1.0)) return fail(ICEPOP_EINVAL, "momentum beta must be in [0, 1)");
+  if (!weight || !grad || n < 0) return fail(ICEPOP_EINVAL, "null weight/grad");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static unsigned* err = nullptr;
+  if (!err) ICP_CUDA(cudaMalloc(&err, 16 * sizeof(unsigned)));
+  int dev = 0;
+  ICP_CUDA(cudaGetDevice(&dev));
+  unsigned* e = err + (dev & 15);
+  ICP_CUDA(cudaMemsetAsync(e, 0, sizeof(unsigned), st));
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  if (n > 0)
+    k_sgd_update<<<std::max(grid, 1), 256, 0, st>>>(weight, grad, velocity,
+                                                    static_cast<__nv_bfloat16*>(weight_bf16), n, (float)lr,
+                                                    (float)beta, e);
+  if (stats) {
+    ICP_CUDA(cudaMemsetAsync(stats, 0, sizeof(double) * ICEPOP_NSTATS, st));
+    k_merge_err<<<1, 1, 0, st>>>(e, stats);
+  }
+  ICP_CUDA(cudaGetLastError());
   return ICEPOP_OK;
 }
 

@@ -8,6 +8,7 @@
 //   k_finalize_stats    : fixed-order reduction of per-block fp64 partials (no atomics).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -293,6 +294,76 @@ __global__ void k_finalize_stats(const double* __restrict__ block_stats, int n_b
     }
     stats[k] = (k == ICEPOP_STAT_ERRORS) ? (double)ee : acc;
   }
+}
+
+// ------------------------------------------------------------------ discrepancy probe (f-4)
+// kl_t = KL(softmax(z_p) || softmax(z_q)) per row from the dual-LSE partials (6 rows per
+// tile); block partial sums of kl in fixed order for the probe-set mean (discrepancy.py:132-141).
+__global__ void __launch_bounds__(TOK_THREADS) k_kl_finish(const float* __restrict__ part, int n_parts, int64_t n,
+                                                          float* __restrict__ kl_out, float* __restrict__ lse_p,
+                                                          float* __restrict__ lse_q, double* __restrict__ block_sums) {
+  double acc = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    float M = -1e30f, Mr = -1e30f;
+    for (int j = 0; j < n_parts; ++j) {
+      const float* p = part + (int64_t)j * 6 * n + t;
+      M = fmaxf(M, p[0]);
+      Mr = fmaxf(Mr, p[3 * n]);
+    }
+    float S = 0.f, Sr = 0.f, X = 0.f;
+    for (int j = 0; j < n_parts; ++j) {
+      const float* p = part + (int64_t)j * 6 * n + t;
+      const float sc = exp2f(p[0] - M);
+      S = fmaf(p[n], sc, S);
+      Sr = fmaf(p[4 * n], exp2f(p[3 * n] - Mr), Sr);
+      X = fmaf(p[5 * n], sc, X);
+    }
+    const float lp = (M + log2f(S)) * LN2_F, lq = (Mr + log2f(Sr)) * LN2_F;
+    const float kl = (X / S) * LN2_F - lp + lq;
+    if (kl_out) kl_out[t] = kl;
+    if (lse_p) lse_p[t] = lp;
+    if (lse_q) lse_q[t] = lq;
+    acc += (double)kl;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double sh[TOK_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TOK_THREADS / 32; ++w) s += sh[w];
+    block_sums[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_sum_blocks(const double* __restrict__ block_sums, int nb, double scale, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += block_sums[b];
+    *out = s * scale;
+  }
+}
+
+// ------------------------------------------------------------------ optimizer step (f-2)
+// Gradient ASCENT as the reference (objective.py:301-326): v = beta v + g (momentum) or v = g,
+// w += lr v; non-finite weights set the error word; optional bf16 copy of w for the GEMMs.
+__global__ void k_sgd_update(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
+                             __nv_bfloat16* __restrict__ w_bf16, int64_t n, float lr, float beta,
+                             unsigned* __restrict__ err) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float step = g[i];
+    if (v) {
+      step = fmaf(beta, v[i], step);
+      v[i] = step;
+    }
+    const float nw = fmaf(lr, step, w[i]);
+    w[i] = nw;
+    if (w_bf16) w_bf16[i] = __float2bfloat16_rn(nw);
+    bad |= !isfinite(nw);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, ICEPOP_ERR_NONFINITE);
 }
 
 // ------------------------------------------------------------------ active-row compaction

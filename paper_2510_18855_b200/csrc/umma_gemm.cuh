@@ -183,7 +183,7 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
                                         int n_blk, int row, uint32_t taddr) {
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
-  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
@@ -288,7 +288,7 @@ __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams
                                             int n_blk, int row, uint32_t taddr) {
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
-  const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_x = 0.f;
   float ref_m = -1e30f, ref_s = 0.f;
 #pragma unroll 1

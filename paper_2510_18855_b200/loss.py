@@ -320,6 +320,33 @@ def icepop_fwd_onpolicy(batch: PackedBatch, lse_old: torch.Tensor, entropy_old: 
     return f
 
 
+def discrepancy(hidden: torch.Tensor, weight_p: torch.Tensor, weight_q: torch.Tensor, layout: str = "vd",
+                temperature: float = 1.0) -> tuple[torch.Tensor, torch.Tensor]:
+    """delta = mean_t KL(pi_p(.|t) || pi_q(.|t)) over the rows of `hidden` (the probe
+    contexts), e.g. p = the inference engine's weights, q = the training weights
+    (discrepancy.py:132-141). Returns (delta as a device fp64 scalar, per-row kl f32)."""
+    lib = _lib_for(hidden)
+    if hidden.dtype != torch.bfloat16 or weight_p.dtype != torch.bfloat16 or weight_q.dtype != torch.bfloat16:
+        raise ValueError("discrepancy runs on bf16 hidden/weights")
+    if weight_p.shape != weight_q.shape:
+        raise ValueError("weight_p and weight_q must have the same shape")
+    hidden, weight_p, weight_q = hidden.contiguous(), weight_p.contiguous(), weight_q.contiguous()
+    n, d = hidden.shape
+    v = weight_p.shape[1] if layout == "dv" else weight_p.shape[0]
+    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=1, n_groups=1,
+                       weight_layout=LAYOUTS[layout])
+    dev = hidden.device
+    fb = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 1, fb, None))
+    ws = torch.empty(max(fb.value, 1), dtype=torch.uint8, device=dev)
+    kl = torch.empty(n, dtype=torch.float32, device=dev)
+    mean = torch.empty((), dtype=torch.float64, device=dev)
+    _lib.check(lib.icepop_kl_bf16(shape, float(temperature), hidden.data_ptr(), weight_p.data_ptr(),
+                                  weight_q.data_ptr(), kl.data_ptr(), None, None, mean.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), _stream(dev)))
+    return mean, kl
+
+
 def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chunk_bytes: int | None = None) -> int:
     """Backward workspace for a dZ chunk of at most `chunk_bytes` (default DZ_CHUNK_BYTES)."""
     lib = _lib.load()

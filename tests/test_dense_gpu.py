@@ -345,3 +345,55 @@ def test_on_policy_forward_equals_full_forward(cuda_device):
     gh1, gw1 = icepop_bwd(H, W, b, full, cfg)
     gh2, gw2 = icepop_bwd(H, W, b, onp, cfg)
     assert torch.equal(gh1, gh2) and torch.equal(gw1, gw2)
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_discrepancy_probe_kl(cuda_device, cta_group, layout):
+    """delta = mean KL(pi_p || pi_q) over probe rows (discrepancy.py:132-141) vs fp64 numpy."""
+    from paper_2510_18855_b200.loss import discrepancy
+
+    rng = np.random.default_rng(5)
+    n, d, V = 300, 256, 1000
+    H = torch.from_numpy(rng.normal(0, 1, (n, d))).to(torch.bfloat16)
+    shp = (V, d) if layout == "vd" else (d, V)
+    Wq = torch.from_numpy(rng.normal(0, 2 / np.sqrt(d), shp)).to(torch.bfloat16)
+    Wp = torch.from_numpy(Wq.double().numpy() + rng.normal(0, 0.1, shp)).to(torch.bfloat16)
+    mean, kl = discrepancy(H.to(cuda_device), Wp.to(cuda_device), Wq.to(cuda_device), layout=layout, temperature=0.9)
+
+    def logp(W):
+        z = H.double().numpy() @ (W.double().numpy().T if layout == "vd" else W.double().numpy()) / 0.9
+        z = z - z.max(1, keepdims=True)
+        return z - np.log(np.exp(z).sum(1, keepdims=True))
+
+    lp, lq = logp(Wp), logp(Wq)
+    ref = (np.exp(lp) * (lp - lq)).sum(1)
+    np.testing.assert_allclose(kl.cpu().numpy(), ref, atol=2e-3, rtol=2e-2)
+    assert mean.item() == pytest.approx(ref.mean(), rel=1e-2)
+
+
+def test_sgd_update_on_device(cuda_device):
+    """objective.py:301-326: ascent, momentum, version semantics left to the caller; errors."""
+    from paper_2510_18855_b200.errors import NumericError
+    from paper_2510_18855_b200.optim import sgd_update_
+
+    g = torch.Generator(device="cpu").manual_seed(0)
+    w0 = torch.randn(1000, 37, generator=g)
+    gr = torch.randn(1000, 37, generator=g)
+    w = w0.clone().to(cuda_device)
+    v = torch.zeros_like(w)
+    wb = torch.empty_like(w, dtype=torch.bfloat16)
+    sgd_update_(w, gr.to(cuda_device), 0.1, v, 0.5, wb)
+    sgd_update_(w, gr.to(cuda_device), 0.1, v, 0.5, wb)
+    ref = w0 + 0.1 * gr + 0.1 * 1.5 * gr
+    torch.testing.assert_close(w.cpu(), ref, rtol=1e-6, atol=1e-6)
+    torch.testing.assert_close(v.cpu(), 1.5 * gr, rtol=1e-6, atol=1e-6)
+    assert torch.equal(wb, w.to(torch.bfloat16))
+    w2 = w0.clone().to(cuda_device)
+    sgd_update_(w2, gr.to(cuda_device), 0.25)
+    torch.testing.assert_close(w2.cpu(), w0 + 0.25 * gr, rtol=1e-6, atol=1e-6)
+    with pytest.raises(ValueError):
+        sgd_update_(w2, gr.to(cuda_device), 0.0)
+    with pytest.raises(ValueError):
+        sgd_update_(w2, gr.to(cuda_device), 0.1, torch.zeros_like(w2), 1.0)
+    with pytest.raises(NumericError):
+        sgd_update_(w2, torch.full_like(w2, 3e38), 10.0)

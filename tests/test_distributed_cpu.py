@@ -142,3 +142,32 @@ def test_token_shards_reproduce_full_batch_objective(world):
     stats, J, n_clipped, n_tok = out[0]
     assert stats[0] == pytest.approx(J, rel=1e-12, abs=1e-15)
     assert stats[1] == n_clipped and stats[2] == n_tok
+
+
+def _sharded_fn(rank, world):
+    from paper_2510_18855_b200.optim import shard_bounds, sharded_sgd_step
+
+    torch.manual_seed(0)
+    w_full = torch.randn(7, 13)
+    grads = [torch.randn(7, 13) for _ in range(world)]
+    s, e, per = shard_bounds(w_full.numel(), world, rank)
+    master = torch.zeros(per)
+    master[: e - s] = w_full.view(-1)[s:e]
+    vel = torch.zeros(per)
+
+    def ref_update(m, gsh, v, out):  # objective.py:314-326 in torch (test stand-in for the CUDA kernel)
+        v.mul_(0.5).add_(gsh)
+        m.add_(0.1 * v)
+        out.copy_(m.to(torch.bfloat16))
+
+    wb = torch.empty(7, 13, dtype=torch.bfloat16)
+    sharded_sgd_step(grads[rank], master, wb, 0.1, vel, 0.5, update_fn=ref_update)
+    return wb.float().numpy(), (w_full + 0.1 * sum(grads)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sgd_step_reduce_scatter_all_gather(world):
+    out = run_ranks(_sharded_fn, world=world)
+    for wb, ref in out:
+        np.testing.assert_allclose(wb, ref, rtol=1e-2, atol=1e-2)
+    assert all(np.array_equal(out[0][0], o[0]) for o in out)
