@@ -42,6 +42,9 @@ CONFIGS = {
                hidden=4096, vocab=157184, group=8, seed=1, sigma_inf=0.233),
     "c3": dict(name="C3 Ling-1T lm_head shard: 8 seqs x 4096 tok/GPU, d=8192, V=157184, G=8", seqs=8, seq_len=4096,
                hidden=8192, vocab=157184, group=8, seed=2, sigma_inf=0.233),
+    "c4": dict(name="C4 Long-CoT: 32 seqs, ragged lognormal lengths (median 16384, <= 32768), d=8192, V=157184, "
+                    "~5% popped", seqs=32, seq_len=0, hidden=8192, vocab=157184, group=8, seed=3, sigma_inf=0.42,
+               lens=dict(median=16384, sigma=0.6, lo=256, hi=32768)),
     "c5": dict(name="C5 scaling point: 32 seqs x 4096 tok/GPU, d=8192, V=157184, G=8", seqs=32, seq_len=4096,
                hidden=8192, vocab=157184, group=8, seed=4, sigma_inf=0.233),
 }
@@ -113,11 +116,16 @@ def make_batch_host(cfg: dict, rank: int, world: int):
     groups of `group` sequences, this rank owns `seqs` whole sequences."""
     rng = np.random.default_rng(cfg["seed"])
     S_global = cfg["seqs"] * world
-    T = cfg["seq_len"]
-    cu = (np.arange(S_global + 1, dtype=np.int64) * T).astype(np.int32)
+    if cfg.get("lens"):  # ragged packed lengths (C4); every rank gets the same per-rank count
+        L = cfg["lens"]
+        per = np.clip(rng.lognormal(np.log(L["median"]), L["sigma"], cfg["seqs"]), L["lo"], L["hi"]).astype(np.int64)
+        lens = np.tile(per, world)
+    else:
+        lens = np.full(S_global, cfg["seq_len"], dtype=np.int64)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     go = np.arange(0, S_global + 1, cfg["group"], dtype=np.int32)
     rewards = rng.integers(0, 2, S_global).astype(np.float64)
-    n_local = cfg["seqs"] * T
+    n_local = int(lens[: cfg["seqs"]].sum())
     return dict(cu=cu, go=go, rewards=rewards, n_local=n_local, token_offset=rank * n_local)
 
 
@@ -276,7 +284,8 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded; random-init lm_head weights)",
-        "config": {"workload": cfg["name"], "global_batch": tokens_total, "seq_len": cfg["seq_len"],
+        "config": {"workload": cfg["name"], "global_batch": tokens_total,
+                   "seq_len": cfg["seq_len"] or "ragged",
                    "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
