@@ -212,16 +212,26 @@ int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
 // 4, 8 and 32 for every GEMM of the path, see profiles/README.md).
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
-  return e ? std::max(1, atoi(e)) : dflt;
+  return e ? std::max(0, atoi(e)) : dflt;
 }
 
-int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k) {
-  static const int g_short = env_int("ICEPOP_GROUP_M", 16);
+int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k, int64_t K) {
+  // Short K (dynamic claim order): the group's A rows stay resident in L2 while B streams, so
+  // size the group for a ~32 MB A-set (measured: 16 pair-rows at K = 4096, 8 at K = 8192).
+  // Long K (waves): 8 pair-rows balances A and B re-reads (measured).
+  static const int g_short = env_int("ICEPOP_GROUP_M", 0);
   static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 8);
   (void)epi;
   (void)n_tiles;
-  (void)cg;
-  const int g = long_k ? g_long : g_short;
+  int g;
+  if (long_k) {
+    g = g_long;
+  } else if (g_short > 0) {
+    g = g_short;
+  } else {
+    const int64_t a_rows_bytes = (int64_t)BM * cg * std::max<int64_t>(K, 1) * 2;
+    g = (int)std::max<int64_t>(4, std::min<int64_t>(32, (32ll << 20) / a_rows_bytes));
+  }
   return std::max(1, std::min(g, m_tiles));
 }
 
@@ -258,7 +268,7 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
-  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, sh.k_blocks >= long_k_blocks());
+  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, sh.k_blocks >= long_k_blocks(), K);
   sh.ext_dev = ext.dev;
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
