@@ -1013,11 +1013,12 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
   if (velocity && !(beta >= 0.0 && beta < 1.0)) return fail(ICEPOP_EINVAL, "momentum beta must be in [0, 1)");
   if (!weight || !grad || n < 0) return fail(ICEPOP_EINVAL, "null weight/grad");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static unsigned* err = nullptr;
-  if (!err) ICP_CUDA(cudaMalloc(&err, 16 * sizeof(unsigned)));
+  static unsigned* err[16] = {nullptr};  // one error word per device
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
-  unsigned* e = err + (dev & 15);
+  if (dev < 0 || dev >= 16) return fail(ICEPOP_EINVAL, "device index out of range");
+  if (!err[dev]) ICP_CUDA(cudaMalloc(&err[dev], sizeof(unsigned)));
+  unsigned* e = err[dev];
   ICP_CUDA(cudaMemsetAsync(e, 0, sizeof(unsigned), st));
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   if (n > 0)
