@@ -501,6 +501,12 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    try:  # torchrun sets OMP_NUM_THREADS=1; rank 0 alone runs here, so give BLAS every host core
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(os.cpu_count())
+    except Exception:  # noqa: BLE001
+        pass
     rng = np.random.default_rng(123)
     W64 = (rng.standard_normal((cfg["vocab"], cfg["hidden"]), dtype=np.float32) * (2.0 / np.sqrt(cfg["hidden"]))
            ).astype(np.float64)
