@@ -397,3 +397,31 @@ def test_sgd_update_on_device(cuda_device):
         sgd_update_(w2, gr.to(cuda_device), 0.1, torch.zeros_like(w2), 1.0)
     with pytest.raises(NumericError):
         sgd_update_(w2, torch.full_like(w2, 3e38), 10.0)
+
+
+def test_cuda_graph_capture_replays_fwd_bwd(cuda_device):
+    """fwd + bwd are sync-free (device-side extents, counters, error word), so one CUDA graph
+    captures the whole step; replays match eager execution bit for bit."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(seed=41)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    b = _batch(c, cuda_device)
+    cfg = IcePopConfig()
+    f0 = icepop_fwd(H, W, b, cfg)
+    gh0, gw0 = icepop_bwd(H, W, b, f0, cfg)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up on the capture stream (allocator, lazy init)
+        f = icepop_fwd(H, W, b, cfg)
+        icepop_bwd(H, W, b, f, cfg)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fg = icepop_fwd(H, W, b, cfg)
+        ghg, gwg = icepop_bwd(H, W, b, fg, cfg)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(fg.stats, f0.stats) and torch.equal(fg.kept, f0.kept)
+        assert torch.equal(ghg, gh0) and torch.equal(gwg, gw0)
