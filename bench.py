@@ -480,14 +480,21 @@ def blas_threads() -> int:
 
 
 def sample_tokens(cfg, W64, target_s: float) -> int:
-    """Tokens per CPU sample so one sample takes about target_s (probe with 4 tokens)."""
-    dt, n = time_oracle(cfg, 4, W64, seed=999)
-    return int(max(4, min(4096, 2 * round(target_s * n / dt / 2))))
+    """Tokens per CPU sample so one sample takes about target_s. The oracle has a fixed
+    per-call cost (e.g. the fp64 gradient buffer), so grow the sample until it is timed."""
+    n, dt = 8, 0.0
+    for _ in range(3):
+        dt, _ = time_oracle(cfg, n, W64, seed=999)
+        if dt >= 0.66 * target_s:
+            break
+        n = int(min(4096, max(n + 2, n * target_s / max(dt, 1e-3))))
+        n += n % 2
+    return n
 
 
 def cpu_baseline(cfg, H, W, batch, meta, n_tokens):
     W64 = W.float().cpu().numpy().astype(np.float64)
-    n_tokens = n_tokens or sample_tokens(cfg, W64, 15.0)
+    n_tokens = n_tokens or sample_tokens(cfg, W64, 15.0)  # ~10-30 s of CPU work
     dt, n = time_oracle(cfg, n_tokens, W64)
     return {"value": round(n / dt, 3), "unit": UNIT, "cores": blas_threads(), "kind": "port",
             "sample": f"{n} tokens (1 group x 2 seqs) at d={cfg['hidden']}, V={cfg['vocab']}, fp64 numpy oracle "
