@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -130,7 +132,8 @@ int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
 // right before it). ICEPOP_SCHED=static selects the static round-robin schedule instead.
 constexpr int N_COUNTERS = 256;
 int* g_counters[16] = {nullptr};
-unsigned g_counter_next[16] = {0};
+std::atomic<unsigned> g_counter_next[16];
+std::mutex g_counter_mutex;
 
 int dynamic_sched() {
   static int v = -1;
@@ -156,8 +159,11 @@ int tile_counter(cudaStream_t st, int32_t** out) {
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return ICEPOP_OK;
-  if (!g_counters[dev]) ICP_CUDA(cudaMalloc(&g_counters[dev], N_COUNTERS * sizeof(int)));
-  int* c = g_counters[dev] + (g_counter_next[dev]++ % N_COUNTERS);
+  {
+    std::lock_guard<std::mutex> lock(g_counter_mutex);
+    if (!g_counters[dev]) ICP_CUDA(cudaMalloc(&g_counters[dev], N_COUNTERS * sizeof(int)));
+  }
+  int* c = g_counters[dev] + (g_counter_next[dev].fetch_add(1) % N_COUNTERS);
   ICP_CUDA(cudaMemsetAsync(c, 0, sizeof(int), st));
   *out = c;
   return ICEPOP_OK;
@@ -176,10 +182,14 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
                    const EpiParams& ep, cudaStream_t st) {
   auto kern = umma_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
   constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI)>::SMEM;
-  static bool attr_done = false;
-  if (!attr_done) {
+  // the smem attribute is per device: one bit per device index that has it set
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  ICP_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     ICP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_done = true;
+    attr_done.fetch_or(bit, std::memory_order_acq_rel);
   }
   const int units = std::min(sh.num_tiles, num_sms() / CG);
   cudaLaunchConfig_t cfg;
@@ -1017,7 +1027,10 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return fail(ICEPOP_EINVAL, "device index out of range");
-  if (!err[dev]) ICP_CUDA(cudaMalloc(&err[dev], sizeof(unsigned)));
+  {
+    std::lock_guard<std::mutex> lock(g_counter_mutex);
+    if (!err[dev]) ICP_CUDA(cudaMalloc(&err[dev], sizeof(unsigned)));
+  }
   unsigned* e = err[dev];
   ICP_CUDA(cudaMemsetAsync(e, 0, sizeof(unsigned), st));
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
