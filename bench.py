@@ -195,9 +195,36 @@ def run_ours(args):
     # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: 4 compaction kernels + (K3, K4, K5) per chunk
     launches_per_step = 6 + 4 + 3 * n_chunks
 
+    # dW collective for N > 1: fused reduce-scatter inside K5's epilogue over NVLink peer memory
+    # (each rank ends with its ZeRO shard of the summed dW), or NCCL all-reduce of the full dW.
+    collective = "none"
+    peer = None
+    dw_shard = None
+    if world > 1:
+        collective = args.dw_collective
+        if collective == "fused":
+            try:
+                from paper_2510_18855_b200.distributed import PeerSlots
+
+                shard_rows = -(-V // world)
+                peer = PeerSlots(shard_rows, d)
+                dw_shard = torch.empty(shard_rows * d, dtype=torch.float32, device=dev)
+            except Exception as e:  # noqa: BLE001 - a peer-mapping failure selects the NCCL collective
+                print(f"fused reduce-scatter unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
+                collective = "nccl"
+
     def step_into():
         # loss = -J: grad_scale -1 gives d(loss)/d(hidden), d(loss)/d(W)
         f = icepop_fwd(H, W, batch, icfg, layout="vd")
+        if collective == "fused":
+            from paper_2510_18855_b200.distributed import stream_barrier
+            from paper_2510_18855_b200.loss import icepop_bwd_reduce_scatter
+
+            icepop_bwd_reduce_scatter(H, W, batch, f, peer.target(), icfg, layout="vd", grad_scale=-1.0)
+            allreduce_stats(f.stats)
+            stream_barrier()
+            peer.fold(dw_shard)
+            return f
         gh, g = icepop_bwd(H, W, batch, f, icfg, layout="vd", grad_scale=-1.0)
         if world > 1:
             allreduce_stats(f.stats)
@@ -289,7 +316,7 @@ def run_ours(args):
                    "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
-                   "popped_fraction": round(diag.clipped_fraction, 6)},
+                   "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective},
         "gpu_launches": launches_per_step * args.steps,
         "step_tflops_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12, 1),
         "step_frac_of_peak_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12 / pk["tflops"], 4),
@@ -552,6 +579,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--no-onpolicy", action="store_true")
+    ap.add_argument("--dw-collective", choices=["fused", "nccl"], default="fused",
+                    help="N>1: dW reduce-scatter fused into K5 over NVLink, or NCCL all-reduce")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)

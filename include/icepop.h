@@ -190,6 +190,37 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
                     float* grad_weight, int32_t accumulate, void* workspace, size_t workspace_bytes,
                     void* stream);
 
+/* ---- fused dW reduce-scatter over NVLink (the step after K5) ---------------- */
+/* grad_weight rows (V for ICEPOP_W_VD, d for ICEPOP_W_DV) are owned ZeRO-style: rank o owns
+ * rows [o*shard_rows, (o+1)*shard_rows). slots[o] is rank o's slot buffer, peer-mapped into
+ * this process (icepop_peer_import): world x shard_rows x row_len floats, row_len = d (VD) or
+ * V (DV). icepop_bwd_bf16_rs is icepop_bwd_bf16 whose last K5 epilogue stores each dW row
+ * (+ this rank's earlier-chunk partial, kept in grad_weight_scratch) straight into the owner's
+ * slot at row rank*shard_rows + (r - o*shard_rows) -- the transfer overlaps the GEMM tile by
+ * tile. After a cross-rank barrier each owner calls icepop_rs_fold on its own slot buffer:
+ * out = sum over ranks in rank order (deterministic). */
+typedef struct icepop_rs_target {
+  int32_t world;      /* 1..8 */
+  int32_t rank;
+  int64_t shard_rows;
+  float* slots[8];
+} icepop_rs_target;
+
+int icepop_bwd_bf16_rs(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
+                       const void* weight, const void* weight_ref, const icepop_saved* saved,
+                       double grad_scale, void* grad_hidden, int32_t grad_hidden_f32,
+                       const icepop_rs_target* rs, float* grad_weight_scratch, void* workspace,
+                       size_t workspace_bytes, void* stream);
+int icepop_rs_fold(const float* slots, int32_t world, int64_t shard_elems, float* out, void* stream);
+
+/* Peer-mapped buffers (CUDA IPC over NVLink): allocate, export a 64-byte handle, import a
+ * peer's handle into this process, close / free. */
+int icepop_peer_alloc(size_t bytes, void** ptr);
+int icepop_peer_free(void* ptr);
+int icepop_peer_export(void* ptr, void* handle64);
+int icepop_peer_import(const void* handle64, void** ptr);
+int icepop_peer_close(void* ptr);
+
 /* K3 alone: dZ[t, v] = grad_scale * coeff_t * (e_{y_t} - softmax(z_t))_v for the
  * shape->n_tokens rows of `hidden`, written as bf16 to dz[t * ldz + v]. The building
  * block icepop_bwd_bf16 chains with K4/K5 (icepop_gemm_bf16); exposed so callers can

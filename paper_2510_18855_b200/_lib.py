@@ -110,6 +110,15 @@ class F64Out(ctypes.Structure):
     ]
 
 
+class RsTarget(ctypes.Structure):
+    _fields_ = [
+        ("world", _i32),
+        ("rank", _i32),
+        ("shard_rows", _i64),
+        ("slots", _c_p * 8),
+    ]
+
+
 _P = ctypes.POINTER
 # name -> (restype, argtypes); every symbol include/icepop.h declares.
 SIGNATURES: dict[str, tuple] = {
@@ -134,6 +143,16 @@ SIGNATURES: dict[str, tuple] = {
         ctypes.c_int,
         [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i32, _c_p, _i32, _c_p, _sz, _c_p],
     ),
+    "icepop_bwd_bf16_rs": (
+        ctypes.c_int,
+        [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i32, _P(RsTarget), _c_p, _c_p, _sz, _c_p],
+    ),
+    "icepop_rs_fold": (ctypes.c_int, [_c_p, _i32, _i64, _c_p, _c_p]),
+    "icepop_peer_alloc": (ctypes.c_int, [_sz, _P(_c_p)]),
+    "icepop_peer_free": (ctypes.c_int, [_c_p]),
+    "icepop_peer_export": (ctypes.c_int, [_c_p, _c_p]),
+    "icepop_peer_import": (ctypes.c_int, [_c_p, _P(_c_p)]),
+    "icepop_peer_close": (ctypes.c_int, [_c_p]),
     "icepop_dz_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i64, _c_p]),
     "icepop_kl_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
     "icepop_sgd_update_f32": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _f64, _f64, _c_p, _c_p]),

@@ -257,7 +257,7 @@ inline int bn_of(int epi) { return epi_dual(epi) ? 128 : BN_; }
 
 int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
              int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent(),
-             const void* B2 = nullptr) {
+             const void* B2 = nullptr, bool keep_empty = false) {
   if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
@@ -279,9 +279,10 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
   sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, sh.k_blocks >= long_k_blocks(), K);
-  sh.ext_dev = ext.dev;
+  sh.ext_dev = ext.dim ? ext.dev : nullptr;
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
+  sh.keep_empty = keep_empty ? 1 : 0;
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;
@@ -714,10 +715,15 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   return ICEPOP_OK;
 }
 
-int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
+}  // extern "C"
+
+// Backward implementation. With `rs`, grad_weight is this rank's LOCAL scratch for earlier
+// token chunks (may be null with a single chunk) and the last chunk's K5 epilogue stores
+// every dW row into its owner's peer slot (fused reduce-scatter over NVLink).
+static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
                     const void* weight_ref, const icepop_saved* saved, double grad_scale, void* grad_hidden,
                     int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate, void* workspace,
-                    size_t workspace_bytes, void* stream) {
+                    size_t workspace_bytes, void* stream, const icepop_rs_target* rs) {
   ICP_TRY(check_shape(shape, true));
   ICP_TRY(check_config(cfg));
   if (!saved || !saved->tokens || !saved->lse || !saved->coeff) return fail(ICEPOP_EINVAL, "null saved tensors");
@@ -733,6 +739,7 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
   const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  if (N == 0 && rs) return fail(ICEPOP_EINVAL, "fused reduce-scatter needs at least one local token");
   if (N == 0) {
     if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
     return ICEPOP_OK;
@@ -772,15 +779,19 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
                                         w.coeff_act, N);
     ICP_CUDA(cudaGetLastError());
     if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));
-    if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
+    if (grad_weight && (!accumulate || rs)) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
     hsrc = w.hid_act;
     tok_src = w.tok_act;
     lse_src = w.lse_act;
     coeff_src = w.coeff_act;
   }
 
+  const int64_t n_chunks = (N + chunk - 1) / chunk;
+  if (rs && n_chunks > 1 && !grad_weight)
+    return fail(ICEPOP_EINVAL, "fused reduce-scatter over several dZ chunks needs a local grad_weight scratch");
   for (int64_t c0 = 0; c0 < N; c0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, N - c0);
+    const bool last = c0 + chunk >= N;
     const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hsrc) + c0 * d;
     Extent ext_m, ext_k;
     if (skip) {
@@ -813,22 +824,100 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
       ICP_TRY(run_umma(EPI_STORE, w.dz, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m));
     }
     // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
-    if (grad_weight) {
+    if (grad_weight || (rs && last)) {
       EpiParams ew;
       memset(&ew, 0, sizeof(ew));
       ew.out = grad_weight;
       ew.out_f32 = 1;
       ew.accumulate = (skip || accumulate || c0 > 0) ? 1 : 0;
-      ew.vec_ok = ((reinterpret_cast<uintptr_t>(grad_weight) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
+      if (rs && last) {
+        // fused reduce-scatter: store each row (+ this rank's earlier-chunk partial) into the
+        // owner's slot over NVLink
+        ew.rs_world = rs->world;
+        ew.rs_rank = rs->rank;
+        ew.rs_shard_rows = rs->shard_rows;
+        for (int o = 0; o < rs->world; ++o) ew.rs_slots[o] = rs->slots[o];
+        ew.acc_src = (n_chunks > 1) ? grad_weight : nullptr;
+        ew.out = nullptr;
+        ext_k.dim = skip ? 2 : 0;
+      }
+      const void* ovec = rs && last ? (const void*)rs->slots[0] : (const void*)grad_weight;
+      ew.vec_ok = ((reinterpret_cast<uintptr_t>(ovec) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
       if (dv) {
         ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st, ext_k));
+        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st, ext_k, nullptr, rs && last));
       } else {
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st, ext_k));
+        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, rs && last));
       }
     }
   }
+  return ICEPOP_OK;
+}
+
+extern "C" {
+
+int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
+                    const void* weight_ref, const icepop_saved* saved, double grad_scale, void* grad_hidden,
+                    int32_t grad_hidden_f32, float* grad_weight, int32_t accumulate, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  return bwd_impl(shape, cfg, hidden, weight, weight_ref, saved, grad_scale, grad_hidden, grad_hidden_f32,
+                  grad_weight, accumulate, workspace, workspace_bytes, stream, nullptr);
+}
+
+int icepop_bwd_bf16_rs(const icepop_shape* shape, const icepop_config* cfg, const void* hidden, const void* weight,
+                       const void* weight_ref, const icepop_saved* saved, double grad_scale, void* grad_hidden,
+                       int32_t grad_hidden_f32, const icepop_rs_target* rs, float* grad_weight_scratch,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!rs || rs->world < 1 || rs->world > 8 || rs->rank < 0 || rs->rank >= rs->world || rs->shard_rows <= 0)
+    return fail(ICEPOP_EINVAL, "invalid reduce-scatter target");
+  const int64_t rows = shape ? (shape->weight_layout == ICEPOP_W_DV ? shape->hidden : shape->vocab) : 0;
+  if ((int64_t)rs->world * rs->shard_rows < rows) return fail(ICEPOP_EINVAL, "shards do not cover grad_weight");
+  for (int o = 0; o < rs->world; ++o)
+    if (!rs->slots[o]) return fail(ICEPOP_EINVAL, "null peer slot %d", o);
+  return bwd_impl(shape, cfg, hidden, weight, weight_ref, saved, grad_scale, grad_hidden, grad_hidden_f32,
+                  grad_weight_scratch, 0, workspace, workspace_bytes, stream, rs);
+}
+
+int icepop_rs_fold(const float* slots, int32_t world, int64_t shard_elems, float* out, void* stream) {
+  if (!slots || !out || world < 1 || shard_elems < 0 || shard_elems % 4 != 0)
+    return fail(ICEPOP_EINVAL, "invalid fold arguments (shard_elems must be a multiple of 4)");
+  const int64_t n4 = shard_elems / 4;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, (int64_t)num_sms() * 8));
+  k_rs_fold<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const float4*>(slots), world, n4,
+                                                                 reinterpret_cast<float4*>(out));
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_peer_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(ICEPOP_EINVAL, "null out pointer");
+  ICP_CUDA(cudaMalloc(ptr, std::max<size_t>(bytes, 256)));
+  return ICEPOP_OK;
+}
+
+int icepop_peer_free(void* ptr) {
+  ICP_CUDA(cudaFree(ptr));
+  return ICEPOP_OK;
+}
+
+int icepop_peer_export(void* ptr, void* handle) {
+  if (!ptr || !handle) return fail(ICEPOP_EINVAL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  ICP_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle), ptr));
+  return ICEPOP_OK;
+}
+
+int icepop_peer_import(const void* handle, void** ptr) {
+  if (!ptr || !handle) return fail(ICEPOP_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  ICP_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ICEPOP_OK;
+}
+
+int icepop_peer_close(void* ptr) {
+  ICP_CUDA(cudaIpcCloseMemHandle(ptr));
   return ICEPOP_OK;
 }
 

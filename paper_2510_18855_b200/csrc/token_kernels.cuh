@@ -366,6 +366,20 @@ __global__ void k_sgd_update(float* __restrict__ w, const float* __restrict__ g,
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, ICEPOP_ERR_NONFINITE);
 }
 
+// ------------------------------------------------------------------ reduce-scatter fold
+// out[i] = sum_r slots[r][i] in rank order (deterministic), the owner's half of the fused
+// dW reduce-scatter (the K5 epilogue already placed every rank's rows in its slot).
+__global__ void k_rs_fold(const float4* __restrict__ slots, int world, int64_t n4, float4* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 s = slots[i];
+    for (int r = 1; r < world; ++r) {
+      const float4 x = slots[(int64_t)r * n4 + i];
+      s.x += x.x; s.y += x.y; s.z += x.z; s.w += x.w;
+    }
+    out[i] = s;
+  }
+}
+
 // ------------------------------------------------------------------ active-row compaction
 // Rows whose gradient coefficient is exactly zero (popped tokens, clip-inactive tokens,
 // zero-advantage sequences) have dZ == 0 (objective.py:250-252), so the backward GEMMs run

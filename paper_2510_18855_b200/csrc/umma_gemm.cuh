@@ -45,6 +45,7 @@ struct GemmShape {
   const int32_t* ext_dev;
   int32_t ext_base;
   int32_t ext_dim;
+  int32_t keep_empty;  // K extent 0: still run the tiles (the epilogue stores zeros + acc_src)
 };
 
 // Resolve a device-side extent into the shape every role of the kernel uses.
@@ -57,7 +58,7 @@ __device__ __forceinline__ void resolve_extent(GemmShape& sh, int tile_m, int bn
   } else {
     sh.K = e;
     sh.k_blocks = (e + 63) / 64;
-    if (sh.k_blocks == 0) sh.m_tiles = 0;  // nothing to accumulate
+    if (sh.k_blocks == 0 && !sh.keep_empty) sh.m_tiles = 0;  // nothing to accumulate
   }
   (void)bn;
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
@@ -89,6 +90,14 @@ struct EpiParams {
   int64_t ldz;
   int32_t zero_rows_to;    // EPI_DZ: rows in [M, zero_rows_to) of the last tile are written as 0
   const int32_t* row_index;  // EPI_STORE: output row of GEMM row m is row_index[m] (scatter), or null
+  // EPI_STORE fused reduce-scatter (dW over NVLink peer memory): output row m belongs to rank
+  // o = m / rs_shard_rows and is stored into rs_slots[o] at slot row rs_rank * rs_shard_rows +
+  // (m - o * rs_shard_rows), plus acc_src[m, :] (this rank's earlier-chunk partial) if given.
+  int32_t rs_world;
+  int32_t rs_rank;
+  int64_t rs_shard_rows;
+  float* rs_slots[8];
+  const float* acc_src;
   // EPI_DZ_REF
   const float* lse_ref;    // [M] natural units
   const float* kl;         // [M] kl_t
@@ -137,6 +146,31 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
     const int col0 = n0 + c * 32;
     if (!row_ok || col0 >= sh.N) continue;
     const bool full = (col0 + 32 <= sh.N) && ep.vec_ok;
+    if (ep.rs_world > 0) {
+      if (sh.k_blocks == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;  // empty K extent: TMEM was never written
+      }
+      const int64_t o = m / ep.rs_shard_rows;
+      float* dst = ep.rs_slots[o] + ((int64_t)ep.rs_rank * ep.rs_shard_rows + (m - o * ep.rs_shard_rows)) * ep.ldo + col0;
+      const float* src = ep.acc_src ? ep.acc_src + (int64_t)m * ep.ldo + col0 : nullptr;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          if (src) {
+            const float4 p = *reinterpret_cast<const float4*>(src + j);
+            x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+          }
+          *reinterpret_cast<float4*>(dst + j) = x;  // NVLink store into the owner's slot
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < sh.N) dst[j] = src ? src[j] + v[j] : v[j];
+      }
+      continue;
+    }
     if (ep.out_f32) {
       float* dst = reinterpret_cast<float*>(ep.out) + (int64_t)m * ep.ldo + col0;
       if (full) {
@@ -669,6 +703,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();

@@ -9,7 +9,10 @@ The only collectives are the ones the objective really needs:
 * ``allreduce_stats`` -- the fp64 partial sums (J, popped / token counts, entropy and
   log-prob sums, KL) summed across ranks, and the device error word OR-ed;
 * ``allreduce_grad``  -- dW summed across ranks, in buckets on a side stream so it can
-  overlap later work (dHidden stays rank-local).
+  overlap later work (dHidden stays rank-local);
+* ``PeerSlots``       -- the fused alternative: K5's epilogue stores every dW row straight
+  into its owner rank's slot over NVLink (CUDA IPC peer memory), so the reduce-scatter
+  overlaps the GEMM tile by tile; the owner then folds the slots in rank order.
 
 All of it is plain ``torch.distributed`` (NCCL on the GPU box, gloo in the CPU tests).
 """
@@ -102,3 +105,108 @@ def allreduce_grad(grad: torch.Tensor, group=None, bucket_bytes: int = 256 << 20
 def wait_grad(handles) -> None:
     for h in handles or ():
         h.wait()
+
+
+def stream_barrier(group=None, device=None) -> None:
+    """Cross-rank barrier ordered on the current stream (a 1-element NCCL all-reduce): work
+    queued after it starts only when every rank has finished the work queued before it."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    t = torch.zeros(1, device=device if device is not None else torch.cuda.current_device())
+    dist.all_reduce(t, group=group)
+
+
+class PeerSlots:
+    """Peer-mapped slot buffers for the fused dW reduce-scatter (include/icepop.h).
+
+    Collective constructor: every rank allocates world x shard_rows x row_len fp32 (its slot
+    buffer), exports a CUDA IPC handle, all-gathers the handles and imports the peers'
+    buffers. ``target()`` is the icepop_rs_target for icepop_bwd_bf16_rs; ``fold(out)`` sums
+    this rank's slots in rank order into `out` (its dW shard) after ``stream_barrier``.
+    """
+
+    def __init__(self, shard_rows: int, row_len: int, group=None, _ops=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 8:
+            raise ValueError("the fused reduce-scatter supports up to 8 ranks (one NVSwitch node)")
+        self.shard_rows, self.row_len = int(shard_rows), int(row_len)
+        self.shard_elems = self.shard_rows * self.row_len
+        if self.shard_elems % 4:
+            raise ValueError("shard_rows * row_len must be a multiple of 4")
+        ops = _ops or _LibPeerOps()
+        self._ops = ops
+        self.local = ops.alloc(self.world * self.shard_elems * 4)
+        handle = ops.export(self.local)
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, handle, group=group)
+        else:
+            handles = [handle]
+        self.slots = []
+        self._imported = []
+        for o, h in enumerate(handles):
+            if o == self.rank:
+                self.slots.append(self.local)
+            else:
+                p = ops.import_(h)
+                self._imported.append(p)
+                self.slots.append(p)
+
+    def target(self) -> _lib.RsTarget:
+        t = _lib.RsTarget(world=self.world, rank=self.rank, shard_rows=self.shard_rows)
+        for o, p in enumerate(self.slots):
+            t.slots[o] = p
+        return t
+
+    def fold(self, out: torch.Tensor) -> torch.Tensor:
+        """out (fp32, shard_elems) = sum of this rank's slots over ranks 0..world-1."""
+        if out.dtype != torch.float32 or out.numel() != self.shard_elems or not out.is_contiguous():
+            raise ValueError("out must be a contiguous fp32 tensor of shard_rows * row_len elements")
+        self._ops.fold(self.local, self.world, self.shard_elems, out)
+        return out
+
+    def close(self) -> None:
+        for p in self._imported:
+            self._ops.close(p)
+        self._imported = []
+        if self.local:
+            self._ops.free(self.local)
+            self.local = None
+
+
+class _LibPeerOps:
+    """libicepop's peer-memory entry points (CUDA IPC)."""
+
+    def __init__(self):
+        import ctypes
+
+        self._ct = ctypes
+        self.lib = _lib.load()
+
+    def alloc(self, nbytes):
+        p = self._ct.c_void_p()
+        _lib.check(self.lib.icepop_peer_alloc(nbytes, self._ct.byref(p)))
+        return p.value
+
+    def export(self, ptr):
+        h = (self._ct.c_ubyte * 64)()
+        _lib.check(self.lib.icepop_peer_export(ptr, h))
+        return bytes(h)
+
+    def import_(self, handle):
+        buf = (self._ct.c_ubyte * 64).from_buffer_copy(handle)
+        p = self._ct.c_void_p()
+        _lib.check(self.lib.icepop_peer_import(buf, self._ct.byref(p)))
+        return p.value
+
+    def fold(self, local, world, shard_elems, out):
+        _lib.check(self.lib.icepop_rs_fold(local, world, shard_elems, out.data_ptr(),
+                                           torch.cuda.current_stream(out.device).cuda_stream))
+
+    def close(self, ptr):
+        _lib.check(self.lib.icepop_peer_close(ptr))
+
+    def free(self, ptr):
+        _lib.check(self.lib.icepop_peer_free(ptr))

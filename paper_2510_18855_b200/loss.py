@@ -433,6 +433,45 @@ def icepop_bwd(
     raise ValueError(f"unsupported dtype {hidden.dtype}")
 
 
+def icepop_bwd_reduce_scatter(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    batch: PackedBatch,
+    fwd: IcePopForward,
+    rs_target,
+    cfg: IcePopConfig = IcePopConfig(),
+    layout: str = "vd",
+    grad_scale: float = 1.0,
+    need_hidden: bool = True,
+    weight_ref: torch.Tensor | None = None,
+    grad_hidden_dtype: torch.dtype | None = None,
+) -> torch.Tensor | None:
+    """Backward whose dW leaves this rank inside K5's epilogue: every row goes to its owner's
+    peer slot (``distributed.PeerSlots.target()``). Returns dHidden; dW is obtained by each
+    owner with ``PeerSlots.fold`` after ``distributed.stream_barrier``."""
+    lib = _lib_for(hidden)
+    if hidden.dtype != torch.bfloat16:
+        raise ValueError("the fused reduce-scatter runs on the bf16 path")
+    hidden, weight = hidden.contiguous(), weight.contiguous()
+    shape = _shape(hidden, weight, layout, batch)
+    dev = hidden.device
+    n, d, v = shape.n_tokens, shape.hidden, shape.vocab
+    gh_dtype = grad_hidden_dtype or torch.bfloat16
+    gh = torch.empty((n, d), dtype=gh_dtype, device=dev) if need_hidden else None
+    cb = _dz_chunk_bytes(dev)
+    rows = cb // (2 * v)
+    chunk = n if rows >= n else max(128, rows // 128 * 128)
+    scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev) if chunk < n else None
+    ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, cb), dtype=torch.uint8, device=dev)
+    wr = weight_ref.contiguous() if weight_ref is not None else None
+    saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
+                       lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")))
+    _lib.check(lib.icepop_bwd_bf16_rs(shape, cfg.to_c(), hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
+                                      float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
+                                      rs_target, _lib.ptr(scratch), ws.data_ptr(), ws.numel(), _stream(dev)))
+    return gh
+
+
 def finish(stats: torch.Tensor) -> None:
     """One host sync; raise NumericError/ValueError from the device error word."""
     lib = _lib.load()

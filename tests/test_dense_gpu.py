@@ -425,3 +425,52 @@ def test_cuda_graph_capture_replays_fwd_bwd(cuda_device):
         torch.cuda.synchronize()
         assert torch.equal(fg.stats, f0.stats) and torch.equal(fg.kept, f0.kept)
         assert torch.equal(ghg, gh0) and torch.equal(gwg, gw0)
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+@pytest.mark.parametrize("world,chunked", [(1, False), (3, False), (3, True), (4, True)])
+def test_fused_reduce_scatter_emulated_ranks(cuda_device, monkeypatch, layout, world, chunked):
+    """K5 epilogue stores each dW row into its owner's slot (the NVLink path), emulated with
+    `world` token-shard ranks run one after another on one GPU against slot buffers in device
+    memory (no kernel waits on another); the owners' ordered folds reassemble dW exactly as
+    the single-rank backward computes it."""
+    import paper_2510_18855_b200.loss as L
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.distributed import shard_range
+
+    c = _case(n_seqs=6, seed=47, layout=layout, lens=[300, 170, 260, 90, 410, 333])
+    c["adv"] = c["adv"].copy()
+    c["adv"][[2, 3]] = 0.0  # exercise row skipping inside the ranks
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = L.IcePopConfig()
+    full_b = _batch(c, cuda_device)
+    f = L.icepop_fwd(H, W, full_b, cfg, layout=layout)
+    _, gw_ref = L.icepop_bwd(H, W, full_b, f, cfg, layout=layout, need_hidden=False)
+    rows, row_len = W.shape  # dW has the weight's layout: rows = V (vd) or d (dv)
+    V = W.shape[0] if layout == "vd" else W.shape[1]
+    shard_rows = -(-rows // world)
+    while (shard_rows * row_len) % 4:  # the fold works on float4
+        shard_rows += 1
+    slot_bufs = [torch.full((world * shard_rows * row_len,), float("nan"), device=cuda_device) for _ in range(world)]
+    if chunked:
+        monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * V * 2)  # 256-row dZ chunks -> local scratch path
+    N = len(c["tokens"])
+    for r in range(world):
+        s, e = shard_range(N, world, r)
+        b = _batch(c, cuda_device, slice(s, e))
+        fr = L.icepop_fwd(H[s:e], W, b, cfg, layout=layout)
+        t = _lib.RsTarget(world=world, rank=r, shard_rows=shard_rows)
+        for o in range(world):
+            t.slots[o] = slot_bufs[o].data_ptr()
+        L.icepop_bwd_reduce_scatter(H[s:e], W, b, fr, t, cfg, layout=layout, need_hidden=False)
+    lib = _lib.ensure_device(0)
+    shards = []
+    for o in range(world):
+        out = torch.empty(shard_rows * row_len, device=cuda_device)
+        _lib.check(lib.icepop_rs_fold(slot_bufs[o].data_ptr(), world, shard_rows * row_len, out.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream))
+        shards.append(out.view(shard_rows, row_len))
+    gw = torch.cat(shards)[:rows]
+    torch.cuda.synchronize()
+    assert torch.isfinite(gw).all()
+    assert _rel(gw.cpu().numpy(), gw_ref.cpu().numpy()) < 1e-5

@@ -171,3 +171,43 @@ def test_sharded_sgd_step_reduce_scatter_all_gather(world):
     for wb, ref in out:
         np.testing.assert_allclose(wb, ref, rtol=1e-2, atol=1e-2)
     assert all(np.array_equal(out[0][0], o[0]) for o in out)
+
+
+class _FakePeerOps:
+    """Host stand-in for the CUDA IPC entry points: 'pointers' are ids, handles are bytes."""
+
+    def __init__(self, rank):
+        self.rank = rank
+
+    def alloc(self, nbytes):
+        return 1000 + self.rank
+
+    def export(self, ptr):
+        return f"handle-{ptr}".encode()
+
+    def import_(self, handle):
+        return 5000 + int(handle.decode().split("-")[1])
+
+    def close(self, ptr):
+        pass
+
+    def free(self, ptr):
+        pass
+
+
+def _peer_slots_fn(rank, world):
+    from paper_2510_18855_b200.distributed import PeerSlots
+
+    ps = PeerSlots(shard_rows=5, row_len=8, _ops=_FakePeerOps(rank))
+    t = ps.target()
+    return [t.slots[o] for o in range(world)], t.world, t.rank, t.shard_rows
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_slots_exchange_handles(world):
+    """Every rank maps every owner's slot buffer: its own locally, the others via import."""
+    out = run_ranks(_peer_slots_fn, world=world)
+    for r, (slots, w, rk, sr) in enumerate(out):
+        assert (w, rk, sr) == (world, r, 5)
+        assert slots[r] == 1000 + r
+        assert [s for o, s in enumerate(slots) if o != r] == [5000 + 1000 + o for o in range(world) if o != r]
