@@ -283,6 +283,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
   sh.keep_empty = keep_empty ? 1 : 0;
+  static const int sleep_ns = env_int("ICEPOP_EPI_SLEEP_NS", 0);
+  sh.epi_sleep_ns = (uint32_t)sleep_ns;
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;

@@ -46,6 +46,7 @@ struct GemmShape {
   int32_t ext_base;
   int32_t ext_dim;
   int32_t keep_empty;  // K extent 0: still run the tiles (the epilogue stores zeros + acc_src)
+  uint32_t epi_sleep_ns;  // backoff of the epilogue warps' wait for a finished accumulator
 };
 
 // Resolve a device-side extent into the shape every role of the kernel uses.
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int m_blk, n_blk;
       tile_coords(sh, tile, m_blk, n_blk);
       const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
-      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
