@@ -178,10 +178,10 @@ int cta_group() {
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
-int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const GemmShape& sh,
-                   const EpiParams& ep, cudaStream_t st) {
+int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
+                   const GemmShape& sh, const EpiParams& ep, cudaStream_t st) {
   auto kern = umma_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
-  constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI)>::SMEM;
+  constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI), EPI == EPI_DZ>::SMEM;
   // the smem attribute is per device: one bit per device index that has it set
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -205,16 +205,16 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tb2, sh, ep));
+  ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tb2, tc, sh, ep));
   return ICEPOP_OK;
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const GemmShape& sh,
-                const EpiParams& ep, cudaStream_t st, int cg) {
+int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
+                const GemmShape& sh, const EpiParams& ep, cudaStream_t st, int cg) {
   constexpr int BN = epi_dual(EPI) ? 128 : BN_;
-  if (cg == 2) return launch_umma_cg<BN, A_MN, B_MN, EPI, 2>(ta, tb, tb2, sh, ep, st);
-  return launch_umma_cg<BN, A_MN, B_MN, EPI, 1>(ta, tb, tb2, sh, ep, st);
+  if (cg == 2) return launch_umma_cg<BN, A_MN, B_MN, EPI, 2>(ta, tb, tb2, tc, sh, ep, st);
+  return launch_umma_cg<BN, A_MN, B_MN, EPI, 1>(ta, tb, tb2, tc, sh, ep, st);
 }
 
 // Tile raster: `group_m` m-tiles sweep the n dimension together. ICEPOP_GROUP_M overrides
@@ -269,6 +269,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, bn / cg));
   if (B2) ICP_TRY(operand_map(&tb2, B2, N, K, ldb, b_mn, bn / cg));
   else tb2 = tb;
+  CUtensorMap tc = tb;  // EPI_DZ: bf16 dZ [zero_rows_to, N] store map (32 rows x 64 cols boxes, SW128)
+  if (epi == EPI_DZ) ICP_TRY(encode_2d(&tc, ep.dz, (uint64_t)N, (uint64_t)ep.zero_rows_to, (uint64_t)ep.ldz, 64, 32));
   GemmShape sh;
   sh.M = (int)M;
   sh.N = (int)N;
@@ -285,6 +287,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.keep_empty = keep_empty ? 1 : 0;
   static const int sleep_ns = env_int("ICEPOP_EPI_SLEEP_NS", 0);
   sh.epi_sleep_ns = (uint32_t)sleep_ns;
+  static const int dz_tma = env_int("ICEPOP_DZ_TMA_STORE", 1);
+  sh.dz_tma_store = dz_tma;
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;
@@ -295,25 +299,25 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
     ICP_TRY(tile_counter(st, &sh.tile_counter));
   }
   if (epi == EPI_STORE) {
-    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
-    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
-    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
-    return launch_umma<true, true, EPI_STORE>(ta, tb, tb2, sh, ep, st, cg);
+    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
+    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
+    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
+    return launch_umma<true, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
   }
   if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
   switch (epi) {
     case EPI_LSE:
-      return b_mn ? launch_umma<false, true, EPI_LSE>(ta, tb, tb2, sh, ep, st, cg)
-                  : launch_umma<false, false, EPI_LSE>(ta, tb, tb2, sh, ep, st, cg);
+      return b_mn ? launch_umma<false, true, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg);
     case EPI_DZ:
-      return b_mn ? launch_umma<false, true, EPI_DZ>(ta, tb, tb2, sh, ep, st, cg)
-                  : launch_umma<false, false, EPI_DZ>(ta, tb, tb2, sh, ep, st, cg);
+      return b_mn ? launch_umma<false, true, EPI_DZ>(ta, tb, tb2, tc, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_DZ>(ta, tb, tb2, tc, sh, ep, st, cg);
     case EPI_LSE_REF:
-      return b_mn ? launch_umma<false, true, EPI_LSE_REF>(ta, tb, tb2, sh, ep, st, cg)
-                  : launch_umma<false, false, EPI_LSE_REF>(ta, tb, tb2, sh, ep, st, cg);
+      return b_mn ? launch_umma<false, true, EPI_LSE_REF>(ta, tb, tb2, tc, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_LSE_REF>(ta, tb, tb2, tc, sh, ep, st, cg);
     case EPI_DZ_REF:
-      return b_mn ? launch_umma<false, true, EPI_DZ_REF>(ta, tb, tb2, sh, ep, st, cg)
-                  : launch_umma<false, false, EPI_DZ_REF>(ta, tb, tb2, sh, ep, st, cg);
+      return b_mn ? launch_umma<false, true, EPI_DZ_REF>(ta, tb, tb2, tc, sh, ep, st, cg)
+                  : launch_umma<false, false, EPI_DZ_REF>(ta, tb, tb2, tc, sh, ep, st, cg);
     default:
       return fail(ICEPOP_EINVAL, "unknown epilogue %d", epi);
   }

@@ -47,6 +47,7 @@ struct GemmShape {
   int32_t ext_dim;
   int32_t keep_empty;  // K extent 0: still run the tiles (the epilogue stores zeros + acc_src)
   uint32_t epi_sleep_ns;  // backoff of the epilogue warps' wait for a finished accumulator
+  int32_t dz_tma_store;   // EPI_DZ: stage dZ tiles in smem and write them with TMA (else direct stores)
 };
 
 // Resolve a device-side extent into the shape every role of the kernel uses.
@@ -109,7 +110,7 @@ struct EpiParams {
 // CG = 2: a CTA pair computes a 256 x BN tile with cta_group::2 MMAs issued by the leader;
 //         each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so the B operand
 //         is read from L2 once per pair instead of once per CTA.
-template <int BN, int CG, bool DUAL = false>
+template <int BN, int CG, bool DUAL = false, bool EPI_STAGING = false>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
@@ -120,7 +121,10 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN * NACC;        // double-buffered
   static constexpr int TILE_M = BM * CG;
   static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
-  static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256;
+  // EPI_DZ TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 128 B, SWIZZLE_128B)
+  static constexpr int EPI_BUF_BYTES = 32 * 128;
+  static constexpr int EPI_STAGE_BYTES = EPI_STAGING ? 4 * 2 * EPI_BUF_BYTES : 0;
+  static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 256;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& m_blk, int& n_blk) {
@@ -314,6 +318,61 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
   }
 }
 
+// dZ epilogue with TMA stores: per 64-column slab the warp stages its 32 rows x 128 B
+// (SWIZZLE_128B, conflict-free 16-byte smem stores) and lane 0 issues one bulk tensor store;
+// two staging buffers per warp alternate. Rows past the device-side extent but inside the
+// tensor map (< zero_rows_to) are stored as zeros; the tensor map clips rows >= zero_rows_to
+// and columns >= V.
+template <int BN>
+__device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
+                                           uint8_t* stage2, int& ebuf, int m0, int n0, int row, int lane,
+                                           int quarter, uint32_t taddr) {
+  const int m = m0 + row;
+  const bool live = m < sh.M;
+  const float lse2 = live ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
+  const float cf = live ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
+  const int y = live ? __ldg(ep.targets + m) : -1;
+  const int row0 = m0 + quarter * 32;  // first row of this warp's slab
+  const bool warp_rows = row0 < ep.zero_rows_to;  // warp-uniform: any of its rows inside the map
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    float v[32], w[32];
+    tmem_ld32(taddr + c * 64, v);
+    tmem_ld32(taddr + c * 64 + 32, w);
+    const int col0 = n0 + c * 64;
+    if (!warp_rows || col0 >= sh.N) continue;  // warp-uniform
+    uint8_t* buf = stage2 + ebuf * (32 * 128);
+    // the bulk store that last read this buffer must be done reading
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    uint32_t pk[32];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float p0 = fast_exp2(fmaf(v[2 * j], ep.scale_log2, -lse2));
+      const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
+      const float q0 = fast_exp2(fmaf(w[2 * j], ep.scale_log2, -lse2));
+      const float q1 = fast_exp2(fmaf(w[2 * j + 1], ep.scale_log2, -lse2));
+      pk[j] = live ? pack_bf16x2(fmaf(-cf, p0, (col0 + 2 * j == y) ? cf : 0.f),
+                                 fmaf(-cf, p1, (col0 + 2 * j + 1 == y) ? cf : 0.f)) : 0u;
+      pk[16 + j] = live ? pack_bf16x2(fmaf(-cf, q0, (col0 + 32 + 2 * j == y) ? cf : 0.f),
+                                      fmaf(-cf, q1, (col0 + 32 + 2 * j + 1 == y) ? cf : 0.f)) : 0u;
+    }
+    // row `lane` of the slab: 8 x 16-byte chunks, chunk k at position k ^ (lane & 7) (SWIZZLE_128B)
+    uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
+          make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmC, smem_u32(buf), col0, row0);
+      bulk_commit();
+    }
+    ebuf ^= 1;
+  }
+}
+
 // KL-to-ref forward epilogue: as epi_lse for z (accumulator 0) plus, for z_ref (accumulator
 // 1 = TMEM column + BN), the ref online (max, sum) and the cross term
 // x = sum_j 2^(u_j - mx) (u_j - ur_j), u = z log2(e): after the merge,
@@ -439,9 +498,11 @@ __device__ __forceinline__ void epi_dz_ref(const GemmShape& sh, const EpiParams&
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmB2, const GemmShape sh_in, const EpiParams ep) {
+                     const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                     const GemmShape sh_in, const EpiParams ep) {
   constexpr bool DUAL = epi_dual(EPI);
-  using Cfg = GemmCfg<BN, CG, DUAL>;
+  constexpr bool STAGING = EPI == EPI_DZ;
+  using Cfg = GemmCfg<BN, CG, DUAL, STAGING>;
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
   constexpr int STAGES = Cfg::STAGES;
@@ -452,7 +513,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sB2 = sB + STAGES * Cfg::B_BYTES;  // DUAL only
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sEpi = smem + STAGES * Cfg::STAGE_BYTES;  // STAGING only (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + Cfg::EPI_STAGE_BYTES);
   // barrier block: full[S] empty[S] tfull[2] tempty[2] rfull[RING] | tmem_holder | ring[RING]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::RING);
   int32_t* ring = reinterpret_cast<int32_t*>(tmem_holder + 1);
@@ -478,6 +540,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     if (DUAL) prefetch_tmap(&tmB2);
+    if (STAGING) prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       // Only the pair leader arrives (with expect_tx covering BOTH CTAs' TMA bytes); the peer's
       // loads just complete_tx on it. A per-k-block remote arrive from the peer would cost a
@@ -682,6 +745,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int ebuf = 0;  // STAGING: which of this warp's two staging buffers is next
+    (void)ebuf;
     for (int j = 0;; ++j) {
       const int tile = ring_get(j, false);
       if (tile < 0) break;
@@ -693,7 +758,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
-      if (EPI == EPI_DZ) epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      if (EPI == EPI_DZ) {
+        if (sh.dz_tma_store)
+          epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
+                         quarter, taddr);
+        else
+          epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      }
       if (EPI == EPI_LSE_REF) epi_lse_ref<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
       if (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       tc_fence_before();
@@ -705,6 +776,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
+    if (STAGING && lane == 0) bulk_wait<0>();  // all dZ tile stores complete
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
