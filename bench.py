@@ -4,7 +4,9 @@
     torchrun --nproc-per-node N bench.py --gpus N ...        (token-sharded, weak scaling)
 
 A step = one IcePop forward (K0 advantages, K1 fused lm_head GEMM + online softmax, K2
-epilogue) + backward (K3 recompute -> bf16 dZ chunks, K4 dHidden, K5 dW) over one batch
+epilogue) + backward (bf16 dZ -- formed in place from the probabilities K1 stored when they
+fit in HBM ("stored-probabilities" mode, the default at C2), else recomputed by the K3 GEMM
+in chunks -- then K4 dHidden, K5 dW) over one batch
 of synthetic inputs of the named config, plus (N>1) the NCCL all-reduce of the fp64
 statistics and of dW. `value` is measured with inputs resident in HBM; `e2e` goes
 through the public API from pinned host buffers with the H2D copies of the step's
@@ -175,7 +177,8 @@ def run_ours(args):
 
     from paper_2510_18855_b200 import _lib  # noqa: F401
     from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
-    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, _dz_chunk_bytes, finish, icepop_bwd, icepop_fwd
+    from paper_2510_18855_b200.loss import (Diagnostics, IcePopConfig, _dz_chunk_bytes, _resolve_store_probs, finish,
+                                            icepop_bwd, icepop_fwd)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -189,11 +192,13 @@ def run_ours(args):
     H, W, batch, onpolicy = build_device_inputs(cfg, meta, dev, rank)
     icfg = IcePopConfig()
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
+    sp = _resolve_store_probs(None, N, V, dev, False)
     rows = _dz_chunk_bytes(dev) // (2 * V)
-    chunk = N if rows >= N else max(128, rows // 128 * 128)
+    chunk = N if (sp or rows >= N) else max(128, rows // 128 * 128)
     n_chunks = -(-N // chunk)
-    # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: 4 compaction kernels + (K3, K4, K5) per chunk
-    launches_per_step = 6 + 4 + 3 * n_chunks
+    # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: stored probabilities -> dZ pass,
+    # K4, K5; recompute -> 4 compaction kernels + (K3, K4, K5) per chunk
+    launches_per_step = 6 + (3 if sp else 4 + 3 * n_chunks)
 
     # dW collective for N > 1: fused reduce-scatter inside K5's epilogue over NVLink peer memory
     # (each rank ends with its ZeRO shard of the summed dW), or NCCL all-reduce of the full dW.
@@ -215,7 +220,7 @@ def run_ours(args):
 
     def step_into():
         # loss = -J: grad_scale -1 gives d(loss)/d(hidden), d(loss)/d(W)
-        f = icepop_fwd(H, W, batch, icfg, layout="vd")
+        f = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=sp)
         if collective == "fused":
             from paper_2510_18855_b200.distributed import stream_barrier
             from paper_2510_18855_b200.loss import icepop_bwd_reduce_scatter
@@ -297,12 +302,12 @@ def run_ours(args):
                    "with lp_train_old recorded by icepop_logprob_bf16: GEMM-free exact forward + full backward"}
 
     # ---------------- per-kernel timing pass (same work, events between launches)
-    kern = kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev) if not args.no_kernel_timing else {}
+    kern = kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp) if not args.no_kernel_timing else {}
 
     # ---------------- end-to-end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(H, W, batch, icfg, args, dev, world)
+        e2e = run_e2e(H, W, batch, icfg, args, dev, world, sp)
 
     tokens_total = N * world
     value = tokens_total / (ms / 1e3)
@@ -315,6 +320,7 @@ def run_ours(args):
                    "seq_len": cfg["seq_len"] or "ragged",
                    "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
+                   "dz_mode": "stored-probabilities" if sp else "recompute",
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
                    "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective},
         "gpu_launches": launches_per_step * args.steps,
@@ -339,7 +345,16 @@ def run_ours(args):
                             "flop_per_launch": kern[dom]["flop"], "peak_kind": "burst (%s)" % pk["source"],
                             "frac_of_sustained": round(ach / pk["tflops_sustained"], 4) if pk["tflops_sustained"]
                             else None}
-        line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()}
+        line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()
+                                  if v["flop"]}
+        if "dZ_from_probs" in kern:  # the HBM-bound pass of the stored-probabilities backward
+            kz = kern["dZ_from_probs"]
+            gbs = kz["bytes"] / (kz["ms"] / 1e3) / 1e9
+            line["roofline_dz"] = {"bound": "hbm", "kernel": "dZ_from_probs", "achieved": round(gbs, 1),
+                                   "peak": pk["hbm"], "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
+                                   "bytes_per_launch": kz["bytes"],
+                                   "bytes_note": "algorithmic: read + write bf16 q/dZ of the active rows, "
+                                                 "write-only zero rows, + tile maxima"}
     if e2e:
         line["e2e"] = e2e
     if onp_res:
@@ -355,8 +370,9 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
 
 
-def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev):
-    """Average device time of K1(+K2), K3, K4, K5 launched one by one on the torch stream."""
+def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
+    """Average device time of K1(+K2), the dZ producer (K3 recompute GEMM, or the in-place
+    pass over the stored probabilities), K4, K5 launched one by one on the torch stream."""
     import torch
 
     from paper_2510_18855_b200 import _lib
@@ -367,7 +383,7 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev):
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
     res = {}
 
-    def timed(name, fn, flop, reps=2):
+    def timed(name, fn, flop, reps=2, nbytes=None):
         fn()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -376,34 +392,54 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev):
         b.record(st)
         torch.cuda.synchronize()
         res[name] = {"ms": a.elapsed_time(b) / reps, "flop": flop, "count": 1}
+        if nbytes is not None:
+            res[name]["bytes"] = nbytes
 
     holder = {}
 
     def fwd():
-        holder["f"] = icepop_fwd(H, W, batch, icfg, layout="vd")
+        holder.clear()
+        holder["f"] = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=sp)
 
     timed("K1_fwd_lse+K2", fwd, 2.0 * N * d * V)
     f = holder["f"]
-    nc = min(chunk, N)
-    dz = torch.empty((nc, V), dtype=torch.bfloat16, device=dev)
+    s = st.cuda_stream
+    if sp:
+        # the stored-probabilities backward without K4/K5 (null gradients) is the dZ pass alone;
+        # repeated passes over the same buffer take the same time
+        nc = N
+        dz = f.extras["probs"]
+        tm = f.extras["tile_max"]
+        shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs,
+                           n_groups=batch.n_groups, weight_layout=_lib.W_VD)
+        saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr(),
+                           probs=dz.data_ptr(), tile_max=tm.data_ptr())
+        active = int((f.coeff != 0).sum())
+        nbytes = 4 * active * V + 2 * (N - active) * V + 4 * active * tm.shape[1]
+        timed("dZ_from_probs", lambda: _lib.check(lib.icepop_bwd_bf16(shape, icfg.to_c(), H.data_ptr(), W.data_ptr(),
+                                                                      None, saved, -1.0, None, 0, None, 0, None, 0,
+                                                                      s)), 0.0, nbytes=nbytes)
+    else:
+        nc = min(chunk, N)
+        dz = torch.empty((nc, V), dtype=torch.bfloat16, device=dev)
+        shape = _lib.Shape(n_tokens=nc, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs,
+                           n_groups=batch.n_groups, weight_layout=_lib.W_VD)
+        saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr())
+        timed("K3_dz", lambda: _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), None, saved,
+                                                             -1.0, dz.data_ptr(), V, s)),
+              2.0 * nc * d * V)
     gh = torch.empty((nc, d), dtype=torch.bfloat16, device=dev)
     gw = torch.zeros((V, d), dtype=torch.float32, device=dev)
-    shape = _lib.Shape(n_tokens=nc, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs, n_groups=batch.n_groups,
-                       weight_layout=_lib.W_VD)
-    s = st.cuda_stream
-    saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr())
-    timed("K3_dz", lambda: _lib.check(lib.icepop_dz_bf16(shape, 1.0, H.data_ptr(), W.data_ptr(), None, saved, -1.0,
-                                                         dz.data_ptr(), V, s)),
-          2.0 * nc * d * V)
     timed("K4_dhidden", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), nc, d, V,
                                                                 0, 1, 0, 0, s)), 2.0 * nc * d * V)
     timed("K5_dweight", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, nc,
                                                                 1, 1, 1, 1, s)), 2.0 * nc * d * V)
     del dz, gh, gw
+    holder.clear()
     return res
 
 
-def run_e2e(H, W, batch, icfg, args, dev, world):
+def run_e2e(H, W, batch, icfg, args, dev, world, sp=False):
     """Public API from pinned host inputs: every step's inputs are copied H2D and its loss
     read back D2H inside the timed region. The copy of step k+1 runs on a side stream while
     step k computes (double-buffered device inputs, as a data-loader prefetch would)."""
@@ -440,7 +476,7 @@ def run_e2e(H, W, batch, icfg, args, dev, world):
         main.wait_event(copied[i])
         d = bufs[i]
         b = PackedBatch(d["tokens"], d["lp_old"], d["lp_inf"], d["cu"], d["go"], None, d["rewards"], batch.token_offset)
-        f = icepop_fwd(d["H"], W, b, icfg, layout="vd")
+        f = icepop_fwd(d["H"], W, b, icfg, layout="vd", store_probs=sp)
         _, g = icepop_bwd(d["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
         if world > 1:
             allreduce_stats(f.stats)

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define ICEPOP_ABI_VERSION 1
+#define ICEPOP_ABI_VERSION 2
 
 enum icepop_status {
   ICEPOP_OK = 0,
@@ -145,10 +145,20 @@ typedef struct icepop_fwd_out {
   float* kl;           /* [n_tokens] kl_t = sum_v p (log p - log p_ref)                    */
   float* lse_ref;      /* [n_tokens] log-sum-exp of z_ref = H.W_ref/T                      */
   float* kl_w;         /* [n_tokens] w_t * gamma / T (the KL gradient's coefficient)       */
+  /* Stored-probabilities mode (optional; both NULL = the backward recomputes the logits):
+   * probs    [n_tokens, vocab] bf16, q = exp(z - m) with m the row's maximum over each
+   *          ICEPOP_PROBS_TILE-column vocab tile (so q is in [0, 1]); needs vocab % 8 == 0 and
+   *          no weight_ref. 2*n_tokens*vocab bytes of HBM buy a backward without the K3 GEMM.
+   * tile_max [n_tokens, ceil(vocab / ICEPOP_PROBS_TILE)] f32, m in log2 units (z log2(e)). */
+  void* probs;
+  float* tile_max;
 } icepop_fwd_out;
 
+#define ICEPOP_PROBS_TILE 256
+
 /* Forward: fused lm_head GEMM + online log-softmax/gather/entropy (tcgen05), then the
- * IcePop epilogue. Logits are never written to HBM. With weight_ref != NULL a second B
+ * IcePop epilogue. Logits are never written to HBM (only the bf16 probabilities when
+ * out->probs is set). With weight_ref != NULL a second B
  * operand shares every hidden tile (dual accumulators) and kl_t enters J as -gamma*kl_t. */
 int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,
                     const void* weight, const void* weight_ref, const icepop_batch* batch,
@@ -177,11 +187,15 @@ typedef struct icepop_saved {
   const float* lse_ref;   /* [n_tokens] KL gradient inputs: used when gamma > 0 and       */
   const float* kl;        /* [n_tokens] weight_ref != NULL, else may be NULL              */
   const float* kl_w;      /* [n_tokens]                                                   */
+  void* probs;            /* out->probs / out->tile_max of the forward, or NULL. CONSUMED: the */
+  const float* tile_max;  /* backward overwrites probs with dZ (a second backward must pass NULL) */
 } icepop_saved;
 
 /* Backward: recompute logits tile by tile, dZ = grad_scale*coeff_t*(e_y - softmax(z_t))
  * [- grad_scale*kl_w_t*p*(log p - log p_ref - kl_t) when gamma > 0] (bf16 chunk), then
- * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05.
+ * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05. With saved->probs the same dZ
+ * is formed in place from the stored probabilities by a bandwidth-bound pass instead (no
+ * logit recompute, no workspace needed: workspace may be NULL; not with gamma > 0).
  * grad_hidden: [n_tokens, d], bf16 if grad_hidden_f32 == 0 else f32; may be NULL.
  * grad_weight: f32 in the weight's layout; accumulate != 0 adds into it; may be NULL. */
 int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,

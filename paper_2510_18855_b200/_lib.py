@@ -20,6 +20,8 @@ OK, EINVAL, ENUMERIC, ECUDA, EARCH = 0, 1, 2, 3, 4
 ALGO_ICEPOP, ALGO_GRPO, ALGO_TIS = 0, 1, 2
 W_DV, W_VD = 0, 1
 NSTATS = 8
+ABI_VERSION = 2
+PROBS_TILE = 256  # ICEPOP_PROBS_TILE: vocab columns per tile_max entry
 STAT_OBJECTIVE, STAT_N_POPPED, STAT_TOKENS, STAT_SUM_ENTROPY = 0, 1, 2, 3
 STAT_SUM_ENTROPY_POPPED, STAT_SUM_LOGP, STAT_SUM_KL, STAT_ERRORS = 4, 5, 6, 7
 
@@ -81,6 +83,8 @@ class FwdOut(ctypes.Structure):
         ("kl", _c_p),
         ("lse_ref", _c_p),
         ("kl_w", _c_p),
+        ("probs", _c_p),
+        ("tile_max", _c_p),
     ]
 
 
@@ -92,6 +96,8 @@ class Saved(ctypes.Structure):
         ("lse_ref", _c_p),
         ("kl", _c_p),
         ("kl_w", _c_p),
+        ("probs", _c_p),
+        ("tile_max", _c_p),
     ]
 
 
@@ -190,7 +196,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.icepop_abi_version() != 1:
+    if lib.icepop_abi_version() != ABI_VERSION:
         raise RuntimeError("libicepop_b200.so ABI version mismatch")
     _lib = lib
     return lib

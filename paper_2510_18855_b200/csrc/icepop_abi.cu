@@ -181,7 +181,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
                    const GemmShape& sh, const EpiParams& ep, cudaStream_t st) {
   auto kern = umma_gemm_kernel<BN, A_MN, B_MN, EPI, CG>;
-  constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI), EPI == EPI_DZ>::SMEM;
+  constexpr size_t smem = GemmCfg<BN, CG, epi_dual(EPI), epi_staging(EPI)>::SMEM;
   // the smem attribute is per device: one bit per device index that has it set
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -269,8 +269,11 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, bn / cg));
   if (B2) ICP_TRY(operand_map(&tb2, B2, N, K, ldb, b_mn, bn / cg));
   else tb2 = tb;
-  CUtensorMap tc = tb;  // EPI_DZ: bf16 dZ [zero_rows_to, N] store map (32 rows x 64 cols boxes, SW128)
+  // bf16 store map of the staging epilogues (32 rows x 64 cols boxes, SW128): EPI_DZ's dZ
+  // [zero_rows_to, N] and EPI_LSE's stored probabilities [M, N]
+  CUtensorMap tc = tb;
   if (epi == EPI_DZ) ICP_TRY(encode_2d(&tc, ep.dz, (uint64_t)N, (uint64_t)ep.zero_rows_to, (uint64_t)ep.ldz, 64, 32));
+  if (epi == EPI_LSE && ep.probs) ICP_TRY(encode_2d(&tc, ep.probs, (uint64_t)N, (uint64_t)M, (uint64_t)N, 64, 32));
   GemmShape sh;
   sh.M = (int)M;
   sh.N = (int)N;
@@ -588,6 +591,13 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  if (out->probs) {
+    if (ref) return fail(ICEPOP_EINVAL, "stored probabilities are not supported with weight_ref");
+    if (!out->tile_max) return fail(ICEPOP_EINVAL, "stored probabilities need out->tile_max");
+    if (V % 8 != 0) return fail(ICEPOP_EINVAL, "stored probabilities need vocab %% 8 == 0");
+    if ((reinterpret_cast<uintptr_t>(out->probs) & 15u) != 0)
+      return fail(ICEPOP_EINVAL, "out->probs must be 16-byte aligned");
+  }
   const double* adv = nullptr;
   ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
   ICP_CUDA(cudaMemsetAsync(w.err, 0, sizeof(unsigned), st));
@@ -602,6 +612,9 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     ep.targets = batch->tokens;
     ep.part = w.part;
     ep.ztok = w.ztok;
+    ep.probs = static_cast<__nv_bfloat16*>(out->probs);
+    ep.tile_max = out->tile_max;
+    ep.tm_ld = (int32_t)((V + BN_ - 1) / BN_);
     const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
     ICP_TRY(run_umma(ref ? EPI_LSE_REF : EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st,
                      Extent(), ref ? weight_ref : nullptr));
@@ -750,22 +763,36 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     if (grad_weight && !accumulate) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
     return ICEPOP_OK;
   }
-  // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
-  const bool skip = skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
-  const int64_t min_rows = std::min<int64_t>(N, BM);
-  const size_t need_min = carve_bf16(shape, nullptr, min_rows, true).bytes;
-  if (!workspace || workspace_bytes < need_min)
-    return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", need_min);
-  const size_t fixed = carve_bf16(shape, nullptr, 0, true).bytes;
-  int64_t chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
-  if (chunk >= N) {
-    chunk = N;
-  } else {
-    chunk = std::max<int64_t>(chunk / BM * BM, BM);
+  // stored-probabilities mode: dZ is formed in place over saved->probs (one chunk, all rows)
+  const bool sp = sv.probs != nullptr;
+  if (sp) {
+    if (kl_grad) return fail(ICEPOP_EINVAL, "stored probabilities carry no KL term: gamma > 0 needs recompute mode");
+    if (!sv.tile_max) return fail(ICEPOP_EINVAL, "saved->probs needs saved->tile_max");
+    if (V % 8 != 0 || (reinterpret_cast<uintptr_t>(sv.probs) & 15u) != 0)
+      return fail(ICEPOP_EINVAL, "saved->probs needs vocab %% 8 == 0 and 16-byte alignment");
   }
-  while (chunk > min_rows && carve_bf16(shape, nullptr, chunk, true).bytes > workspace_bytes) chunk -= BM;
-  BF16Workspace w = carve_bf16(shape, workspace, chunk, true);
-  if (w.bytes > workspace_bytes) return fail(ICEPOP_EINVAL, "backward workspace carve overflow");
+  // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
+  const bool skip = !sp && skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
+  int64_t chunk = N;
+  BF16Workspace w;
+  memset(&w, 0, sizeof(w));
+  if (!sp) {
+    const int64_t min_rows = std::min<int64_t>(N, BM);
+    const size_t need_min = carve_bf16(shape, nullptr, min_rows, true).bytes;
+    if (!workspace || workspace_bytes < need_min)
+      return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", need_min);
+    const size_t fixed = carve_bf16(shape, nullptr, 0, true).bytes;
+    chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
+    if (chunk >= N) {
+      chunk = N;
+    } else {
+      chunk = std::max<int64_t>(chunk / BM * BM, BM);
+    }
+    while (chunk > min_rows && carve_bf16(shape, nullptr, chunk, true).bytes > workspace_bytes) chunk -= BM;
+    w = carve_bf16(shape, workspace, chunk, true);
+    if (w.bytes > workspace_bytes) return fail(ICEPOP_EINVAL, "backward workspace carve overflow");
+  }
+  __nv_bfloat16* dzb = sp ? static_cast<__nv_bfloat16*>(sv.probs) : w.dz;
 
   const void* hsrc = hidden;
   const int32_t* tok_src = tokens;
@@ -814,8 +841,16 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       cs.lse = lse_src + c0;
       cs.coeff = coeff_src + c0;
     }
-    ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V, nc,
-                      st, ext_m));
+    if (sp) {
+      const int32_t n_tiles = (int32_t)((V + BN_ - 1) / BN_);
+      const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
+      k_dz_probs<<<grid, DZP_THREADS, n_tiles * sizeof(float), st>>>(
+          reinterpret_cast<uint4*>(dzb), sv.tile_max, n_tiles, lse, coeff, (float)grad_scale, tokens, nc, V / 8);
+      ICP_CUDA(cudaGetLastError());
+    } else {
+      ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V,
+                        nc, st, ext_m));
+    }
     // K4: grad_hidden = dZ . W^T   (M = nc, N = d, K = V)
     if (grad_hidden) {
       EpiParams eh;
@@ -827,7 +862,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       eh.out_f32 = grad_hidden_f32 ? 1 : 0;
       eh.vec_ok = ((reinterpret_cast<uintptr_t>(eh.out) & 15u) == 0) && (d % 8 == 0);
       // B operand viewed [N = d, K = V]: W[d,V] is K-major, W[V,d] is MN-major
-      ICP_TRY(run_umma(EPI_STORE, w.dz, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m));
+      ICP_TRY(run_umma(EPI_STORE, dzb, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m));
     }
     // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
     if (grad_weight || (rs && last)) {
@@ -851,10 +886,10 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       ew.vec_ok = ((reinterpret_cast<uintptr_t>(ovec) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
       if (dv) {
         ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, h, d, true, w.dz, V, true, d, V, nc, ew, st, ext_k, nullptr, rs && last));
+        ICP_TRY(run_umma(EPI_STORE, h, d, true, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, rs && last));
       } else {
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, w.dz, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, rs && last));
+        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, rs && last));
       }
     }
   }

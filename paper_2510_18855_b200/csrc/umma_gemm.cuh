@@ -104,12 +104,20 @@ struct EpiParams {
   const float* lse_ref;    // [M] natural units
   const float* kl;         // [M] kl_t
   const float* kl_w;       // [M] w_t * gamma / T
+  // EPI_LSE stored-probabilities mode: q[m, v] = 2^(u - tile max) as bf16 through the tensor
+  // map (row stride = N), tile_max[m * tm_ld + n_blk] = the tile maximum (log2 units)
+  __nv_bfloat16* probs;
+  float* tile_max;
+  int32_t tm_ld;
 };
 
 // CG = 1: one CTA computes a 128 x BN tile (cta_group::1).
 // CG = 2: a CTA pair computes a 256 x BN tile with cta_group::2 MMAs issued by the leader;
 //         each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so the B operand
 //         is read from L2 once per pair instead of once per CTA.
+// Epilogues that stage bf16 tiles in smem for TMA stores: K3's dZ and K1's stored probabilities.
+__host__ __device__ constexpr bool epi_staging(int epi) { return epi == EPI_DZ || epi == EPI_LSE; }
+
 template <int BN, int CG, bool DUAL = false, bool EPI_STAGING = false>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -214,16 +222,44 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
   }
 }
 
-// Online log-sum-exp over this tile's BN columns for one row, in log2 units:
-//   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z*log2(e)
-// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge.
+// Stage one warp's 32 rows x 64 columns of packed bf16 (pk[0..31] = this lane's row) in a
+// SWIZZLE_128B smem buffer and store it with one TMA bulk tensor store issued by lane 0. Two
+// buffers per warp alternate; the store that last read a buffer must be done reading it.
+__device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t* stage2, int& ebuf,
+                                                 const uint32_t (&pk)[32], int col0, int row0, int lane) {
+  uint8_t* buf = stage2 + ebuf * (32 * 128);
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+  // row `lane` of the slab: 8 x 16-byte chunks, chunk k at position k ^ (lane & 7) (SWIZZLE_128B)
+  uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
+        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmC, smem_u32(buf), col0, row0);
+    bulk_commit();
+  }
+  ebuf ^= 1;
+}
+
+// K1 epilogue: log-sum-exp statistics of this tile's BN columns for one row, in log2 units,
+//   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
+// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2).
+// Pass 1 takes mx (and gathers z[y]); pass 2 accumulates s, q. In stored-probabilities mode
+// (ep.probs) pass 2 also emits q[m, v] = 2^(u_v - mx) in [0, 1] as bf16 (TMA stores, clipped to
+// M rows / N columns) and tile_max[m, n_blk] = mx, from which the backward forms dZ without
+// recomputing logits. The statistics are the same bits in both modes.
 template <int BN>
-__device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
-                                        int n_blk, int row, uint32_t taddr) {
+__device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
+                                              uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row,
+                                              int lane, int quarter, uint32_t taddr) {
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
-  float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
+  float mx = -1e30f;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
@@ -231,47 +267,50 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
     const int col0 = n0 + c * 32;
     if (col0 >= sh.N) continue;  // warp-uniform
     const int rel = y - col0;
-    if ((unsigned)rel < 32u) {  // the sampled token's logit lives in this chunk
+    if ((unsigned)rel < 32u) {
       float zt = 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j) zt = (j == rel) ? v[j] : zt;
       if (row_ok) ep.ztok[m] = zt * ep.inv_t;
     }
-    float cm = -1e30f;
-    if (col0 + 32 <= sh.N) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        v[j] *= ep.scale_log2;
-        cm = fmaxf(cm, v[j]);
+    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, (col0 + j < sh.N) ? v[j] * ep.scale_log2 : -1e30f);
+  }
+  const int row0 = m0 + quarter * 32;
+  const bool warp_rows = row0 < sh.M;  // warp-uniform
+  const bool store = ep.probs != nullptr;
+  float s = 0.f, q = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    float v[32], w[32];
+    tmem_ld32(taddr + c * 64, v);
+    tmem_ld32(taddr + c * 64 + 32, w);
+    const int col0 = n0 + c * 64;
+    if (col0 >= sh.N) continue;  // warp-uniform
+    uint32_t pk[32];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float e[4], d[4];
+      const float x[4] = {v[2 * j], v[2 * j + 1], w[2 * j], w[2 * j + 1]};
+      const int cc[4] = {col0 + 2 * j, col0 + 2 * j + 1, col0 + 32 + 2 * j, col0 + 33 + 2 * j};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        d[i] = fmaf(x[i], ep.scale_log2, -mx);
+        e[i] = cc[i] < sh.N ? fast_exp2(d[i]) : 0.f;
+        s += e[i];
+        q = fmaf(e[i], cc[i] < sh.N ? d[i] : 0.f, q);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        v[j] = (col0 + j < sh.N) ? v[j] * ep.scale_log2 : -1e30f;
-        cm = fmaxf(cm, v[j]);
-      }
+      pk[j] = pack_bf16x2(e[0], e[1]);
+      pk[16 + j] = pack_bf16x2(e[2], e[3]);
     }
-    const float nm = fmaxf(run_m, cm);
-    const float a = fast_exp2(run_m - nm);
-    run_q = a * (run_q + (run_m - nm) * run_s);
-    run_s = a * run_s;
-    float s = 0.f, q = 0.f;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float d = v[j] - nm;
-      const float e = fast_exp2(d);
-      s += e;
-      q = fmaf(e, d, q);
-    }
-    run_s += s;
-    run_q += q;
-    run_m = nm;
+    if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
   }
   if (row_ok) {
     float* p = ep.part + (int64_t)n_blk * 3 * sh.M + m;
-    p[0] = run_m;
-    p[sh.M] = run_s;
-    p[2 * (int64_t)sh.M] = run_q;
+    p[0] = mx;
+    p[sh.M] = s;
+    p[2 * (int64_t)sh.M] = q;
+    if (store) ep.tile_max[(int64_t)m * ep.tm_ld + n_blk] = mx;
   }
 }
 
@@ -341,10 +380,6 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
     tmem_ld32(taddr + c * 64 + 32, w);
     const int col0 = n0 + c * 64;
     if (!warp_rows || col0 >= sh.N) continue;  // warp-uniform
-    uint8_t* buf = stage2 + ebuf * (32 * 128);
-    // the bulk store that last read this buffer must be done reading
-    if (lane == 0) bulk_wait_read<1>();
-    __syncwarp();
     uint32_t pk[32];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -357,19 +392,7 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
       pk[16 + j] = live ? pack_bf16x2(fmaf(-cf, q0, (col0 + 32 + 2 * j == y) ? cf : 0.f),
                                       fmaf(-cf, q1, (col0 + 32 + 2 * j + 1 == y) ? cf : 0.f)) : 0u;
     }
-    // row `lane` of the slab: 8 x 16-byte chunks, chunk k at position k ^ (lane & 7) (SWIZZLE_128B)
-    uint8_t* rowp = buf + lane * 128;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
-          make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(tmC, smem_u32(buf), col0, row0);
-      bulk_commit();
-    }
-    ebuf ^= 1;
+    stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
   }
 }
 
@@ -501,7 +524,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                      const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                      const GemmShape sh_in, const EpiParams ep) {
   constexpr bool DUAL = epi_dual(EPI);
-  constexpr bool STAGING = EPI == EPI_DZ;
+  constexpr bool STAGING = epi_staging(EPI);
   using Cfg = GemmCfg<BN, CG, DUAL, STAGING>;
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
@@ -757,7 +780,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
-      if (EPI == EPI_LSE) epi_lse<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
+      if (EPI == EPI_LSE)
+        epi_lse<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
+                    quarter, taddr);
       if (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
           epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
@@ -776,7 +801,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
-    if (STAGING && lane == 0) bulk_wait<0>();  // all dZ tile stores complete
+    if (STAGING && lane == 0) bulk_wait<0>();  // all staged tile stores complete
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();

@@ -3,8 +3,9 @@
 Three layers, all on device, none with a CPU fallback:
 
 * :func:`icepop_fwd` / :func:`icepop_bwd` -- functional forward (K1 fused lm_head GEMM +
-  online log-softmax, K2 IcePop epilogue) and backward (K3 recompute -> bf16 dZ chunk,
-  K4 dHidden, K5 dW), dispatched on dtype: bfloat16 -> tcgen05 path, float64 -> SIMT
+  online log-softmax, K2 IcePop epilogue) and backward (bf16 dZ -- formed in place from the
+  probabilities K1 stored when they fit in HBM, else recomputed by the K3 GEMM in chunks --
+  then K4 dHidden, K5 dW), dispatched on dtype: bfloat16 -> tcgen05 path, float64 -> SIMT
   validation path.
 * :func:`icepop_loss` -- a ``torch.library`` custom op with autograd (loss = -J), for
   training code that wants ``loss.backward()``.
@@ -37,10 +38,46 @@ LAYOUTS = {"dv": _lib.W_DV, "vd": _lib.W_VD}
 DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(96 * 10**9)))
 
 
-def _dz_chunk_bytes(device) -> int:
+# Stored-probabilities mode (include/icepop.h): K1 also writes bf16 q = exp(z - tile max)
+# [N, V] so the backward needs no K3 logit recompute (6 instead of 8 N.d.V FLOPs per step).
+# "auto" stores them when 2.N.V bytes fit in STORE_PROBS_FRACTION of the free device memory.
+STORE_PROBS = os.environ.get("ICEPOP_STORE_PROBS", "auto")
+STORE_PROBS_FRACTION = 0.6
+
+
+def _resolve_store_probs(store_probs, n: int, v: int, device, with_ref: bool) -> bool:
+    if store_probs is None:
+        store_probs = {"auto": None, "1": True, "0": False}.get(STORE_PROBS.lower(), None)
+    if store_probs is False or with_ref or v % 8 != 0 or n == 0:
+        return False
+    if store_probs is True:
+        return True
+    need = 2 * n * v + 4 * n * ((v + _lib.PROBS_TILE - 1) // _lib.PROBS_TILE)
+    free = _free_bytes(device)
+    return free is not None and need <= STORE_PROBS_FRACTION * free
+
+
+def _free_bytes(device) -> int | None:
+    """Device memory available to a new allocation: free in the driver plus what torch's
+    caching allocator holds unused (e.g. the previous step's probabilities / dZ block)."""
     try:
         free, _ = torch.cuda.mem_get_info(device)
+        return free + torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
     except Exception:  # noqa: BLE001
+        return None
+
+
+def _take_probs(fwd: "IcePopForward", kl_grad: bool):
+    """(probs, tile_max) of a stored-probabilities forward, or (None, None). The backward
+    overwrites probs with dZ, so they are handed out once (a second backward recomputes)."""
+    if kl_grad or fwd.extras.get("probs") is None:
+        return None, None
+    return fwd.extras.pop("probs"), fwd.extras.pop("tile_max")
+
+
+def _dz_chunk_bytes(device) -> int:
+    free = _free_bytes(device)
+    if free is None:
         return DZ_CHUNK_BYTES
     return max(1, min(DZ_CHUNK_BYTES, int(0.6 * free)))
 
@@ -180,8 +217,13 @@ def icepop_fwd(
     cfg: IcePopConfig = IcePopConfig(),
     layout: str = "vd",
     weight_ref: torch.Tensor | None = None,
+    store_probs: bool | None = None,
 ) -> IcePopForward:
-    """Forward of the IcePop objective on this rank's tokens (objective.py:215-278)."""
+    """Forward of the IcePop objective on this rank's tokens (objective.py:215-278).
+
+    ``store_probs`` (bf16 path): keep the bf16 probabilities for the backward (True / False /
+    None = ``ICEPOP_STORE_PROBS``, default "auto": when they fit in device memory).
+    """
     lib = _lib_for(hidden)
     batch.validate()
     hidden = hidden.contiguous()
@@ -213,6 +255,10 @@ def icepop_fwd(
             kl = torch.empty(n, dtype=torch.float32, device=dev)
             lse_ref = torch.empty(n, dtype=torch.float32, device=dev)
             kl_w = torch.empty(n, dtype=torch.float32, device=dev)
+        probs = tile_max = None
+        if _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
+            probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
+            tile_max = torch.empty((n, -(-shape.vocab // _lib.PROBS_TILE)), dtype=torch.float32, device=dev)
         fwd_b = _lib._sz()
         _lib.check(lib.icepop_workspace_bytes(shape, 0, 1 if wr is not None else 0, fwd_b, None))
         ws = torch.empty(max(fwd_b.value, 1), dtype=torch.uint8, device=dev)
@@ -228,11 +274,15 @@ def icepop_fwd(
             kl=_lib.ptr(kl),
             lse_ref=_lib.ptr(lse_ref),
             kl_w=_lib.ptr(kl_w),
+            probs=_lib.ptr(probs),
+            tile_max=_lib.ptr(tile_max),
         )
         _lib.check(lib.icepop_fwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), c_batch,
                                        out, ws.data_ptr(), ws.numel(), st))
         f = IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats, kl=kl, lse_ref=lse_ref)
         f.extras["kl_w"] = kl_w
+        if probs is not None:
+            f.extras["probs"], f.extras["tile_max"] = probs, tile_max
         return f
     if hidden.dtype == torch.float64:
         if weight.dtype != torch.float64:
@@ -396,14 +446,19 @@ def icepop_bwd(
         gw = grad_weight if accumulate else (torch.empty(wshape, dtype=torch.float32, device=dev) if need_weight else None)
         if gw is not None and (gw.dtype != torch.float32 or tuple(gw.shape) != wshape or not gw.is_contiguous()):
             raise ValueError("grad_weight must be a contiguous float32 tensor shaped like weight")
-        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, _dz_chunk_bytes(dev)), dtype=torch.uint8,
-                         device=dev)
         wr = weight_ref.contiguous() if weight_ref is not None else None
+        probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
+        ws = None
+        if probs is None:
+            ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, _dz_chunk_bytes(dev)), dtype=torch.uint8,
+                             device=dev)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
-                           lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")))
+                           lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
+                           probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
         _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
                                        float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
-                                       _lib.ptr(gw), 1 if accumulate else 0, ws.data_ptr(), ws.numel(), st))
+                                       _lib.ptr(gw), 1 if accumulate else 0, _lib.ptr(ws),
+                                       0 if ws is None else ws.numel(), st))
         return gh, gw
     if hidden.dtype == torch.float64:
         gh = torch.empty((n, d), dtype=torch.float64, device=dev) if need_hidden else None
@@ -458,17 +513,22 @@ def icepop_bwd_reduce_scatter(
     n, d, v = shape.n_tokens, shape.hidden, shape.vocab
     gh_dtype = grad_hidden_dtype or torch.bfloat16
     gh = torch.empty((n, d), dtype=gh_dtype, device=dev) if need_hidden else None
-    cb = _dz_chunk_bytes(dev)
-    rows = cb // (2 * v)
-    chunk = n if rows >= n else max(128, rows // 128 * 128)
-    scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev) if chunk < n else None
-    ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, cb), dtype=torch.uint8, device=dev)
     wr = weight_ref.contiguous() if weight_ref is not None else None
+    probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
+    scratch = ws = None
+    if probs is None:
+        cb = _dz_chunk_bytes(dev)
+        rows = cb // (2 * v)
+        chunk = n if rows >= n else max(128, rows // 128 * 128)
+        scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev) if chunk < n else None
+        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, cb), dtype=torch.uint8, device=dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
-                       lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")))
+                       lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
+                       probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
     _lib.check(lib.icepop_bwd_bf16_rs(shape, cfg.to_c(), hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
                                       float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
-                                      rs_target, _lib.ptr(scratch), ws.data_ptr(), ws.numel(), _stream(dev)))
+                                      rs_target, _lib.ptr(scratch), _lib.ptr(ws), 0 if ws is None else ws.numel(),
+                                      _stream(dev)))
     return gh
 
 
@@ -525,37 +585,52 @@ def _icepop_loss_op(
     algo: int,
     layout: int,
     token_offset: int,
-) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    store_probs: bool,
+) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor,
+           torch.Tensor, torch.Tensor]:
     cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
     batch = PackedBatch(tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages,
                         token_offset=token_offset)
-    f = icepop_fwd(hidden, weight, batch, cfg, "dv" if layout == _lib.W_DV else "vd")
+    sp = store_probs and hidden.dtype == torch.bfloat16
+    f = icepop_fwd(hidden, weight, batch, cfg, "dv" if layout == _lib.W_DV else "vd", store_probs=sp)
     loss = -f.stats[_lib.STAT_OBJECTIVE]
-    return loss, f.stats, f.lse, f.lp_cur, f.entropy, f.kept, f.coeff.to(torch.float64)
+    probs = f.extras.get("probs")
+    tile_max = f.extras.get("tile_max")
+    if probs is None:  # outputs must be fresh tensors of the shapes the fake promises
+        probs = hidden.new_empty((0,), dtype=torch.bfloat16)
+        tile_max = hidden.new_empty((0,), dtype=torch.float32)
+    return loss, f.stats, f.lse, f.lp_cur, f.entropy, f.kept, f.coeff.to(torch.float64), probs, tile_max
 
 
 @_icepop_loss_op.register_fake
 def _(hidden, weight, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages, alpha, beta,
-      clip_eps, tis_cap, temperature, algo, layout, token_offset):
+      clip_eps, tis_cap, temperature, algo, layout, token_offset, store_probs):
     n = hidden.shape[0]
     f64 = dict(dtype=torch.float64, device=hidden.device)
     # lse / entropy are f32 on the bf16 path and f64 on the validation path
     f32 = dict(dtype=torch.float64 if hidden.dtype == torch.float64 else torch.float32, device=hidden.device)
+    v = weight.shape[1] if layout == _lib.W_DV else weight.shape[0]
+    sp = store_probs and hidden.dtype == torch.bfloat16
+    probs_shape = (n, v) if sp else (0,)
+    tm_shape = (n, -(-v // _lib.PROBS_TILE)) if sp else (0,)
     return (hidden.new_empty((), dtype=torch.float64), hidden.new_empty((_lib.NSTATS,), **{"dtype": torch.float64}),
             torch.empty(n, **f32), torch.empty(n, **f64), torch.empty(n, **f32),
-            torch.empty(n, dtype=torch.uint8, device=hidden.device), torch.empty(n, **f64))
+            torch.empty(n, dtype=torch.uint8, device=hidden.device), torch.empty(n, **f64),
+            torch.empty(probs_shape, dtype=torch.bfloat16, device=hidden.device),
+            torch.empty(tm_shape, dtype=torch.float32, device=hidden.device))
 
 
 def _setup_context(ctx, inputs, output):
     (hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, alpha, beta, clip_eps, tis_cap, temperature, algo, layout,
-     token_offset) = inputs
-    loss, stats, lse, lp_cur, entropy, kept, coeff = output
-    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff)
+     token_offset, store_probs) = inputs
+    loss, stats, lse, lp_cur, entropy, kept, coeff, probs, tile_max = output
+    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff, probs, tile_max)
     ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset)
+    ctx.probs_live = probs.numel() > 0  # consumed (overwritten with dZ) by the first backward
 
 
 def _backward(ctx, grad_loss, *unused):
-    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff = ctx.saved_tensors
+    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff, probs, tile_max = ctx.saved_tensors
     alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset = ctx.cfg
     cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
     batch = PackedBatch(tokens, lp_old, lp_inf, cu, go, adv, token_offset=token_offset)
@@ -564,6 +639,9 @@ def _backward(ctx, grad_loss, *unused):
     if hidden.dtype == torch.bfloat16:
         c = (coeff * scale).to(torch.float32)
         fwd = IcePopForward(lse, None, None, None, None, None, c, None)
+        if ctx.probs_live:  # a second backward (retain_graph) falls back to the recompute
+            fwd.extras["probs"], fwd.extras["tile_max"] = probs, tile_max
+            ctx.probs_live = False
     else:
         fwd = IcePopForward(lse, torch.empty_like(lse, dtype=torch.float64),
                             torch.empty_like(lse, dtype=torch.float64), None, None, None, coeff * scale,
@@ -574,7 +652,7 @@ def _backward(ctx, grad_loss, *unused):
         gw = gw.to(weight.dtype)
     if gh is not None:
         gh = gh.to(hidden.dtype)
-    return (gh, gw) + (None,) * 14
+    return (gh, gw) + (None,) * 15
 
 
 _icepop_loss_op.register_autograd(_backward, setup_context=_setup_context)
@@ -586,21 +664,28 @@ def icepop_loss(
     batch: PackedBatch,
     cfg: IcePopConfig = IcePopConfig(),
     layout: str = "vd",
+    store_probs: bool | None = None,
 ):
     """Differentiable IcePop loss (= -J on this rank's tokens) and per-token aux.
 
     Returns ``(loss, aux)`` with aux = dict(stats, lse, lp_cur, entropy, kept, coeff).
     ``batch.advantages`` must be given (compute them with K0 via
-    :func:`group_advantages` when starting from rewards).
+    :func:`group_advantages` when starting from rewards). ``store_probs``: as in
+    :func:`icepop_fwd` (the probabilities live until the first backward consumes them).
     """
     if batch.advantages is None:
         raise ValueError("icepop_loss needs batch.advantages (see group_advantages)")
     if cfg.kl_coeff != 0.0:
         raise ValueError("icepop_loss: kl_coeff must be 0 (KL-to-ref is the fp64 functional path)")
-    loss, stats, lse, lp_cur, entropy, kept, coeff = _icepop_loss_op(
+    if layout not in LAYOUTS:
+        raise ValueError(f"weight layout must be 'dv' or 'vd', got {layout!r}")
+    v = weight.shape[1] if layout == "dv" else weight.shape[0]
+    sp = hidden.is_cuda and hidden.dtype == torch.bfloat16 and _resolve_store_probs(
+        store_probs, hidden.shape[0], v, hidden.device, False)
+    loss, stats, lse, lp_cur, entropy, kept, coeff, _probs, _tile_max = _icepop_loss_op(
         hidden, weight, batch.tokens, batch.lp_train_old, batch.lp_infer_old, batch.cu_seqlens,
         batch.group_offsets, batch.advantages, cfg.alpha, cfg.beta, cfg.clip_eps, cfg.tis_cap, cfg.temperature,
-        ALGOS[cfg.algo], LAYOUTS[layout], batch.token_offset)
+        ALGOS[cfg.algo], LAYOUTS[layout], batch.token_offset, bool(sp))
     return loss, dict(stats=stats, lse=lse, lp_cur=lp_cur, entropy=entropy, kept=kept, coeff=coeff)
 
 

@@ -68,15 +68,17 @@ def cta_group(request):
     _lib.check(lib.icepop_set_cta_group(2))
 
 
+@pytest.mark.parametrize("store_probs", [True, False], ids=["probs", "recompute"])
 @pytest.mark.parametrize("layout", ["vd", "dv"])
 @pytest.mark.parametrize("algo", ["icepop", "grpo", "tis"])
-def test_dense_bf16_vs_oracle(cuda_device, cta_group, layout, algo):
+def test_dense_bf16_vs_oracle(cuda_device, cta_group, layout, algo, store_probs):
     from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
 
     c = _case(seed=3, layout=layout)
     cfg = IcePopConfig(algo=algo)
     b = _batch(c, cuda_device)
-    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), b, cfg, layout=layout)
+    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), b, cfg, layout=layout, store_probs=store_probs)
+    assert ("probs" in f.extras) == store_probs
     gh, gw = icepop_bwd(c["H"].to(cuda_device), c["W"].to(cuda_device), b, f, cfg, layout=layout,
                         grad_hidden_dtype=torch.float32)
     finish(f.stats)
@@ -127,7 +129,7 @@ def test_backward_chunking_matches_single_chunk(cuda_device, monkeypatch):
 
     c = _case(n_seqs=4, seed=11, lens=[300, 260, 130, 500])
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
-    f = L.icepop_fwd(H, W, _batch(c, cuda_device), L.IcePopConfig())
+    f = L.icepop_fwd(H, W, _batch(c, cuda_device), L.IcePopConfig(), store_probs=False)  # chunks: recompute mode
     gh1, gw1 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
     monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * 1000 * 2)  # 256-row chunks
     gh2, gw2 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
@@ -183,7 +185,7 @@ def test_config_validation_matches_reference():
                 IcePopConfig(tis_cap=0.0), IcePopConfig(temperature=0.0)):
         with pytest.raises(ValueError):
             icepop_fwd(c["H"].to(dev), c["W"].to(dev), _batch(c, dev), bad)
-    assert _lib.load().icepop_abi_version() == 1
+    assert _lib.load().icepop_abi_version() == _lib.ABI_VERSION
 
 
 def test_custom_op_autograd_matches_functional(cuda_device):
@@ -263,7 +265,7 @@ def test_skip_inactive_rows_matches_full_backward(cuda_device, cta_group, layout
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
     cfg = IcePopConfig()
     b = _batch(c, cuda_device)
-    f = icepop_fwd(H, W, b, cfg, layout=layout)
+    f = icepop_fwd(H, W, b, cfg, layout=layout, store_probs=False)  # row skipping is a recompute-mode feature
     n_zero = int((f.coeff == 0).sum())
     assert n_zero > len(c["tokens"]) // 3
     lib = _lib.ensure_device(0)
@@ -338,7 +340,7 @@ def test_on_policy_forward_equals_full_forward(cuda_device):
     b = PackedBatch(b.tokens, lp, lp - torch.from_numpy(np.random.default_rng(0).normal(0, 0.3, len(c["tokens"]))).to(
         cuda_device), b.cu_seqlens, b.group_offsets, b.advantages)
     cfg = IcePopConfig()
-    full = icepop_fwd(H, W, b, cfg)
+    full = icepop_fwd(H, W, b, cfg, store_probs=False)  # both backwards recompute -> bit-identical
     onp = icepop_fwd_onpolicy(b, lse, ent, cfg, hidden_dim=H.shape[1], vocab=W.shape[0])
     for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff", "stats"):
         assert torch.equal(getattr(full, name), getattr(onp, name)), name
@@ -399,7 +401,8 @@ def test_sgd_update_on_device(cuda_device):
         sgd_update_(w2, torch.full_like(w2, 3e38), 10.0)
 
 
-def test_cuda_graph_capture_replays_fwd_bwd(cuda_device):
+@pytest.mark.parametrize("store_probs", [True, False], ids=["probs", "recompute"])
+def test_cuda_graph_capture_replays_fwd_bwd(cuda_device, store_probs):
     """fwd + bwd are sync-free (device-side extents, counters, error word), so one CUDA graph
     captures the whole step; replays match eager execution bit for bit."""
     from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
@@ -408,17 +411,17 @@ def test_cuda_graph_capture_replays_fwd_bwd(cuda_device):
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
     b = _batch(c, cuda_device)
     cfg = IcePopConfig()
-    f0 = icepop_fwd(H, W, b, cfg)
+    f0 = icepop_fwd(H, W, b, cfg, store_probs=store_probs)
     gh0, gw0 = icepop_bwd(H, W, b, f0, cfg)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):  # warm-up on the capture stream (allocator, lazy init)
-        f = icepop_fwd(H, W, b, cfg)
+        f = icepop_fwd(H, W, b, cfg, store_probs=store_probs)
         icepop_bwd(H, W, b, f, cfg)
     torch.cuda.current_stream().wait_stream(s)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        fg = icepop_fwd(H, W, b, cfg)
+        fg = icepop_fwd(H, W, b, cfg, store_probs=store_probs)
         ghg, gwg = icepop_bwd(H, W, b, fg, cfg)
     for _ in range(2):
         g.replay()
@@ -444,7 +447,8 @@ def test_fused_reduce_scatter_emulated_ranks(cuda_device, monkeypatch, layout, w
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
     cfg = L.IcePopConfig()
     full_b = _batch(c, cuda_device)
-    f = L.icepop_fwd(H, W, full_b, cfg, layout=layout)
+    sp = not chunked  # dZ chunks exist only in recompute mode
+    f = L.icepop_fwd(H, W, full_b, cfg, layout=layout, store_probs=sp)
     _, gw_ref = L.icepop_bwd(H, W, full_b, f, cfg, layout=layout, need_hidden=False)
     rows, row_len = W.shape  # dW has the weight's layout: rows = V (vd) or d (dv)
     V = W.shape[0] if layout == "vd" else W.shape[1]
@@ -458,7 +462,7 @@ def test_fused_reduce_scatter_emulated_ranks(cuda_device, monkeypatch, layout, w
     for r in range(world):
         s, e = shard_range(N, world, r)
         b = _batch(c, cuda_device, slice(s, e))
-        fr = L.icepop_fwd(H[s:e], W, b, cfg, layout=layout)
+        fr = L.icepop_fwd(H[s:e], W, b, cfg, layout=layout, store_probs=sp)
         t = _lib.RsTarget(world=world, rank=r, shard_rows=shard_rows)
         for o in range(world):
             t.slots[o] = slot_bufs[o].data_ptr()

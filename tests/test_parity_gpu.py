@@ -96,8 +96,9 @@ def cta_group(request):
     _lib.check(lib.icepop_set_cta_group(2))
 
 
+@pytest.mark.parametrize("store_probs", [None, False], ids=["auto", "recompute"])
 @pytest.mark.parametrize("name", [n for n in golden_cases() if "kl" not in n and "refdiag" not in n])
-def test_bf16_path_matches_reference_golden(cuda_device, cta_group, name):
+def test_bf16_path_matches_reference_golden(cuda_device, cta_group, name, store_probs):
     from paper_2510_18855_b200.loss import Diagnostics, finish, icepop_bwd, icepop_fwd
 
     d = load_golden(name)
@@ -106,7 +107,7 @@ def test_bf16_path_matches_reference_golden(cuda_device, cta_group, name):
     assert torch.equal(W.double().cpu(), torch.from_numpy(d["weight"])), "fixture weights must be bf16-exact"
     batch = _batch(d, cuda_device)
     cfg = _cfg(d)
-    f = icepop_fwd(H, W, batch, cfg, layout="dv")
+    f = icepop_fwd(H, W, batch, cfg, layout="dv", store_probs=store_probs)  # auto: probs when vocab % 8 == 0
     gh, gw = icepop_bwd(H, W, batch, f, cfg, layout="dv", grad_hidden_dtype=torch.float32)
     finish(f.stats)
     diag = Diagnostics.from_stats(f.stats.cpu())

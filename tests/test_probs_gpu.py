@@ -1,0 +1,221 @@
+"""Stored-probabilities mode (include/icepop.h `icepop_fwd_out.probs`): K1 also writes
+q = exp(z - tile max) as bf16 and the backward forms dZ from it in place instead of
+recomputing the logits with the K3 GEMM.
+
+Checked here: the forward statistics are the same bits in both modes; q and tile_max
+against an fp32 torch reference of the same logits (q within bf16 rounding, 2^-8 relative);
+gradients against the recompute mode and the fp64 oracle (relative Frobenius <= 1e-2, the
+bf16 path's tolerance); consumption semantics (a second backward recomputes); ABI errors;
+and that the clipped TMA stores never write outside [N, V].
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from test_dense_gpu import _batch, _case, _oracle, _rel
+
+pytestmark = pytest.mark.gpu
+
+FWD_FIELDS = ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff", "stats")
+
+
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request):
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    _lib.check(lib.icepop_set_cta_group(request.param))
+    yield request.param
+    _lib.check(lib.icepop_set_cta_group(2))
+
+
+def _logits(c, dev, temperature=1.0):
+    H = c["H"].to(dev).float()
+    W = c["W"].to(dev).float()
+    return (H @ (W.T if c["layout"] == "vd" else W)) / temperature
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_forward_statistics_identical_in_both_modes(cuda_device, cta_group, layout):
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=51, layout=layout, V=1000)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    a = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, store_probs=True)
+    b = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, store_probs=False)
+    assert "probs" in a.extras and "probs" not in b.extras
+    for name in FWD_FIELDS:
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+
+
+@pytest.mark.parametrize("temperature", [1.0, 0.7])
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_stored_probabilities_match_fp32_softmax(cuda_device, cta_group, layout, temperature):
+    """q * 2^(tile_max - lse log2 e) is the softmax; V = 1000 leaves a ragged last tile and a
+    ragged last 64-column slab, N is not a multiple of 128."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=52, layout=layout, V=1000)
+    f = icepop_fwd(c["H"].to(cuda_device), c["W"].to(cuda_device), _batch(c, cuda_device),
+                   IcePopConfig(temperature=temperature), layout=layout, store_probs=True)
+    probs, tmax = f.extras["probs"].float(), f.extras["tile_max"]
+    N, V = probs.shape
+    assert N % 128 != 0 and tmax.shape == (N, -(-V // _lib.PROBS_TILE))
+    z = _logits(c, cuda_device, temperature)
+    u = z * (1.0 / np.log(2.0))
+    pad = tmax.shape[1] * _lib.PROBS_TILE - V
+    ref_max = torch.nn.functional.pad(u, (0, pad), value=-1e30).view(N, -1, _lib.PROBS_TILE).amax(-1)
+    torch.testing.assert_close(tmax, ref_max, rtol=0, atol=2e-4)
+    assert float(probs.min()) >= 0.0 and float(probs.max()) <= 1.0
+    # each tile's maximum entry is stored as exactly 1 (q = 2^0)
+    tiles = torch.nn.functional.pad(probs, (0, pad)).view(N, -1, _lib.PROBS_TILE)
+    assert torch.all(tiles.amax(-1) == 1.0)
+    scale = torch.exp2(tmax - (f.lse * (1.0 / np.log(2.0)))[:, None])
+    p = probs * scale.repeat_interleave(_lib.PROBS_TILE, dim=1)[:, :V]
+    ref = torch.softmax(z, dim=1)
+    torch.testing.assert_close(p, ref, rtol=8e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+@pytest.mark.parametrize("algo", ["icepop", "tis"])
+def test_backward_from_probs_matches_recompute_and_oracle(cuda_device, cta_group, layout, algo):
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(seed=53, layout=layout, V=1000)
+    c["adv"] = c["adv"].copy()
+    c["adv"][[0, 1, 2]] = 0.0  # a zero-advantage group: its rows' dZ must come out exactly 0
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig(algo=algo)
+    res = {}
+    for sp in (True, False):
+        f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=sp)
+        res[sp] = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
+        assert "probs" not in f.extras  # consumed
+    (gh_p, gw_p), (gh_r, gw_r) = res[True], res[False]
+    zero = (f.coeff == 0)
+    assert int(zero.sum()) > 0 and torch.all(gh_p[zero] == 0)
+    assert _rel(gw_p.cpu().numpy(), gw_r.cpu().numpy()) < 5e-3
+    assert _rel(gh_p.cpu().numpy(), gh_r.cpu().numpy()) < 5e-3
+    o = _oracle(c, algo=algo)
+    assert _rel(gw_p.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh_p.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_second_backward_recomputes(cuda_device):
+    """The first backward overwrites the probabilities with dZ; a second one on the same
+    forward falls back to the logit recompute and equals a recompute-mode backward exactly."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(seed=54)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, store_probs=True)
+    icepop_bwd(H, W, _batch(c, cuda_device), f, cfg)
+    gh2, gw2 = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg)
+    fr = icepop_fwd(H, W, _batch(c, cuda_device), cfg, store_probs=False)
+    gh3, gw3 = icepop_bwd(H, W, _batch(c, cuda_device), fr, cfg)
+    assert torch.equal(gh2, gh3) and torch.equal(gw2, gw3)
+
+
+def test_autograd_retain_graph_second_backward(cuda_device):
+    """icepop_loss with stored probabilities: backward twice (retain_graph) gives the same
+    gradients within tolerance (the second pass recomputes)."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_loss
+
+    c = _case(seed=55)
+    H = c["H"].to(cuda_device).requires_grad_(True)
+    W = c["W"].to(cuda_device).requires_grad_(True)
+    loss, _ = icepop_loss(H, W, _batch(c, cuda_device), IcePopConfig(), store_probs=True)
+    loss.backward(retain_graph=True)
+    g1 = (H.grad.float().clone(), W.grad.float().clone())
+    H.grad = W.grad = None
+    loss.backward()
+    assert _rel(H.grad.float().cpu().numpy(), g1[0].cpu().numpy()) < 1e-2
+    assert _rel(W.grad.float().cpu().numpy(), g1[1].cpu().numpy()) < 1e-2
+
+
+def test_auto_mode_skips_probs_with_weight_ref(cuda_device):
+    """weight_ref (KL term): the forward keeps the recompute mode even when asked."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=56, V=1000)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), weight_ref=W.clone(), store_probs=True)
+    assert "probs" not in f.extras
+
+
+def _c_fwd(c, dev, probs, tile_max, weight_ref=None):
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, _shape
+
+    H, W = c["H"].to(dev), c["W"].to(dev)
+    b = _batch(c, dev)
+    shape = _shape(H, W, c["layout"], b)
+    n = shape.n_tokens
+    outs = {k: torch.empty(n, dtype=t, device=dev) for k, t in
+            (("lse", torch.float32), ("lp_cur", torch.float64), ("entropy", torch.float32), ("kept", torch.uint8),
+             ("calib", torch.float64), ("surrogate", torch.float64), ("coeff", torch.float32))}
+    stats = torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev)
+    kl = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)] if weight_ref is not None else [None] * 3
+    fb = _lib._sz()
+    lib = _lib.ensure_device(0)
+    _lib.check(lib.icepop_workspace_bytes(shape, 0, 1 if weight_ref is not None else 0, fb, None))
+    ws = torch.empty(fb.value, dtype=torch.uint8, device=dev)
+    out = _lib.FwdOut(stats=stats.data_ptr(), kl=_lib.ptr(kl[0]), lse_ref=_lib.ptr(kl[1]), kl_w=_lib.ptr(kl[2]),
+                      probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max),
+                      **{k: v.data_ptr() for k, v in outs.items()})
+    rc = lib.icepop_fwd_bf16(shape, IcePopConfig().to_c(), H.data_ptr(), W.data_ptr(), _lib.ptr(weight_ref),
+                             b.to_c(), out, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
+    return rc, shape, b, outs
+
+
+def test_abi_rejects_invalid_probs_arguments(cuda_device):
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig
+
+    lib = _lib.ensure_device(0)
+    c = _case(seed=57, V=1000)
+    N = len(c["tokens"])
+    probs = torch.empty((N, 1000), dtype=torch.bfloat16, device=cuda_device)
+    tm = torch.empty((N, 4), dtype=torch.float32, device=cuda_device)
+    rc, *_ = _c_fwd(c, cuda_device, probs, None)
+    assert rc == _lib.EINVAL  # tile_max missing
+    rc, *_ = _c_fwd(c, cuda_device, probs, tm, weight_ref=c["W"].to(cuda_device))
+    assert rc == _lib.EINVAL  # no stored probabilities with the KL term
+    flat = torch.empty(N * 1000 + 8, dtype=torch.bfloat16, device=cuda_device)
+    rc, *_ = _c_fwd(c, cuda_device, flat[1:1 + N * 1000], tm)
+    assert rc == _lib.EINVAL  # probs not 16-byte aligned
+    # backward: saved probs with gamma > 0 is rejected
+    rc, shape, b, outs = _c_fwd(c, cuda_device, probs, tm)
+    assert rc == _lib.OK
+    saved = _lib.Saved(tokens=b.tokens.data_ptr(), lse=outs["lse"].data_ptr(), coeff=outs["coeff"].data_ptr(),
+                       lse_ref=outs["lse"].data_ptr(), kl=outs["lse"].data_ptr(), kl_w=outs["lse"].data_ptr(),
+                       probs=probs.data_ptr(), tile_max=tm.data_ptr())
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    rc = lib.icepop_bwd_bf16(shape, IcePopConfig(kl_coeff=0.3).to_c(), H.data_ptr(), W.data_ptr(), W.data_ptr(),
+                             saved, 1.0, None, 0, None, 0, None, 0, torch.cuda.current_stream().cuda_stream)
+    assert rc == _lib.EINVAL
+
+
+def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group):
+    """The TMA stores of q are clipped to [N, V]: guard bands around the buffer stay intact
+    (N = 1,111 rows is not a multiple of 32 or 128; V = 1,000 ends mid 64-column slab)."""
+    from paper_2510_18855_b200 import _lib
+
+    c = _case(seed=58, V=1000, lens=[500, 411, 200], n_seqs=3)
+    N, V, G = len(c["tokens"]), 1000, 4096
+    buf = torch.full((N * V + 2 * G,), 12345.0, dtype=torch.bfloat16, device=cuda_device)
+    # 16-byte aligned start G elements in (G * 2 bytes)
+    probs = buf[G:G + N * V].view(N, V)
+    tm_buf = torch.full((N * 4 + 2 * 64,), 777.0, dtype=torch.float32, device=cuda_device)
+    tm = tm_buf[64:64 + N * 4].view(N, 4)
+    rc, *_ = _c_fwd(c, cuda_device, probs, tm)
+    assert rc == _lib.OK
+    torch.cuda.synchronize()
+    assert torch.all(buf[:G] == 12345.0) and torch.all(buf[G + N * V:] == 12345.0)
+    assert torch.all(tm_buf[:64] == 777.0) and torch.all(tm_buf[64 + N * 4:] == 777.0)
+    assert torch.isfinite(probs.float()).all() and float(probs.float().max()) == 1.0
