@@ -231,11 +231,9 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
   if (lane == 0) bulk_wait_read<1>();
   __syncwarp();
   // row `lane` of the slab: 8 x 16-byte chunks, chunk k at position k ^ (lane & 7) (SWIZZLE_128B)
-  uint8_t* rowp = buf + lane * 128;
+  const uint32_t rowp = smem_u32(buf) + lane * 128;
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
-        make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+  for (int k = 0; k < 8; ++k) sts128(rowp + ((k ^ (lane & 7)) << 4), pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
