@@ -311,6 +311,11 @@ int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N
  * ICEPOP_CTA_GROUP environment variable sets the initial value. */
 int icepop_set_cta_group(int32_t cta_group);
 
+/* Tile shape of the long-K plain GEMMs (K4, K5) on CTA pairs: 1 (default) = 256 x 512 tiles
+ * (two N = 256 MMAs per k step into one TMEM accumulator), 0 = 256 x 256. Process-wide; the
+ * ICEPOP_WIDE_TILES environment variable sets the initial value. */
+int icepop_set_wide_tiles(int32_t enable);
+
 /* Backward row skipping: rows whose gradient coefficient is exactly zero (popped tokens,
  * clip-inactive tokens, zero-advantage sequences; objective.py:250) contribute nothing to
  * dW and get dHidden = 0, so icepop_bwd_bf16 compacts the active rows on the device and

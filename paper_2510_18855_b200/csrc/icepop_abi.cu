@@ -125,6 +125,7 @@ int operand_map(CUtensorMap* map, const void* ptr, int64_t mn, int64_t k, int64_
 }
 
 constexpr int BN_ = 256;
+constexpr int BN_WIDE = 512;
 
 int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
 
@@ -211,8 +212,11 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
 
 template <bool A_MN, bool B_MN, int EPI>
 int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
-                const GemmShape& sh, const EpiParams& ep, cudaStream_t st, int cg) {
+                const GemmShape& sh, const EpiParams& ep, cudaStream_t st, int cg, bool wide = false) {
   constexpr int BN = epi_dual(EPI) ? 128 : BN_;
+  if constexpr (EPI == EPI_STORE) {
+    if (wide && cg == 2) return launch_umma_cg<BN_WIDE, A_MN, B_MN, EPI, 2>(ta, tb, tb2, tc, sh, ep, st);
+  }
   if (cg == 2) return launch_umma_cg<BN, A_MN, B_MN, EPI, 2>(ta, tb, tb2, tc, sh, ep, st);
   return launch_umma_cg<BN, A_MN, B_MN, EPI, 1>(ta, tb, tb2, tc, sh, ep, st);
 }
@@ -255,6 +259,17 @@ struct Extent {
 // BN of a GEMM with epilogue `epi` (the dual-accumulator KL variants use 128-column tiles).
 inline int bn_of(int epi) { return epi_dual(epi) ? 128 : BN_; }
 
+// Long-K plain GEMMs (K4, K5) on CTA pairs use 256 x 512 tiles (two N = 256 MMAs per k step,
+// one TMEM accumulator): a third fewer operand bytes per FLOP from L2 into smem than 256 x 256
+// (K1/K3 keep 256 x 256: their heavy epilogues need the double-buffered accumulator).
+// ICEPOP_WIDE_TILES=0 / icepop_set_wide_tiles(0) select 256 x 256.
+int g_wide_tiles = -1;
+
+bool wide_tiles() {
+  if (g_wide_tiles < 0) g_wide_tiles = env_int("ICEPOP_WIDE_TILES", 1) ? 1 : 0;
+  return g_wide_tiles == 1;
+}
+
 int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
              int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent(),
              const void* B2 = nullptr, bool keep_empty = false) {
@@ -262,7 +277,9 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
   const int cg = cta_group();
-  const int bn = bn_of(epi);
+  const bool long_k = (K + BK - 1) / BK >= long_k_blocks();
+  const bool wide = epi == EPI_STORE && cg == 2 && long_k && wide_tiles();
+  const int bn = wide ? BN_WIDE : bn_of(epi);
   if (epi_dual(epi) && !B2) return fail(ICEPOP_EINVAL, "dual-accumulator GEMM needs a second B operand");
   CUtensorMap ta, tb, tb2;
   ICP_TRY(operand_map(&ta, A, M, K, lda, a_mn, BM));
@@ -283,7 +300,7 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
-  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, sh.k_blocks >= long_k_blocks(), K);
+  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, long_k, K);
   sh.ext_dev = ext.dim ? ext.dev : nullptr;
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
@@ -295,17 +312,17 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;
-  if (sh.k_blocks >= long_k_blocks()) {
+  if (long_k) {
     ICP_TRY(tile_counter(st, &sh.wave_counter));
     sh.tile_counter = nullptr;
   } else {
     ICP_TRY(tile_counter(st, &sh.tile_counter));
   }
   if (epi == EPI_STORE) {
-    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
-    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
-    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
-    return launch_umma<true, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg);
+    if (!a_mn && !b_mn) return launch_umma<false, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg, wide);
+    if (!a_mn && b_mn) return launch_umma<false, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg, wide);
+    if (a_mn && !b_mn) return launch_umma<true, false, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg, wide);
+    return launch_umma<true, true, EPI_STORE>(ta, tb, tb2, tc, sh, ep, st, cg, wide);
   }
   if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
   switch (epi) {
@@ -1179,6 +1196,11 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
 int icepop_set_cta_group(int32_t cta_group) {
   if (cta_group != 1 && cta_group != 2) return fail(ICEPOP_EINVAL, "cta_group must be 1 or 2");
   g_cta_group = cta_group;
+  return ICEPOP_OK;
+}
+
+int icepop_set_wide_tiles(int32_t enable) {
+  g_wide_tiles = enable ? 1 : 0;
   return ICEPOP_OK;
 }
 

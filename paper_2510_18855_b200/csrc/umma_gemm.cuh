@@ -126,7 +126,15 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + B2_BYTES;
   static constexpr int STAGES = (220 * 1024 / STAGE_BYTES) < 6 ? (220 * 1024 / STAGE_BYTES) : 6;
   static constexpr int NACC = DUAL ? 2 : 1;              // accumulators per tile
-  static constexpr int TMEM_COLS = 2 * BN * NACC;        // double-buffered
+  // double-buffered accumulators while they fit the 512 TMEM columns; 512-wide tiles (long-K
+  // GEMMs, where one tile's MMAs take milliseconds and the epilogue microseconds) use one
+  static constexpr int ACC_BUFS = 2 * BN * NACC <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = ACC_BUFS * BN * NACC;
+  // MMAs per k16 step: N <= 256 per tcgen05.mma, so a 512-wide tile issues two, the second
+  // reading B at +B_SUB_BYTES (its rows in each CTA's slab) into TMEM columns [256, 512)
+  static constexpr int NSUB = BN > 256 ? BN / 256 : 1;
+  static constexpr int N_MMA = BN / NSUB;
+  static constexpr int B_SUB_BYTES = (N_MMA / CG) * 128;  // K-major: rows x 128 B; MN-major: boxes x 8 KB
   static constexpr int TILE_M = BM * CG;
   static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
   // EPI_DZ TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 128 B, SWIZZLE_128B)
@@ -146,7 +154,19 @@ __device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& 
 }
 
 // ------------------------------------------------------------------ epilogues
-template <int BN>
+// Output column of TMEM column tc of a tile whose n range starts at n0. With CTA pairs and a
+// 512-wide tile each CTA stages a contiguous 256-row slab of B; MMA h (columns [256h, 256h+256))
+// reads rows [128h, 128h+128) of both slabs, so its column j is B row (j / 128) * 256 + 128h + j % 128.
+template <int BN, int CG>
+__device__ __forceinline__ int tile_col(int n0, int tc) {
+  if (CG == 2 && BN > 256) {
+    const int h = tc >> 8, j = tc & 255;
+    return n0 + (j >> 7) * 256 + h * 128 + (j & 127);
+  }
+  return n0 + tc;
+}
+
+template <int BN, int CG>
 __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
                                           int row, uint32_t taddr) {
   const int mm = m0 + row;
@@ -156,7 +176,7 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);  // warp-collective: never inside a per-thread branch
-    const int col0 = n0 + c * 32;
+    const int col0 = tile_col<BN, CG>(n0, c * 32);
     if (!row_ok || col0 >= sh.N) continue;
     const bool full = (col0 + 32 <= sh.N) && ep.vec_ok;
     if (ep.rs_world > 0) {
@@ -688,7 +708,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (the pair leader only) + dynamic tile scheduler
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = idesc_bf16(BM * CG, Cfg::N_MMA, A_MN, B_MN);
       auto publish = [&](int j, int tile) {
         const int s = j & (Cfg::RING - 1);
         ring[s] = tile;
@@ -736,8 +756,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
                                      : sdesc_sw128(b_base + kk * 32, 16, 1024);
             const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-            if (CG == 2) umma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
-            else umma_bf16(d_tmem, ad, bd, idesc, accum);
+#pragma unroll
+            for (int h = 0; h < Cfg::NSUB; ++h) {
+              // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
+              const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
+              if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
+              else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
+            }
             if (DUAL) {
               const uint64_t bd2 = B_MN ? sdesc_sw128(b2_base + kk * 2048, BK * 128, 1024)
                                         : sdesc_sw128(b2_base + kk * 32, 16, 1024);
@@ -751,7 +776,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         // accumulator ready for the epilogue warps (of both CTAs)
         if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
         if (dynamic) {
           cur = nxt1;
           nxt1 = nxt2;
@@ -777,7 +802,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
-      if (EPI == EPI_STORE) epi_store<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      if (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
       if (EPI == EPI_LSE)
         epi_lse<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
                     quarter, taddr);
@@ -796,7 +821,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (CG == 2) mbar_arrive_cluster(mapa_shared(tempty0 + 8 * acc, 0));
         else mbar_arrive(tempty0 + 8 * acc);
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
     if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
     if (STAGING && lane == 0) bulk_wait<0>();  // all staged tile stores complete

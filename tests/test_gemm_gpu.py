@@ -55,3 +55,38 @@ def test_gemm_bf16_out_and_accumulate(cuda_device, cta_group):
     C0 = torch.ones(M, N, device=cuda_device)
     C1 = _gemm(A, B, M, N, K, 1, 1, accumulate=True, C=C0)
     assert torch.allclose(C1.double(), ref + 1.0, atol=1e-2, rtol=1e-4)
+
+
+@pytest.fixture
+def wide_tiles():
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+
+    def set_(on):
+        _lib.check(lib.icepop_set_wide_tiles(int(on)))
+
+    yield set_
+    set_(True)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(600, 1304, 16448), (256, 512, 16384), (136, 2104, 20000)])
+def test_gemm_long_k_wide_tiles(cuda_device, wide_tiles, a_mn, b_mn, M, N, K):
+    """K >= 16384 runs the static-wave schedule; on CTA pairs the 256 x 512 tiles (two N = 256
+    MMAs into one accumulator, pair-interleaved B rows). Same per-element k order as the
+    256 x 256 tiles, so the two agree bit for bit; both vs fp64."""
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).to(cuda_device)
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16).to(cuda_device)
+    wide_tiles(True)
+    Cw = _gemm(A, B, M, N, K, a_mn, b_mn)
+    Cw_acc = _gemm(A, B, M, N, K, a_mn, b_mn, accumulate=True, C=torch.full((M, N), 0.5, device=cuda_device))
+    Cw_bf = _gemm(A, B, M, N, K, a_mn, b_mn, c_f32=False)
+    wide_tiles(False)
+    Cn = _gemm(A, B, M, N, K, a_mn, b_mn)
+    ref = A.double() @ B.double().T
+    assert (Cw.double() - ref).abs().max().item() <= 1e-3 * (K ** 0.5)
+    assert torch.equal(Cw, Cn)
+    assert torch.equal(Cw_acc, Cw + 0.5)
+    assert torch.equal(Cw_bf, Cw.to(torch.bfloat16))
