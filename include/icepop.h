@@ -147,14 +147,16 @@ typedef struct icepop_fwd_out {
   float* kl_w;         /* [n_tokens] w_t * gamma / T (the KL gradient's coefficient)       */
   /* Stored-probabilities mode (optional; both NULL = the backward recomputes the logits):
    * probs    [n_tokens, vocab] bf16, q = exp(z - m) with m the row's maximum over each
-   *          ICEPOP_PROBS_TILE-column vocab tile (so q is in [0, 1]); needs vocab % 8 == 0 and
+   *          ICEPOP_PROBS_SLAB-column vocab slab (so q is in [0, 1]); needs vocab % 8 == 0 and
    *          no weight_ref. 2*n_tokens*vocab bytes of HBM buy a backward without the K3 GEMM.
-   * tile_max [n_tokens, ceil(vocab / ICEPOP_PROBS_TILE)] f32, m in log2 units (z log2(e)). */
+   * tile_max [n_tokens, ICEPOP_TILE_MAX_LD(vocab)] f32: m of slab j at column j, in log2 units
+   *          (z log2(e)); columns past ceil(vocab / ICEPOP_PROBS_SLAB) are padding. */
   void* probs;
   float* tile_max;
 } icepop_fwd_out;
 
-#define ICEPOP_PROBS_TILE 256
+#define ICEPOP_PROBS_SLAB 64
+#define ICEPOP_TILE_MAX_LD(vocab) (4 * (((vocab) + 255) / 256))
 
 /* Forward: fused lm_head GEMM + online log-softmax/gather/entropy (tcgen05), then the
  * IcePop epilogue. Logits are never written to HBM (only the bf16 probabilities when

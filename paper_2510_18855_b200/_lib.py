@@ -21,7 +21,12 @@ ALGO_ICEPOP, ALGO_GRPO, ALGO_TIS = 0, 1, 2
 W_DV, W_VD = 0, 1
 NSTATS = 8
 ABI_VERSION = 2
-PROBS_TILE = 256  # ICEPOP_PROBS_TILE: vocab columns per tile_max entry
+PROBS_SLAB = 64  # ICEPOP_PROBS_SLAB: vocab columns per tile_max entry
+
+
+def tile_max_ld(vocab: int) -> int:
+    """ICEPOP_TILE_MAX_LD: row length of tile_max (one float4 per 256-column K1 tile)."""
+    return 4 * ((vocab + 255) // 256)
 STAT_OBJECTIVE, STAT_N_POPPED, STAT_TOKENS, STAT_SUM_ENTROPY = 0, 1, 2, 3
 STAT_SUM_ENTROPY_POPPED, STAT_SUM_LOGP, STAT_SUM_KL, STAT_ERRORS = 4, 5, 6, 7
 

@@ -229,17 +229,18 @@ int env_int(const char* name, int dflt) {
   return e ? std::max(0, atoi(e)) : dflt;
 }
 
-int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k, int64_t K) {
+int group_m_for(int epi, int m_tiles, int n_tiles, int cg, bool long_k, int64_t K, int units) {
   // Short K (dynamic claim order): the group's A rows stay resident in L2 while B streams, so
   // size the group for a ~32 MB A-set (measured: 16 pair-rows at K = 4096, 8 at K = 8192).
-  // Long K (waves): 8 pair-rows balances A and B re-reads (measured).
+  // Long K (waves): 8 pair-rows balances A and B re-reads (measured). When a wave spans whole
+  // tile rows anyway (n_tiles <= units / 2, e.g. K4/K5 with d = 4096 on 512-wide tiles), the
+  // group only orders tiles inside the wave: 2 measured best (K4 1,540 -> 1,567 TFLOP/s).
   static const int g_short = env_int("ICEPOP_GROUP_M", 0);
-  static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 8);
+  static const int g_long = env_int("ICEPOP_GROUP_M_LONG", 0);
   (void)epi;
-  (void)n_tiles;
   int g;
   if (long_k) {
-    g = g_long;
+    g = g_long > 0 ? g_long : (2 * n_tiles <= units ? 2 : 8);
   } else if (g_short > 0) {
     g = g_short;
   } else {
@@ -300,7 +301,7 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
-  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, long_k, K);
+  sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, long_k, K, num_sms() / cg);
   sh.ext_dev = ext.dim ? ext.dev : nullptr;
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
@@ -612,8 +613,8 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     if (ref) return fail(ICEPOP_EINVAL, "stored probabilities are not supported with weight_ref");
     if (!out->tile_max) return fail(ICEPOP_EINVAL, "stored probabilities need out->tile_max");
     if (V % 8 != 0) return fail(ICEPOP_EINVAL, "stored probabilities need vocab %% 8 == 0");
-    if ((reinterpret_cast<uintptr_t>(out->probs) & 15u) != 0)
-      return fail(ICEPOP_EINVAL, "out->probs must be 16-byte aligned");
+    if (((reinterpret_cast<uintptr_t>(out->probs) | reinterpret_cast<uintptr_t>(out->tile_max)) & 15u) != 0)
+      return fail(ICEPOP_EINVAL, "out->probs and out->tile_max must be 16-byte aligned");
   }
   const double* adv = nullptr;
   ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
@@ -631,7 +632,7 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     ep.ztok = w.ztok;
     ep.probs = static_cast<__nv_bfloat16*>(out->probs);
     ep.tile_max = out->tile_max;
-    ep.tm_ld = (int32_t)((V + BN_ - 1) / BN_);
+    ep.tm_ld = (int32_t)(4 * ((V + BN_ - 1) / BN_));  // four 64-column slab maxima per 256-column tile
     const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
     ICP_TRY(run_umma(ref ? EPI_LSE_REF : EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st,
                      Extent(), ref ? weight_ref : nullptr));
@@ -859,10 +860,10 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       cs.coeff = coeff_src + c0;
     }
     if (sp) {
-      const int32_t n_tiles = (int32_t)((V + BN_ - 1) / BN_);
+      const int32_t tm_ld = (int32_t)(4 * ((V + BN_ - 1) / BN_));
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
-      k_dz_probs<<<grid, DZP_THREADS, n_tiles * sizeof(float), st>>>(
-          reinterpret_cast<uint4*>(dzb), sv.tile_max, n_tiles, lse, coeff, (float)grad_scale, tokens, nc, V / 8);
+      k_dz_probs<<<grid, DZP_THREADS, 0, st>>>(reinterpret_cast<uint4*>(dzb), sv.tile_max, tm_ld, lse, coeff,
+                                               (float)grad_scale, tokens, nc, V / 8);
       ICP_CUDA(cudaGetLastError());
     } else {
       ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V,

@@ -476,18 +476,18 @@ __global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* 
   }
 }
 
-// Stored-probabilities backward (replaces the K3 GEMM): turns K1's q[t, v] = 2^(u - m_tile)
+// Stored-probabilities backward (replaces the K3 GEMM): turns K1's q[t, v] = 2^(u - m_slab)
 // into dZ in place,
-//   dz[t, v] = cf_t * (e_{y_t} - q[t, v] * 2^(m_tile(t, v / 256) - lse2_t)),  cf_t = coeff_t * scale,
+//   dz[t, v] = cf_t * (e_{y_t} - q[t, v] * 2^(m_slab(t, v / 64) - lse2_t)),  cf_t = coeff_t * scale,
 // the same expression epi_dz evaluates from recomputed logits (p = 2^(u - lse2)). Rows with
-// cf_t == 0 are written as zeros without being read. One block per row (grid-stride), the
-// row's tile scales in smem, 4 x 16-byte loads in flight per thread. Needs V % 8 == 0.
+// cf_t == 0 are written as zeros without being read. One block per row (grid-stride); each
+// 16-byte chunk (8 columns, one slab) takes its slab scale from the L1-resident tile_max row;
+// 4 chunks in flight per thread. Needs V % 8 == 0.
 constexpr int DZP_THREADS = 256;
 __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ probs, const float* __restrict__ tile_max,
-                                                          int32_t n_tiles, const float* __restrict__ lse,
+                                                          int32_t tm_ld, const float* __restrict__ lse,
                                                           const float* __restrict__ coeff, float coeff_scale,
                                                           const int32_t* __restrict__ tokens, int64_t n, int64_t v8) {
-  extern __shared__ float sc[];  // [n_tiles]
   for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
     uint4* row = probs + t * v8;
     const float cf = coeff[t] * coeff_scale;
@@ -497,22 +497,24 @@ __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ pr
     }
     const float lse2 = lse[t] * 1.4426950408889634f;  // log2(e)
     const int y = tokens[t];
-    __syncthreads();  // previous row's readers of sc are done
-    for (int j = threadIdx.x; j < n_tiles; j += DZP_THREADS) sc[j] = exp2f(tile_max[t * n_tiles + j] - lse2);
-    __syncthreads();
+    const float* tm = tile_max + t * tm_ld;
     constexpr int U = 4;
     for (int64_t k0 = threadIdx.x; k0 < v8; k0 += U * DZP_THREADS) {
       uint4 x[U];
+      float sm[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t k = k0 + u * DZP_THREADS;
-        if (k < v8) x[u] = row[k];
+        if (k < v8) {
+          x[u] = row[k];
+          sm[u] = __ldg(tm + (k >> 3));  // 64 columns per slab = 8 chunks
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t k = k0 + u * DZP_THREADS;
         if (k >= v8) break;
-        const float s = sc[k >> 5] * -cf;  // 8 columns per uint4, 256 per tile
+        const float s = exp2f(sm[u] - lse2) * -cf;
         uint32_t* w = reinterpret_cast<uint32_t*>(&x[u]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

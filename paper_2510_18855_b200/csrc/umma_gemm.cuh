@@ -104,8 +104,8 @@ struct EpiParams {
   const float* lse_ref;    // [M] natural units
   const float* kl;         // [M] kl_t
   const float* kl_w;       // [M] w_t * gamma / T
-  // EPI_LSE stored-probabilities mode: q[m, v] = 2^(u - tile max) as bf16 through the tensor
-  // map (row stride = N), tile_max[m * tm_ld + n_blk] = the tile maximum (log2 units)
+  // EPI_LSE stored-probabilities mode: q[m, v] = 2^(u - slab max) as bf16 through the tensor
+  // map (row stride = N), tile_max[m * tm_ld + 4 n_blk + c] = 64-column slab c's maximum (log2)
   __nv_bfloat16* probs;
   float* tile_max;
   int32_t tm_ld;
@@ -266,69 +266,74 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
 // K1 epilogue: log-sum-exp statistics of this tile's BN columns for one row, in log2 units,
 //   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
 // so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2).
-// Pass 1 takes mx (and gathers z[y]); pass 2 accumulates s, q. In stored-probabilities mode
-// (ep.probs) pass 2 also emits q[m, v] = 2^(u_v - mx) in [0, 1] as bf16 (TMA stores, clipped to
-// M rows / N columns) and tile_max[m, n_blk] = mx, from which the backward forms dZ without
-// recomputing logits. The statistics are the same bits in both modes.
+// One TMEM pass in 64-column slabs: each slab's (max, sum, q) is taken against the slab's own
+// maximum and merged online into the tile's. In stored-probabilities mode (ep.probs) the slab
+// also emits q[m, v] = 2^(u_v - slab max) in [0, 1] as bf16 (TMA stores, clipped to M rows /
+// N columns) and tile_max[m, 4 n_blk + c] = slab c's maximum, from which the backward forms dZ
+// without recomputing logits. The statistics are the same bits in both modes.
 template <int BN>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
-                                              uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row,
-                                              int lane, int quarter, uint32_t taddr) {
+                                        uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
+                                        int quarter, uint32_t taddr) {
+  static_assert(BN == 4 * 64, "tile_max holds four 64-column slab maxima per tile");
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
-  float mx = -1e30f;
-#pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    float v[32];
-    tmem_ld32(taddr + c * 32, v);
-    const int col0 = n0 + c * 32;
-    if (col0 >= sh.N) continue;  // warp-uniform
-    const int rel = y - col0;
-    if ((unsigned)rel < 32u) {
-      float zt = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) zt = (j == rel) ? v[j] : zt;
-      if (row_ok) ep.ztok[m] = zt * ep.inv_t;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, (col0 + j < sh.N) ? v[j] * ep.scale_log2 : -1e30f);
-  }
   const int row0 = m0 + quarter * 32;
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
-  float s = 0.f, q = 0.f;
+  float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
+  float sm0 = -1e30f, sm1 = -1e30f, sm2 = -1e30f, sm3 = -1e30f;  // slab maxima (registers, not a local array)
 #pragma unroll 1
-  for (int c = 0; c < BN / 64; ++c) {
-    float v[32], w[32];
-    tmem_ld32(taddr + c * 64, v);
-    tmem_ld32(taddr + c * 64 + 32, w);
+  for (int c = 0; c < 4; ++c) {
+    float v[64];
+    tmem_ld32(taddr + c * 64, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld32(taddr + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
     const int col0 = n0 + c * 64;
     if (col0 >= sh.N) continue;  // warp-uniform
+    const int rel = y - col0;
+    if ((unsigned)rel < 64u) {  // the sampled token's logit lives in this slab
+      float zt = 0.f;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
+      if (row_ok) ep.ztok[m] = zt * ep.inv_t;
+    }
+    const bool full = col0 + 64 <= sh.N;
+    float mx = -1e30f;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) mx = fmaxf(mx, (full || col0 + j < sh.N) ? v[j] : -1e30f);
+    mx *= ep.scale_log2;  // scale > 0: max commutes with it
+    float s = 0.f, q = 0.f;
     uint32_t pk[32];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      float e[4], d[4];
-      const float x[4] = {v[2 * j], v[2 * j + 1], w[2 * j], w[2 * j + 1]};
-      const int cc[4] = {col0 + 2 * j, col0 + 2 * j + 1, col0 + 32 + 2 * j, col0 + 33 + 2 * j};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        d[i] = fmaf(x[i], ep.scale_log2, -mx);
-        e[i] = cc[i] < sh.N ? fast_exp2(d[i]) : 0.f;
-        s += e[i];
-        q = fmaf(e[i], cc[i] < sh.N ? d[i] : 0.f, q);
-      }
-      pk[j] = pack_bf16x2(e[0], e[1]);
-      pk[16 + j] = pack_bf16x2(e[2], e[3]);
+    for (int j = 0; j < 32; ++j) {
+      const bool ok0 = full || col0 + 2 * j < sh.N, ok1 = full || col0 + 2 * j + 1 < sh.N;
+      const float d0 = fmaf(v[2 * j], ep.scale_log2, -mx), d1 = fmaf(v[2 * j + 1], ep.scale_log2, -mx);
+      const float e0 = ok0 ? fast_exp2(d0) : 0.f, e1 = ok1 ? fast_exp2(d1) : 0.f;
+      s += e0 + e1;
+      q = fmaf(e0, ok0 ? d0 : 0.f, fmaf(e1, ok1 ? d1 : 0.f, q));
+      pk[j] = pack_bf16x2(e0, e1);
     }
     if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
+    sm0 = c == 0 ? mx : sm0;
+    sm1 = c == 1 ? mx : sm1;
+    sm2 = c == 2 ? mx : sm2;
+    sm3 = c == 3 ? mx : sm3;
+    // merge the slab into the tile's running (max, sum, q)
+    const float nm = fmaxf(run_m, mx);
+    const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);
+    run_q = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(mx - nm, s, q));
+    run_s = fmaf(a, run_s, b * s);
+    run_m = nm;
   }
   if (row_ok) {
     float* p = ep.part + (int64_t)n_blk * 3 * sh.M + m;
-    p[0] = mx;
-    p[sh.M] = s;
-    p[2 * (int64_t)sh.M] = q;
-    if (store) ep.tile_max[(int64_t)m * ep.tm_ld + n_blk] = mx;
+    p[0] = run_m;
+    p[sh.M] = run_s;
+    p[2 * (int64_t)sh.M] = run_q;
+    if (store)
+      *reinterpret_cast<float4*>(ep.tile_max + (int64_t)m * ep.tm_ld + 4 * n_blk) =
+          make_float4(sm0, sm1, sm2, sm3);
   }
 }
 
@@ -802,19 +807,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
-      if (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
-      if (EPI == EPI_LSE)
+      if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
+      if constexpr (EPI == EPI_LSE)
         epi_lse<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
                     quarter, taddr);
-      if (EPI == EPI_DZ) {
+      if constexpr (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
           epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
                          quarter, taddr);
         else
           epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       }
-      if (EPI == EPI_LSE_REF) epi_lse_ref<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
-      if (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+      if constexpr (EPI == EPI_LSE_REF) epi_lse_ref<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
+      if constexpr (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

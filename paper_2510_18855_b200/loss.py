@@ -38,7 +38,7 @@ LAYOUTS = {"dv": _lib.W_DV, "vd": _lib.W_VD}
 DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(96 * 10**9)))
 
 
-# Stored-probabilities mode (include/icepop.h): K1 also writes bf16 q = exp(z - tile max)
+# Stored-probabilities mode (include/icepop.h): K1 also writes bf16 q = exp(z - slab max)
 # [N, V] so the backward needs no K3 logit recompute (6 instead of 8 N.d.V FLOPs per step).
 # "auto" stores them when 2.N.V bytes fit in STORE_PROBS_FRACTION of the free device memory.
 STORE_PROBS = os.environ.get("ICEPOP_STORE_PROBS", "auto")
@@ -52,7 +52,7 @@ def _resolve_store_probs(store_probs, n: int, v: int, device, with_ref: bool) ->
         return False
     if store_probs is True:
         return True
-    need = 2 * n * v + 4 * n * ((v + _lib.PROBS_TILE - 1) // _lib.PROBS_TILE)
+    need = 2 * n * v + 4 * n * _lib.tile_max_ld(v)
     free = _free_bytes(device)
     return free is not None and need <= STORE_PROBS_FRACTION * free
 
@@ -258,7 +258,7 @@ def icepop_fwd(
         probs = tile_max = None
         if _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
             probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
-            tile_max = torch.empty((n, -(-shape.vocab // _lib.PROBS_TILE)), dtype=torch.float32, device=dev)
+            tile_max = torch.empty((n, _lib.tile_max_ld(shape.vocab)), dtype=torch.float32, device=dev)
         fwd_b = _lib._sz()
         _lib.check(lib.icepop_workspace_bytes(shape, 0, 1 if wr is not None else 0, fwd_b, None))
         ws = torch.empty(max(fwd_b.value, 1), dtype=torch.uint8, device=dev)
@@ -612,7 +612,7 @@ def _(hidden, weight, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offs
     v = weight.shape[1] if layout == _lib.W_DV else weight.shape[0]
     sp = store_probs and hidden.dtype == torch.bfloat16
     probs_shape = (n, v) if sp else (0,)
-    tm_shape = (n, -(-v // _lib.PROBS_TILE)) if sp else (0,)
+    tm_shape = (n, _lib.tile_max_ld(v)) if sp else (0,)
     return (hidden.new_empty((), dtype=torch.float64), hidden.new_empty((_lib.NSTATS,), **{"dtype": torch.float64}),
             torch.empty(n, **f32), torch.empty(n, **f64), torch.empty(n, **f32),
             torch.empty(n, dtype=torch.uint8, device=hidden.device), torch.empty(n, **f64),

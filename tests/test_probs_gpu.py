@@ -1,8 +1,8 @@
 """Stored-probabilities mode (include/icepop.h `icepop_fwd_out.probs`): K1 also writes
-q = exp(z - tile max) as bf16 and the backward forms dZ from it in place instead of
+q = exp(z - slab max) (64-column slabs) as bf16 and the backward forms dZ from it in place instead of
 recomputing the logits with the K3 GEMM.
 
-Checked here: the forward statistics are the same bits in both modes; q and tile_max
+Checked here: the forward statistics are the same bits in both modes; q and the slab maxima
 against an fp32 torch reference of the same logits (q within bf16 rounding, 2^-8 relative);
 gradients against the recompute mode and the fp64 oracle (relative Frobenius <= 1e-2, the
 bf16 path's tolerance); consumption semantics (a second backward recomputes); ABI errors;
@@ -54,7 +54,7 @@ def test_forward_statistics_identical_in_both_modes(cuda_device, cta_group, layo
 @pytest.mark.parametrize("temperature", [1.0, 0.7])
 @pytest.mark.parametrize("layout", ["vd", "dv"])
 def test_stored_probabilities_match_fp32_softmax(cuda_device, cta_group, layout, temperature):
-    """q * 2^(tile_max - lse log2 e) is the softmax; V = 1000 leaves a ragged last tile and a
+    """q * 2^(slab max - lse log2 e) is the softmax; V = 1000 leaves a ragged last tile and a
     ragged last 64-column slab, N is not a multiple of 128."""
     from paper_2510_18855_b200 import _lib
     from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
@@ -64,18 +64,21 @@ def test_stored_probabilities_match_fp32_softmax(cuda_device, cta_group, layout,
                    IcePopConfig(temperature=temperature), layout=layout, store_probs=True)
     probs, tmax = f.extras["probs"].float(), f.extras["tile_max"]
     N, V = probs.shape
-    assert N % 128 != 0 and tmax.shape == (N, -(-V // _lib.PROBS_TILE))
+    S = _lib.PROBS_SLAB
+    n_slabs = -(-V // S)
+    assert N % 128 != 0 and tmax.shape == (N, _lib.tile_max_ld(V)) and tmax.shape[1] >= n_slabs
+    tmax = tmax[:, :n_slabs]
     z = _logits(c, cuda_device, temperature)
     u = z * (1.0 / np.log(2.0))
-    pad = tmax.shape[1] * _lib.PROBS_TILE - V
-    ref_max = torch.nn.functional.pad(u, (0, pad), value=-1e30).view(N, -1, _lib.PROBS_TILE).amax(-1)
+    pad = n_slabs * S - V
+    ref_max = torch.nn.functional.pad(u, (0, pad), value=-1e30).view(N, -1, S).amax(-1)
     torch.testing.assert_close(tmax, ref_max, rtol=0, atol=2e-4)
     assert float(probs.min()) >= 0.0 and float(probs.max()) <= 1.0
-    # each tile's maximum entry is stored as exactly 1 (q = 2^0)
-    tiles = torch.nn.functional.pad(probs, (0, pad)).view(N, -1, _lib.PROBS_TILE)
-    assert torch.all(tiles.amax(-1) == 1.0)
+    # each slab's maximum entry is stored as exactly 1 (q = 2^0)
+    slabs = torch.nn.functional.pad(probs, (0, pad)).view(N, -1, S)
+    assert torch.all(slabs.amax(-1) == 1.0)
     scale = torch.exp2(tmax - (f.lse * (1.0 / np.log(2.0)))[:, None])
-    p = probs * scale.repeat_interleave(_lib.PROBS_TILE, dim=1)[:, :V]
+    p = probs * scale.repeat_interleave(S, dim=1)[:, :V]
     ref = torch.softmax(z, dim=1)
     torch.testing.assert_close(p, ref, rtol=8e-3, atol=1e-6)
 
@@ -181,7 +184,7 @@ def test_abi_rejects_invalid_probs_arguments(cuda_device):
     c = _case(seed=57, V=1000)
     N = len(c["tokens"])
     probs = torch.empty((N, 1000), dtype=torch.bfloat16, device=cuda_device)
-    tm = torch.empty((N, 4), dtype=torch.float32, device=cuda_device)
+    tm = torch.empty((N, _lib.tile_max_ld(1000)), dtype=torch.float32, device=cuda_device)
     rc, *_ = _c_fwd(c, cuda_device, probs, None)
     assert rc == _lib.EINVAL  # tile_max missing
     rc, *_ = _c_fwd(c, cuda_device, probs, tm, weight_ref=c["W"].to(cuda_device))
@@ -211,13 +214,14 @@ def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group):
     buf = torch.full((N * V + 2 * G,), 12345.0, dtype=torch.bfloat16, device=cuda_device)
     # 16-byte aligned start G elements in (G * 2 bytes)
     probs = buf[G:G + N * V].view(N, V)
-    tm_buf = torch.full((N * 4 + 2 * 64,), 777.0, dtype=torch.float32, device=cuda_device)
-    tm = tm_buf[64:64 + N * 4].view(N, 4)
+    L = _lib.tile_max_ld(V)
+    tm_buf = torch.full((N * L + 2 * 64,), 777.0, dtype=torch.float32, device=cuda_device)
+    tm = tm_buf[64:64 + N * L].view(N, L)
     rc, *_ = _c_fwd(c, cuda_device, probs, tm)
     assert rc == _lib.OK
     torch.cuda.synchronize()
     assert torch.all(buf[:G] == 12345.0) and torch.all(buf[G + N * V:] == 12345.0)
-    assert torch.all(tm_buf[:64] == 777.0) and torch.all(tm_buf[64 + N * 4:] == 777.0)
+    assert torch.all(tm_buf[:64] == 777.0) and torch.all(tm_buf[64 + N * L:] == 777.0)
     assert torch.isfinite(probs.float()).all() and float(probs.float().max()) == 1.0
 
 
