@@ -75,6 +75,20 @@ def _take_probs(fwd: "IcePopForward", kl_grad: bool):
     return fwd.extras.pop("probs"), fwd.extras.pop("tile_max")
 
 
+def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
+    """The recompute-mode backward workspace with the largest dZ chunk that allocates: the
+    free-memory estimate counts torch's cached blocks, which fragmentation can make unusable
+    for one large block, so an out-of-memory halves the chunk (down to 128 rows)."""
+    cb = _dz_chunk_bytes(device)
+    while True:
+        try:
+            return torch.empty(bwd_workspace_bytes(n, d, v, n_seqs, cb), dtype=torch.uint8, device=device)
+        except torch.OutOfMemoryError:
+            if cb <= 128 * 2 * v:
+                raise
+            cb = max(128 * 2 * v, cb // 2)
+
+
 def _dz_chunk_bytes(device) -> int:
     free = _free_bytes(device)
     if free is None:
@@ -257,8 +271,13 @@ def icepop_fwd(
             kl_w = torch.empty(n, dtype=torch.float32, device=dev)
         probs = tile_max = None
         if _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
-            probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
-            tile_max = torch.empty((n, _lib.tile_max_ld(shape.vocab)), dtype=torch.float32, device=dev)
+            try:
+                probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
+                tile_max = torch.empty((n, _lib.tile_max_ld(shape.vocab)), dtype=torch.float32, device=dev)
+            except torch.OutOfMemoryError:
+                if store_probs is True:
+                    raise
+                probs = tile_max = None  # "auto": the recompute mode needs no [N, V] buffer
         fwd_b = _lib._sz()
         _lib.check(lib.icepop_workspace_bytes(shape, 0, 1 if wr is not None else 0, fwd_b, None))
         ws = torch.empty(max(fwd_b.value, 1), dtype=torch.uint8, device=dev)
@@ -450,8 +469,7 @@ def icepop_bwd(
         probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
         ws = None
         if probs is None:
-            ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, _dz_chunk_bytes(dev)), dtype=torch.uint8,
-                             device=dev)
+            ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                            lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                            probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
@@ -517,11 +535,9 @@ def icepop_bwd_reduce_scatter(
     probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
     scratch = ws = None
     if probs is None:
-        cb = _dz_chunk_bytes(dev)
-        rows = cb // (2 * v)
-        chunk = n if rows >= n else max(128, rows // 128 * 128)
-        scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev) if chunk < n else None
-        ws = torch.empty(bwd_workspace_bytes(n, d, v, shape.n_seqs, cb), dtype=torch.uint8, device=dev)
+        ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
+        single_chunk = ws.numel() >= bwd_workspace_bytes(n, d, v, shape.n_seqs, 2 * n * v)
+        scratch = None if single_chunk else torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                        lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                        probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
