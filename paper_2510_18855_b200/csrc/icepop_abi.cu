@@ -313,6 +313,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;
+  static const int sync_kb = env_int("ICEPOP_SYNC_KB", 64);  // K5 at C2: 1,495 -> 1,529 TFLOP/s (64 ~ 256 > 16)
+  sh.sync_kb = sync_kb;
   if (long_k) {
     ICP_TRY(tile_counter(st, &sh.wave_counter));
     sh.tile_counter = nullptr;

@@ -40,6 +40,7 @@ struct GemmShape {
   int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
   int32_t* wave_counter;  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr
+  int32_t sync_kb;        // waves: k-blocks per barrier chunk (0 = one barrier per wave)
   // Device-side extent (sync-free compaction): if ext_dev, the M (ext_dim = 1) or K (ext_dim = 2)
   // extent is clamp(*ext_dev - ext_base, 0, static extent), read at kernel start.
   const int32_t* ext_dev;
@@ -637,30 +638,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // Waves are split into k-chunks of `skb` k-blocks: no unit issues the loads of chunk g
+      // before every unit has issued those of chunk g-1 (one monotonic counter over the whole
+      // launch; skb = k_blocks is a plain barrier per wave). This keeps the tiles of a wave
+      // within ~2 chunks of each other in k, so the operand slices they share stay in L2 even
+      // when K is long (K5: K = tokens). The grid is sized so every unit is co-resident; the
+      // watchdog guards the spin.
+      const int skb = (sh.sync_kb > 0 && sh.sync_kb < sh.k_blocks) ? sh.sync_kb : max(sh.k_blocks, 1);
+      const int spt = max(1, (sh.k_blocks + skb - 1) / skb);  // chunks per tile
+      auto chunk_wait = [&](int g) {
+        const int target = n_units * g;
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_gpu(sh.wave_counter) < target) {
+          __nanosleep(128);
+          if (globaltimer_ns() - t0 > 20000000000ull) {
+            printf("icepop: wave barrier watchdog (block %d)\n", blockIdx.x);
+            __trap();
+          }
+        }
+      };
       for (int j = 0;; ++j) {
         const int tile = ring_get(j, CG == 2 && rank == 1);
         if (tile < 0) {
-          if (waves && rank == 0 && n_waves > j) atomicAdd(sh.wave_counter, n_waves - j);  // pre-pay
+          if (waves && rank == 0 && n_waves > j) atomicAdd(sh.wave_counter, (n_waves - j) * spt);  // pre-pay
           break;
         }
-        if (waves && rank == 0 && j > 0) {
-          // all units must have issued every load of wave j-1 before anyone starts wave j
-          // (the grid is sized so every unit is co-resident; the watchdog guards the spin)
-          const int target = n_units * j;
-          const uint64_t t0 = globaltimer_ns();
-          while (ld_acquire_gpu(sh.wave_counter) < target) {
-            __nanosleep(128);
-            if (globaltimer_ns() - t0 > 20000000000ull) {
-              printf("icepop: wave barrier watchdog (block %d)\n", blockIdx.x);
-              __trap();
-            }
-          }
+        if (waves && rank == 0 && sh.k_blocks == 0) {  // empty K extent: one chunk without loads
+          chunk_wait(j * spt);
+          atomicAdd(sh.wave_counter, 1);
         }
         int m_blk, n_blk;
         tile_coords(sh, tile, m_blk, n_blk);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
         const int n0 = n_blk * BN + (int)rank * B_ROWS;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb_local = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -706,8 +718,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (waves && rank == 0 && (kb % skb == skb - 1 || kb == sh.k_blocks - 1)) atomicAdd(sh.wave_counter, 1);
         }
-        if (waves && rank == 0) atomicAdd(sh.wave_counter, 1);
       }
     }
   } else if (warp == 1) {
