@@ -63,6 +63,7 @@ def main():
     ap.add_argument("--fused-only", action="store_true")
     ap.add_argument("--cgs", default="1,2")
     ap.add_argument("--majors", action="store_true", help="also K4's shape with an MN-major A operand")
+    ap.add_argument("--only", default="", help="comma list of kernel names to run (K1,K1p,K3,K4,K5)")
     a = ap.parse_args()
     cgs = [int(x) for x in a.cgs.split(",")]
     dev = torch.device("cuda", 0)
@@ -95,20 +96,32 @@ def main():
     gw = torch.zeros((V, d), dtype=torch.float32, device=dev)
     shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=d, vocab=V, n_seqs=S, n_groups=1, weight_layout=_lib.W_VD)
     flop = 2.0 * N * d * V
+    only = set(x for x in a.only.split(",") if x)
+
+    def want(k):
+        return not only or k in only
+
     for cg in cgs:
         _lib.check(lib.icepop_set_cta_group(cg))
         f = icepop_fwd(H, W, batch, IcePopConfig(), layout="vd", store_probs=False)
-        run(f"K1 fwd cta{cg}", lambda: icepop_fwd(H, W, batch, IcePopConfig(), layout="vd", store_probs=False), flop,
-            a.seconds)
-        run(f"K1 fwd+probs cta{cg}", lambda: icepop_fwd(H, W, batch, IcePopConfig(), layout="vd", store_probs=True),
-            flop, a.seconds)
-        run(f"K3 dz cta{cg}", lambda: _lib.check(lib.icepop_dz_bf16(
-            shape, 1.0, H.data_ptr(), W.data_ptr(), None, _lib.Saved(tokens=tokens.data_ptr(), lse=f.lse.data_ptr(),
-            coeff=f.coeff.data_ptr()), -1.0, dz.data_ptr(), V, st)), flop, a.seconds)
-        run(f"K4 dhidden cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
-            dz.data_ptr(), W.data_ptr(), gh.data_ptr(), N, d, V, 0, 1, 0, 0, st)), flop, a.seconds)
-        run(f"K5 dweight cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
-            dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, N, 1, 1, 1, 1, st)), flop, a.seconds)
+        if want("K1"):
+            run(f"K1 fwd cta{cg}", lambda: icepop_fwd(H, W, batch, IcePopConfig(), layout="vd", store_probs=False),
+                flop, a.seconds)
+        if want("K1p"):
+            del dz  # the stored probabilities take its place
+            run(f"K1 fwd+probs cta{cg}", lambda: icepop_fwd(H, W, batch, IcePopConfig(), layout="vd",
+                                                            store_probs=True), flop, a.seconds)
+            dz = torch.empty((N, V), dtype=torch.bfloat16, device=dev)
+        if want("K3"):
+            run(f"K3 dz cta{cg}", lambda: _lib.check(lib.icepop_dz_bf16(
+                shape, 1.0, H.data_ptr(), W.data_ptr(), None, _lib.Saved(tokens=tokens.data_ptr(),
+                lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr()), -1.0, dz.data_ptr(), V, st)), flop, a.seconds)
+        if want("K4"):
+            run(f"K4 dhidden cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
+                dz.data_ptr(), W.data_ptr(), gh.data_ptr(), N, d, V, 0, 1, 0, 0, st)), flop, a.seconds)
+        if want("K5"):
+            run(f"K5 dweight cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
+                dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, N, 1, 1, 0, 0, st)), flop, a.seconds)
         if a.majors:  # same GEMM as K4 with A stored [K, M] (dZ^T): the cost of an MN-major A
             dzt = dz.t().contiguous()
             run(f"K4 shape, A MN-major cta{cg}", lambda: _lib.check(lib.icepop_gemm_bf16(
