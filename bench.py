@@ -113,9 +113,11 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- inputs
-def make_batch_host(cfg: dict, rank: int, world: int):
+def make_batch_host(cfg: dict, rank: int, world: int, zero_adv_frac: float = 0.0):
     """Seeded synthetic rollout batch for this rank: rewards ~ Bernoulli(0.5),
-    groups of `group` sequences, this rank owns `seqs` whole sequences."""
+    groups of `group` sequences, this rank owns `seqs` whole sequences. `zero_adv_frac` of the
+    groups (every k-th) get identical rewards -> zero advantages, as all-solved / all-failed
+    prompts do in real RL batches (their rows drop out of the block-sparse backward)."""
     rng = np.random.default_rng(cfg["seed"])
     S_global = cfg["seqs"] * world
     if cfg.get("lens"):  # ragged packed lengths (C4); every rank gets the same per-rank count
@@ -127,6 +129,10 @@ def make_batch_host(cfg: dict, rank: int, world: int):
     cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     go = np.arange(0, S_global + 1, cfg["group"], dtype=np.int32)
     rewards = rng.integers(0, 2, S_global).astype(np.float64)
+    n_groups = len(go) - 1
+    n_zero = int(round(zero_adv_frac * n_groups))
+    for g in np.linspace(0, n_groups, n_zero, endpoint=False).astype(int) if n_zero else []:
+        rewards[go[g]:go[g + 1]] = 1.0
     n_local = int(lens[: cfg["seqs"]].sum())
     return dict(cu=cu, go=go, rewards=rewards, n_local=n_local, token_offset=rank * n_local)
 
@@ -188,7 +194,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
-    meta = make_batch_host(cfg, rank, world)
+    meta = make_batch_host(cfg, rank, world, args.zero_adv_frac)
     H, W, batch, onpolicy = build_device_inputs(cfg, meta, dev, rank)
     icfg = IcePopConfig()
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
@@ -322,7 +328,8 @@ def run_ours(args):
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
                    "dz_mode": "stored-probabilities" if sp else "recompute",
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
-                   "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective},
+                   "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective,
+                   "zero_adv_group_frac": args.zero_adv_frac},
         "gpu_launches": launches_per_step * args.steps,
         "step_tflops_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12, 1),
         "step_frac_of_peak_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12 / pk["tflops"], 4),
@@ -615,6 +622,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--no-onpolicy", action="store_true")
+    ap.add_argument("--zero-adv-frac", type=float, default=0.0,
+                    help="fraction of prompt groups with identical rewards (zero advantages)")
     ap.add_argument("--dw-collective", choices=["fused", "nccl"], default="fused",
                     help="N>1: dW reduce-scatter fused into K5 over NVLink, or NCCL all-reduce")
     args = ap.parse_args()

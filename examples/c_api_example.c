@@ -11,7 +11,7 @@
  * the lm_head [V, d] layout, rewards -> K0 advantages). The forward keeps the bf16
  * probabilities (stored-probabilities mode) and the backward forms dZ from them in place.
  * Prints the statistics and a checksum; with a path argument it also dumps inputs and
- * outputs (tests/test_c_api_gpu.py replays them through the Python layer and compares bits).
+ * outputs (tests/test_c_api.py replays them through the Python layer and compares bits).
  */
 #include <cuda_runtime.h>
 #include <math.h>
@@ -82,7 +82,7 @@ int main(int argc, char** argv) {
   for (int s = 0; s <= N_SEQS; ++s) cu[s] = s * SEQ_LEN;
 
   /* device buffers */
-  void *d_hid, *d_w, *d_probs, *d_gh, *d_fws;
+  void *d_hid, *d_w, *d_probs, *d_gh, *d_fws, *d_bws;
   int32_t *d_tok, *d_cu, *d_go;
   double *d_lpo, *d_lpi, *d_rew, *d_lp, *d_calib, *d_sur, *d_stats;
   float *d_lse, *d_ent, *d_coeff, *d_tmax, *d_gw;
@@ -119,9 +119,11 @@ int main(int argc, char** argv) {
   icepop_shape shape = {N_TOK, 0, HID, VOCAB, N_SEQS, 2, ICEPOP_W_VD, 0};
   icepop_config cfg = {0.5, 5.0, 0.2, 2.0, 1.0, 0.0, ICEPOP_ALGO_ICEPOP, 0};
   icepop_batch batch = {d_tok, d_lpo, d_lpi, d_cu, d_go, NULL, d_rew};
-  size_t fwd_bytes = 0;
+  size_t fwd_bytes = 0, bwd_bytes = 0;
   IK(icepop_workspace_bytes(&shape, 0, 0, &fwd_bytes, NULL));
+  IK(icepop_workspace_bytes(&shape, -1, 0, NULL, &bwd_bytes)); /* stored-probabilities backward */
   CK(cudaMalloc(&d_fws, fwd_bytes));
+  CK(cudaMalloc(&d_bws, bwd_bytes));
   cudaStream_t st;
   CK(cudaStreamCreate(&st));
 
@@ -146,8 +148,8 @@ int main(int argc, char** argv) {
   saved.coeff = d_coeff;
   saved.probs = d_probs;
   saved.tile_max = d_tmax;
-  /* loss = -J: grad_scale = -1; stored probabilities need no backward workspace */
-  IK(icepop_bwd_bf16(&shape, &cfg, d_hid, d_w, NULL, &saved, -1.0, d_gh, 0, d_gw, 0, NULL, 0, st));
+  /* loss = -J: grad_scale = -1; the workspace lets the backward compact zero-coefficient rows */
+  IK(icepop_bwd_bf16(&shape, &cfg, d_hid, d_w, NULL, &saved, -1.0, d_gh, 0, d_gw, 0, d_bws, bwd_bytes, st));
   IK(icepop_finish(d_stats, st));
 
   double stats[ICEPOP_NSTATS];

@@ -128,7 +128,9 @@ int icepop_group_advantages(const double* rewards, const int32_t* group_offsets,
 /* hidden: [n_tokens, d] bf16 row-major. weight (and weight_ref): bf16 in `weight_layout`.
  * Workspace sizes (bytes) for icepop_fwd_bf16 / icepop_bwd_bf16 (with_ref: a weight_ref
  * will be passed). The backward materialises bf16 dZ chunks of at most `max_chunk_tokens`
- * rows (0 = all rows); a smaller workspace than recommended shrinks the chunk (>= 128 rows). */
+ * rows (0 = all rows); a smaller workspace than recommended shrinks the chunk (>= 128 rows).
+ * max_chunk_tokens < 0: the stored-probabilities backward's workspace (row-compaction
+ * buffers only; without it that backward runs every row through the GEMMs). */
 int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, int32_t with_ref,
                            size_t* fwd_bytes, size_t* bwd_bytes);
 
@@ -197,7 +199,9 @@ typedef struct icepop_saved {
  * [- grad_scale*kl_w_t*p*(log p - log p_ref - kl_t) when gamma > 0] (bf16 chunk), then
  * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05. With saved->probs the same dZ
  * is formed in place from the stored probabilities by a bandwidth-bound pass instead (no
- * logit recompute, no workspace needed: workspace may be NULL; not with gamma > 0).
+ * logit recompute; not with gamma > 0). Its workspace (icepop_workspace_bytes with
+ * max_chunk_tokens < 0) lets it compact zero-coefficient rows away in place; with a NULL or
+ * smaller workspace every row goes through K4/K5.
  * grad_hidden: [n_tokens, d], bf16 if grad_hidden_f32 == 0 else f32; may be NULL.
  * grad_weight: f32 in the weight's layout; accumulate != 0 adds into it; may be NULL. */
 int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,

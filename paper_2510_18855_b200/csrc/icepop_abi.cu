@@ -271,9 +271,17 @@ bool wide_tiles() {
   return g_wide_tiles == 1;
 }
 
+// Device-side block lists of a block-sparse GEMM (GemmShape::kb_map ...), or none.
+struct Sparse {
+  const int32_t* kb_map = nullptr;
+  const int32_t* kb_cnt = nullptr;
+  const int32_t* mt_map = nullptr;
+  const int32_t* mt_cnt = nullptr;
+};
+
 int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
              int64_t M, int64_t N, int64_t K, EpiParams ep, cudaStream_t st, Extent ext = Extent(),
-             const void* B2 = nullptr, bool keep_empty = false) {
+             const void* B2 = nullptr, bool keep_empty = false, Sparse sparse = Sparse()) {
   if (M <= 0 || N <= 0 || K <= 0) return ICEPOP_OK;
   if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2)
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
@@ -306,6 +314,10 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.ext_base = ext.base;
   sh.ext_dim = ext.dim;
   sh.keep_empty = keep_empty ? 1 : 0;
+  sh.kb_map = sparse.kb_map;
+  sh.kb_cnt = sparse.kb_cnt;
+  sh.mt_map = sparse.mt_map;
+  sh.mt_cnt = sparse.mt_cnt;
   static const int sleep_ns = env_int("ICEPOP_EPI_SLEEP_NS", 0);
   sh.epi_sleep_ns = (uint32_t)sleep_ns;
   static const int dz_tma = env_int("ICEPOP_DZ_TMA_STORE", 1);
@@ -490,13 +502,15 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   BF16Workspace w;
   memset(&w, 0, sizeof(w));
   const int64_t n = std::max<int64_t>(s->n_tokens, 1);
-  const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
-  const int64_t n_tiles = (s->vocab + bn - 1) / bn;
-  w.part = c.take<float>((size_t)n_tiles * (ref ? 6 : 3) * n);
-  w.ztok = c.take<float>((size_t)n);
-  w.adv = c.take<double>((size_t)s->n_seqs);
-  w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
-  w.err = c.take<unsigned>(4);
+  if (!bwd) {  // the backward reads none of the forward's scratch
+    const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
+    const int64_t n_tiles = (s->vocab + bn - 1) / bn;
+    w.part = c.take<float>((size_t)n_tiles * (ref ? 6 : 3) * n);
+    w.ztok = c.take<float>((size_t)n);
+    w.adv = c.take<double>((size_t)s->n_seqs);
+    w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
+    w.err = c.take<unsigned>(4);
+  }
   if (bwd && skip_inactive()) {
     const int64_t nb = (n + COMPACT_BLOCK - 1) / COMPACT_BLOCK;
     w.idx = c.take<int32_t>((size_t)n);
@@ -510,6 +524,27 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   }
   w.dz = c.take<__nv_bfloat16>((size_t)chunk * (size_t)s->vocab);
   w.chunk = chunk;
+  w.bytes = align_up(c.off, 256);
+  return w;
+}
+
+// Stored-probabilities backward: block lists of the block-sparse K4/K5 (k_block_lists).
+struct SparseWorkspace {
+  int32_t* flags;   // [nb] active 64-token blocks
+  int32_t* kb_map;  // [nb]
+  int32_t* mt_map;  // [nb]
+  int32_t* cnt;     // [2]: active blocks, active m-tiles
+  size_t bytes;
+};
+
+SparseWorkspace carve_sparse(const icepop_shape* s, void* base) {
+  Carver c(base);
+  SparseWorkspace w;
+  const int64_t nb = (std::max<int64_t>(s->n_tokens, 1) + 63) / 64;
+  w.flags = c.take<int32_t>((size_t)nb);
+  w.kb_map = c.take<int32_t>((size_t)nb);
+  w.mt_map = c.take<int32_t>((size_t)nb);
+  w.cnt = c.take<int32_t>(4);
   w.bytes = align_up(c.off, 256);
   return w;
 }
@@ -595,7 +630,8 @@ int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, 
   if (max_chunk_tokens > 0) chunk = std::min<int64_t>(chunk, max_chunk_tokens);
   chunk = std::max<int64_t>(chunk, 1);
   if (fwd_bytes) *fwd_bytes = (size_t)fwd_part_bytes(shape, with_ref != 0);
-  if (bwd_bytes) *bwd_bytes = carve_bf16(shape, nullptr, chunk, true).bytes;
+  if (bwd_bytes)  // max_chunk_tokens < 0: the stored-probabilities backward (block lists only)
+    *bwd_bytes = max_chunk_tokens < 0 ? carve_sparse(shape, nullptr).bytes : carve_bf16(shape, nullptr, chunk, true).bytes;
   return ICEPOP_OK;
 }
 
@@ -792,11 +828,21 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       return fail(ICEPOP_EINVAL, "saved->probs needs vocab %% 8 == 0 and 16-byte alignment");
   }
   // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
-  const bool skip = !sp && skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
+  bool skip = skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
   int64_t chunk = N;
   BF16Workspace w;
   memset(&w, 0, sizeof(w));
-  if (!sp) {
+  // stored probabilities: dZ in place over all rows (zero-coefficient rows become zero rows),
+  // then K4/K5 skip the 64-token blocks / 256-token tiles without any active row when the
+  // workspace holds the block lists (block-sparse GEMMs; no data moves)
+  bool sparse = false;
+  SparseWorkspace sw;
+  memset(&sw, 0, sizeof(sw));
+  if (sp) {
+    sparse = skip && workspace && workspace_bytes >= carve_sparse(shape, nullptr).bytes;
+    if (sparse) sw = carve_sparse(shape, workspace);
+    skip = false;
+  } else {
     const int64_t min_rows = std::min<int64_t>(N, BM);
     const size_t need_min = carve_bf16(shape, nullptr, min_rows, true).bytes;
     if (!workspace || workspace_bytes < need_min)
@@ -832,7 +878,6 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
                                         w.coeff_act, N);
     ICP_CUDA(cudaGetLastError());
     if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));
-    if (grad_weight && (!accumulate || rs)) ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
     hsrc = w.hid_act;
     tok_src = w.tok_act;
     lse_src = w.lse_act;
@@ -863,6 +908,12 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     }
     if (sp) {
       const int32_t tm_ld = (int32_t)(4 * ((V + BN_ - 1) / BN_));
+      if (sparse) {
+        const int64_t nb = (nc + 63) / 64;
+        k_block_flags<<<(int)((nb * 32 + 255) / 256), 256, 0, st>>>(coeff, nc, sw.flags);
+        k_block_lists<<<1, BL_THREADS, 0, st>>>(sw.flags, nb, BM * cta_group() / 64, sw.kb_map, sw.mt_map, sw.cnt);
+        if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));  // skipped tiles
+      }
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
       k_dz_probs<<<grid, DZP_THREADS, 0, st>>>(reinterpret_cast<uint4*>(dzb), sv.tile_max, tm_ld, lse, coeff,
                                                (float)grad_scale, tokens, nc, V / 8);
@@ -882,7 +933,12 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       eh.out_f32 = grad_hidden_f32 ? 1 : 0;
       eh.vec_ok = ((reinterpret_cast<uintptr_t>(eh.out) & 15u) == 0) && (d % 8 == 0);
       // B operand viewed [N = d, K = V]: W[d,V] is K-major, W[V,d] is MN-major
-      ICP_TRY(run_umma(EPI_STORE, dzb, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m));
+      Sparse sp4;
+      if (sparse) {
+        sp4.mt_map = sw.mt_map;
+        sp4.mt_cnt = sw.cnt + 1;
+      }
+      ICP_TRY(run_umma(EPI_STORE, dzb, V, false, weight, dv ? V : d, !dv, nc, d, V, eh, st, ext_m, nullptr, false, sp4));
     }
     // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
     if (grad_weight || (rs && last)) {
@@ -890,7 +946,9 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       memset(&ew, 0, sizeof(ew));
       ew.out = grad_weight;
       ew.out_f32 = 1;
-      ew.accumulate = (skip || accumulate || c0 > 0) ? 1 : 0;
+      // with compacted rows the K extent may be empty: K5 still runs its tiles (keep_empty) and
+      // stores zeros, so dW needs no memset
+      ew.accumulate = (accumulate || c0 > 0) ? 1 : 0;
       if (rs && last) {
         // fused reduce-scatter: store each row (+ this rank's earlier-chunk partial) into the
         // owner's slot over NVLink
@@ -902,14 +960,22 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.out = nullptr;
         ext_k.dim = skip ? 2 : 0;
       }
+      // an empty K extent must still store (zeros, or the local partial to the peers) when
+      // nothing else writes the result
+      const bool keep_empty = ((skip || sparse) && !ew.accumulate) || (rs && last);
+      Sparse sp5;
+      if (sparse) {
+        sp5.kb_map = sw.kb_map;
+        sp5.kb_cnt = sw.cnt;
+      }
       const void* ovec = rs && last ? (const void*)rs->slots[0] : (const void*)grad_weight;
       ew.vec_ok = ((reinterpret_cast<uintptr_t>(ovec) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
       if (dv) {
         ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, h, d, true, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, rs && last));
+        ICP_TRY(run_umma(EPI_STORE, h, d, true, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
       } else {
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, rs && last));
+        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
       }
     }
   }

@@ -531,4 +531,62 @@ __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ pr
   }
 }
 
+// Block-sparse backward lists (stored-probabilities mode). flags[b] = 1 if any token of the
+// 64-token block b has a nonzero gradient coefficient (one warp per block, coalesced).
+__global__ void k_block_flags(const float* __restrict__ coeff, int64_t n, int32_t* __restrict__ flags) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nb = (n + 63) / 64;
+  if (b >= nb) return;
+  const int64_t t0 = b * 64 + lane, t1 = t0 + 32;
+  const bool act = (t0 < n && coeff[t0] != 0.f) || (t1 < n && coeff[t1] != 0.f);
+  const unsigned any = __ballot_sync(0xffffffffu, act);
+  if (lane == 0) flags[b] = any != 0u;
+}
+
+// One CTA, increasing order (deterministic): kb_map = active 64-token blocks (the k-blocks of
+// K5, K = tokens), mt_map = tiles of `tile_blocks` blocks with any active block (the m-tiles
+// of K4, M = tokens); *cnt[0] / *cnt[1] their counts.
+constexpr int BL_THREADS = 1024;
+__global__ void __launch_bounds__(BL_THREADS) k_block_lists(const int32_t* __restrict__ flags, int64_t nb,
+                                                            int tile_blocks, int32_t* __restrict__ kb_map,
+                                                            int32_t* __restrict__ mt_map, int32_t* __restrict__ cnt) {
+  __shared__ int warp_tot[BL_THREADS / 32];
+  __shared__ int base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nt = (nb + tile_blocks - 1) / tile_blocks;
+  for (int list = 0; list < 2; ++list) {
+    const int64_t count = list == 0 ? nb : nt;
+    int32_t* map = list == 0 ? kb_map : mt_map;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int64_t i0 = 0; i0 < count; i0 += BL_THREADS) {
+      const int64_t i = i0 + threadIdx.x;
+      bool p = false;
+      if (i < count) {
+        if (list == 0) {
+          p = flags[i] != 0;
+        } else {
+          for (int j = 0; j < tile_blocks && i * tile_blocks + j < nb; ++j) p = p || flags[i * tile_blocks + j] != 0;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, p);
+      if (lane == 0) warp_tot[warp] = __popc(bal);
+      __syncthreads();
+      int off = base;
+      for (int w = 0; w < warp; ++w) off += warp_tot[w];
+      if (p) map[off + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < BL_THREADS / 32; ++w) tot += warp_tot[w];
+        base += tot;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) cnt[list] = base;
+    __syncthreads();
+  }
+}
+
 }  // namespace icp

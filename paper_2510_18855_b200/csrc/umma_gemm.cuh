@@ -41,6 +41,12 @@ struct GemmShape {
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
   int32_t* wave_counter;  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr
   int32_t sync_kb;        // waves: k-blocks per barrier chunk (0 = one barrier per wave)
+  // Block sparsity (device lists, or null): the GEMM runs only k-blocks kb_map[0 .. *kb_cnt)
+  // of K and m-tiles mt_map[0 .. *mt_cnt) of M; the skipped ones hold only zero rows.
+  const int32_t* kb_map;
+  const int32_t* kb_cnt;
+  const int32_t* mt_map;
+  const int32_t* mt_cnt;
   // Device-side extent (sync-free compaction): if ext_dev, the M (ext_dim = 1) or K (ext_dim = 2)
   // extent is clamp(*ext_dev - ext_base, 0, static extent), read at kernel start.
   const int32_t* ext_dev;
@@ -64,6 +70,16 @@ __device__ __forceinline__ void resolve_extent(GemmShape& sh, int tile_m, int bn
     if (sh.k_blocks == 0 && !sh.keep_empty) sh.m_tiles = 0;  // nothing to accumulate
   }
   (void)bn;
+  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+}
+
+// Apply the device-side block lists (block-sparse backward): fewer m-tiles / k-blocks.
+__device__ __forceinline__ void resolve_sparsity(GemmShape& sh) {
+  if (sh.mt_cnt) sh.m_tiles = max(0, min(*sh.mt_cnt, sh.m_tiles));
+  if (sh.kb_cnt) {
+    sh.k_blocks = max(0, min(*sh.kb_cnt, sh.k_blocks));
+    if (sh.k_blocks == 0 && !sh.keep_empty) sh.m_tiles = 0;
+  }
   sh.num_tiles = sh.m_tiles * sh.n_tiles;
 }
 
@@ -152,6 +168,7 @@ __device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& 
   const int r = tile - g * group;
   m_blk = first_m + r % gm;
   n_blk = r / gm;
+  if (sh.mt_map) m_blk = __ldg(sh.mt_map + m_blk);
 }
 
 // ------------------------------------------------------------------ epilogues
@@ -180,11 +197,11 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
     const int col0 = tile_col<BN, CG>(n0, c * 32);
     if (!row_ok || col0 >= sh.N) continue;
     const bool full = (col0 + 32 <= sh.N) && ep.vec_ok;
-    if (ep.rs_world > 0) {
-      if (sh.k_blocks == 0) {
+    if (sh.k_blocks == 0) {  // empty K extent (keep_empty): TMEM was never written
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;  // empty K extent: TMEM was never written
-      }
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
+    if (ep.rs_world > 0) {
       const int64_t o = m / ep.rs_shard_rows;
       float* dst = ep.rs_slots[o] + ((int64_t)ep.rs_rank * ep.rs_shard_rows + (m - o * ep.rs_shard_rows)) * ep.ldo + col0;
       const float* src = ep.acc_src ? ep.acc_src + (int64_t)m * ep.ldo + col0 : nullptr;
@@ -552,6 +569,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using Cfg = GemmCfg<BN, CG, DUAL, STAGING>;
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
+  resolve_sparsity(sh);
   constexpr int STAGES = Cfg::STAGES;
   constexpr int B_ROWS = BN / CG;  // rows of B staged by this CTA
   extern __shared__ uint8_t smem_raw[];
@@ -673,6 +691,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int n0 = n_blk * BN + (int)rank * B_ROWS;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
+          const int kc = (sh.kb_map ? __ldg(sh.kb_map + kb) : kb) * BK;  // k coordinate of this block
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb_local = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -682,38 +701,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (CG == 1) {
             mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
             if (!A_MN) {
-              tma_load_2d(a_dst, &tmA, fb_local, kb * BK, m0);
+              tma_load_2d(a_dst, &tmA, fb_local, kc, m0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kb * BK);
+              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kc);
             }
             if (!B_MN) {
-              tma_load_2d(b_dst, &tmB, fb_local, kb * BK, n0);
-              if (DUAL) tma_load_2d(b2_dst, &tmB2, fb_local, kb * BK, n0);
+              tma_load_2d(b_dst, &tmB, fb_local, kc, n0);
+              if (DUAL) tma_load_2d(b2_dst, &tmB2, fb_local, kc, n0);
             } else {
 #pragma unroll
               for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
-                tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kb * BK);
-                if (DUAL) tma_load_2d(b2_dst + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kb * BK);
+                tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kc);
+                if (DUAL) tma_load_2d(b2_dst + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kc);
               }
             }
           } else {
             const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
             if (rank == 0) mbar_arrive_expect_tx(fb_local, CG * Cfg::STAGE_BYTES);
             if (!A_MN) {
-              tma_load_2d_cg2(a_dst, &tmA, fb, kb * BK, m0);
+              tma_load_2d_cg2(a_dst, &tmA, fb, kc, m0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kb * BK);
+              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kc);
             }
             if (!B_MN) {
-              tma_load_2d_cg2(b_dst, &tmB, fb, kb * BK, n0);
-              if (DUAL) tma_load_2d_cg2(b2_dst, &tmB2, fb, kb * BK, n0);
+              tma_load_2d_cg2(b_dst, &tmB, fb, kc, n0);
+              if (DUAL) tma_load_2d_cg2(b2_dst, &tmB2, fb, kc, n0);
             } else {
 #pragma unroll
               for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
-                tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kb * BK);
-                if (DUAL) tma_load_2d_cg2(b2_dst + j2 * (BK * 128), &tmB2, fb, n0 + 64 * j2, kb * BK);
+                tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kc);
+                if (DUAL) tma_load_2d_cg2(b2_dst + j2 * (BK * 128), &tmB2, fb, n0 + 64 * j2, kc);
               }
             }
           }

@@ -89,6 +89,20 @@ def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
             cb = max(128 * 2 * v, cb // 2)
 
 
+def _sp_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor | None:
+    """Workspace of the stored-probabilities backward (row-compaction buffers, no dZ chunk),
+    or None: without it every row goes through K4/K5 (same result, more work)."""
+    lib = _lib.load()
+    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=max(n_seqs, 1), n_groups=1,
+                       weight_layout=_lib.W_VD)
+    b = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, -1, 0, None, b))
+    try:
+        return torch.empty(max(b.value, 1), dtype=torch.uint8, device=device)
+    except torch.OutOfMemoryError:
+        return None
+
+
 def _dz_chunk_bytes(device) -> int:
     free = _free_bytes(device)
     if free is None:
@@ -467,9 +481,10 @@ def icepop_bwd(
             raise ValueError("grad_weight must be a contiguous float32 tensor shaped like weight")
         wr = weight_ref.contiguous() if weight_ref is not None else None
         probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
-        ws = None
         if probs is None:
             ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
+        else:
+            ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                            lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                            probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
@@ -533,11 +548,13 @@ def icepop_bwd_reduce_scatter(
     gh = torch.empty((n, d), dtype=gh_dtype, device=dev) if need_hidden else None
     wr = weight_ref.contiguous() if weight_ref is not None else None
     probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
-    scratch = ws = None
+    scratch = None
     if probs is None:
         ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
         single_chunk = ws.numel() >= bwd_workspace_bytes(n, d, v, shape.n_seqs, 2 * n * v)
         scratch = None if single_chunk else torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
+    else:
+        ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                        lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                        probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))

@@ -240,6 +240,7 @@ def test_long_k_backward_wide_tiles(cuda_device, layout):
     cfg = IcePopConfig()
     res = {}
     try:
+        _lib.check(lib.icepop_set_skip_inactive(0))  # keep dZ rows in token order for the reference below
         for wide in (1, 0):
             _lib.check(lib.icepop_set_wide_tiles(wide))
             f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
@@ -248,6 +249,7 @@ def test_long_k_backward_wide_tiles(cuda_device, layout):
             res[wide] = (gh, gw, dz)
     finally:
         _lib.check(lib.icepop_set_wide_tiles(1))
+        _lib.check(lib.icepop_set_skip_inactive(1))
     (gh1, gw1, dz1), (gh0, gw0, _) = res[1], res[0]
     assert torch.equal(gh1, gh0) and torch.equal(gw1, gw0)
     ref = dz1.double().T @ H.double()  # [V, d]
@@ -258,3 +260,54 @@ def test_long_k_backward_wide_tiles(cuda_device, layout):
     Wd = W.double()
     ref_h = dz1.double() @ (Wd if layout == "vd" else Wd.T)
     assert _rel(gh1.cpu().numpy(), ref_h.cpu().numpy()) < 1e-4
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_stored_probs_block_sparse_backward(cuda_device, cta_group, layout):
+    """Stored-probabilities backward with block-sparse K4/K5 (two zero-advantage groups +
+    scattered popped/clip-inactive tokens): 64-token blocks / 256-token tiles without an
+    active row are skipped. They hold only zero dZ rows, so dH and dW equal the dense pass bit
+    for bit; both vs the oracle."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=8, seed=71, group=2, layout=layout, V=1000, lens=[300, 170, 260, 90, 410, 333, 129, 257])
+    c["adv"] = c["adv"].copy()
+    c["adv"][[0, 1, 4, 5]] = 0.0
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    lib = _lib.ensure_device(0)
+    res = {}
+    try:
+        for skip in (0, 1):
+            _lib.check(lib.icepop_set_skip_inactive(skip))
+            f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
+            res[skip] = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout,
+                                   grad_hidden_dtype=torch.float32)
+    finally:
+        _lib.check(lib.icepop_set_skip_inactive(1))
+    (gh0, gw0), (gh1, gw1) = res[0], res[1]
+    assert int((f.coeff == 0).sum()) > len(c["tokens"]) // 3
+    assert torch.equal(gh0, gh1)
+    assert torch.all(gh1[f.coeff == 0] == 0)
+    assert torch.equal(gw1, gw0)
+    o = _oracle(c)
+    assert _rel(gw1.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh1.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+def test_stored_probs_compaction_accumulates_into_grad_weight(cuda_device):
+    """grad_weight given (accumulate) with compacted rows: adds onto the existing values."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=4, seed=72, group=2, V=1000)
+    c["adv"] = c["adv"].copy()
+    c["adv"][[0, 1]] = 0.0
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, store_probs=True)
+    _, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, need_hidden=False)
+    base = torch.full_like(gw, 0.25)
+    f2 = icepop_fwd(H, W, _batch(c, cuda_device), cfg, store_probs=True)
+    icepop_bwd(H, W, _batch(c, cuda_device), f2, cfg, need_hidden=False, grad_weight=base)
+    torch.testing.assert_close(base, gw + 0.25, rtol=0, atol=1e-6)
