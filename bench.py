@@ -184,7 +184,7 @@ def run_ours(args):
     from paper_2510_18855_b200 import _lib  # noqa: F401
     from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
     from paper_2510_18855_b200.loss import (Diagnostics, IcePopConfig, _dz_chunk_bytes, _resolve_store_probs, finish,
-                                            icepop_bwd, icepop_fwd)
+                                            icepop_bwd, icepop_fwd, icepop_fwd_bwd, probs_chunk_tokens)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -199,12 +199,27 @@ def run_ours(args):
     icfg = IcePopConfig()
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
     sp = _resolve_store_probs(None, N, V, dev, False)
+    # stored probabilities for the whole batch; else in token chunks that fit (icepop_fwd_bwd);
+    # else the logit recompute
+    sp_chunk = 0 if sp else probs_chunk_tokens(N, V, dev)
+    if os.environ.get("ICEPOP_STORE_PROBS", "auto") == "0":
+        sp_chunk = 0
     rows = _dz_chunk_bytes(dev) // (2 * V)
     chunk = N if (sp or rows >= N) else max(128, rows // 128 * 128)
+    if sp_chunk:
+        chunk = sp_chunk
     n_chunks = -(-N // chunk)
-    # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: stored probabilities -> dZ pass,
-    # K4, K5; recompute -> 4 compaction kernels + (K3, K4, K5) per chunk
-    launches_per_step = 6 + (3 if sp else 4 + 3 * n_chunks)
+    # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: stored probabilities -> block
+    # flags + lists, dZ pass, K4, K5 (per token chunk when chunked); recompute -> 4 compaction
+    # kernels + (K3, K4, K5) per dZ chunk
+    if sp:
+        launches_per_step = 6 + 5
+    elif sp_chunk:
+        launches_per_step = n_chunks * (6 + 5)
+    else:
+        launches_per_step = 6 + 4 + 3 * n_chunks
+    dz_mode = "stored-probabilities" if sp else (
+        f"stored-probabilities in {n_chunks} token chunks" if sp_chunk else "recompute")
 
     # dW collective for N > 1: fused reduce-scatter inside K5's epilogue over NVLink peer memory
     # (each rank ends with its ZeRO shard of the summed dW), or NCCL all-reduce of the full dW.
@@ -212,7 +227,7 @@ def run_ours(args):
     peer = None
     dw_shard = None
     if world > 1:
-        collective = args.dw_collective
+        collective = args.dw_collective if not sp_chunk else "nccl"
         if collective == "fused":
             try:
                 from paper_2510_18855_b200.distributed import PeerSlots
@@ -226,6 +241,12 @@ def run_ours(args):
 
     def step_into():
         # loss = -J: grad_scale -1 gives d(loss)/d(hidden), d(loss)/d(W)
+        if sp_chunk:
+            f, gh, g = icepop_fwd_bwd(H, W, batch, icfg, layout="vd", grad_scale=-1.0, max_chunk_tokens=sp_chunk)
+            if world > 1:
+                allreduce_stats(f.stats)
+                wait_grad(allreduce_grad(g))
+            return f
         f = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=sp)
         if collective == "fused":
             from paper_2510_18855_b200.distributed import stream_barrier
@@ -308,12 +329,13 @@ def run_ours(args):
                    "with lp_train_old recorded by icepop_logprob_bf16: GEMM-free exact forward + full backward"}
 
     # ---------------- per-kernel timing pass (same work, events between launches)
-    kern = kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp) if not args.no_kernel_timing else {}
+    kern = (kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp or bool(sp_chunk))
+            if not args.no_kernel_timing else {})
 
     # ---------------- end-to-end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(H, W, batch, icfg, args, dev, world, sp)
+        e2e = run_e2e(H, W, batch, icfg, args, dev, world, sp, sp_chunk)
 
     tokens_total = N * world
     value = tokens_total / (ms / 1e3)
@@ -326,7 +348,7 @@ def run_ours(args):
                    "seq_len": cfg["seq_len"] or "ragged",
                    "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
-                   "dz_mode": "stored-probabilities" if sp else "recompute",
+                   "dz_mode": dz_mode,
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
                    "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective,
                    "zero_adv_group_frac": args.zero_adv_frac},
@@ -379,15 +401,22 @@ def run_ours(args):
 
 def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     """Average device time of K1(+K2), the dZ producer (K3 recompute GEMM, or the in-place
-    pass over the stored probabilities), K4, K5 launched one by one on the torch stream."""
+    pass over the stored probabilities), K4, K5 launched one by one on the torch stream. With
+    stored probabilities in token chunks (chunk < N) they are timed on the first chunk."""
     import torch
 
     from paper_2510_18855_b200 import _lib
-    from paper_2510_18855_b200.loss import icepop_fwd
+    from paper_2510_18855_b200.loss import PackedBatch, icepop_fwd
 
     lib = _lib.ensure_device(dev.index)
     st = torch.cuda.current_stream(dev)
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
+    if sp and chunk < N:
+        H = H[:chunk]
+        batch = PackedBatch(batch.tokens[:chunk], batch.lp_train_old[:chunk], batch.lp_infer_old[:chunk],
+                            batch.cu_seqlens, batch.group_offsets, batch.advantages, batch.rewards,
+                            token_offset=batch.token_offset)
+        N = chunk
     res = {}
 
     def timed(name, fn, flop, reps=2, nbytes=None):
@@ -446,7 +475,7 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     return res
 
 
-def run_e2e(H, W, batch, icfg, args, dev, world, sp=False):
+def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
     """Public API from pinned host inputs: every step's inputs are copied H2D and its loss
     read back D2H inside the timed region. The copy of step k+1 runs on a side stream while
     step k computes (double-buffered device inputs, as a data-loader prefetch would)."""
@@ -454,7 +483,7 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False):
     import torch.distributed as dist
 
     from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
-    from paper_2510_18855_b200.loss import PackedBatch, icepop_bwd, icepop_fwd
+    from paper_2510_18855_b200.loss import PackedBatch, icepop_bwd, icepop_fwd, icepop_fwd_bwd
 
     host = {k: v.cpu().pin_memory() for k, v in dict(H=H, tokens=batch.tokens, lp_old=batch.lp_train_old,
                                                      lp_inf=batch.lp_infer_old, cu=batch.cu_seqlens,
@@ -483,8 +512,11 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False):
         main.wait_event(copied[i])
         d = bufs[i]
         b = PackedBatch(d["tokens"], d["lp_old"], d["lp_inf"], d["cu"], d["go"], None, d["rewards"], batch.token_offset)
-        f = icepop_fwd(d["H"], W, b, icfg, layout="vd", store_probs=sp)
-        _, g = icepop_bwd(d["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
+        if sp_chunk:
+            f, _, g = icepop_fwd_bwd(d["H"], W, b, icfg, layout="vd", grad_scale=-1.0, max_chunk_tokens=sp_chunk)
+        else:
+            f = icepop_fwd(d["H"], W, b, icfg, layout="vd", store_probs=sp)
+            _, g = icepop_bwd(d["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
         if world > 1:
             allreduce_stats(f.stats)
             wait_grad(allreduce_grad(g))

@@ -565,6 +565,86 @@ def icepop_bwd_reduce_scatter(
     return gh
 
 
+def probs_chunk_tokens(n: int, vocab: int, device) -> int:
+    """Largest token count (multiple of 4096, or n) whose stored probabilities fit in
+    STORE_PROBS_FRACTION of the device memory available now; 0 if not even 4096 do."""
+    per = 2 * vocab + 4 * _lib.tile_max_ld(vocab)
+    free = _free_bytes(device)
+    if free is None:
+        return 0
+    rows = int(STORE_PROBS_FRACTION * free) // per
+    if rows >= n:
+        return n
+    return rows // 4096 * 4096
+
+
+def icepop_fwd_bwd(
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    batch: PackedBatch,
+    cfg: IcePopConfig = IcePopConfig(),
+    layout: str = "vd",
+    grad_scale: float = 1.0,
+    need_hidden: bool = True,
+    grad_weight: torch.Tensor | None = None,
+    weight_ref: torch.Tensor | None = None,
+    grad_hidden_dtype: torch.dtype | None = None,
+    max_chunk_tokens: int | None = None,
+) -> tuple[IcePopForward, torch.Tensor | None, torch.Tensor]:
+    """Forward and gradient in one call, as objective_and_grad returns them (objective.py:172-298).
+
+    On the bf16 path the backward forms dZ from stored probabilities. When the whole batch's
+    probabilities (2*N*V bytes) do not fit in device memory, the batch runs in token chunks
+    that do fit. Each chunk is a token range with its global offset, exactly like a token
+    shard (distributed.py): the statistics are summed (error bits OR-ed) and dW is accumulated.
+    So the backward still executes 6.d.V instead of 8.d.V FLOPs per token. It falls back to
+    icepop_fwd + icepop_bwd (logit recompute) for the KL gradient, fp64 inputs, or when not
+    even 4096 tokens' probabilities fit. Returns (forward outputs, dHidden or None, dW f32).
+    """
+    n = hidden.shape[0]
+    v = weight.shape[1] if layout == "dv" else weight.shape[0]
+    usable = hidden.dtype == torch.bfloat16 and weight_ref is None and v % 8 == 0 and n > 0 and hidden.is_cuda
+    chunk = 0
+    if usable:
+        chunk = probs_chunk_tokens(n, v, hidden.device)
+        if max_chunk_tokens:
+            chunk = min(chunk, max_chunk_tokens)
+    if chunk <= 0:
+        f = icepop_fwd(hidden, weight, batch, cfg, layout, weight_ref=weight_ref)
+        gh, gw = icepop_bwd(hidden, weight, batch, f, cfg, layout, grad_scale, need_hidden, True, grad_weight,
+                            weight_ref, grad_hidden_dtype)
+        return f, gh, gw
+    if chunk >= n:
+        f = icepop_fwd(hidden, weight, batch, cfg, layout, store_probs=True)
+        gh, gw = icepop_bwd(hidden, weight, batch, f, cfg, layout, grad_scale, need_hidden, True, grad_weight,
+                            grad_hidden_dtype=grad_hidden_dtype)
+        return f, gh, gw
+    dev = hidden.device
+    gw = grad_weight if grad_weight is not None else torch.zeros(tuple(weight.shape), dtype=torch.float32, device=dev)
+    gh = torch.empty((n, hidden.shape[1]), dtype=grad_hidden_dtype or torch.bfloat16, device=dev) if need_hidden \
+        else None
+    parts = []
+    stats = torch.zeros(_lib.NSTATS, dtype=torch.float64, device=dev)
+    for s0 in range(0, n, chunk):
+        e0 = min(n, s0 + chunk)
+        sub = PackedBatch(batch.tokens[s0:e0], batch.lp_train_old[s0:e0], batch.lp_infer_old[s0:e0],
+                          batch.cu_seqlens, batch.group_offsets, batch.advantages, batch.rewards,
+                          token_offset=batch.token_offset + s0)
+        f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, store_probs=True)
+        ghc, _ = icepop_bwd(hidden[s0:e0], weight, sub, f, cfg, layout, grad_scale, need_hidden, True, gw,
+                            grad_hidden_dtype=grad_hidden_dtype)
+        if gh is not None:
+            gh[s0:e0] = ghc
+        stats[: _lib.STAT_ERRORS] += f.stats[: _lib.STAT_ERRORS]
+        stats[_lib.STAT_ERRORS] = (stats[_lib.STAT_ERRORS].long() | f.stats[_lib.STAT_ERRORS].long()).double()
+        parts.append(f)
+    cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
+    out = IcePopForward(cat("lse"), cat("lp_cur"), cat("entropy"), cat("kept"), cat("calib"), cat("surrogate"),
+                        cat("coeff"), stats)
+    out.extras["chunks"] = len(parts)
+    return out, gh, gw
+
+
 def finish(stats: torch.Tensor) -> None:
     """One host sync; raise NumericError/ValueError from the device error word."""
     lib = _lib.load()

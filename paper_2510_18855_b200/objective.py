@@ -227,7 +227,7 @@ def objective_and_grad(
     import torch
 
     from .features import multihot
-    from .loss import Diagnostics, IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd
+    from .loss import Diagnostics, IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd, icepop_fwd_bwd
 
     if temperature <= 0:
         raise ValueError("temperature must be positive")
@@ -264,8 +264,8 @@ def objective_and_grad(
         H = torch.from_numpy(multihot(p.feats, nf_pad)).to(torch.bfloat16).to(dev)
         W = pad_bf16(theta.weights)
         Wr = pad_bf16(ref.weights) if ref is not None else None
-        fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
-        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
+        # value and gradient together: stored probabilities (in token chunks if needed)
+        fwd, _, gw = icepop_fwd_bwd(H, W, batch, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
         gw = gw[:n_features]
     else:
         raise ValueError("precision must be 'fp64' or 'bf16'")
