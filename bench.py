@@ -582,21 +582,23 @@ def blas_threads() -> int:
 
 
 def sample_tokens(cfg, W64, target_s: float) -> int:
-    """Tokens per CPU sample so one sample takes about target_s. The oracle has a fixed
-    per-call cost (e.g. the fp64 gradient buffer), so grow the sample until it is timed."""
-    n, dt = 8, 0.0
-    for _ in range(3):
-        dt, _ = time_oracle(cfg, n, W64, seed=999)
-        if dt >= 0.66 * target_s:
-            break
-        n = int(min(4096, max(n + 2, n * target_s / max(dt, 1e-3))))
-        n += n % 2
-    return n
+    """Tokens per CPU sample so one sample takes about target_s. A call costs a + b*n: a fixed
+    part (the fp64 V x d gradient buffer the reference also allocates per call) plus a
+    per-token part. Fit both from two timed sizes so the sample is large enough that the
+    measured throughput approaches the per-token rate (a small sample would understate the
+    CPU and overstate the GPU's speed-up)."""
+    n1, n2 = 16, 128
+    t1, _ = time_oracle(cfg, n1, W64, seed=998)
+    t2, _ = time_oracle(cfg, n2, W64, seed=999)
+    b = max((t2 - t1) / (n2 - n1), 1e-6)
+    a = max(t1 - b * n1, 0.0)
+    n = int(max(n2, min(16384, (target_s - a) / b)))
+    return n + n % 2
 
 
 def cpu_baseline(cfg, H, W, batch, meta, n_tokens):
     W64 = W.float().cpu().numpy().astype(np.float64)
-    n_tokens = n_tokens or sample_tokens(cfg, W64, 15.0)  # ~10-30 s of CPU work
+    n_tokens = n_tokens or sample_tokens(cfg, W64, 20.0)  # ~10-30 s of CPU work
     dt, n = time_oracle(cfg, n_tokens, W64)
     return {"value": round(n / dt, 3), "unit": UNIT, "cores": blas_threads(), "kind": "port",
             "sample": f"{n} tokens (1 group x 2 seqs) at d={cfg['hidden']}, V={cfg['vocab']}, fp64 numpy oracle "
@@ -619,7 +621,7 @@ def run_reference(args):
     rng = np.random.default_rng(123)
     W64 = (rng.standard_normal((cfg["vocab"], cfg["hidden"]), dtype=np.float32) * (2.0 / np.sqrt(cfg["hidden"]))
            ).astype(np.float64)
-    n_tok = args.cpu_tokens or sample_tokens(cfg, W64, 6.0)
+    n_tok = args.cpu_tokens or sample_tokens(cfg, W64, 12.0)  # 8 calls of ~12 s at the defaults
     for i in range(args.warmup):
         time_oracle(cfg, n_tok, W64, seed=i)
     tot_t, tot_n = 0.0, 0
