@@ -468,8 +468,10 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     gw = torch.zeros((V, d), dtype=torch.float32, device=dev)
     timed("K4_dhidden", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), nc, d, V,
                                                                 0, 1, 0, 0, s)), 2.0 * nc * d * V)
+    # as in the step: a single (or first) chunk overwrites dW; recompute-mode later chunks accumulate
+    k5_acc = 0 if (sp or nc >= N) else 1
     timed("K5_dweight", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, nc,
-                                                                1, 1, 1, 1, s)), 2.0 * nc * d * V)
+                                                                1, 1, 1, k5_acc, s)), 2.0 * nc * d * V)
     del dz, gh, gw
     holder.clear()
     return res
