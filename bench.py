@@ -204,6 +204,11 @@ def run_ours(args):
     sp_chunk = 0 if sp else probs_chunk_tokens(N, V, dev)
     if os.environ.get("ICEPOP_STORE_PROBS", "auto") == "0":
         sp_chunk = 0
+    if world > 1:  # one mode on every rank (free memory may differ): the collectives must match
+        agree = torch.tensor([int(sp), sp_chunk if not sp else N], dtype=torch.int64, device=dev)
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        sp = bool(agree[0].item())
+        sp_chunk = 0 if sp else int(agree[1].item())
     rows = _dz_chunk_bytes(dev) // (2 * V)
     chunk = N if (sp or rows >= N) else max(128, rows // 128 * 128)
     if sp_chunk:
