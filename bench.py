@@ -612,6 +612,55 @@ def cpu_baseline(cfg, H, W, batch, meta, n_tokens):
                       f"(objective.py:172-298 restated densely, oracle/icepop_oracle.py), {dt:.1f} s"}
 
 
+def time_reference_own(cfg, target_s: float = 10.0, seed: int = 0):
+    """The unmodified reference's own objective_and_grad (the baseline/_ref install, imported
+    as a package, none of our code on the path) on one group of 2 synthetic rollouts at the
+    config's vocabulary with n_features = d. Its policy is a 4-hot gather (policy.py:279-289),
+    so a token costs O(V) regardless of d, plus np.add.at into the full [d, V] gradient
+    (objective.py:265-266). Sized like the oracle sample (fixed + per-token fit). None if the
+    reference is not installed."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "mismatchlab").exists():
+        return None
+    if str(ref_dir) not in sys.path:
+        sys.path.insert(0, str(ref_dir))
+    import mismatchlab as ml
+    from mismatchlab.tasks import TaskKind
+
+    rng = np.random.default_rng(seed)
+    d, V = cfg["hidden"], cfg["vocab"]
+    theta = ml.PolicyParams(weights=rng.standard_normal((d, V), dtype=np.float32).astype(np.float64) * 0.02)
+    ocfg = ml.ObjectiveConfig(group_size=2)
+
+    def call(n_tok):
+        task = ml.TaskSpec(TaskKind.PARITY_MATCH, 100, 0, 4)
+        rollouts = []
+        for r in range(2):
+            recs = []
+            for _ in range(max(1, n_tok // 2)):
+                lp_old = float(-np.log(V) + rng.normal(0, 0.3))
+                recs.append(ml.TokenRecord(token=int(rng.integers(0, V)), logp_infer_old=lp_old - float(rng.normal(0, 0.2)),
+                                           logp_train_old=lp_old, logp_train_cur=lp_old, gen_version=0))
+            rollouts.append(ml.Rollout(task=task, stream=np.random.default_rng(r), uid=r, group_uid=0, tokens=recs,
+                                       terminal=True))
+        group = ml.PromptGroup(task=task, rollouts=rollouts, rewards=[1.0, 0.0], advantages=[1.0, -1.0])
+        t0 = time.perf_counter()
+        ml.objective_and_grad([group], theta, theta, None, ocfg, ml.MaskingBounds())
+        return time.perf_counter() - t0, 2 * max(1, n_tok // 2)
+
+    t1, n1 = call(8)
+    t2, n2 = call(64)
+    b = max((t2 - t1) / (n2 - n1), 1e-6)
+    a = max(t1 - b * n1, 0.0)
+    n = int(max(64, min(4096, (target_s - a) / b)))
+    dt, n = call(n)
+    return {"value": round(n / dt, 3), "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{n} tokens (1 group x 2 synthetic rollouts), n_features = d = {d}, V = {V}, "
+                      f"unmodified mismatchlab.objective_and_grad (baseline/_ref), {dt:.1f} s",
+            "note": "the reference's own 4-hot-gather numpy path (single-threaded); the line's value is "
+                    "the dense fp64 restatement on all cores (faster, so the conservative baseline)"}
+
+
 def run_reference(args):
     """--impl reference: the reference's algorithm on host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -648,6 +697,12 @@ def run_reference(args):
                                    "of objective.py:172-298 (oracle/icepop_oracle.py)"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:  # the reference's own objective_and_grad, reported beside the port
+        own = time_reference_own(cfg)
+        if own:
+            line["reference_own"] = own
+    except Exception as e:  # noqa: BLE001 - informational only
+        line["reference_own"] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
     print(json.dumps(line), flush=True)
 
 
