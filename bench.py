@@ -215,12 +215,13 @@ def run_ours(args):
         chunk = sp_chunk
     n_chunks = -(-N // chunk)
     # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: stored probabilities -> block
-    # flags + lists, dZ pass, K4, K5 (per token chunk when chunked); recompute -> 4 compaction
-    # kernels + (K3, K4, K5) per dZ chunk
+    # flags + lists, row prep, exception-row dZ, K4, K5, iota + one-hot scatter (CUB's radix
+    # sort kernels are library code, not counted); per token chunk when chunked; recompute ->
+    # 4 compaction kernels + (K3, K4, K5) per dZ chunk
     if sp:
-        launches_per_step = 6 + 5
+        launches_per_step = 6 + 8
     elif sp_chunk:
-        launches_per_step = n_chunks * (6 + 5)
+        launches_per_step = n_chunks * (6 + 8)
     else:
         launches_per_step = 6 + 4 + 3 * n_chunks
     dz_mode = "stored-probabilities" if sp else (
@@ -381,14 +382,15 @@ def run_ours(args):
                             else None}
         line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()
                                   if v["flop"]}
-        if "dZ_from_probs" in kern:  # the HBM-bound pass of the stored-probabilities backward
-            kz = kern["dZ_from_probs"]
+        if "bwd_prep" in kern:  # the HBM-bound part of the stored-probabilities backward
+            kz = kern["bwd_prep"]
             gbs = kz["bytes"] / (kz["ms"] / 1e3) / 1e9
-            line["roofline_dz"] = {"bound": "hbm", "kernel": "dZ_from_probs", "achieved": round(gbs, 1),
-                                   "peak": pk["hbm"], "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
-                                   "bytes_per_launch": kz["bytes"],
-                                   "bytes_note": "algorithmic: read + write bf16 q/dZ of the active rows, "
-                                                 "write-only zero rows, + tile maxima"}
+            line["roofline_bwd_prep"] = {
+                "bound": "hbm", "kernel": "bwd_prep (k_sp_prep + exception-row dZ + block lists)",
+                "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
+                "bytes_per_launch": kz["bytes"],
+                "bytes_note": "algorithmic: read H + write s*H (bf16), read the slab references; "
+                              "exception rows (none in this batch) add a read + write of their q/dZ row"}
     if e2e:
         line["e2e"] = e2e
     if onp_res:
@@ -446,8 +448,12 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     f = holder["f"]
     s = st.cuda_stream
     if sp:
-        # the stored-probabilities backward without K4/K5 (null gradients) is the dZ pass alone;
-        # repeated passes over the same buffer take the same time
+        # the stored-probabilities backward with null gradients and its workspace runs only its
+        # preparation (block lists, row scales and s*H, dZ of exception rows); K4/K5 follow as
+        # plain GEMMs on the stored probabilities (their row-scale / one-hot epilogue work is
+        # negligible). Repeated calls over the same buffers take the same time.
+        from paper_2510_18855_b200.loss import _sp_workspace
+
         nc = N
         dz = f.extras["probs"]
         tm = f.extras["tile_max"]
@@ -455,11 +461,14 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
                            n_groups=batch.n_groups, weight_layout=_lib.W_VD)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr(),
                            probs=dz.data_ptr(), tile_max=tm.data_ptr())
-        active = int((f.coeff != 0).sum())
-        nbytes = 4 * active * V + 2 * (N - active) * V + 4 * active * tm.shape[1]
-        timed("dZ_from_probs", lambda: _lib.check(lib.icepop_bwd_bf16(shape, icfg.to_c(), H.data_ptr(), W.data_ptr(),
-                                                                      None, saved, -1.0, None, 0, None, 0, None, 0,
-                                                                      s)), 0.0, nbytes=nbytes)
+        wsp = _sp_workspace(N, d, V, batch.n_seqs, dev)
+        nbytes = 4 * N * d + 4 * N * tm.shape[1] + N
+        if wsp is not None:
+            timed("bwd_prep", lambda: _lib.check(lib.icepop_bwd_bf16(shape, icfg.to_c(), H.data_ptr(), W.data_ptr(),
+                                                                     None, saved, -1.0, None, 0, None, 0,
+                                                                     wsp.data_ptr(), wsp.numel(), s)),
+                  0.0, nbytes=nbytes)
+            del wsp
     else:
         nc = min(chunk, N)
         dz = torch.empty((nc, V), dtype=torch.bfloat16, device=dev)

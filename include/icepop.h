@@ -148,16 +148,19 @@ typedef struct icepop_fwd_out {
   float* lse_ref;      /* [n_tokens] log-sum-exp of z_ref = H.W_ref/T                      */
   float* kl_w;         /* [n_tokens] w_t * gamma / T (the KL gradient's coefficient)       */
   /* Stored-probabilities mode (optional; both NULL = the backward recomputes the logits):
-   * probs    [n_tokens, vocab] bf16, q = exp(z - m) with m the row's maximum over each
-   *          ICEPOP_PROBS_SLAB-column vocab slab (so q is in [0, 1]); needs vocab % 8 == 0 and
-   *          no weight_ref. 2*n_tokens*vocab bytes of HBM buy a backward without the K3 GEMM.
-   * tile_max [n_tokens, ICEPOP_TILE_MAX_LD(vocab)] f32: m of slab j at column j, in log2 units
-   *          (z log2(e)); columns past ceil(vocab / ICEPOP_PROBS_SLAB) are padding. */
+   * probs    [n_tokens, vocab] bf16, q = 2^(u - R), u = z log2(e), with one reference R per
+   *          ICEPOP_PROBS_SLAB-column vocab slab: R = 0 while the slab's maximum of u lies within
+   *          +-ICEPOP_PROBS_REF_RANGE (then p = q 2^(-lse log2 e) needs one scale per row), else R
+   *          = that maximum. Needs vocab % 8 == 0 and no weight_ref. 2*n_tokens*vocab bytes of
+   *          HBM buy a backward without the K3 GEMM.
+   * tile_max [n_tokens, ICEPOP_TILE_MAX_LD(vocab)] f32: R of slab j at column j; columns past
+   *          ceil(vocab / ICEPOP_PROBS_SLAB) are padding (0). */
   void* probs;
   float* tile_max;
 } icepop_fwd_out;
 
 #define ICEPOP_PROBS_SLAB 64
+#define ICEPOP_PROBS_REF_RANGE 60.0f
 #define ICEPOP_TILE_MAX_LD(vocab) (4 * (((vocab) + 255) / 256))
 
 /* Forward: fused lm_head GEMM + online log-softmax/gather/entropy (tcgen05), then the
@@ -192,16 +195,18 @@ typedef struct icepop_saved {
   const float* kl;        /* [n_tokens] weight_ref != NULL, else may be NULL              */
   const float* kl_w;      /* [n_tokens]                                                   */
   void* probs;            /* out->probs / out->tile_max of the forward, or NULL. CONSUMED: the */
-  const float* tile_max;  /* backward overwrites probs with dZ (a second backward must pass NULL) */
+  const float* tile_max;  /* backward may overwrite rows of probs (a second backward passes NULL) */
 } icepop_saved;
 
 /* Backward: recompute logits tile by tile, dZ = grad_scale*coeff_t*(e_y - softmax(z_t))
  * [- grad_scale*kl_w_t*p*(log p - log p_ref - kl_t) when gamma > 0] (bf16 chunk), then
- * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05. With saved->probs the same dZ
- * is formed in place from the stored probabilities by a bandwidth-bound pass instead (no
- * logit recompute; not with gamma > 0). Its workspace (icepop_workspace_bytes with
- * max_chunk_tokens < 0) lets it compact zero-coefficient rows away in place; with a NULL or
- * smaller workspace every row goes through K4/K5.
+ * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05. With saved->probs there is no
+ * logit recompute (not with gamma > 0). Given its workspace (icepop_workspace_bytes with
+ * max_chunk_tokens < 0) the backward is row-scaled: dH = s (Q.W) + c W[y] and
+ * dW = Q^T.(s H) + scatter_y(c H), s = -c 2^(-lse2), c = grad_scale coeff. Rows with a
+ * reference R != 0 get their dZ formed in place in probs first. Blocks without an active row
+ * are skipped. With a NULL or smaller workspace, dZ is formed in place for every row
+ * instead; probs is consumed either way.
  * grad_hidden: [n_tokens, d], bf16 if grad_hidden_f32 == 0 else f32; may be NULL.
  * grad_weight: f32 in the weight's layout; accumulate != 0 adds into it; may be NULL. */
 int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const void* hidden,

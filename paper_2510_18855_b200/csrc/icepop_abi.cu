@@ -15,6 +15,8 @@
 #include <cstring>
 #include <string>
 
+#include <cub/cub.cuh>
+
 #include "../../include/icepop.h"
 #include "f64_kernels.cuh"
 #include "token_kernels.cuh"
@@ -528,23 +530,53 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   return w;
 }
 
-// Stored-probabilities backward: block lists of the block-sparse K4/K5 (k_block_lists).
+// Stored-probabilities backward workspace: block lists of the block-sparse K4/K5
+// (k_block_lists) and the row-scaled GEMM inputs (k_sp_prep, the one-hot scatter's sort).
 struct SparseWorkspace {
   int32_t* flags;   // [nb] active 64-token blocks
   int32_t* kb_map;  // [nb]
   int32_t* mt_map;  // [nb]
   int32_t* cnt;     // [2]: active blocks, active m-tiles
+  float* rscale;    // [n] s_t
+  float* ohc;       // [n] c_t
+  uint8_t* exc;     // [n] exception rows (dZ formed in place)
+  __nv_bfloat16* hid_s;  // [n, d] s_t H[t]
+  int32_t* keys;    // [n] tokens sorted
+  int32_t* iota;    // [n]
+  int32_t* vals;    // [n] token indices sorted by token
+  void* sort_tmp;
+  size_t sort_bytes;
   size_t bytes;
 };
+
+int sort_key_bits(int64_t vocab) {
+  int b = 1;
+  while ((int64_t(1) << b) < vocab) ++b;
+  return b;
+}
 
 SparseWorkspace carve_sparse(const icepop_shape* s, void* base) {
   Carver c(base);
   SparseWorkspace w;
-  const int64_t nb = (std::max<int64_t>(s->n_tokens, 1) + 63) / 64;
+  memset(&w, 0, sizeof(w));
+  const int64_t n = std::max<int64_t>(s->n_tokens, 1);
+  const int64_t nb = (n + 63) / 64;
   w.flags = c.take<int32_t>((size_t)nb);
   w.kb_map = c.take<int32_t>((size_t)nb);
   w.mt_map = c.take<int32_t>((size_t)nb);
   w.cnt = c.take<int32_t>(4);
+  w.rscale = c.take<float>((size_t)n);
+  w.ohc = c.take<float>((size_t)n);
+  w.exc = c.take<uint8_t>((size_t)n);
+  w.hid_s = c.take<__nv_bfloat16>((size_t)n * s->hidden);
+  w.keys = c.take<int32_t>((size_t)n);
+  w.iota = c.take<int32_t>((size_t)n);
+  w.vals = c.take<int32_t>((size_t)n);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)n, 0, sort_key_bits(s->vocab));
+  w.sort_bytes = std::max<size_t>(tb, 1);
+  w.sort_tmp = c.take<uint8_t>(w.sort_bytes);
   w.bytes = align_up(c.off, 256);
   return w;
 }
@@ -835,12 +867,18 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
   // stored probabilities: dZ in place over all rows (zero-coefficient rows become zero rows),
   // then K4/K5 skip the 64-token blocks / 256-token tiles without any active row when the
   // workspace holds the block lists (block-sparse GEMMs; no data moves)
-  bool sparse = false;
+  // With its workspace the stored-probabilities backward is row-scaled: no dZ pass except for
+  // exception rows (k_sp_prep), K4 scales rows and adds c W[y], K5 reads s H, and the one-hot
+  // part of dW is a deterministic scatter. Without it: dZ in place over every row.
+  bool sparse = false, scaled = false;
   SparseWorkspace sw;
   memset(&sw, 0, sizeof(sw));
   if (sp) {
-    sparse = skip && workspace && workspace_bytes >= carve_sparse(shape, nullptr).bytes;
-    if (sparse) sw = carve_sparse(shape, workspace);
+    if (workspace && workspace_bytes >= carve_sparse(shape, nullptr).bytes) {
+      sw = carve_sparse(shape, workspace);
+      scaled = !rs || grad_weight;  // the fused reduce-scatter takes the one-hot part as acc_src
+      sparse = skip;
+    }
     skip = false;
   } else {
     const int64_t min_rows = std::min<int64_t>(N, BM);
@@ -915,8 +953,13 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));  // skipped tiles
       }
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
+      if (scaled) {
+        k_sp_prep<<<grid, SPP_THREADS, 0, st>>>(sv.tile_max, tm_ld, (int32_t)((V + 63) / 64), lse, coeff,
+                                                (float)grad_scale, reinterpret_cast<const uint4*>(hidden), d / 8,
+                                                sw.rscale, sw.ohc, sw.exc, reinterpret_cast<uint4*>(sw.hid_s), nc);
+      }
       k_dz_probs<<<grid, DZP_THREADS, 0, st>>>(reinterpret_cast<uint4*>(dzb), sv.tile_max, tm_ld, lse, coeff,
-                                               (float)grad_scale, tokens, nc, V / 8);
+                                               (float)grad_scale, tokens, nc, V / 8, scaled ? sw.exc : nullptr);
       ICP_CUDA(cudaGetLastError());
     } else {
       ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V,
@@ -932,6 +975,14 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       eh.ldo = d;
       eh.out_f32 = grad_hidden_f32 ? 1 : 0;
       eh.vec_ok = ((reinterpret_cast<uintptr_t>(eh.out) & 15u) == 0) && (d % 8 == 0);
+      if (scaled) {  // dH = s (Q.W) + c W[y]
+        eh.row_scale = sw.rscale;
+        eh.oh_coef = sw.ohc;
+        eh.oh_tok = tokens;
+        eh.oh_w = static_cast<const __nv_bfloat16*>(weight);
+        eh.oh_sy = dv ? 1 : d;  // W(y, n): [V,d] row y / [d,V] column y
+        eh.oh_sn = dv ? V : 1;
+      }
       // B operand viewed [N = d, K = V]: W[d,V] is K-major, W[V,d] is MN-major
       Sparse sp4;
       if (sparse) {
@@ -942,6 +993,19 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     }
     // K5: grad_weight (+)= H^T . dZ   (K = nc tokens)
     if (grad_weight || (rs && last)) {
+      // row-scaled stored probabilities: dW = Q^T.(s H) + scatter_y(c H); the one-hot part
+      // is scattered after K5 into grad_weight, or (fused reduce-scatter) first into the local
+      // scratch that K5's epilogue adds to every row it sends
+      auto onehot_scatter = [&](float* dst) -> int {
+        k_iota<<<(int)std::min<int64_t>((nc + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(sw.iota, nc);
+        size_t tb = sw.sort_bytes;
+        ICP_CUDA(cub::DeviceRadixSort::SortPairs(sw.sort_tmp, tb, tokens, sw.keys, sw.iota, sw.vals, (int)nc, 0,
+                                                 sort_key_bits(V), st));
+        k_onehot_scatter<<<(int)std::min<int64_t>(nc, (int64_t)num_sms() * 8), OHS_THREADS, 0, st>>>(
+            sw.keys, sw.vals, nc, sw.ohc, reinterpret_cast<const uint4*>(hidden), d / 8, dst, dv ? 1 : d, dv ? V : 1);
+        ICP_CUDA(cudaGetLastError());
+        return ICEPOP_OK;
+      };
       EpiParams ew;
       memset(&ew, 0, sizeof(ew));
       ew.out = grad_weight;
@@ -959,7 +1023,13 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.acc_src = (n_chunks > 1) ? grad_weight : nullptr;
         ew.out = nullptr;
         ext_k.dim = skip ? 2 : 0;
+        if (scaled) {
+          ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
+          ICP_TRY(onehot_scatter(grad_weight));
+          ew.acc_src = grad_weight;
+        }
       }
+      if (scaled) h = sw.hid_s;
       // an empty K extent must still store (zeros, or the local partial to the peers) when
       // nothing else writes the result
       const bool keep_empty = ((skip || sparse) && !ew.accumulate) || (rs && last);
@@ -977,6 +1047,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
         ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
       }
+      if (scaled && !(rs && last)) ICP_TRY(onehot_scatter(grad_weight));
     }
   }
   return ICEPOP_OK;

@@ -488,8 +488,10 @@ constexpr int DZP_THREADS = 256;
 __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ probs, const float* __restrict__ tile_max,
                                                           int32_t tm_ld, const float* __restrict__ lse,
                                                           const float* __restrict__ coeff, float coeff_scale,
-                                                          const int32_t* __restrict__ tokens, int64_t n, int64_t v8) {
+                                                          const int32_t* __restrict__ tokens, int64_t n, int64_t v8,
+                                                          const uint8_t* __restrict__ only = nullptr) {
   for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (only && !only[t]) continue;  // block-uniform: rows the GEMMs scale themselves stay as they are
     uint4* row = probs + t * v8;
     const float cf = coeff[t] * coeff_scale;
     if (cf == 0.f) {
@@ -587,6 +589,100 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const int32_t* __res
     }
     if (threadIdx.x == 0) cnt[list] = base;
     __syncthreads();
+  }
+}
+
+// Row-scaled stored-probabilities backward, per row t. q was stored as 2^(u - R_slab) with
+// R_slab = 0 except for slabs whose maximum left the finite range (exception rows, any R != 0).
+// For the other rows p = q 2^(-lse2) has one scale per row, so the GEMMs take it directly:
+//   dH = s (Q.W) + c W[y],  dW = Q^T.(s H) + scatter_y(c H),  s = -c 2^(-lse2), c = coeff * gs.
+// Exception rows get their dZ in place (k_dz_probs with `only`) and enter the GEMMs unscaled
+// (s = 1, c = 0). Writes s, c, the exception flag and H'[t] = bf16(s H[t]).
+constexpr int SPP_THREADS = 128;
+__global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict__ tile_max, int32_t tm_ld,
+                                                         int32_t n_slabs, const float* __restrict__ lse,
+                                                         const float* __restrict__ coeff, float gs,
+                                                         const uint4* __restrict__ hid, int64_t d8,
+                                                         float* __restrict__ rscale, float* __restrict__ ohc,
+                                                         uint8_t* __restrict__ exc, uint4* __restrict__ hid_s, int64_t n) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    const float* tm = tile_max + t * tm_ld;
+    int any = 0;
+    for (int j = threadIdx.x; j < n_slabs; j += SPP_THREADS) any |= tm[j] != 0.f;
+    const bool ex = __syncthreads_or(any) != 0;
+    const float cf = coeff[t] * gs;
+    const float sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
+    if (threadIdx.x == 0) {
+      rscale[t] = sc;
+      ohc[t] = ex ? 0.f : cf;
+      exc[t] = ex ? 1 : 0;
+    }
+    const uint4* src = hid + t * d8;
+    uint4* dst = hid_s + t * d8;
+    for (int64_t k = threadIdx.x; k < d8; k += SPP_THREADS) {
+      uint4 x = src[k];
+      uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+        const __nv_bfloat162 o = __floats2bfloat162_rn(h.x * sc, h.y * sc);
+        w[i] = *reinterpret_cast<const uint32_t*>(&o);
+      }
+      dst[k] = x;
+    }
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+// One-hot part of dW: dW[y, :] += sum over tokens t with y_t = y of c_t H[t, :], in increasing t
+// (the token indices are radix-sorted by y, a stable sort), one block per run of equal y that
+// starts in its stride: deterministic, no atomics. dW element (y, col) at y * sy + col * sc.
+constexpr int OHS_THREADS = 256;
+__global__ void __launch_bounds__(OHS_THREADS) k_onehot_scatter(const int32_t* __restrict__ ys,
+                                                                const int32_t* __restrict__ ts, int64_t n,
+                                                                const float* __restrict__ ohc,
+                                                                const uint4* __restrict__ hid, int64_t d8,
+                                                                float* __restrict__ dw, int64_t sy, int64_t sc) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int32_t y = ys[i];
+    if (i > 0 && ys[i - 1] == y) continue;  // not the start of a run (block-uniform)
+    int64_t e = i + 1;
+    while (e < n && ys[e] == y) ++e;
+    for (int64_t k = threadIdx.x; k < d8; k += OHS_THREADS) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      bool any = false;
+      for (int64_t r = i; r < e; ++r) {
+        const int32_t t = ts[r];
+        const float c = ohc[t];
+        if (c == 0.f) continue;
+        any = true;
+        uint4 x = hid[(int64_t)t * d8 + k];
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+          acc[2 * j] = fmaf(c, h.x, acc[2 * j]);
+          acc[2 * j + 1] = fmaf(c, h.y, acc[2 * j + 1]);
+        }
+      }
+      if (!any) continue;
+      float* dst = dw + (int64_t)y * sy + k * 8 * sc;
+      if (sc == 1) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        float4 a = d4[0], b = d4[1];
+        a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
+        b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
+        d4[0] = a;
+        d4[1] = b;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j * sc] += acc[j];
+      }
+    }
   }
 }
 

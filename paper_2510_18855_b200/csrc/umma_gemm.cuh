@@ -26,6 +26,9 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int GEMM_THREADS = 192;
 constexpr float LOG2E_F = 1.4426950408889634f;
+// Stored probabilities: slabs whose maximum (log2 units) lies within +-PROBS_REF_RANGE are
+// stored as 2^u (reference 0), so Q.W and Q^T.H' stay finite (|q| <= 2^60) in fp32.
+constexpr float PROBS_REF_RANGE = 60.f;
 
 // EPI_LSE_REF / EPI_DZ_REF are the KL-to-ref variants (objective.py:254-263): a second B
 // operand (W_ref) shares every A (hidden) tile and accumulates into a second TMEM accumulator.
@@ -121,8 +124,16 @@ struct EpiParams {
   const float* lse_ref;    // [M] natural units
   const float* kl;         // [M] kl_t
   const float* kl_w;       // [M] w_t * gamma / T
-  // EPI_LSE stored-probabilities mode: q[m, v] = 2^(u - slab max) as bf16 through the tensor
-  // map (row stride = N), tile_max[m * tm_ld + 4 n_blk + c] = 64-column slab c's maximum (log2)
+  // EPI_STORE row-scaled mode (dH from the stored probabilities): out[m, n] = row_scale[m] * acc
+  // + oh_coef[m] * W(oh_tok[m], n), W(y, n) at oh_w[y * oh_sy + n * oh_sn]
+  const float* row_scale;
+  const float* oh_coef;
+  const int32_t* oh_tok;
+  const __nv_bfloat16* oh_w;
+  int64_t oh_sy, oh_sn;
+  // EPI_LSE stored-probabilities mode: q[m, v] = 2^(u - R) as bf16 through the tensor map (row
+  // stride = N), tile_max[m * tm_ld + 4 n_blk + c] = R of 64-column slab c (0 unless its
+  // maximum leaves +-PROBS_REF_RANGE, then that maximum; log2 units)
   __nv_bfloat16* probs;
   float* tile_max;
   int32_t tm_ld;
@@ -190,6 +201,9 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
   const int mm = m0 + row;
   const bool row_ok = mm < sh.M;
   const int m = (row_ok && ep.row_index) ? __ldg(ep.row_index + mm) : mm;
+  const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + mm) : 1.f;
+  const float oc = (row_ok && ep.oh_coef) ? __ldg(ep.oh_coef + mm) : 0.f;
+  const __nv_bfloat16* wrow = oc != 0.f ? ep.oh_w + (int64_t)__ldg(ep.oh_tok + mm) * ep.oh_sy : nullptr;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
@@ -200,6 +214,15 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
     if (sh.k_blocks == 0) {  // empty K extent (keep_empty): TMEM was never written
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
+    if (ep.row_scale) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= rs;
+      if (wrow) {
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < sh.N) v[j] = fmaf(oc, __bfloat162float(wrow[(int64_t)(col0 + j) * ep.oh_sn]), v[j]);
+      }
     }
     if (ep.rs_world > 0) {
       const int64_t o = m / ep.rs_shard_rows;
@@ -301,7 +324,7 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
-  float sm0 = -1e30f, sm1 = -1e30f, sm2 = -1e30f, sm3 = -1e30f;  // slab maxima (registers, not a local array)
+  float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;  // slab references (registers, not a local array)
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {
     float v[64];
@@ -321,6 +344,10 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
 #pragma unroll
     for (int j = 0; j < 64; ++j) mx = fmaxf(mx, (full || col0 + j < sh.N) ? v[j] : -1e30f);
     mx *= ep.scale_log2;  // scale > 0: max commutes with it
+    // stored q = 2^(u - R): R = 0 while the slab maximum is within [-PROBS_REF_RANGE, +..] (one
+    // scale per row then turns q into probabilities), else R = the slab maximum (exception)
+    const float ref = fabsf(mx) <= PROBS_REF_RANGE ? 0.f : mx;
+    const float qs = exp2f(mx - ref);
     float s = 0.f, q = 0.f;
     uint32_t pk[32];
 #pragma unroll
@@ -330,13 +357,13 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
       const float e0 = ok0 ? fast_exp2(d0) : 0.f, e1 = ok1 ? fast_exp2(d1) : 0.f;
       s += e0 + e1;
       q = fmaf(e0, ok0 ? d0 : 0.f, fmaf(e1, ok1 ? d1 : 0.f, q));
-      pk[j] = pack_bf16x2(e0, e1);
+      pk[j] = pack_bf16x2(e0 * qs, e1 * qs);
     }
     if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
-    sm0 = c == 0 ? mx : sm0;
-    sm1 = c == 1 ? mx : sm1;
-    sm2 = c == 2 ? mx : sm2;
-    sm3 = c == 3 ? mx : sm3;
+    sm0 = c == 0 ? ref : sm0;
+    sm1 = c == 1 ? ref : sm1;
+    sm2 = c == 2 ? ref : sm2;
+    sm3 = c == 3 ? ref : sm3;
     // merge the slab into the tile's running (max, sum, q)
     const float nm = fmaxf(run_m, mx);
     const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);

@@ -89,9 +89,15 @@ def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
             cb = max(128 * 2 * v, cb // 2)
 
 
+SP_ROWSCALE = os.environ.get("ICEPOP_SP_ROWSCALE", "1") != "0"
+
+
 def _sp_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor | None:
-    """Workspace of the stored-probabilities backward (row-compaction buffers, no dZ chunk),
-    or None: without it every row goes through K4/K5 (same result, more work)."""
+    """Workspace of the stored-probabilities backward: block lists, row scales, s*H and the
+    one-hot sort buffers (about 2*n*d bytes). None (no memory, or ICEPOP_SP_ROWSCALE=0): the
+    backward then forms dZ in place over every row instead (same result up to rounding)."""
+    if not SP_ROWSCALE:
+        return None
     lib = _lib.load()
     shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=max(n_seqs, 1), n_groups=1,
                        weight_layout=_lib.W_VD)
@@ -555,6 +561,8 @@ def icepop_bwd_reduce_scatter(
         scratch = None if single_chunk else torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     else:
         ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
+        if ws is not None:  # the row-scaled backward sends the one-hot part of dW from this scratch
+            scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                        lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                        probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))

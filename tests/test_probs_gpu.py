@@ -54,8 +54,8 @@ def test_forward_statistics_identical_in_both_modes(cuda_device, cta_group, layo
 @pytest.mark.parametrize("temperature", [1.0, 0.7])
 @pytest.mark.parametrize("layout", ["vd", "dv"])
 def test_stored_probabilities_match_fp32_softmax(cuda_device, cta_group, layout, temperature):
-    """q * 2^(slab max - lse log2 e) is the softmax; V = 1000 leaves a ragged last tile and a
-    ragged last 64-column slab, N is not a multiple of 128."""
+    """q * 2^(R - lse log2 e) is the softmax (R: the per-slab reference in tile_max); V = 1000
+    leaves a ragged last tile and a ragged last 64-column slab, N is not a multiple of 128."""
     from paper_2510_18855_b200 import _lib
     from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
 
@@ -71,12 +71,11 @@ def test_stored_probabilities_match_fp32_softmax(cuda_device, cta_group, layout,
     z = _logits(c, cuda_device, temperature)
     u = z * (1.0 / np.log(2.0))
     pad = n_slabs * S - V
-    ref_max = torch.nn.functional.pad(u, (0, pad), value=-1e30).view(N, -1, S).amax(-1)
-    torch.testing.assert_close(tmax, ref_max, rtol=0, atol=2e-4)
-    assert float(probs.min()) >= 0.0 and float(probs.max()) <= 1.0
-    # each slab's maximum entry is stored as exactly 1 (q = 2^0)
-    slabs = torch.nn.functional.pad(probs, (0, pad)).view(N, -1, S)
-    assert torch.all(slabs.amax(-1) == 1.0)
+    slab_max = torch.nn.functional.pad(u, (0, pad), value=-1e30).view(N, -1, S).amax(-1)
+    # slab reference R: 0 while |slab max| <= 60 (log2 units), else the slab maximum
+    assert torch.all(tmax == 0) and float(slab_max.abs().max()) < 60
+    # q = 2^(u - R) = 2^u here, within bf16 rounding
+    torch.testing.assert_close(probs, torch.exp2(u), rtol=8e-3, atol=0)
     scale = torch.exp2(tmax - (f.lse * (1.0 / np.log(2.0)))[:, None])
     p = probs * scale.repeat_interleave(S, dim=1)[:, :V]
     ref = torch.softmax(z, dim=1)
@@ -222,14 +221,14 @@ def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group):
     torch.cuda.synchronize()
     assert torch.all(buf[:G] == 12345.0) and torch.all(buf[G + N * V:] == 12345.0)
     assert torch.all(tm_buf[:64] == 777.0) and torch.all(tm_buf[64 + N * L:] == 777.0)
-    assert torch.isfinite(probs.float()).all() and float(probs.float().max()) == 1.0
+    assert torch.isfinite(probs.float()).all() and float(probs.float().min()) >= 0.0
 
 
 @pytest.mark.parametrize("layout", ["vd", "dv"])
 def test_long_k_backward_wide_tiles(cuda_device, layout):
     """V >= 16384 (K4 long-K) and N >= 16384 tokens (K5 long-K): the backward GEMMs run on
-    256 x 512 tiles; dW and dH equal the 256 x 256 tiles' bit for bit, and dW matches
-    dZ^T H from the dZ left in the probabilities buffer."""
+    256 x 512 tiles; dW and dH equal the 256 x 256 tiles' bit for bit and the recompute-mode
+    backward within the bf16 tolerance."""
     from paper_2510_18855_b200 import _lib
     from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
 
@@ -244,22 +243,17 @@ def test_long_k_backward_wide_tiles(cuda_device, layout):
         for wide in (1, 0):
             _lib.check(lib.icepop_set_wide_tiles(wide))
             f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
-            dz = f.extras["probs"]
             gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
-            res[wide] = (gh, gw, dz)
+            res[wide] = (gh, gw)
+        fr = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=False)
+        ghr, gwr = icepop_bwd(H, W, _batch(c, cuda_device), fr, cfg, layout=layout, grad_hidden_dtype=torch.float32)
     finally:
         _lib.check(lib.icepop_set_wide_tiles(1))
         _lib.check(lib.icepop_set_skip_inactive(1))
-    (gh1, gw1, dz1), (gh0, gw0, _) = res[1], res[0]
+    (gh1, gw1), (gh0, gw0) = res[1], res[0]
     assert torch.equal(gh1, gh0) and torch.equal(gw1, gw0)
-    ref = dz1.double().T @ H.double()  # [V, d]
-    if layout == "dv":
-        ref = ref.T
-    # fp32 accumulation over ~16.6K mostly cancelling terms: rel ~2.5e-5 measured
-    assert _rel(gw1.cpu().numpy(), ref.cpu().numpy()) < 1e-4
-    Wd = W.double()
-    ref_h = dz1.double() @ (Wd if layout == "vd" else Wd.T)
-    assert _rel(gh1.cpu().numpy(), ref_h.cpu().numpy()) < 1e-4
+    assert _rel(gw1.cpu().numpy(), gwr.cpu().numpy()) < 5e-3
+    assert _rel(gh1.cpu().numpy(), ghr.cpu().numpy()) < 5e-3
 
 
 @pytest.mark.parametrize("layout", ["vd", "dv"])
@@ -367,3 +361,52 @@ def test_odd_shapes_all_modes(cuda_device, n_tok, d, V, layout):
         if np.linalg.norm(o["grad_weight"]) > 0:
             assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2, sp
             assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2, sp
+
+
+
+@pytest.mark.parametrize("kind", ["large", "shifted"])
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_exception_rows_out_of_reference_range(cuda_device, layout, kind):
+    """Rows whose logits leave the +-60 (log2) range of the stored-probabilities reference:
+    "large" = logits of std ~40 (slab maxima beyond +60), "shifted" = every logit of half the
+    rows moved by -100 through a constant feature (maxima below -60). Those rows take the dZ
+    pass in place, the others the row-scaled GEMMs; both vs the recompute mode and the oracle."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(n_seqs=4, d=64, V=1000, seed=95, layout=layout, lens=[120, 90, 150, 70], group=2)
+    Hn, Wn = c["H"].double().numpy().copy(), c["W"].double().numpy().copy()
+    if kind == "large":
+        Wn *= 20.0
+    else:
+        Hn[:, 0] = 0.0
+        Hn[: len(Hn) // 2, 0] = 1.0
+        if layout == "vd":
+            Wn[:, 0] = -100.0
+        else:
+            Wn[0, :] = -100.0
+    c["H"], c["W"] = torch.from_numpy(Hn).to(torch.bfloat16), torch.from_numpy(Wn).to(torch.bfloat16)
+    # lp_old near the new model's own log-probs so the ratios stay in range
+    from oracle.icepop_oracle import icepop_dense
+
+    o0 = icepop_dense(c["H"].double().numpy(), c["W"].double().numpy(), c["tokens"], c["lp_old"], c["lp_old"],
+                      c["cu"], c["go"], c["adv"], layout=layout)
+    rng = np.random.default_rng(3)
+    c["lp_old"] = o0["lp_cur"] + rng.normal(0, 0.1, len(c["tokens"]))
+    c["lp_inf"] = c["lp_old"] - rng.normal(0, 0.2, len(c["tokens"]))
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
+    assert bool((f.extras["tile_max"] != 0).any())  # some slabs carry their own reference
+    gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
+    fr = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=False)
+    ghr, gwr = icepop_bwd(H, W, _batch(c, cuda_device), fr, cfg, layout=layout, grad_hidden_dtype=torch.float32)
+    assert torch.isfinite(gw).all() and torch.isfinite(gh).all()
+    # "shifted": dH along the constant feature is -100 * sum_v dZ[t, v], exactly 0 -- pure
+    # cancellation noise in any bf16 mode (the recompute mode's included), so compare the rest
+    cols = slice(1, None) if kind == "shifted" else slice(None)
+    assert _rel(gw.cpu().numpy(), gwr.cpu().numpy()) < 5e-3
+    assert _rel(gh[:, cols].cpu().numpy(), ghr[:, cols].cpu().numpy()) < 5e-3
+    o = _oracle(c)
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), o["kept"])
+    assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
+    assert _rel(gh[:, cols].cpu().numpy(), o["grad_hidden"][:, cols]) < 1e-2
