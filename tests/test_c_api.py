@@ -38,8 +38,11 @@ def test_c_example_compiles_and_links(tmp_path):
 def test_c_example_matches_python_layer(tmp_path, cuda_device):
     import torch
 
+    import paper_2510_18855_b200.loss as L
     from paper_2510_18855_b200.loss import IcePopConfig, PackedBatch, icepop_bwd, icepop_fwd
 
+    if not L.SP_ROWSCALE:
+        pytest.skip("ICEPOP_SP_ROWSCALE=0 takes another backward path than the C example")
     exe = _build(tmp_path)
     dump = tmp_path / "dump.bin"
     r = subprocess.run([str(exe), str(dump)], capture_output=True, text=True, timeout=120)
