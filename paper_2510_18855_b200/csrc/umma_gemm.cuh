@@ -219,9 +219,24 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] *= rs;
       if (wrow) {
+        if (ep.oh_sn == 1 && col0 + 32 <= sh.N) {  // [V,d] weight: 32 contiguous bf16 = 4 x 16 B
+          const uint4* w4 = reinterpret_cast<const uint4*>(wrow + col0);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 x = __ldg(w4 + q4);
+            const uint32_t* xw = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xw[i]));
+              v[8 * q4 + 2 * i] = fmaf(oc, f.x, v[8 * q4 + 2 * i]);
+              v[8 * q4 + 2 * i + 1] = fmaf(oc, f.y, v[8 * q4 + 2 * i + 1]);
+            }
+          }
+        } else {
 #pragma unroll 4
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < sh.N) v[j] = fmaf(oc, __bfloat162float(wrow[(int64_t)(col0 + j) * ep.oh_sn]), v[j]);
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < sh.N) v[j] = fmaf(oc, __bfloat162float(wrow[(int64_t)(col0 + j) * ep.oh_sn]), v[j]);
+        }
       }
     }
     if (ep.rs_world > 0) {
