@@ -476,9 +476,9 @@ __global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* 
   }
 }
 
-// Stored-probabilities backward (replaces the K3 GEMM): turns K1's q[t, v] = 2^(u - m_slab)
-// into dZ in place,
-//   dz[t, v] = cf_t * (e_{y_t} - q[t, v] * 2^(m_slab(t, v / 64) - lse2_t)),  cf_t = coeff_t * scale,
+// Stored-probabilities dZ in place (exception rows of the row-scaled backward, or every row when
+// the backward has no workspace): turns K1's q[t, v] = 2^(u - R_slab) into
+//   dz[t, v] = cf_t * (e_{y_t} - q[t, v] * 2^(R_slab(t, v / 64) - lse2_t)),  cf_t = coeff_t * scale,
 // the same expression epi_dz evaluates from recomputed logits (p = 2^(u - lse2)). Rows with
 // cf_t == 0 are written as zeros without being read. One block per row (grid-stride); each
 // 16-byte chunk (8 columns, one slab) takes its slab scale from the L1-resident tile_max row;

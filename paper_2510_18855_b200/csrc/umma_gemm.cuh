@@ -324,14 +324,16 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
 // so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2).
 // One TMEM pass in 64-column slabs: each slab's (max, sum, q) is taken against the slab's own
 // maximum and merged online into the tile's. In stored-probabilities mode (ep.probs) the slab
-// also emits q[m, v] = 2^(u_v - slab max) in [0, 1] as bf16 (TMA stores, clipped to M rows /
-// N columns) and tile_max[m, 4 n_blk + c] = slab c's maximum, from which the backward forms dZ
-// without recomputing logits. The statistics are the same bits in both modes.
+// also emits q[m, v] = 2^(u_v - R) as bf16 (TMA stores, clipped to M rows / N columns) and
+// tile_max[m, 4 n_blk + c] = R, the slab's reference: 0 while its maximum is within
+// +-PROBS_REF_RANGE, else that maximum. The backward needs no logit recompute: for rows whose
+// references are all 0 the probabilities are q 2^(-lse2), one scale per row. The statistics are
+// the same bits in both modes.
 template <int BN>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
                                         uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
                                         int quarter, uint32_t taddr) {
-  static_assert(BN == 4 * 64, "tile_max holds four 64-column slab maxima per tile");
+  static_assert(BN == 4 * 64, "tile_max holds four 64-column slab references per tile");
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;

@@ -3,10 +3,12 @@
 Three layers, all on device, none with a CPU fallback:
 
 * :func:`icepop_fwd` / :func:`icepop_bwd` -- functional forward (K1 fused lm_head GEMM +
-  online log-softmax, K2 IcePop epilogue) and backward (bf16 dZ -- formed in place from the
-  probabilities K1 stored when they fit in HBM, else recomputed by the K3 GEMM in chunks --
-  then K4 dHidden, K5 dW), dispatched on dtype: bfloat16 -> tcgen05 path, float64 -> SIMT
-  validation path.
+  online log-softmax, K2 IcePop epilogue) and backward. The backward is either row-scaled
+  GEMMs on the probabilities K1 stored when they fit in HBM (dH = s(Q.W) + cW[y],
+  dW = Q^T(sH) + scatter), or bf16 dZ recomputed by the K3 GEMM in chunks, then K4 dHidden,
+  K5 dW. Dispatched on dtype: bfloat16 -> tcgen05 path, float64 -> SIMT validation path.
+* :func:`icepop_fwd_bwd` -- both in one call (objective_and_grad's shape), in token chunks
+  when the whole batch's probabilities do not fit.
 * :func:`icepop_loss` -- a ``torch.library`` custom op with autograd (loss = -J), for
   training code that wants ``loss.backward()``.
 * :class:`PackedBatch` -- the packed per-token / per-sequence metadata the kernels read
@@ -38,7 +40,7 @@ LAYOUTS = {"dv": _lib.W_DV, "vd": _lib.W_VD}
 DZ_CHUNK_BYTES = int(os.environ.get("ICEPOP_DZ_CHUNK_BYTES", str(96 * 10**9)))
 
 
-# Stored-probabilities mode (include/icepop.h): K1 also writes bf16 q = exp(z - slab max)
+# Stored-probabilities mode (include/icepop.h): K1 also writes bf16 q = 2^(z log2e - R)
 # [N, V] so the backward needs no K3 logit recompute (6 instead of 8 N.d.V FLOPs per step).
 # "auto" stores them when 2.N.V bytes fit in STORE_PROBS_FRACTION of the free device memory.
 STORE_PROBS = os.environ.get("ICEPOP_STORE_PROBS", "auto")
@@ -68,8 +70,8 @@ def _free_bytes(device) -> int | None:
 
 
 def _take_probs(fwd: "IcePopForward", kl_grad: bool):
-    """(probs, tile_max) of a stored-probabilities forward, or (None, None). The backward
-    overwrites probs with dZ, so they are handed out once (a second backward recomputes)."""
+    """(probs, tile_max) of a stored-probabilities forward, or (None, None). The backward may
+    overwrite rows of probs with dZ, so they are handed out once (a second backward recomputes)."""
     if kl_grad or fwd.extras.get("probs") is None:
         return None, None
     return fwd.extras.pop("probs"), fwd.extras.pop("tile_max")
@@ -747,7 +749,7 @@ def _setup_context(ctx, inputs, output):
     loss, stats, lse, lp_cur, entropy, kept, coeff, probs, tile_max = output
     ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff, probs, tile_max)
     ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset)
-    ctx.probs_live = probs.numel() > 0  # consumed (overwritten with dZ) by the first backward
+    ctx.probs_live = probs.numel() > 0  # consumed by the first backward (rows may become dZ)
 
 
 def _backward(ctx, grad_loss, *unused):
