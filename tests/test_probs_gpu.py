@@ -410,3 +410,34 @@ def test_exception_rows_out_of_reference_range(cuda_device, layout, kind):
     assert np.array_equal(f.kept.cpu().numpy().astype(bool), o["kept"])
     assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
     assert _rel(gh[:, cols].cpu().numpy(), o["grad_hidden"][:, cols]) < 1e-2
+
+
+@pytest.mark.parametrize("pattern", ["all_same", "last_column", "few_ids"])
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_onehot_scatter_token_patterns(cuda_device, layout, pattern):
+    """The row-scaled backward's one-hot scatter (dW[y] += c H[t], tokens radix-sorted by id)
+    and K4's W[y] gather under skewed token streams: one id for every token (a single run of
+    N), ids in the last (ragged) vocab slab, a handful of ids. Same gradients as the
+    recompute mode; repeated runs bit-identical."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    V = 1000
+    c = _case(n_seqs=4, d=96, V=V, seed=97, layout=layout, lens=[400, 300, 350, 250], group=2)
+    N = len(c["tokens"])
+    rng = np.random.default_rng(5)
+    if pattern == "all_same":
+        c["tokens"] = np.full(N, 17, dtype=np.int32)
+    elif pattern == "last_column":
+        c["tokens"] = rng.integers(V - 40, V, N).astype(np.int32)
+    else:
+        c["tokens"] = rng.choice(np.array([0, 5, 999, 500], dtype=np.int32), N)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig(algo="tis")
+    out = []
+    for sp in (True, True, False):
+        f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=sp)
+        out.append(icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32))
+    (gh1, gw1), (gh2, gw2), (ghr, gwr) = out
+    assert torch.equal(gh1, gh2) and torch.equal(gw1, gw2)
+    assert _rel(gw1.cpu().numpy(), gwr.cpu().numpy()) < 5e-3
+    assert _rel(gh1.cpu().numpy(), ghr.cpu().numpy()) < 5e-3
