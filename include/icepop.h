@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define ICEPOP_ABI_VERSION 2
+#define ICEPOP_ABI_VERSION 3
 
 enum icepop_status {
   ICEPOP_OK = 0,

@@ -20,7 +20,7 @@ OK, EINVAL, ENUMERIC, ECUDA, EARCH = 0, 1, 2, 3, 4
 ALGO_ICEPOP, ALGO_GRPO, ALGO_TIS = 0, 1, 2
 W_DV, W_VD = 0, 1
 NSTATS = 8
-ABI_VERSION = 2
+ABI_VERSION = 3
 PROBS_SLAB = 64  # ICEPOP_PROBS_SLAB: vocab columns per tile_max entry
 
 

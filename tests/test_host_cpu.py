@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
                          check=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}$", out, re.M), f"{name} not a defined text symbol"
-    assert lib.icepop_abi_version() == 2
+    assert lib.icepop_abi_version() == 3
 
 
 def test_library_has_sm100a_tensor_core_code():
