@@ -193,7 +193,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.seqs:
+        cfg["seqs"] = args.seqs
+        cfg["name"] += f" [seqs/rank = {args.seqs}]"
     meta = make_batch_host(cfg, rank, world, args.zero_adv_frac)
     H, W, batch, onpolicy = build_device_inputs(cfg, meta, dev, rank)
     icfg = IcePopConfig()
@@ -729,6 +732,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--no-onpolicy", action="store_true")
+    ap.add_argument("--seqs", type=int, default=0,
+                    help="override the config's sequences per rank (e.g. the C5 sweep: 16/32/64/128/256)")
     ap.add_argument("--zero-adv-frac", type=float, default=0.0,
                     help="fraction of prompt groups with identical rewards (zero advantages)")
     ap.add_argument("--dw-collective", choices=["fused", "nccl"], default="fused",

@@ -94,19 +94,24 @@ def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
 SP_ROWSCALE = os.environ.get("ICEPOP_SP_ROWSCALE", "1") != "0"
 
 
+def sp_workspace_bytes(n: int, d: int, v: int, n_seqs: int) -> int:
+    """Bytes of the stored-probabilities (row-scaled) backward workspace for n tokens."""
+    lib = _lib.load()
+    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=max(n_seqs, 1), n_groups=1,
+                       weight_layout=_lib.W_VD)
+    b = _lib._sz()
+    _lib.check(lib.icepop_workspace_bytes(shape, -1, 0, None, b))
+    return max(b.value, 1)
+
+
 def _sp_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor | None:
     """Workspace of the stored-probabilities backward: block lists, row scales, s*H and the
     one-hot sort buffers (about 2*n*d bytes). None (no memory, or ICEPOP_SP_ROWSCALE=0): the
     backward then forms dZ in place over every row instead (same result up to rounding)."""
     if not SP_ROWSCALE:
         return None
-    lib = _lib.load()
-    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=max(n_seqs, 1), n_groups=1,
-                       weight_layout=_lib.W_VD)
-    b = _lib._sz()
-    _lib.check(lib.icepop_workspace_bytes(shape, -1, 0, None, b))
     try:
-        return torch.empty(max(b.value, 1), dtype=torch.uint8, device=device)
+        return torch.empty(sp_workspace_bytes(n, d, v, n_seqs), dtype=torch.uint8, device=device)
     except torch.OutOfMemoryError:
         return None
 
@@ -254,11 +259,14 @@ def icepop_fwd(
     layout: str = "vd",
     weight_ref: torch.Tensor | None = None,
     store_probs: bool | None = None,
+    probs_buffers: tuple[torch.Tensor, torch.Tensor] | None = None,
 ) -> IcePopForward:
     """Forward of the IcePop objective on this rank's tokens (objective.py:215-278).
 
     ``store_probs`` (bf16 path): keep the bf16 probabilities for the backward (True / False /
     None = ``ICEPOP_STORE_PROBS``, default "auto": when they fit in device memory).
+    ``probs_buffers``: caller-owned (probs [>=N, V] bf16, tile_max [>=N, tile_max_ld(V)] f32)
+    to store them in (implies store_probs; icepop_fwd_bwd reuses one pair across token chunks).
     """
     lib = _lib_for(hidden)
     batch.validate()
@@ -292,7 +300,16 @@ def icepop_fwd(
             lse_ref = torch.empty(n, dtype=torch.float32, device=dev)
             kl_w = torch.empty(n, dtype=torch.float32, device=dev)
         probs = tile_max = None
-        if _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
+        if probs_buffers is not None:
+            pb, tb = probs_buffers
+            tm_ld = _lib.tile_max_ld(shape.vocab)
+            if (pb.dtype != torch.bfloat16 or pb.dim() != 2 or pb.shape[0] < n or pb.shape[1] != shape.vocab
+                    or tb.dtype != torch.float32 or tb.dim() != 2 or tb.shape[0] < n or tb.shape[1] != tm_ld
+                    or not pb.is_contiguous() or not tb.is_contiguous() or wr is not None):
+                raise ValueError("probs_buffers must be contiguous (bf16 [>=N, V], f32 [>=N, tile_max_ld(V)]) "
+                                 "and cannot be combined with weight_ref")
+            probs, tile_max = pb[:n], tb[:n]
+        elif _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
             try:
                 probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
                 tile_max = torch.empty((n, _lib.tile_max_ld(shape.vocab)), dtype=torch.float32, device=dev)
@@ -464,10 +481,13 @@ def icepop_bwd(
     grad_weight: torch.Tensor | None = None,
     weight_ref: torch.Tensor | None = None,
     grad_hidden_dtype: torch.dtype | None = None,
+    workspace: torch.Tensor | None = None,
 ) -> tuple[torch.Tensor | None, torch.Tensor | None]:
     """Gradients of grad_scale * J: (d/dhidden, d/dweight), objective.py:250-266.
 
     ``grad_weight`` (f32 for bf16 inputs, f64 for fp64), if given, is accumulated into.
+    ``workspace`` (bf16, stored-probabilities forward): a caller-owned uint8 buffer of at least
+    sp_workspace_bytes(...) used instead of allocating one.
     """
     lib = _lib_for(hidden)
     hidden = hidden.contiguous()
@@ -491,6 +511,8 @@ def icepop_bwd(
         probs, tile_max = _take_probs(fwd, wr is not None and cfg.kl_coeff > 0.0)
         if probs is None:
             ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
+        elif workspace is not None and SP_ROWSCALE and workspace.numel() >= sp_workspace_bytes(n, d, v, shape.n_seqs):
+            ws = workspace
         else:
             ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
@@ -633,6 +655,21 @@ def icepop_fwd_bwd(
     gw = grad_weight if grad_weight is not None else torch.zeros(tuple(weight.shape), dtype=torch.float32, device=dev)
     gh = torch.empty((n, hidden.shape[1]), dtype=grad_hidden_dtype or torch.bfloat16, device=dev) if need_hidden \
         else None
+    # One probabilities buffer (and backward workspace) for all chunks: re-allocating tens of GB
+    # per chunk lets smaller allocations fragment torch's cache between chunks. If the estimate
+    # was too optimistic for one block, the chunk halves (down to 4096 tokens).
+    n_seqs = batch.n_seqs
+    while True:
+        try:
+            bufs = (torch.empty((chunk, v), dtype=torch.bfloat16, device=dev),
+                    torch.empty((chunk, _lib.tile_max_ld(v)), dtype=torch.float32, device=dev))
+            break
+        except torch.OutOfMemoryError:
+            torch.cuda.empty_cache()
+            if chunk <= 4096:
+                raise
+            chunk = max(4096, chunk // 2 // 4096 * 4096)
+    ws = _sp_workspace(chunk, hidden.shape[1], v, n_seqs, dev)
     parts = []
     stats = torch.zeros(_lib.NSTATS, dtype=torch.float64, device=dev)
     for s0 in range(0, n, chunk):
@@ -640,9 +677,9 @@ def icepop_fwd_bwd(
         sub = PackedBatch(batch.tokens[s0:e0], batch.lp_train_old[s0:e0], batch.lp_infer_old[s0:e0],
                           batch.cu_seqlens, batch.group_offsets, batch.advantages, batch.rewards,
                           token_offset=batch.token_offset + s0)
-        f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, store_probs=True)
+        f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, probs_buffers=bufs)
         ghc, _ = icepop_bwd(hidden[s0:e0], weight, sub, f, cfg, layout, grad_scale, need_hidden, True, gw,
-                            grad_hidden_dtype=grad_hidden_dtype)
+                            grad_hidden_dtype=grad_hidden_dtype, workspace=ws)
         if gh is not None:
             gh[s0:e0] = ghc
         stats[: _lib.STAT_ERRORS] += f.stats[: _lib.STAT_ERRORS]

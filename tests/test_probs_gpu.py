@@ -335,6 +335,33 @@ def test_fwd_bwd_token_chunks_match_whole_batch(cuda_device, layout):
     assert _rel(-gw2.cpu().numpy(), o["grad_weight"]) < 1e-2
 
 
+def test_caller_owned_probs_buffers_and_workspace(cuda_device):
+    """icepop_fwd(probs_buffers=...) with buffers longer than N and icepop_bwd(workspace=...)
+    (how icepop_fwd_bwd reuses one allocation across token chunks) give the same bits as
+    the self-allocating calls; malformed buffers are rejected before any launch."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd, sp_workspace_bytes
+
+    c = _case(n_seqs=6, seed=93, V=1000)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    n, d, V = H.shape[0], H.shape[1], W.shape[0]
+    cfg = IcePopConfig()
+    f1 = icepop_fwd(H, W, _batch(c, cuda_device), cfg, store_probs=True)
+    gh1, gw1 = icepop_bwd(H, W, _batch(c, cuda_device), f1, cfg)
+    bufs = (torch.full((n + 100, V), 7.0, dtype=torch.bfloat16, device=cuda_device),
+            torch.empty((n + 100, _lib.tile_max_ld(V)), dtype=torch.float32, device=cuda_device))
+    ws = torch.empty(sp_workspace_bytes(n, d, V, len(c["cu"]) - 1) + 512, dtype=torch.uint8, device=cuda_device)
+    f2 = icepop_fwd(H, W, _batch(c, cuda_device), cfg, probs_buffers=bufs)
+    gh2, gw2 = icepop_bwd(H, W, _batch(c, cuda_device), f2, cfg, workspace=ws)
+    assert torch.equal(f1.stats, f2.stats) and torch.equal(f1.kept, f2.kept)
+    assert torch.equal(gh1, gh2) and torch.equal(gw1, gw2)
+    assert torch.all(bufs[0][n:] == 7.0)  # rows past N untouched
+    with pytest.raises(ValueError):
+        icepop_fwd(H, W, _batch(c, cuda_device), cfg, probs_buffers=(bufs[0][:, :-8], bufs[1]))
+    with pytest.raises(ValueError):
+        icepop_fwd(H, W, _batch(c, cuda_device), cfg, probs_buffers=(bufs[0][: n - 1], bufs[1]))
+
+
 @pytest.mark.parametrize("n_tok,d,V,layout", [
     (1, 64, 64, "vd"), (7, 8, 72, "dv"), (63, 24, 136, "vd"), (65, 32, 1000, "dv"), (129, 256, 520, "vd"),
     (300, 40, 2056, "dv"),
