@@ -216,7 +216,7 @@ template <bool A_MN, bool B_MN, int EPI>
 int launch_umma(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
                 const GemmShape& sh, const EpiParams& ep, cudaStream_t st, int cg, bool wide = false) {
   constexpr int BN = epi_dual(EPI) ? 128 : BN_;
-  if constexpr (EPI == EPI_STORE) {
+  if constexpr (EPI == EPI_STORE || EPI == EPI_LSE) {
     if (wide && cg == 2) return launch_umma_cg<BN_WIDE, A_MN, B_MN, EPI, 2>(ta, tb, tb2, tc, sh, ep, st);
   }
   if (cg == 2) return launch_umma_cg<BN, A_MN, B_MN, EPI, 2>(ta, tb, tb2, tc, sh, ep, st);
@@ -273,6 +273,18 @@ bool wide_tiles() {
   return g_wide_tiles == 1;
 }
 
+// K1 (EPI_LSE) on 256 x 512 tiles: one TMEM accumulator released to the MMA warp in halves
+// (umma_gemm.cuh SPLIT). ICEPOP_K1_WIDE=1 selects it (CTA pairs only).
+int g_k1_wide = -1;
+
+bool k1_wide() {
+  if (g_k1_wide < 0) g_k1_wide = env_int("ICEPOP_K1_WIDE", 0) ? 1 : 0;
+  return g_k1_wide == 1 && cta_group() == 2;
+}
+
+// Column tile of K1 (the number of partial (max, sum, q) rows per token is ceil(V / k1_bn())).
+int k1_bn() { return k1_wide() ? BN_WIDE : BN_; }
+
 // Device-side block lists of a block-sparse GEMM (GemmShape::kb_map ...), or none.
 struct Sparse {
   const int32_t* kb_map = nullptr;
@@ -289,7 +301,7 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
   const int cg = cta_group();
   const bool long_k = (K + BK - 1) / BK >= long_k_blocks();
-  const bool wide = epi == EPI_STORE && cg == 2 && long_k && wide_tiles();
+  const bool wide = (epi == EPI_STORE && cg == 2 && long_k && wide_tiles()) || (epi == EPI_LSE && k1_wide());
   const int bn = wide ? BN_WIDE : bn_of(epi);
   if (epi_dual(epi) && !B2) return fail(ICEPOP_EINVAL, "dual-accumulator GEMM needs a second B operand");
   CUtensorMap ta, tb, tb2;
@@ -344,8 +356,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if (a_mn) return fail(ICEPOP_EINVAL, "fused epilogues need a K-major hidden operand");
   switch (epi) {
     case EPI_LSE:
-      return b_mn ? launch_umma<false, true, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg)
-                  : launch_umma<false, false, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg);
+      return b_mn ? launch_umma<false, true, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg, wide)
+                  : launch_umma<false, false, EPI_LSE>(ta, tb, tb2, tc, sh, ep, st, cg, wide);
     case EPI_DZ:
       return b_mn ? launch_umma<false, true, EPI_DZ>(ta, tb, tb2, tc, sh, ep, st, cg)
                   : launch_umma<false, false, EPI_DZ>(ta, tb, tb2, tc, sh, ep, st, cg);
@@ -712,7 +724,7 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
   fill_token_args(a, shape, cfg, batch, adv);
   if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
   a.part = w.part;
-  const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
+  const int bn = ref ? bn_of(EPI_LSE_REF) : k1_bn();
   a.n_parts = (int32_t)((V + bn - 1) / bn);
   a.part_rows = ref ? 6 : 3;
   a.kl_f = ref ? out->kl : nullptr;
@@ -816,7 +828,7 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   ep.ztok = w.ztok;
   const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
   ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
-  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)((V + BN_ - 1) / BN_), w.ztok, N, lse, lp,
+  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)((V + k1_bn() - 1) / k1_bn()), w.ztok, N, lse, lp,
                                                           entropy);
   ICP_CUDA(cudaGetLastError());
   return ICEPOP_OK;

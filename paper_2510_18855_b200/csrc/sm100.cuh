@@ -47,7 +47,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if ((++spins & 1023u) == 0u && globaltimer_ns() - t0 > 20000000000ull) {
-      printf("icepop: mbarrier watchdog (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      printf("icepop: mbarrier watchdog (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x, bar,
+             parity);
       __trap();
     }
   }
@@ -61,7 +62,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, u
   while (!mbar_try_wait(bar, parity)) {
     if (ns) __nanosleep(ns);
     if ((++spins & 255u) == 0u && globaltimer_ns() - t0 > 20000000000ull) {
-      printf("icepop: mbarrier watchdog (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      printf("icepop: mbarrier watchdog (block %d thread %d bar 0x%x parity %u)\n", blockIdx.x, threadIdx.x, bar,
+             parity);
       __trap();
     }
   }
@@ -170,6 +172,45 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
       : "memory");
 }
 
+// Split-phase form: tmem_ld32_issue starts the load, tmem_wait_ld32 waits for every load this
+// thread issued and takes the destination registers as in/out operands, so the compiler keeps
+// them live and cannot read them before the wait. Used to load the next slab while computing
+// on the current one (the caller must not let the registers spill in between: check ptxas).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld32(float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+
+// max of three floats in one instruction (sm_100 three-input max)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits (=1 at bit 46).
 //   K-major  operand: LBO unused (16 B), SBO = 1024 B (8 rows x 128 B swizzle atom).
 //   MN-major operand: LBO = byte stride between 64-element MN blocks,
@@ -207,6 +248,14 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Epilogue -> MMA "accumulator columns free" arrive (local or peer CTA). Relaxed: the TMEM reads
+// it publishes have completed (tcgen05.wait::ld returned; tcgen05.fence::before_thread_sync is
+// issued before it) and no generic memory is handed over, so the release form's GPU-scope
+// MEMBAR + ERRBAR -- which waits for this warp's outstanding global stores, ~8% of K1's
+// epilogue time in an ncu source profile -- is not needed.
+__device__ __forceinline__ void mbar_arrive_tmem_free(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem whose completion is counted on a (possibly peer) barrier.
 __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster,

@@ -187,7 +187,7 @@ __device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& 
 // 512-wide tile each CTA stages a contiguous 256-row slab of B; MMA h (columns [256h, 256h+256))
 // reads rows [128h, 128h+128) of both slabs, so its column j is B row (j / 128) * 256 + 128h + j % 128.
 template <int BN, int CG>
-__device__ __forceinline__ int tile_col(int n0, int tc) {
+__host__ __device__ constexpr int tile_col(int n0, int tc) {
   if (CG == 2 && BN > 256) {
     const int h = tc >> 8, j = tc & 255;
     return n0 + (j >> 7) * 256 + h * 128 + (j & 127);
@@ -319,21 +319,75 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
   ebuf ^= 1;
 }
 
+// One 64-column slab of K1's epilogue (FULL: all 64 columns < N, else the first `valid`):
+// slab maximum mx (log2 units), reference R, partial sums (s, q) against mx as two float2 lanes,
+// and the packed bf16 q = 2^(u - R).
+template <bool FULL>
+__device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_log2, float& mx, float& ref,
+                                         float2& sum2, float2& q2, uint32_t (&pk)[32]) {
+  if (!FULL) {
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = j < valid ? v[j] : -1e30f;
+  }
+  float t[22];
+#pragma unroll
+  for (int i = 0; i < 21; ++i) t[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  t[21] = v[63];
+  float u[8];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) u[i] = fmax3(t[3 * i], t[3 * i + 1], t[3 * i + 2]);
+  u[7] = t[21];
+  mx = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7])) *
+       scale_log2;  // scale > 0: max commutes with it
+  // stored q = 2^(u - R): R = 0 while the slab maximum is within [-PROBS_REF_RANGE, +..] (one
+  // scale per row then turns q into probabilities), else R = the slab maximum (exception)
+  ref = fabsf(mx) <= PROBS_REF_RANGE ? 0.f : mx;
+  const float qs = exp2f(mx - ref);
+  const float2 qs2 = make_float2(qs, qs);
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float2 nmx = make_float2(-mx, -mx);
+  float2 sa = make_float2(0.f, 0.f), sb = sa, qa = sa, qb = sa;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    // masked columns: d ~ -1e30 -> e = 0 and e * d = -0
+    const float2 d = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nmx);
+    const float2 e = make_float2(fast_exp2(d.x), fast_exp2(d.y));
+    if (j & 1) {
+      sb = __fadd2_rn(sb, e);
+      qb = __ffma2_rn(e, d, qb);
+    } else {
+      sa = __fadd2_rn(sa, e);
+      qa = __ffma2_rn(e, d, qa);
+    }
+    const float2 p = __fmul2_rn(e, qs2);
+    pk[j] = pack_bf16x2(p.x, p.y);
+  }
+  sum2 = __fadd2_rn(sa, sb);
+  q2 = __fadd2_rn(qa, qb);
+}
+
 // K1 epilogue: log-sum-exp statistics of this tile's BN columns for one row, in log2 units,
 //   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
 // so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2).
 // One TMEM pass in 64-column slabs: each slab's (max, sum, q) is taken against the slab's own
 // maximum and merged online into the tile's. In stored-probabilities mode (ep.probs) the slab
 // also emits q[m, v] = 2^(u_v - R) as bf16 (TMA stores, clipped to M rows / N columns) and
-// tile_max[m, 4 n_blk + c] = R, the slab's reference: 0 while its maximum is within
+// tile_max[m, v / 64] = R, the slab's reference: 0 while its maximum is within
 // +-PROBS_REF_RANGE, else that maximum. The backward needs no logit recompute: for rows whose
 // references are all 0 the probabilities are q 2^(-lse2), one scale per row. The statistics are
 // the same bits in both modes.
-template <int BN>
+// The slab loop is software-pipelined (slab c+1's TMEM load is in flight while slab c is
+// computed), the slab maximum is a tree of three-input maxima and the sums run on packed
+// f32x2 FMA/FADD with two accumulators each, so one warp per TMEM lane quarter is bound by
+// the exp2 throughput rather than by dependency chains. On a 512-wide tile with one TMEM
+// accumulator (K1 wide), `half_bar` is arrived on once TMEM columns [0, 256) are read, so the
+// MMA warp can start the next tile's first half while the second half is still being read.
+template <int BN, int CG>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
                                         uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
-                                        int quarter, uint32_t taddr) {
-  static_assert(BN == 4 * 64, "tile_max holds four 64-column slab references per tile");
+                                        int quarter, uint32_t taddr, uint32_t half_bar) {
+  static_assert(BN == 256 || BN == 512, "64-column slabs, four or eight per tile");
+  constexpr int NS = BN / 64;
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
@@ -341,61 +395,72 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
-  float sm0 = 0.f, sm1 = 0.f, sm2 = 0.f, sm3 = 0.f;  // slab references (registers, not a local array)
-#pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    float v[64];
-    tmem_ld32(taddr + c * 64, *reinterpret_cast<float(*)[32]>(v));
-    tmem_ld32(taddr + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-    const int col0 = n0 + c * 64;
-    if (col0 >= sh.N) continue;  // warp-uniform
-    const int rel = y - col0;
-    if ((unsigned)rel < 64u) {  // the sampled token's logit lives in this slab
-      float zt = 0.f;
+  float refs[NS];  // slab references (the loop is unrolled: registers)
+  float va[64], vb[64];
+  tmem_ld32_issue(taddr, *reinterpret_cast<float(*)[32]>(va));
+  tmem_ld32_issue(taddr + 32, *reinterpret_cast<float(*)[32]>(va + 32));
 #pragma unroll
-      for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
-      if (row_ok) ep.ztok[m] = zt * ep.inv_t;
+  for (int c = 0; c < NS; ++c) {
+    float* v = (c & 1) ? vb : va;
+    tmem_wait_ld32(*reinterpret_cast<float(*)[32]>(v));
+    tmem_wait_ld32(*reinterpret_cast<float(*)[32]>(v + 32));
+    if (c + 1 < NS) {  // warp-collective, outside any per-thread branch
+      float* nv = (c & 1) ? va : vb;
+      tmem_ld32_issue(taddr + (c + 1) * 64, *reinterpret_cast<float(*)[32]>(nv));
+      tmem_ld32_issue(taddr + (c + 1) * 64 + 32, *reinterpret_cast<float(*)[32]>(nv + 32));
     }
-    const bool full = col0 + 64 <= sh.N;
-    float mx = -1e30f;
+    refs[c] = 0.f;
+    const int col0 = tile_col<BN, CG>(n0, c * 64);
+    if (col0 < sh.N) {  // warp-uniform
+      const int rel = y - col0;
+      if (__any_sync(0xffffffffu, (unsigned)rel < 64u)) {  // some row's sampled token is in this slab (rare)
+        float zt = 0.f;
 #pragma unroll
-    for (int j = 0; j < 64; ++j) mx = fmaxf(mx, (full || col0 + j < sh.N) ? v[j] : -1e30f);
-    mx *= ep.scale_log2;  // scale > 0: max commutes with it
-    // stored q = 2^(u - R): R = 0 while the slab maximum is within [-PROBS_REF_RANGE, +..] (one
-    // scale per row then turns q into probabilities), else R = the slab maximum (exception)
-    const float ref = fabsf(mx) <= PROBS_REF_RANGE ? 0.f : mx;
-    const float qs = exp2f(mx - ref);
-    float s = 0.f, q = 0.f;
-    uint32_t pk[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const bool ok0 = full || col0 + 2 * j < sh.N, ok1 = full || col0 + 2 * j + 1 < sh.N;
-      const float d0 = fmaf(v[2 * j], ep.scale_log2, -mx), d1 = fmaf(v[2 * j + 1], ep.scale_log2, -mx);
-      const float e0 = ok0 ? fast_exp2(d0) : 0.f, e1 = ok1 ? fast_exp2(d1) : 0.f;
-      s += e0 + e1;
-      q = fmaf(e0, ok0 ? d0 : 0.f, fmaf(e1, ok1 ? d1 : 0.f, q));
-      pk[j] = pack_bf16x2(e0 * qs, e1 * qs);
+        for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
+        if (row_ok && (unsigned)rel < 64u) ep.ztok[m] = zt * ep.inv_t;
+      }
+      float mx, ref;
+      float2 sum2, q2;
+      uint32_t pk[32];
+      // the ragged last slab (columns past N take no part) is a separate, warp-uniform path so
+      // the common one carries no per-column predicates
+      if (col0 + 64 <= sh.N) lse_slab<true>(*reinterpret_cast<float(*)[64]>(v), 64, ep.scale_log2, mx, ref, sum2, q2, pk);
+      else lse_slab<false>(*reinterpret_cast<float(*)[64]>(v), sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk);
+      const float s = sum2.x + sum2.y, q = q2.x + q2.y;
+      if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
+      refs[c] = ref;
+      // merge the slab into the tile's running (max, sum, q)
+      const float nm = fmaxf(run_m, mx);
+      const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);
+      run_q = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(mx - nm, s, q));
+      run_s = fmaf(a, run_s, b * s);
+      run_m = nm;
     }
-    if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
-    sm0 = c == 0 ? ref : sm0;
-    sm1 = c == 1 ? ref : sm1;
-    sm2 = c == 2 ? ref : sm2;
-    sm3 = c == 3 ? ref : sm3;
-    // merge the slab into the tile's running (max, sum, q)
-    const float nm = fmaxf(run_m, mx);
-    const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);
-    run_q = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(mx - nm, s, q));
-    run_s = fmaf(a, run_s, b * s);
-    run_m = nm;
+    if (half_bar != 0u && c == NS / 2 - 1) {  // TMEM columns [0, BN/2) are read
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_tmem_free(half_bar);
+      }
+    }
+    __syncwarp();  // the next slab's tcgen05.wait/ld are warp-collective (.sync.aligned)
   }
   if (row_ok) {
     float* p = ep.part + (int64_t)n_blk * 3 * sh.M + m;
     p[0] = run_m;
     p[sh.M] = run_s;
     p[2 * (int64_t)sh.M] = run_q;
-    if (store)
-      *reinterpret_cast<float4*>(ep.tile_max + (int64_t)m * ep.tm_ld + 4 * n_blk) =
-          make_float4(sm0, sm1, sm2, sm3);
+    if (store) {
+      // references in output-column order (TMEM slab c holds output slab tile_col(0, 64 c) / 64)
+      float r[NS];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) r[tile_col<BN, CG>(0, c * 64) / 64] = refs[c];
+      float* tm = ep.tile_max + (int64_t)m * ep.tm_ld + n0 / 64;
+      *reinterpret_cast<float4*>(tm) = make_float4(r[0], r[1], r[2], r[3]);
+      if constexpr (NS == 8) {
+        if (n0 / 64 + 8 <= ep.tm_ld) *reinterpret_cast<float4*>(tm + 4) = make_float4(r[4], r[5], r[6], r[7]);
+      }
+    }
   }
 }
 
@@ -611,6 +676,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr bool DUAL = epi_dual(EPI);
   constexpr bool STAGING = epi_staging(EPI);
   using Cfg = GemmCfg<BN, CG, DUAL, STAGING>;
+  // K1 on 512-wide tiles: one accumulator, released to the MMA warp in two halves
+  constexpr bool SPLIT = EPI == EPI_LSE && Cfg::ACC_BUFS == 1 && Cfg::NSUB == 2;
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
   resolve_sparsity(sh);
@@ -632,6 +699,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * STAGES);
   const uint32_t tempty0 = smem_u32(bars + 2 * STAGES + 2);
   const uint32_t rfull0 = smem_u32(bars + 2 * STAGES + 4);
+  const uint32_t thalf0 = tempty0 + 8;  // SPLIT: tempty[1] (unused with one accumulator)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -813,7 +881,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int j = 0; cur >= 0; ++j) {
-        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        // SPLIT: wait only for the epilogue to have read TMEM columns [0, BN/2) (thalf)
+        mbar_wait(SPLIT ? thalf0 : tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         int nxt2 = -1;
         if (dynamic) {
@@ -823,12 +892,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
         }
         const uint32_t d_tmem = tmem_base + acc * BN * Cfg::NACC;
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
-          mbar_wait(full0 + 8 * stage, phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
-          const uint32_t b2_base = smem_u32(sB2 + stage * Cfg::B_BYTES);
+        // MMAs of k-block kb on smem stage st for sub-tiles [h0, h1)
+        auto issue = [&](int kb, int st, int h0, int h1) {
+          const uint32_t a_base = smem_u32(sA + st * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + st * Cfg::B_BYTES);
+          const uint32_t b2_base = smem_u32(sB2 + st * Cfg::B_BYTES);
+          (void)b2_base;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
@@ -838,6 +907,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
 #pragma unroll
             for (int h = 0; h < Cfg::NSUB; ++h) {
+              if (h < h0 || h >= h1) continue;
               // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
               const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
               if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
@@ -850,6 +920,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               else umma_bf16(d_tmem + BN, ad, bd2, idesc, accum);
             }
           }
+        };
+        // SPLIT: the first-half MMAs of the first `pre` k-blocks run while the epilogue still
+        // reads the previous tile's second half; their stages stay full until the second-half
+        // MMAs (issued once the whole accumulator is free) have read them too.
+        const int pre = SPLIT ? min(STAGES, sh.k_blocks) : 0;
+        if (SPLIT) {
+          int st2 = stage;
+          uint32_t ph2 = phase;
+          for (int kb = 0; kb < pre; ++kb) {
+            mbar_wait(full0 + 8 * st2, ph2);
+            tc_fence_after();
+            issue(kb, st2, 0, 1);
+            if (++st2 == STAGES) { st2 = 0; ph2 ^= 1; }
+          }
+          mbar_wait(tempty0, acc_phase ^ 1);
+          tc_fence_after();
+        }
+        for (int kb = 0; kb < sh.k_blocks; ++kb) {
+          if (kb >= pre) {
+            mbar_wait(full0 + 8 * stage, phase);
+            tc_fence_after();
+          }
+          issue(kb, stage, kb < pre ? 1 : 0, Cfg::NSUB);
           // frees the smem slot (in both CTAs) when these MMAs finish
           if (CG == 2) umma_commit_cg2(empty0 + 8 * stage, 0x3); else umma_commit(empty0 + 8 * stage);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -884,8 +977,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
       if constexpr (EPI == EPI_LSE)
-        epi_lse<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
-                    quarter, taddr);
+        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row,
+                        lane, quarter, taddr, SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u);
       if constexpr (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
           epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
@@ -898,8 +991,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(mapa_shared(tempty0 + 8 * acc, 0));
-        else mbar_arrive(tempty0 + 8 * acc);
+        mbar_arrive_tmem_free(CG == 2 ? mapa_shared(tempty0 + 8 * acc, 0) : tempty0 + 8 * acc);
       }
       if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
