@@ -198,7 +198,7 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)(units * CG));
-  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.blockDim = dim3(gemm_threads(EPI));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -282,8 +282,10 @@ bool k1_wide() {
   return g_k1_wide == 1 && cta_group() == 2;
 }
 
-// Column tile of K1 (the number of partial (max, sum, q) rows per token is ceil(V / k1_bn())).
+// Column tile of K1.
 int k1_bn() { return k1_wide() ? BN_WIDE : BN_; }
+// Partial (max, sum, q) triples per token that K1 writes: one per tile half (umma_gemm.cuh epi_lse).
+int64_t k1_parts(int64_t V) { return 2 * ((V + k1_bn() - 1) / k1_bn()); }
 
 // Device-side block lists of a block-sparse GEMM (GemmShape::kb_map ...), or none.
 struct Sparse {
@@ -517,9 +519,9 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   memset(&w, 0, sizeof(w));
   const int64_t n = std::max<int64_t>(s->n_tokens, 1);
   if (!bwd) {  // the backward reads none of the forward's scratch
-    const int bn = ref ? bn_of(EPI_LSE_REF) : BN_;
-    const int64_t n_tiles = (s->vocab + bn - 1) / bn;
-    w.part = c.take<float>((size_t)n_tiles * (ref ? 6 : 3) * n);
+    // K1: two partials per 256-column tile (the most any K1 tile width writes); KL: one per 128
+    const int64_t n_parts = ref ? (s->vocab + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : 2 * ((s->vocab + BN_ - 1) / BN_);
+    w.part = c.take<float>((size_t)n_parts * (ref ? 6 : 3) * n);
     w.ztok = c.take<float>((size_t)n);
     w.adv = c.take<double>((size_t)s->n_seqs);
     w.block_stats = c.take<double>((size_t)num_sms() * 8 * ICEPOP_NSTATS);
@@ -724,8 +726,7 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
   fill_token_args(a, shape, cfg, batch, adv);
   if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
   a.part = w.part;
-  const int bn = ref ? bn_of(EPI_LSE_REF) : k1_bn();
-  a.n_parts = (int32_t)((V + bn - 1) / bn);
+  a.n_parts = (int32_t)(ref ? (V + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : k1_parts(V));
   a.part_rows = ref ? 6 : 3;
   a.kl_f = ref ? out->kl : nullptr;
   a.lse_ref_f = ref ? out->lse_ref : nullptr;
@@ -828,7 +829,7 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   ep.ztok = w.ztok;
   const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
   ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
-  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)((V + k1_bn() - 1) / k1_bn()), w.ztok, N, lse, lp,
+  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)k1_parts(V), w.ztok, N, lse, lp,
                                                           entropy);
   ICP_CUDA(cudaGetLastError());
   return ICEPOP_OK;

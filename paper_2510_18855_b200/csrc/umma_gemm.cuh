@@ -24,7 +24,13 @@ namespace icp {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int GEMM_THREADS = 192;
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (+ tile scheduler), 2.. = epilogue. K1 (EPI_LSE)
+// runs two epilogue warps per TMEM lane quarter, each on half of the tile's columns: its
+// softmax epilogue is exp2-throughput and latency bound, and a second warp per SM sub-partition
+// roughly halves its time (it must hide behind -- or, on 512-wide tiles, partly expose -- the
+// next tile's MMAs). The other epilogues use one warp per quarter.
+__host__ __device__ constexpr int epi_warps(int epi) { return epi == 1 /*EPI_LSE*/ ? 8 : 4; }
+__host__ __device__ constexpr int gemm_threads(int epi) { return 64 + 32 * epi_warps(epi); }
 constexpr float LOG2E_F = 1.4426950408889634f;
 // Stored probabilities: slabs whose maximum (log2 units) lies within +-PROBS_REF_RANGE are
 // stored as 2^u (reference 0), so Q.W and Q^T.H' stay finite (|q| <= 2^60) in fp32.
@@ -165,9 +171,10 @@ struct GemmCfg {
   static constexpr int B_SUB_BYTES = (N_MMA / CG) * 128;  // K-major: rows x 128 B; MN-major: boxes x 8 KB
   static constexpr int TILE_M = BM * CG;
   static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
-  // EPI_DZ TMA-store staging: 4 epilogue warps x 2 buffers x (32 rows x 128 B, SWIZZLE_128B)
+  // TMA-store staging (32 rows x 128 B, SWIZZLE_128B per buffer): EPI_DZ 4 epilogue warps x 2
+  // buffers, EPI_LSE 8 warps x 1 buffer
   static constexpr int EPI_BUF_BYTES = 32 * 128;
-  static constexpr int EPI_STAGE_BYTES = EPI_STAGING ? 4 * 2 * EPI_BUF_BYTES : 0;
+  static constexpr int EPI_STAGE_BYTES = EPI_STAGING ? 8 * EPI_BUF_BYTES : 0;
   static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 256;
 };
 
@@ -301,10 +308,16 @@ __device__ __forceinline__ void epi_store(const GemmShape& sh, const EpiParams& 
 // Stage one warp's 32 rows x 64 columns of packed bf16 (pk[0..31] = this lane's row) in a
 // SWIZZLE_128B smem buffer and store it with one TMA bulk tensor store issued by lane 0. Two
 // buffers per warp alternate; the store that last read a buffer must be done reading it.
+// With NBUF = 1 the warp waits for its previous store to finish reading the buffer (the other
+// warp on the sub-partition keeps it busy meanwhile).
+template <int NBUF = 2>
 __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t* stage2, int& ebuf,
                                                  const uint32_t (&pk)[32], int col0, int row0, int lane) {
-  uint8_t* buf = stage2 + ebuf * (32 * 128);
-  if (lane == 0) bulk_wait_read<1>();
+  uint8_t* buf = stage2 + (NBUF == 2 ? ebuf : 0) * (32 * 128);
+  if (lane == 0) {
+    if (NBUF == 2) bulk_wait_read<1>();
+    else bulk_wait_read<0>();
+  }
   __syncwarp();
   // row `lane` of the slab: 8 x 16-byte chunks, chunk k at position k ^ (lane & 7) (SWIZZLE_128B)
   const uint32_t rowp = smem_u32(buf) + lane * 128;
@@ -337,7 +350,7 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
 #pragma unroll
   for (int i = 0; i < 7; ++i) u[i] = fmax3(t[3 * i], t[3 * i + 1], t[3 * i + 2]);
   u[7] = t[21];
-  mx = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7])) *
+  mx = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmax3(u[6], u[7], u[7])) *
        scale_log2;  // scale > 0: max commutes with it
   // stored q = 2^(u - R): R = 0 while the slab maximum is within [-PROBS_REF_RANGE, +..] (one
   // scale per row then turns q into probabilities), else R = the slab maximum (exception)
@@ -351,7 +364,8 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
   for (int j = 0; j < 32; ++j) {
     // masked columns: d ~ -1e30 -> e = 0 and e * d = -0
     const float2 d = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nmx);
-    const float2 e = make_float2(fast_exp2(d.x), fast_exp2(d.y));
+    // every third pair of a full slab on the FMA pipe (masked columns need the MUFU's exact 0)
+    const float2 e = (FULL && j % 3 == 2) ? exp2_fma2(d) : make_float2(fast_exp2(d.x), fast_exp2(d.y));
     if (j & 1) {
       sb = __fadd2_rn(sb, e);
       qb = __ffma2_rn(e, d, qb);
@@ -366,28 +380,27 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
   q2 = __fadd2_rn(qa, qb);
 }
 
-// K1 epilogue: log-sum-exp statistics of this tile's BN columns for one row, in log2 units,
+// K1 epilogue: log-sum-exp statistics of half of this tile's BN columns (`half`: TMEM columns
+// [half BN/2, (half+1) BN/2)) for one row, in log2 units,
 //   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
-// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2).
-// One TMEM pass in 64-column slabs: each slab's (max, sum, q) is taken against the slab's own
-// maximum and merged online into the tile's. In stored-probabilities mode (ep.probs) the slab
-// also emits q[m, v] = 2^(u_v - R) as bf16 (TMA stores, clipped to M rows / N columns) and
-// tile_max[m, v / 64] = R, the slab's reference: 0 while its maximum is within
-// +-PROBS_REF_RANGE, else that maximum. The backward needs no logit recompute: for rows whose
-// references are all 0 the probabilities are q 2^(-lse2), one scale per row. The statistics are
-// the same bits in both modes.
-// The slab loop is software-pipelined (slab c+1's TMEM load is in flight while slab c is
-// computed), the slab maximum is a tree of three-input maxima and the sums run on packed
-// f32x2 FMA/FADD with two accumulators each, so one warp per TMEM lane quarter is bound by
-// the exp2 throughput rather than by dependency chains. On a 512-wide tile with one TMEM
-// accumulator (K1 wide), `half_bar` is arrived on once TMEM columns [0, 256) are read, so the
-// MMA warp can start the next tile's first half while the second half is still being read.
+// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2); the
+// half's triple is partial 2 n_blk + half. One TMEM pass in 64-column slabs: each slab's
+// (max, sum, q) is taken against the slab's own maximum and merged online. In
+// stored-probabilities mode (ep.probs) the slab also emits q[m, v] = 2^(u_v - R) as bf16 (TMA
+// stores, clipped to M rows / N columns) and tile_max[m, v / 64] = R, the slab's reference: 0
+// while its maximum is within +-PROBS_REF_RANGE, else that maximum. The backward needs no logit
+// recompute: for rows whose references are all 0 the probabilities are q 2^(-lse2), one scale
+// per row. The statistics are the same bits in both modes.
+// 512-wide tiles (one accumulator, SPLIT): the MMA warp may start the next tile's first-half
+// MMAs once TMEM columns [0, 256) are read, so both warps of a quarter first read two slabs of
+// that half each (then arrive on `half_bar`) and only then two of the second half: `half` then
+// selects slabs {2 half, 2 half + 1, 4 + 2 half, 5 + 2 half}, output slabs 4 half .. 4 half + 3.
 template <int BN, int CG>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
-                                        uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
+                                        uint8_t* stage1, int m0, int n0, int n_blk, int half, int row, int lane,
                                         int quarter, uint32_t taddr, uint32_t half_bar) {
   static_assert(BN == 256 || BN == 512, "64-column slabs, four or eight per tile");
-  constexpr int NS = BN / 64;
+  constexpr int NH = BN / 128;  // slabs per warp
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
@@ -395,21 +408,22 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
-  float refs[NS];  // slab references (the loop is unrolled: registers)
-  float va[64], vb[64];
-  tmem_ld32_issue(taddr, *reinterpret_cast<float(*)[32]>(va));
-  tmem_ld32_issue(taddr + 32, *reinterpret_cast<float(*)[32]>(va + 32));
+  float refs[NH];
+  int ebuf = 0;
 #pragma unroll
-  for (int c = 0; c < NS; ++c) {
-    float* v = (c & 1) ? vb : va;
-    tmem_wait_ld32(*reinterpret_cast<float(*)[32]>(v));
-    tmem_wait_ld32(*reinterpret_cast<float(*)[32]>(v + 32));
-    if (c + 1 < NS) {  // warp-collective, outside any per-thread branch
-      float* nv = (c & 1) ? va : vb;
-      tmem_ld32_issue(taddr + (c + 1) * 64, *reinterpret_cast<float(*)[32]>(nv));
-      tmem_ld32_issue(taddr + (c + 1) * 64 + 32, *reinterpret_cast<float(*)[32]>(nv + 32));
+  for (int i = 0; i < NH; ++i) {
+    const int c = NH == 4 ? (i < 2 ? 2 * half + i : 2 + 2 * half + i) : half * NH + i;  // TMEM slab
+    if (NH == 4 && i == 2 && half_bar != 0u) {  // TMEM columns [0, BN/2): read by both warps
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_tmem_free(half_bar);
     }
-    refs[c] = 0.f;
+    // (a software-pipelined variant loading slab i+1 during slab i measured no faster with two
+    // warps per quarter, and its 128 live registers exceed the 168 available at 320 threads)
+    float v[64];
+    tmem_ld32(taddr + c * 64, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld32(taddr + c * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+    refs[i] = 0.f;
     const int col0 = tile_col<BN, CG>(n0, c * 64);
     if (col0 < sh.N) {  // warp-uniform
       const int rel = y - col0;
@@ -424,41 +438,33 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
       uint32_t pk[32];
       // the ragged last slab (columns past N take no part) is a separate, warp-uniform path so
       // the common one carries no per-column predicates
-      if (col0 + 64 <= sh.N) lse_slab<true>(*reinterpret_cast<float(*)[64]>(v), 64, ep.scale_log2, mx, ref, sum2, q2, pk);
-      else lse_slab<false>(*reinterpret_cast<float(*)[64]>(v), sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk);
+      if (col0 + 64 <= sh.N) lse_slab<true>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk);
+      else lse_slab<false>(v, sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk);
+      if (store && warp_rows) stage_store_slab<1>(tmC, stage1, ebuf, pk, col0, row0, lane);
       const float s = sum2.x + sum2.y, q = q2.x + q2.y;
-      if (store && warp_rows) stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
-      refs[c] = ref;
-      // merge the slab into the tile's running (max, sum, q)
+      refs[i] = ref;
+      // merge the slab into the warp's running (max, sum, q)
       const float nm = fmaxf(run_m, mx);
       const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);
       run_q = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(mx - nm, s, q));
       run_s = fmaf(a, run_s, b * s);
       run_m = nm;
     }
-    if (half_bar != 0u && c == NS / 2 - 1) {  // TMEM columns [0, BN/2) are read
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_tmem_free(half_bar);
-      }
-    }
-    __syncwarp();  // the next slab's tcgen05.wait/ld are warp-collective (.sync.aligned)
+    __syncwarp();  // the next slab's tcgen05.ld is warp-collective (.sync.aligned)
   }
   if (row_ok) {
-    float* p = ep.part + (int64_t)n_blk * 3 * sh.M + m;
+    float* p = ep.part + (int64_t)(2 * n_blk + half) * 3 * sh.M + m;
     p[0] = run_m;
     p[sh.M] = run_s;
     p[2 * (int64_t)sh.M] = run_q;
     if (store) {
-      // references in output-column order (TMEM slab c holds output slab tile_col(0, 64 c) / 64)
-      float r[NS];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) r[tile_col<BN, CG>(0, c * 64) / 64] = refs[c];
+      // references in output-column order: TMEM slabs c, c+1 (c even) hold output slabs k, k+1
       float* tm = ep.tile_max + (int64_t)m * ep.tm_ld + n0 / 64;
-      *reinterpret_cast<float4*>(tm) = make_float4(r[0], r[1], r[2], r[3]);
-      if constexpr (NS == 8) {
-        if (n0 / 64 + 8 <= ep.tm_ld) *reinterpret_cast<float4*>(tm + 4) = make_float4(r[4], r[5], r[6], r[7]);
+#pragma unroll
+      for (int i = 0; i < NH; i += 2) {
+        const int c = NH == 4 ? (i < 2 ? 2 * half + i : 2 + 2 * half + i) : half * NH + i;
+        const int k = tile_col<BN, CG>(0, c * 64) / 64;
+        if (n0 / 64 + k + 2 <= ep.tm_ld) *reinterpret_cast<float2*>(tm + k) = make_float2(refs[i], refs[i + 1]);
       }
     }
   }
@@ -669,7 +675,7 @@ __device__ __forceinline__ void epi_dz_ref(const GemmShape& sh, const EpiParams&
 
 // ------------------------------------------------------------------ mainloop
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(gemm_threads(EPI), 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
                      const GemmShape sh_in, const EpiParams ep) {
@@ -678,6 +684,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using Cfg = GemmCfg<BN, CG, DUAL, STAGING>;
   // K1 on 512-wide tiles: one accumulator, released to the MMA warp in two halves
   constexpr bool SPLIT = EPI == EPI_LSE && Cfg::ACC_BUFS == 1 && Cfg::NSUB == 2;
+  constexpr int EW = epi_warps(EPI);
   GemmShape sh = sh_in;
   resolve_extent(sh, Cfg::TILE_M, BN);
   resolve_sparsity(sh);
@@ -727,7 +734,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull0 + 8 * s, 1);
-      mbar_init(tempty0 + 8 * s, 4 * CG);  // one arrive per epilogue warp of the pair
+      // one arrive per epilogue warp of the pair (SPLIT's thalf, s = 1, likewise)
+      mbar_init(tempty0 + 8 * s, EW * CG);
     }
     for (int s = 0; s < Cfg::RING; ++s) mbar_init(rfull0 + 8 * s, 1);
     fence_mbar_init();
@@ -959,9 +967,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps: this CTA's 128 rows of the pair tile
+    // ---------------- epilogue warps: this CTA's 128 rows of the pair tile (EW = 8: warps
+    // 2-5 take the first half of the columns, 6-9 the second; a warp reads TMEM lanes of its
+    // quarter warp % 4)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
+    const int ehalf = EW == 8 ? (warp - 2) >> 2 : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int ebuf = 0;  // STAGING: which of this warp's two staging buffers is next
@@ -977,7 +988,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
       if constexpr (EPI == EPI_LSE)
-        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row,
+        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN, n_blk, ehalf, row,
                         lane, quarter, taddr, SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u);
       if constexpr (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
