@@ -338,8 +338,6 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.epi_sleep_ns = (uint32_t)sleep_ns;
   static const int dz_tma = env_int("ICEPOP_DZ_TMA_STORE", 1);
   sh.dz_tma_store = dz_tma;
-  static const int a_coll = env_int("ICEPOP_A_COLLECTOR", 1);
-  sh.a_collector = a_coll;
   // short K: dynamic claim order keeps in-flight tiles contiguous (L2 reuse across tiles);
   // long K: static waves with a grid barrier keep in-flight tiles aligned in k.
   sh.wave_counter = nullptr;

@@ -308,29 +308,6 @@ __device__ __forceinline__ void umma_bf16_cg2(uint32_t d_tmem, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// A-operand collector variants: COLL = 1 reads A from smem and keeps it in the collector
-// buffer (.collector::a::fill), COLL = 2 takes A from the collector and releases it
-// (::lastuse; same A descriptor as the fill). Two MMAs sharing one A tile -- the two N = 256
-// halves of a 512-wide tile -- then read A from shared memory once instead of twice.
-template <int COLL>
-__device__ __forceinline__ void umma_bf16_cg2_coll(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                                   uint32_t accumulate) {
-  static_assert(COLL == 1 || COLL == 2, "fill or lastuse");
-  if constexpr (COLL == 1)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  else
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
 // Arrive once on the barrier at the same smem offset in every CTA of `mask`.
 __device__ __forceinline__ void umma_commit_cg2(uint32_t bar, uint16_t mask) {
   asm volatile(

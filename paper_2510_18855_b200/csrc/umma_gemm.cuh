@@ -64,7 +64,6 @@ struct GemmShape {
   int32_t keep_empty;  // K extent 0: still run the tiles (the epilogue stores zeros + acc_src)
   uint32_t epi_sleep_ns;  // backoff of the epilogue warps' wait for a finished accumulator
   int32_t dz_tma_store;   // EPI_DZ: stage dZ tiles in smem and write them with TMA (else direct stores)
-  int32_t a_collector;    // 512-wide tiles: the two N = 256 MMAs of a k-step share A via the collector
 };
 
 // Resolve a device-side extent into the shape every role of the kernel uses.
@@ -914,19 +913,13 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
                                      : sdesc_sw128(b_base + kk * 32, 16, 1024);
             const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-            if (CG == 2 && Cfg::NSUB == 2 && sh.a_collector && h0 == 0 && h1 == 2) {
-              // both halves of a 512-wide tile: A read from smem once (collector fill / lastuse)
-              umma_bf16_cg2_coll<1>(d_tmem, ad, bd, idesc, accum);
-              umma_bf16_cg2_coll<2>(d_tmem + Cfg::N_MMA, ad, bd + (uint64_t)(Cfg::B_SUB_BYTES >> 4), idesc, accum);
-            } else {
 #pragma unroll
-              for (int h = 0; h < Cfg::NSUB; ++h) {
-                if (h < h0 || h >= h1) continue;
-                // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
-                const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
-                if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
-                else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
-              }
+            for (int h = 0; h < Cfg::NSUB; ++h) {
+              if (h < h0 || h >= h1) continue;
+              // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
+              const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
+              if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
+              else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
             }
             if (DUAL) {
               const uint64_t bd2 = B_MN ? sdesc_sw128(b2_base + kk * 2048, BK * 128, 1024)
