@@ -608,12 +608,15 @@ def sample_tokens(cfg, W64, target_s: float) -> int:
     per-token part. Fit both from two timed sizes so the sample is large enough that the
     measured throughput approaches the per-token rate (a small sample would understate the
     CPU and overstate the GPU's speed-up)."""
-    n1, n2 = 16, 128
+    n1, n2 = 32, 256
+    time_oracle(cfg, 16, W64, seed=997)  # warm-up: first-touch of the fp64 buffers, BLAS threads
     t1, _ = time_oracle(cfg, n1, W64, seed=998)
     t2, _ = time_oracle(cfg, n2, W64, seed=999)
-    b = max((t2 - t1) / (n2 - n1), 1e-6)
+    # slope floor 1 ms/token (measured 5-7 ms on the pool's hosts): a noisy fit cannot blow the
+    # sample up past ~target_s / 1 ms tokens
+    b = max((t2 - t1) / (n2 - n1), 1e-3)
     a = max(t1 - b * n1, 0.0)
-    n = int(max(n2, min(16384, (target_s - a) / b)))
+    n = int(max(n2, min(8192, (target_s - a) / b)))
     return n + n % 2
 
 
