@@ -327,6 +327,13 @@ int icepop_set_cta_group(int32_t cta_group);
  * ICEPOP_WIDE_TILES environment variable sets the initial value. */
 int icepop_set_wide_tiles(int32_t enable);
 
+/* Tile shape of K1 (the forward GEMM with the softmax epilogue) on CTA pairs: 0 (default) =
+ * 256 x 256 with a double-buffered TMEM accumulator, 1 = 256 x 512 with one accumulator whose
+ * halves are released separately (a quarter fewer operand bytes; measured equal on B200).
+ * The stored probabilities and slab references are the same bits either way; the statistics
+ * differ only by the summation grouping. Process-wide; ICEPOP_K1_WIDE sets the initial value. */
+int icepop_set_k1_wide(int32_t enable);
+
 /* Backward row skipping: rows whose gradient coefficient is exactly zero (popped tokens,
  * clip-inactive tokens, zero-advantage sequences; objective.py:250) contribute nothing to
  * dW and get dHidden = 0, so icepop_bwd_bf16 compacts the active rows on the device and

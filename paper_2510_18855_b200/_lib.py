@@ -180,6 +180,7 @@ SIGNATURES: dict[str, tuple] = {
     "icepop_gemm_bf16": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _c_p]),
     "icepop_set_cta_group": (ctypes.c_int, [_i32]),
     "icepop_set_wide_tiles": (ctypes.c_int, [_i32]),
+    "icepop_set_k1_wide": (ctypes.c_int, [_i32]),
     "icepop_set_skip_inactive": (ctypes.c_int, [_i32]),
 }
 

@@ -274,7 +274,7 @@ bool wide_tiles() {
 }
 
 // K1 (EPI_LSE) on 256 x 512 tiles: one TMEM accumulator released to the MMA warp in halves
-// (umma_gemm.cuh SPLIT). ICEPOP_K1_WIDE=1 selects it (CTA pairs only).
+// (umma_gemm.cuh SPLIT). ICEPOP_K1_WIDE=1 / icepop_set_k1_wide(1) select it (CTA pairs only).
 int g_k1_wide = -1;
 
 bool k1_wide() {
@@ -1354,6 +1354,11 @@ int icepop_set_cta_group(int32_t cta_group) {
 
 int icepop_set_wide_tiles(int32_t enable) {
   g_wide_tiles = enable ? 1 : 0;
+  return ICEPOP_OK;
+}
+
+int icepop_set_k1_wide(int32_t enable) {
+  g_k1_wide = enable ? 1 : 0;
   return ICEPOP_OK;
 }
 

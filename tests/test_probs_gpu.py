@@ -468,3 +468,40 @@ def test_onehot_scatter_token_patterns(cuda_device, layout, pattern):
     assert torch.equal(gh1, gh2) and torch.equal(gw1, gw2)
     assert _rel(gw1.cpu().numpy(), gwr.cpu().numpy()) < 5e-3
     assert _rel(gh1.cpu().numpy(), ghr.cpu().numpy()) < 5e-3
+
+
+@pytest.mark.parametrize("V,layout", [(1000, "vd"), (520, "dv"), (2048, "vd")])
+def test_k1_wide_tile_matches_default(cuda_device, V, layout):
+    """K1 on 256x512 tiles (icepop_set_k1_wide(1): one accumulator released in halves, columns
+    of a tile interleaved across the CTA pair) against the default 256x256 tiles: the same
+    logits per element, so the stored probabilities and slab references are the same bits and
+    the kept mask is identical; the statistics differ only by the partial grouping. V = 520
+    leaves a wide tile whose second half lies past V (slab references beyond tile_max_ld)."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd
+
+    c = _case(seed=97, layout=layout, V=V)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    lib = _lib.ensure_device(0)
+    res = {}
+    try:
+        for wide in (0, 1):
+            _lib.check(lib.icepop_set_k1_wide(wide))
+            f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
+            probs, tmax = f.extras["probs"].clone(), f.extras["tile_max"].clone()
+            gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
+            res[wide] = (f, probs, tmax, gh, gw)
+    finally:
+        _lib.check(lib.icepop_set_k1_wide(0))
+    (f0, p0, t0, gh0, gw0), (f1, p1, t1, gh1, gw1) = res[0], res[1]
+    n_slabs = -(-V // _lib.PROBS_SLAB)
+    assert torch.equal(p0, p1)
+    assert torch.equal(t0[:, :n_slabs], t1[:, :n_slabs])
+    assert torch.equal(f0.kept, f1.kept)
+    torch.testing.assert_close(f1.lse, f0.lse, rtol=1e-6, atol=1e-6)
+    torch.testing.assert_close(f1.lp_cur, f0.lp_cur, rtol=0, atol=1e-5)
+    assert _rel(gw1.cpu().numpy(), gw0.cpu().numpy()) < 1e-4
+    assert _rel(gh1.cpu().numpy(), gh0.cpu().numpy()) < 1e-4
+    o = _oracle(c)
+    assert _rel(gw1.cpu().numpy(), o["grad_weight"]) < 1e-2
