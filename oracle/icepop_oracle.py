@@ -11,6 +11,10 @@ SURVEY.md load-bearing fact 2):
 
 * ``group_advantages``     follows objective.py:153-159
 * ``log_softmax_rows``     follows policy.py:350-355
+* ``token_terms``          the per-token part of objective.py:215-252 (weights, calibration
+                           mask, ratio, clip, surrogate, gradient coefficient) vectorised over
+                           a whole packed batch, for checks at full size where the logits come
+                           from a chunked GPU fp32 reference instead of numpy
 * ``icepop_dense``         follows objective.py:204-298 line by line, with
                            ``batched_train_logits`` (policy.py:279-289) replaced by H.W
                            and the ``np.add.at`` scatter (objective.py:265-266) by H^T.dZ;
@@ -193,6 +197,38 @@ def icepop_dense(
         out["grad_weight"] = grad_w
         out["grad_hidden"] = grad_h
     return out
+
+
+def token_terms(lp_cur, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages, *, alpha=0.5, beta=5.0,
+                clip_eps=0.2, tis_cap=2.0, temperature=1.0, algo="icepop") -> dict:
+    """Per-token IcePop terms given lp_cur, fp64, vectorised (objective.py:215-252; the same
+    expressions as icepop_dense's inner loop): calib, kept, ratio, active, surrogate, coeff."""
+    if algo not in ALGOS:
+        raise ValueError(f"unknown algo {algo!r}")
+    lp_cur = np.asarray(lp_cur, dtype=np.float64)
+    lp_old = np.asarray(lp_train_old, dtype=np.float64)
+    lp_inf = np.asarray(lp_infer_old, dtype=np.float64)
+    cu = np.asarray(cu_seqlens, dtype=np.int64)
+    seq_of = np.repeat(np.arange(len(cu) - 1), np.diff(cu))
+    adv = np.asarray(advantages, dtype=np.float64)[seq_of]
+    weight_t = per_token_weights(cu, np.asarray(group_offsets, dtype=np.int64))  # objective.py:215
+    calib = np.exp(lp_old - lp_inf)  # objective.py:227
+    if algo == "icepop":
+        kept = (calib >= alpha) & (calib <= beta)
+        factor = np.where(kept, calib, 0.0)
+    elif algo == "grpo":
+        kept = np.ones(lp_cur.size, dtype=bool)
+        factor = calib
+    else:
+        kept = np.ones(lp_cur.size, dtype=bool)
+        factor = np.minimum(calib, tis_cap)
+    ratio = np.exp(lp_cur - lp_old)  # objective.py:240
+    unclipped = ratio * adv
+    clipped = np.clip(ratio, 1.0 - clip_eps, 1.0 + clip_eps) * adv
+    active = unclipped <= clipped
+    surrogate = factor * np.where(active, unclipped, clipped)
+    coeff = np.where(active, weight_t * factor * ratio * adv / temperature, 0.0)  # objective.py:250
+    return dict(calib=calib, kept=kept, ratio=ratio, active=active, surrogate=surrogate, coeff=coeff)
 
 
 def per_token_weights(cu_seqlens: np.ndarray, group_offsets: np.ndarray) -> np.ndarray:

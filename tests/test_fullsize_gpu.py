@@ -1,0 +1,167 @@
+"""Full-size checks at BASELINE's C2 shape (64 x 4,096 = 262,144 tokens, d = 4,096,
+V = 157,184, [V, d] weight), where the fp64 oracle cannot finish: the bf16 path is checked
+through properties that hold at any size.
+
+* Input-only quantities against the oracle's vectorised per-token terms
+  (oracle.token_terms, objective.py:215-252). The calibration mask, token count and popped
+  count are bit-exact. The calibration ratio agrees to fp64 rounding.
+* lse, lp_cur and entropy against a chunked torch reference of the same logits. TF32 is
+  exact for bf16 inputs (exact products, fp32 accumulation). Tolerance: the bf16 path's
+  2e-3 absolute.
+* The gradient coefficients against token_terms evaluated on the reference lp_cur. Tokens
+  within 1e-3 of a clip boundary are excluded.
+* dW and dH against the chunked reference dZ = coeff (e_y - softmax(z)). Tolerance:
+  relative Frobenius error 1e-2.
+* Linearity: grad_scale = 2 gives exactly twice the gradients. A power of two scales every
+  term exactly.
+* Determinism: a second step gives the same bits.
+* Token chunks (icepop_fwd_bwd, 2 chunks) match the whole batch.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle.icepop_oracle import group_advantages, token_terms  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+N_SEQS, SEQ_LEN, D, V, G = 64, 4096, 4096, 157184, 8
+CHUNK = 4096
+
+
+def _rel(a, b):
+    return float(torch.linalg.vector_norm((a - b).double()) / torch.linalg.vector_norm(b.double()))
+
+
+@pytest.fixture(scope="module")
+def c2(cuda_device):
+    from paper_2510_18855_b200.loss import IcePopConfig, PackedBatch, icepop_logprob
+
+    dev = cuda_device
+    n = N_SEQS * SEQ_LEN
+    g = torch.Generator(device=dev).manual_seed(2510)
+    H = torch.randn(n, D, device=dev, generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, D, device=dev, generator=g) * (2.0 / D ** 0.5)).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32, generator=g)
+    lp0, _, _ = icepop_logprob(H, W, tokens)
+    rng = np.random.default_rng(2510)
+    lp_old = lp0.cpu().numpy() + rng.normal(0.0, 0.1, n)  # ~5% of tokens outside the clip band
+    lp_inf = lp_old - rng.normal(0.0, 0.233, n)  # ~0.15% popped
+    rewards = rng.integers(0, 2, N_SEQS).astype(np.float64)
+    go = np.arange(0, N_SEQS + 1, G, dtype=np.int32)
+    adv = np.concatenate([group_advantages(rewards[go[i]:go[i + 1]]) for i in range(len(go) - 1)])
+    cu = np.arange(0, n + 1, SEQ_LEN, dtype=np.int32)
+    batch = PackedBatch(tokens, torch.from_numpy(lp_old).to(dev), torch.from_numpy(lp_inf).to(dev),
+                        torch.from_numpy(cu).to(dev), torch.from_numpy(go).to(dev), torch.from_numpy(adv).to(dev),
+                        None)
+    host = dict(lp_old=lp_old, lp_inf=lp_inf, cu=cu, go=go, adv=adv, tokens=tokens.cpu().numpy())
+    return H, W, batch, host, IcePopConfig()
+
+
+def _step(c2, grad_scale=1.0):
+    from paper_2510_18855_b200.loss import icepop_bwd, icepop_fwd
+
+    H, W, batch, _, cfg = c2
+    f = icepop_fwd(H, W, batch, cfg, store_probs=True)
+    assert "probs" in f.extras  # C2 fits: the stored-probabilities backward is the one under test
+    gh, gw = icepop_bwd(H, W, batch, f, cfg, grad_scale=grad_scale, grad_hidden_dtype=torch.float32)
+    return f, gh, gw
+
+
+def _reference(H, W, tokens, coeff):
+    """Chunked torch reference: lse, lp_cur, entropy and the ascent gradients for the given
+    per-token coefficients (dZ = coeff (e_y - p), objective.py:250-252)."""
+    n = H.shape[0]
+    Wf = W.float()
+    lse = torch.empty(n, device=H.device)
+    lp = torch.empty(n, device=H.device)
+    ent = torch.empty(n, device=H.device)
+    gw = torch.zeros(V, D, device=H.device)
+    gh = torch.empty(n, D, device=H.device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        for s in range(0, n, CHUNK):
+            e = min(n, s + CHUNK)
+            hc = H[s:e].float()
+            z = hc @ Wf.T
+            lse[s:e] = torch.logsumexp(z, dim=1)
+            lz = z.sub_(lse[s:e, None])  # log-probabilities, in place
+            tk = tokens[s:e].long()
+            lp[s:e] = lz.gather(1, tk[:, None])[:, 0]
+            p = lz.exp()
+            ent[s:e] = -(p * lz).sum(1)
+            dz = p.mul_(-coeff[s:e, None])
+            dz.scatter_add_(1, tk[:, None], coeff[s:e, None])
+            gw += dz.T @ hc
+            gh[s:e] = dz @ Wf
+            del z, lz, p, dz
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return lse, lp, ent, gw, gh
+
+
+def test_c2_full_size_against_chunked_reference(c2):
+    from paper_2510_18855_b200 import _lib
+
+    H, W, batch, host, cfg = c2
+    f, gh, gw = _step(c2)
+    n = H.shape[0]
+
+    # input-only quantities: bit-exact mask and counts
+    tt_inputs = token_terms(np.zeros(n), host["lp_old"], host["lp_inf"], host["cu"], host["go"], host["adv"])
+    kept = f.kept.cpu().numpy().astype(bool)
+    assert np.array_equal(kept, tt_inputs["kept"])
+    np.testing.assert_allclose(f.calib.cpu().numpy(), tt_inputs["calib"], rtol=1e-15, atol=0)
+    stats = f.stats.cpu().numpy()
+    assert stats[_lib.STAT_TOKENS] == n
+    assert stats[_lib.STAT_N_POPPED] == int((~tt_inputs["kept"]).sum()) > 0
+
+    # statistics against the reference logits
+    lse_r, lp_r, ent_r, gw_r, gh_r = _reference(H, W, batch.tokens, f.coeff.float())
+    assert float((f.lse - lse_r).abs().max()) < 2e-3
+    assert float((f.lp_cur.float() - lp_r).abs().max()) < 2e-3
+    assert float((f.entropy - ent_r).abs().max()) < 2e-3
+
+    # gradient coefficients: the oracle's per-token terms on the reference lp_cur
+    tt = token_terms(lp_r.double().cpu().numpy(), host["lp_old"], host["lp_inf"], host["cu"], host["go"],
+                     host["adv"])
+    ratio = tt["ratio"]
+    safe = (np.abs(ratio - 0.8) > 1e-3) & (np.abs(ratio - 1.2) > 1e-3)
+    assert safe.mean() > 0.99
+    ours = f.coeff.double().cpu().numpy()
+    scale = np.abs(tt["coeff"]).max()
+    np.testing.assert_allclose(ours[safe], tt["coeff"][safe], rtol=2e-3, atol=1e-6 * scale)
+
+    # gradients
+    assert _rel(gw, gw_r) < 1e-2
+    assert _rel(gh, gh_r) < 1e-2
+
+
+def test_c2_linearity_determinism_and_token_chunks(c2):
+    from paper_2510_18855_b200.loss import icepop_fwd_bwd
+
+    H, W, batch, _, cfg = c2
+    f1, gh1, gw1 = _step(c2)
+    f2, gh2, gw2 = _step(c2)
+    assert torch.equal(f1.stats, f2.stats) and torch.equal(f1.lse, f2.lse)
+    assert torch.equal(gw1, gw2) and torch.equal(gh1, gh2)
+    _, gh3, gw3 = _step(c2, grad_scale=2.0)
+    assert torch.equal(gw3, 2.0 * gw1) and torch.equal(gh3, 2.0 * gh1)
+    del gh2, gw2, gh3, gw3
+    fc, ghc, gwc = icepop_fwd_bwd(H, W, batch, cfg, grad_hidden_dtype=torch.float32,
+                                  max_chunk_tokens=H.shape[0] // 2)
+    assert fc.extras["chunks"] == 2
+    for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff"):
+        assert torch.equal(getattr(fc, name), getattr(f1, name)), name
+    assert torch.equal(ghc, gh1)
+    assert _rel(gwc, gw1) < 5e-5
