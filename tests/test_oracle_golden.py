@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN, golden_cases, golden_hidden, load_golden, oracle_kwargs
-from oracle.icepop_oracle import group_advantages, icepop_dense, per_token_weights
+from oracle.icepop_oracle import group_advantages, icepop_dense, per_token_weights, token_terms
 
 
 @pytest.mark.parametrize("name", golden_cases())
@@ -33,6 +33,20 @@ def test_oracle_matches_reference_golden(name):
         assert o["entropy_clipped"] == pytest.approx(d["out_entropy_clipped"], rel=1e-13)
     # dense H^T dZ vs the reference's 4x np.add.at scatter
     np.testing.assert_allclose(o["grad_weight"], d["out_grad"], rtol=1e-11, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_token_terms_match_reference_golden(name):
+    """The vectorised per-token terms (used by the full-size GPU checks) on the reference's own
+    lp_cur reproduce its mask, calibration and surrogate (KL cases: surrogate excludes kl)."""
+    d = load_golden(name)
+    kw = oracle_kwargs(d)
+    t = token_terms(d["out_lp_cur"], d["lp_train_old"], d["lp_infer_old"], d["cu_seqlens"], d["group_offsets"],
+                    d["advantages"], alpha=kw["alpha"], beta=kw["beta"], clip_eps=kw["clip_eps"],
+                    tis_cap=kw["tis_cap"], temperature=kw["temperature"], algo=kw["algo"])
+    assert np.array_equal(t["kept"], d["out_kept"])
+    assert np.array_equal(t["calib"], d["out_calibration"])
+    np.testing.assert_allclose(t["surrogate"], d["out_surrogate"], rtol=1e-12, atol=1e-15)
 
 
 def test_oracle_layouts_agree():
