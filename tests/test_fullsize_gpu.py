@@ -165,3 +165,74 @@ def test_c2_linearity_determinism_and_token_chunks(c2):
         assert torch.equal(getattr(fc, name), getattr(f1, name)), name
     assert torch.equal(ghc, gh1)
     assert _rel(gwc, gw1) < 5e-5
+
+
+def test_c4_long_cot_ragged_token_chunks(cuda_device):
+    """C4 at full size (32 ragged sequences, lognormal lengths of median 16,384 clipped to
+    [256, 32,768]; d = 8,192; ~5% popped). Its 2 N V bytes of probabilities do not fit, so
+    icepop_fwd_bwd runs in token chunks that cut sequences. Checks:
+    * the mask and counts are bit-exact against the oracle's token terms;
+    * the rows at both ends are checked against the chunked reference (lse, lp_cur and dH rows
+      for the same coefficients);
+    * a second chunking (131,072 tokens) gives the same per-token bits and dH, with dW within
+      fp32 regrouping."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, PackedBatch, icepop_fwd_bwd, icepop_logprob
+
+    dev = cuda_device
+    d4, S = 8192, 32
+    rng = np.random.default_rng(3)
+    lens = np.clip(rng.lognormal(np.log(16384), 0.6, S), 256, 32768).astype(np.int64)
+    n = int(lens.sum())
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    g = torch.Generator(device=dev).manual_seed(3)
+    H = torch.randn(n, d4, device=dev, generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, d4, device=dev, generator=g) * (2.0 / d4 ** 0.5)).to(torch.bfloat16)
+    tokens = torch.randint(0, V, (n,), device=dev, dtype=torch.int32, generator=g)
+    lp0, _, _ = icepop_logprob(H, W, tokens)
+    lp_old = lp0.cpu().numpy() + rng.normal(0.0, 0.1, n)
+    lp_inf = lp_old - rng.normal(0.0, 0.42, n)
+    rewards = rng.integers(0, 2, S).astype(np.float64)
+    go = np.arange(0, S + 1, G, dtype=np.int32)
+    adv = np.concatenate([group_advantages(rewards[go[i]:go[i + 1]]) for i in range(len(go) - 1)])
+    batch = PackedBatch(tokens, torch.from_numpy(lp_old).to(dev), torch.from_numpy(lp_inf).to(dev),
+                        torch.from_numpy(cu).to(dev), torch.from_numpy(go).to(dev), torch.from_numpy(adv).to(dev),
+                        None)
+    cfg = IcePopConfig()
+    f1, gh1, gw1 = icepop_fwd_bwd(H, W, batch, cfg)
+    assert f1.extras.get("chunks", 1) >= 2  # 173 GB of probabilities: chunked
+    tt = token_terms(np.zeros(n), lp_old, lp_inf, cu, go, adv)
+    assert np.array_equal(f1.kept.cpu().numpy().astype(bool), tt["kept"])
+    stats = f1.stats.cpu().numpy()
+    assert stats[_lib.STAT_TOKENS] == n
+    popped = int((~tt["kept"]).sum())
+    assert stats[_lib.STAT_N_POPPED] == popped and 0.03 < popped / n < 0.08
+
+    # both ends of the batch against the reference (dH rows depend on their own token only)
+    for s0 in (0, n - CHUNK):
+        sl = slice(s0, s0 + CHUNK)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        try:
+            z = H[sl].float() @ W.float().T
+            lse = torch.logsumexp(z, dim=1)
+            lz = z.sub_(lse[:, None])
+            tk = tokens[sl].long()
+            lp = lz.gather(1, tk[:, None])[:, 0]
+            coeff = f1.coeff[sl].float()
+            dz = lz.exp_().mul_(-coeff[:, None])
+            dz.scatter_add_(1, tk[:, None], coeff[:, None])
+            gh_r = dz @ W.float()
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        assert float((f1.lse[sl] - lse).abs().max()) < 2e-3
+        assert float((f1.lp_cur[sl].float() - lp).abs().max()) < 2e-3
+        assert _rel(gh1[sl].float(), gh_r) < 1e-2
+        del z, lz, dz, gh_r
+
+    f2, gh2, gw2 = icepop_fwd_bwd(H, W, batch, cfg, max_chunk_tokens=131072)
+    assert f2.extras["chunks"] == -(-n // 131072)
+    for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff"):
+        assert torch.equal(getattr(f2, name), getattr(f1, name)), name
+    assert torch.equal(gh2, gh1)
+    assert _rel(gw2, gw1) < 5e-5
