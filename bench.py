@@ -528,6 +528,8 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
                 bufs[i][name].copy_(host[name], non_blocking=True)
             copied[i].record(copy_stream)
 
+    last = {}
+
     def compute(k):
         i = k % 2
         main.wait_event(copied[i])
@@ -535,6 +537,7 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
         b = PackedBatch(d["tokens"], d["lp_old"], d["lp_inf"], d["cu"], d["go"], None, d["rewards"], batch.token_offset)
         if sp_chunk:
             f, _, g = icepop_fwd_bwd(d["H"], W, b, icfg, layout="vd", grad_scale=-1.0, max_chunk_tokens=sp_chunk)
+            last["chunks"] = f.extras.get("chunks", 1)
         else:
             f = icepop_fwd(d["H"], W, b, icfg, layout="vd", store_probs=sp)
             _, g = icepop_bwd(d["H"], W, b, f, icfg, layout="vd", grad_scale=-1.0)
@@ -564,9 +567,12 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": round(H.shape[0] * world / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": 64, "ms_per_step": round(ms, 3), "steps": steps,
-            "note": "pinned host inputs; step k+1's H2D overlaps step k on a copy stream"}
+    out = {"value": round(H.shape[0] * world / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 64, "ms_per_step": round(ms, 3), "steps": steps,
+           "note": "pinned host inputs; step k+1's H2D overlaps step k on a copy stream"}
+    if "chunks" in last:
+        out["token_chunks"] = last["chunks"]
+    return out
 
 
 # ----------------------------------------------------------------------------- CPU baseline

@@ -597,6 +597,9 @@ def icepop_bwd_reduce_scatter(
     return gh
 
 
+_PROBS_CHUNK_OK: dict = {}  # (device index, vocab) -> a token-chunk size whose buffers allocated
+
+
 def probs_chunk_tokens(n: int, vocab: int, device) -> int:
     """Largest token count (multiple of 4096, or n) whose stored probabilities fit in
     STORE_PROBS_FRACTION of the device memory available now; 0 if not even 4096 do."""
@@ -657,18 +660,22 @@ def icepop_fwd_bwd(
         else None
     # One probabilities buffer (and backward workspace) for all chunks: re-allocating tens of GB
     # per chunk lets smaller allocations fragment torch's cache between chunks. If the estimate
-    # was too optimistic for one block, the chunk halves (down to 4096 tokens).
+    # was too optimistic for one block, the chunk halves (down to 4096 tokens), and the size that
+    # allocated is remembered for this device and vocabulary, so a training loop does not pay a
+    # failed allocation (and torch's cache flush behind it) on every step.
     n_seqs = batch.n_seqs
+    key = (dev.index, v)
+    chunk = min(chunk, _PROBS_CHUNK_OK.get(key, chunk))
     while True:
         try:
             bufs = (torch.empty((chunk, v), dtype=torch.bfloat16, device=dev),
                     torch.empty((chunk, _lib.tile_max_ld(v)), dtype=torch.float32, device=dev))
             break
         except torch.OutOfMemoryError:
-            torch.cuda.empty_cache()
             if chunk <= 4096:
                 raise
             chunk = max(4096, chunk // 2 // 4096 * 4096)
+            _PROBS_CHUNK_OK[key] = chunk
     ws = _sp_workspace(chunk, hidden.shape[1], v, n_seqs, dev)
     parts = []
     stats = torch.zeros(_lib.NSTATS, dtype=torch.float64, device=dev)
