@@ -20,7 +20,24 @@ def pytest_configure(config):
 
 
 def golden_cases() -> list[str]:
-    return sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "advantages")
+    """The small/medium reference cases (c1_config0, BASELINE configs[0] at full size, has its
+    own schema and tests)."""
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem not in ("advantages", "c1_config0"))
+
+
+def load_c1() -> tuple[dict, np.ndarray]:
+    """BASELINE configs[0] fixture (tests/golden/make_golden.py c1_case) and its regenerated
+    bf16-exact weights [n_features = 1024, V = 32768] (fp64)."""
+    import torch
+
+    with np.load(GOLDEN / "c1_config0.npz") as z:
+        d = {k: z[k] for k in z.files}
+    w = np.random.default_rng(2510).normal(0.0, 0.8, (1024, 32768))
+    w = torch.from_numpy(w).to(torch.bfloat16).to(torch.float64).numpy()
+    return d, w
+
+
+C1_PROJ_SEED = 7
 
 
 def load_golden(name: str) -> dict:

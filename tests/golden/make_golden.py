@@ -207,5 +207,67 @@ def main() -> None:
     print(f"advantages: {len(sets)} groups")
 
 
+C1_SEQS, C1_LEN, C1_D, C1_V = 8, 512, 1024, 32768
+C1_W_SEED, C1_W_SCALE, C1_PROJ_SEED = 2510, 0.8, 7
+
+
+def c1_weights() -> np.ndarray:
+    """BASELINE configs[0]'s weights, regenerated identically by tests/test_parity_gpu.py
+    (numpy PCG64 is platform-independent), so the 268 MB matrix never enters the repo."""
+    w = np.random.default_rng(C1_W_SEED).normal(0.0, C1_W_SCALE, (C1_D, C1_V))
+    return bf16_exact(w)
+
+
+def c1_case() -> None:
+    """BASELINE configs[0] at full size, through the reference's own objective_and_grad: one
+    GRPO group of 8 rollouts x 512 tokens, n_features (hidden) 1,024, vocab 32,768, default
+    alpha/beta, IcePop. lp_train_old = lp_cur + N(0, 0.1) (from a first reference pass, which
+    writes logp_train_cur back into the records) and lp_infer_old = lp_train_old - N(0, 0.233),
+    as in SURVEY.md 8d. The gradient is stored as its Frobenius norm and a fixed random
+    projection (grad @ R, R ~ N(0, 1) [V, 4]) instead of 268 MB of fp64."""
+    rng = np.random.default_rng(123)
+    theta = PolicyParams(c1_weights(), 0)
+    task = TaskSpec(TaskKind.PARITY_MATCH, 4242, 0, C1_LEN)
+    rollouts = []
+    for i in range(C1_SEQS):
+        toks = rng.integers(0, C1_V, C1_LEN)
+        recs = [TokenRecord(token=int(t), logp_infer_old=0.0, logp_train_old=0.0, logp_train_cur=0.0, gen_version=0)
+                for t in toks]
+        rollouts.append(Rollout(task=task, stream=np.random.default_rng(i), uid=i, group_uid=0, tokens=recs,
+                                terminal=True))
+    rewards = [float(x) for x in rng.normal(0.5, 0.5, C1_SEQS)]
+    group = PromptGroup(task=task, rollouts=rollouts, rewards=rewards,
+                        advantages=[float(a) for a in group_advantages(rewards)])
+    cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C1_SEQS)
+    bounds = MaskingBounds(0.5, 5.0)
+    objective_and_grad([group], theta, theta, None, cfg, bounds, 1.0)  # writes logp_train_cur
+    for r in rollouts:
+        for rec in r.tokens:
+            rec.logp_train_old = rec.logp_train_cur + float(rng.normal(0.0, 0.1))
+            rec.logp_infer_old = rec.logp_train_old - float(rng.normal(0.0, 0.233))
+    out = objective_and_grad([group], theta, theta, None, cfg, bounds, 1.0)
+    lp_written = np.asarray([rec.logp_train_cur for r in rollouts for rec in r.tokens])
+    data = pack([group], C1_D)
+    proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((C1_V, 4))
+    data.update(
+        out_kept=out.per_token_mask_kept,
+        out_lp_cur=lp_written,
+        out_surrogate=out.per_token_surrogate,
+        out_calibration=out.per_token_calibration,
+        out_entropy=out.per_token_entropy,
+        out_objective=np.asarray(out.objective_value),
+        out_clipped_fraction=np.asarray(out.clipped_fraction),
+        out_token_count=np.asarray(out.token_count),
+        out_mean_logp=np.asarray(out.mean_logp),
+        out_entropy_all=np.asarray(out.entropy_all),
+        out_grad_norm=np.asarray(np.linalg.norm(out.grad)),
+        out_grad_proj=out.grad @ proj,
+    )
+    np.savez_compressed(OUT / "c1_config0.npz", **data)
+    print(f"c1_config0: tokens={out.token_count} popped={int((~out.per_token_mask_kept).sum())} "
+          f"J={out.objective_value:.6g} |grad|={out.grad_norm:.4g}")
+
+
 if __name__ == "__main__":
     main()
+    c1_case()

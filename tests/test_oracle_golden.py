@@ -147,3 +147,25 @@ def test_oracle_error_semantics(bad):
     with pytest.raises(ValueError):
         icepop_dense(golden_hidden(d), d["weight"], d["tokens"], d["lp_train_old"], d["lp_infer_old"], cu, go,
                      np.concatenate([[0.0], d["advantages"]]))
+
+
+def test_oracle_matches_reference_at_config0_full_size():
+    """BASELINE configs[0] (8 x 512 tokens, hidden 1,024, vocab 32K, GRPO group 8) through the
+    reference's own objective_and_grad vs the oracle: mask bit-exact, lp_cur / surrogate /
+    entropy / objective to fp64 rounding, gradient through its norm and a fixed projection."""
+    from conftest import C1_PROJ_SEED, load_c1
+    from paper_2510_18855_b200.features import multihot
+
+    d, w = load_c1()
+    h = multihot(d["feats"], w.shape[0])
+    o = icepop_dense(h, w, d["tokens"], d["lp_train_old"], d["lp_infer_old"], d["cu_seqlens"], d["group_offsets"],
+                     d["advantages"], layout="dv")
+    assert np.array_equal(o["kept"], d["out_kept"]) and o["token_count"] == int(d["out_token_count"]) == 4096
+    assert np.array_equal(o["calib"], d["out_calibration"])
+    np.testing.assert_allclose(o["lp_cur"], d["out_lp_cur"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(o["surrogate"], d["out_surrogate"], rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(o["entropy"], d["out_entropy"], rtol=1e-12)
+    assert o["objective"] == pytest.approx(float(d["out_objective"]), rel=1e-10)
+    proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((w.shape[1], 4))
+    np.testing.assert_allclose(o["grad_weight"] @ proj, d["out_grad_proj"], rtol=1e-9, atol=1e-12)
+    assert np.linalg.norm(o["grad_weight"]) == pytest.approx(float(d["out_grad_norm"]), rel=1e-10)

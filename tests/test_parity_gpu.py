@@ -152,3 +152,46 @@ def test_rewards_path_uses_k0(cuda_device, dtype):
     b = icepop_fwd(H, W, _batch(d, cuda_device, use_rewards=True), _cfg(d), layout="dv")
     assert torch.equal(a.surrogate, b.surrogate)
     assert torch.equal(a.stats, b.stats)
+
+
+@pytest.mark.parametrize("path", ["fp64", "bf16_probs", "bf16_recompute"])
+def test_config0_full_size_matches_reference(cuda_device, path):
+    """BASELINE configs[0] at full size (8 x 512 tokens, hidden 1,024, vocab 32,768, GRPO
+    group 8, default alpha/beta) against the reference's own objective_and_grad
+    (tests/golden/c1_config0.npz): mask, token and popped counts bit-exact on every path;
+    fp64 path to fp64 rounding; bf16 path within the stated tolerances; dW through its norm
+    and a fixed random projection (the fixture stores grad @ R, not 268 MB)."""
+    from conftest import C1_PROJ_SEED, load_c1
+    from paper_2510_18855_b200.features import multihot
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    d, w = load_c1()
+    h = multihot(d["feats"], w.shape[0])
+    dt = torch.float64 if path == "fp64" else torch.bfloat16
+    H = torch.from_numpy(h).to(dt).to(cuda_device)
+    W = torch.from_numpy(w).to(dt).to(cuda_device)
+    batch = _batch(d, cuda_device)
+    cfg = IcePopConfig()
+    kw = {} if path == "fp64" else dict(store_probs=(path == "bf16_probs"))
+    f = icepop_fwd(H, W, batch, cfg, layout="dv", **kw)
+    _, gw = icepop_bwd(H, W, batch, f, cfg, layout="dv", need_hidden=False)
+    finish(f.stats)
+    diag = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
+    assert diag.token_count == int(d["out_token_count"]) == 4096
+    assert diag.clipped_fraction == float(d["out_clipped_fraction"]) > 0
+    np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=4.5e-16, atol=0)
+    proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((w.shape[1], 4))
+    g = gw.double().cpu().numpy()
+    if path == "fp64":
+        np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(f.entropy.cpu().numpy(), d["out_entropy"], rtol=1e-12)
+        assert diag.objective_value == pytest.approx(float(d["out_objective"]), rel=1e-10)
+        np.testing.assert_allclose(g @ proj, d["out_grad_proj"], rtol=1e-9, atol=1e-12)
+        assert np.linalg.norm(g) == pytest.approx(float(d["out_grad_norm"]), rel=1e-10)
+    else:
+        np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], atol=2e-3, rtol=1e-3)
+        np.testing.assert_allclose(f.entropy.cpu().numpy(), d["out_entropy"], atol=2e-3, rtol=1e-3)
+        assert diag.objective_value == pytest.approx(float(d["out_objective"]), rel=1e-3, abs=1e-5)
+        assert _rel(g @ proj, d["out_grad_proj"]) < 1e-2
+        assert np.linalg.norm(g) == pytest.approx(float(d["out_grad_norm"]), rel=1e-2)
