@@ -40,6 +40,18 @@ def load_c1() -> tuple[dict, np.ndarray]:
 C1_PROJ_SEED = 7
 
 
+def load_c2_slice():
+    """C2-width slice fixture (make_golden.py c2_slice_case: 8 x 4,096 tokens, d = 4,096,
+    V = 157,184) and its regenerated weights as a bf16 torch tensor [4096, 157184] (exact: the
+    reference saw the same bf16-rounded values in fp64)."""
+    import torch
+
+    with np.load(GOLDEN / "c2_slice.npz") as z:
+        d = {k: z[k] for k in z.files}
+    w = np.random.default_rng(2511).normal(0.0, 0.5, (4096, 157184))
+    return d, torch.from_numpy(w).to(torch.bfloat16)
+
+
 def load_golden(name: str) -> dict:
     with np.load(GOLDEN / f"{name}.npz") as z:
         d = {k: z[k] for k in z.files}

@@ -268,6 +268,70 @@ def c1_case() -> None:
           f"J={out.objective_value:.6g} |grad|={out.grad_norm:.4g}")
 
 
+C2S_SEQS, C2S_LEN, C2S_D, C2S_V = 8, 4096, 4096, 157184
+C2S_W_SEED, C2S_W_SCALE = 2511, 0.5
+
+
+def c2s_weights() -> np.ndarray:
+    """Weights of the C2-width slice (n_features = d = 4,096, V = 157,184), regenerated by the
+    GPU test from the same seed."""
+    w = np.random.default_rng(C2S_W_SEED).normal(0.0, C2S_W_SCALE, (C2S_D, C2S_V))
+    return bf16_exact(w)
+
+
+def c2_slice_case() -> None:
+    """One GRPO group (8 rollouts x 4,096 tokens = 32,768 tokens) at BASELINE configs[1]'s full
+    width (hidden 4,096, vocab 157,184) through the reference's own objective_and_grad (one
+    pass, ~10 min on one core: a 4-hot gather and np.add.at over T x V per rollout). lp_train_old
+    comes from the same 4-hot logits (policy.py:279-289, computed here with numpy) plus N(0, 0.1),
+    lp_infer_old = lp_train_old - N(0, 0.233). Stored like c1_config0 (gradient norm and
+    projection)."""
+    rng = np.random.default_rng(321)
+    theta = PolicyParams(c2s_weights(), 0)
+    task = TaskSpec(TaskKind.PARITY_MATCH, 5151, 0, C2S_LEN)
+    toks_all = rng.integers(0, C2S_V, (C2S_SEQS, C2S_LEN))
+    rollouts = []
+    for i in range(C2S_SEQS):
+        recs = [TokenRecord(token=int(t), logp_infer_old=0.0, logp_train_old=0.0, logp_train_cur=0.0, gen_version=0)
+                for t in toks_all[i]]
+        rollouts.append(Rollout(task=task, stream=np.random.default_rng(i), uid=i, group_uid=0, tokens=recs,
+                                terminal=True))
+        feats = _rollout_feats(task, recs, C2S_D)
+        z = theta.weights[feats[:, 0]] + theta.weights[feats[:, 1]] + theta.weights[feats[:, 2]] + \
+            theta.weights[feats[:, 3]]
+        m = z.max(axis=1)
+        lse = m + np.log(np.exp(z - m[:, None]).sum(axis=1))
+        lp = z[np.arange(C2S_LEN), toks_all[i]] - lse
+        del z
+        for rec, l in zip(recs, lp):
+            rec.logp_train_old = float(l) + float(rng.normal(0.0, 0.1))
+            rec.logp_infer_old = rec.logp_train_old - float(rng.normal(0.0, 0.233))
+    rewards = [float(x) for x in rng.normal(0.5, 0.5, C2S_SEQS)]
+    group = PromptGroup(task=task, rollouts=rollouts, rewards=rewards,
+                        advantages=[float(a) for a in group_advantages(rewards)])
+    cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C2S_SEQS)
+    out = objective_and_grad([group], theta, theta, None, cfg, MaskingBounds(0.5, 5.0), 1.0)
+    lp_written = np.asarray([rec.logp_train_cur for r in rollouts for rec in r.tokens])
+    data = pack([group], C2S_D)
+    proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((C2S_V, 4))
+    data.update(
+        out_kept=out.per_token_mask_kept,
+        out_lp_cur=lp_written,
+        out_surrogate=out.per_token_surrogate,
+        out_calibration=out.per_token_calibration,
+        out_entropy=out.per_token_entropy,
+        out_objective=np.asarray(out.objective_value),
+        out_clipped_fraction=np.asarray(out.clipped_fraction),
+        out_token_count=np.asarray(out.token_count),
+        out_grad_norm=np.asarray(np.linalg.norm(out.grad)),
+        out_grad_proj=out.grad @ proj,
+    )
+    np.savez_compressed(OUT / "c2_slice.npz", **data)
+    print(f"c2_slice: tokens={out.token_count} popped={int((~out.per_token_mask_kept).sum())} "
+          f"J={out.objective_value:.6g} |grad|={out.grad_norm:.4g}")
+
+
 if __name__ == "__main__":
     main()
     c1_case()
+    c2_slice_case()

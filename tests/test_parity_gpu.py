@@ -195,3 +195,36 @@ def test_config0_full_size_matches_reference(cuda_device, path):
         assert diag.objective_value == pytest.approx(float(d["out_objective"]), rel=1e-3, abs=1e-5)
         assert _rel(g @ proj, d["out_grad_proj"]) < 1e-2
         assert np.linalg.norm(g) == pytest.approx(float(d["out_grad_norm"]), rel=1e-2)
+
+
+@pytest.mark.parametrize("store_probs", [True, False], ids=["probs", "recompute"])
+def test_c2_width_slice_matches_reference(cuda_device, store_probs):
+    """One GRPO group (8 x 4,096 = 32,768 tokens) at BASELINE configs[1]'s full width (hidden
+    4,096, vocab 157,184 = the Ling-2.0 lm_head) against the reference's own objective_and_grad
+    (tests/golden/c2_slice.npz, H = the reference's 4-hot features, exact in bf16): mask and
+    counts bit-exact; lp_cur / entropy / objective / dW (norm and fixed projection) within the
+    bf16 path's tolerances."""
+    from conftest import C1_PROJ_SEED, load_c2_slice
+    from paper_2510_18855_b200.features import multihot
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    d, w = load_c2_slice()
+    H = torch.from_numpy(multihot(d["feats"], w.shape[0])).to(torch.bfloat16).to(cuda_device)
+    W = w.to(cuda_device)
+    batch = _batch(d, cuda_device)
+    cfg = IcePopConfig()
+    f = icepop_fwd(H, W, batch, cfg, layout="dv", store_probs=store_probs)
+    _, gw = icepop_bwd(H, W, batch, f, cfg, layout="dv", need_hidden=False)
+    finish(f.stats)
+    diag = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
+    assert diag.token_count == int(d["out_token_count"]) == 32768
+    assert diag.clipped_fraction == float(d["out_clipped_fraction"])
+    np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=4.5e-16, atol=0)
+    np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], atol=2e-3, rtol=1e-3)
+    np.testing.assert_allclose(f.entropy.cpu().numpy(), d["out_entropy"], atol=2e-3, rtol=1e-3)
+    assert diag.objective_value == pytest.approx(float(d["out_objective"]), rel=1e-3, abs=1e-5)
+    proj = torch.from_numpy(np.random.default_rng(C1_PROJ_SEED).standard_normal((w.shape[1], 4))).to(cuda_device)
+    gp = (gw.double() @ proj).cpu().numpy()
+    assert _rel(gp, d["out_grad_proj"]) < 1e-2
+    assert float(torch.linalg.vector_norm(gw.double())) == pytest.approx(float(d["out_grad_norm"]), rel=1e-2)
