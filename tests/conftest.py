@@ -3,6 +3,7 @@ everything else runs on the CPU build container."""
 
 from __future__ import annotations
 
+import functools
 import sys
 from pathlib import Path
 
@@ -22,7 +23,8 @@ def pytest_configure(config):
 def golden_cases() -> list[str]:
     """The small/medium reference cases (c1_config0, BASELINE configs[0] at full size, has its
     own schema and tests)."""
-    return sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem not in ("advantages", "c1_config0"))
+    return sorted(p.stem for p in GOLDEN.glob("*.npz")
+                  if p.stem not in ("advantages", "c1_config0", "c2_slice", "c3_slice"))
 
 
 def load_c1() -> tuple[dict, np.ndarray]:
@@ -40,15 +42,21 @@ def load_c1() -> tuple[dict, np.ndarray]:
 C1_PROJ_SEED = 7
 
 
-def load_c2_slice():
-    """C2-width slice fixture (make_golden.py c2_slice_case: 8 x 4,096 tokens, d = 4,096,
-    V = 157,184) and its regenerated weights as a bf16 torch tensor [4096, 157184] (exact: the
-    reference saw the same bf16-rounded values in fp64)."""
+# full-width slice fixtures (make_golden.py c2_slice_case): name -> (weight seed, hidden d)
+SLICES = {"c2_slice": (2511, 4096), "c3_slice": (2512, 8192)}
+
+
+@functools.lru_cache(maxsize=2)
+def load_slice(name: str):
+    """A full-width slice fixture (one GRPO group of 8 rollouts at V = 157,184) and its
+    regenerated weights as a bf16 torch tensor [d, V] (exact: the reference saw the same
+    bf16-rounded values in fp64)."""
     import torch
 
-    with np.load(GOLDEN / "c2_slice.npz") as z:
+    seed, d_hidden = SLICES[name]
+    with np.load(GOLDEN / f"{name}.npz") as z:
         d = {k: z[k] for k in z.files}
-    w = np.random.default_rng(2511).normal(0.0, 0.5, (4096, 157184))
+    w = np.random.default_rng(seed).normal(0.0, 0.5, (d_hidden, 157184))
     return d, torch.from_numpy(w).to(torch.bfloat16)
 
 

@@ -279,7 +279,8 @@ def c2s_weights() -> np.ndarray:
     return bf16_exact(w)
 
 
-def c2_slice_case() -> None:
+def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN, w_seed: int = C2S_W_SEED,
+                  w_scale: float = C2S_W_SCALE) -> None:
     """One GRPO group (8 rollouts x 4,096 tokens = 32,768 tokens) at BASELINE configs[1]'s full
     width (hidden 4,096, vocab 157,184) through the reference's own objective_and_grad (one
     pass, ~10 min on one core: a 4-hot gather and np.add.at over T x V per rollout). lp_train_old
@@ -287,21 +288,21 @@ def c2_slice_case() -> None:
     lp_infer_old = lp_train_old - N(0, 0.233). Stored like c1_config0 (gradient norm and
     projection)."""
     rng = np.random.default_rng(321)
-    theta = PolicyParams(c2s_weights(), 0)
-    task = TaskSpec(TaskKind.PARITY_MATCH, 5151, 0, C2S_LEN)
-    toks_all = rng.integers(0, C2S_V, (C2S_SEQS, C2S_LEN))
+    theta = PolicyParams(bf16_exact(np.random.default_rng(w_seed).normal(0.0, w_scale, (d, C2S_V))), 0)
+    task = TaskSpec(TaskKind.PARITY_MATCH, 5151, 0, seq_len)
+    toks_all = rng.integers(0, C2S_V, (C2S_SEQS, seq_len))
     rollouts = []
     for i in range(C2S_SEQS):
         recs = [TokenRecord(token=int(t), logp_infer_old=0.0, logp_train_old=0.0, logp_train_cur=0.0, gen_version=0)
                 for t in toks_all[i]]
         rollouts.append(Rollout(task=task, stream=np.random.default_rng(i), uid=i, group_uid=0, tokens=recs,
                                 terminal=True))
-        feats = _rollout_feats(task, recs, C2S_D)
+        feats = _rollout_feats(task, recs, d)
         z = theta.weights[feats[:, 0]] + theta.weights[feats[:, 1]] + theta.weights[feats[:, 2]] + \
             theta.weights[feats[:, 3]]
         m = z.max(axis=1)
         lse = m + np.log(np.exp(z - m[:, None]).sum(axis=1))
-        lp = z[np.arange(C2S_LEN), toks_all[i]] - lse
+        lp = z[np.arange(seq_len), toks_all[i]] - lse
         del z
         for rec, l in zip(recs, lp):
             rec.logp_train_old = float(l) + float(rng.normal(0.0, 0.1))
@@ -312,7 +313,7 @@ def c2_slice_case() -> None:
     cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C2S_SEQS)
     out = objective_and_grad([group], theta, theta, None, cfg, MaskingBounds(0.5, 5.0), 1.0)
     lp_written = np.asarray([rec.logp_train_cur for r in rollouts for rec in r.tokens])
-    data = pack([group], C2S_D)
+    data = pack([group], d)
     proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((C2S_V, 4))
     data.update(
         out_kept=out.per_token_mask_kept,
@@ -326,8 +327,8 @@ def c2_slice_case() -> None:
         out_grad_norm=np.asarray(np.linalg.norm(out.grad)),
         out_grad_proj=out.grad @ proj,
     )
-    np.savez_compressed(OUT / "c2_slice.npz", **data)
-    print(f"c2_slice: tokens={out.token_count} popped={int((~out.per_token_mask_kept).sum())} "
+    np.savez_compressed(OUT / f"{name}.npz", **data)
+    print(f"{name}: tokens={out.token_count} popped={int((~out.per_token_mask_kept).sum())} "
           f"J={out.objective_value:.6g} |grad|={out.grad_norm:.4g}")
 
 
@@ -335,3 +336,5 @@ if __name__ == "__main__":
     main()
     c1_case()
     c2_slice_case()
+    # BASELINE configs[2]/[4] width (hidden 8,192), a shorter group (8 x 2,048 tokens)
+    c2_slice_case("c3_slice", d=8192, seq_len=2048, w_seed=2512, w_scale=0.5)

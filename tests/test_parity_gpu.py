@@ -198,17 +198,20 @@ def test_config0_full_size_matches_reference(cuda_device, path):
 
 
 @pytest.mark.parametrize("store_probs", [True, False], ids=["probs", "recompute"])
-def test_c2_width_slice_matches_reference(cuda_device, store_probs):
-    """One GRPO group (8 x 4,096 = 32,768 tokens) at BASELINE configs[1]'s full width (hidden
-    4,096, vocab 157,184 = the Ling-2.0 lm_head) against the reference's own objective_and_grad
-    (tests/golden/c2_slice.npz, H = the reference's 4-hot features, exact in bf16): mask and
-    counts bit-exact; lp_cur / entropy / objective / dW (norm and fixed projection) within the
-    bf16 path's tolerances."""
-    from conftest import C1_PROJ_SEED, load_c2_slice
+@pytest.mark.parametrize("name", ["c2_slice", "c3_slice"])
+def test_full_width_slice_matches_reference(cuda_device, name, store_probs):
+    """One GRPO group at BASELINE's full lm_head width against the reference's own
+    objective_and_grad (H = the reference's 4-hot features, exact in bf16): c2_slice = 8 x 4,096
+    tokens at hidden 4,096 (configs[1]), c3_slice = 8 x 2,048 tokens at hidden 8,192
+    (configs[2]-[4]), vocab 157,184. Mask and counts bit-exact; lp_cur / entropy / objective /
+    dW (norm and a fixed projection) within the bf16 path's tolerances."""
+    from conftest import C1_PROJ_SEED, GOLDEN, load_slice
     from paper_2510_18855_b200.features import multihot
     from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
 
-    d, w = load_c2_slice()
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip(f"{name}.npz not generated")
+    d, w = load_slice(name)
     H = torch.from_numpy(multihot(d["feats"], w.shape[0])).to(torch.bfloat16).to(cuda_device)
     W = w.to(cuda_device)
     batch = _batch(d, cuda_device)
@@ -218,7 +221,7 @@ def test_c2_width_slice_matches_reference(cuda_device, store_probs):
     finish(f.stats)
     diag = Diagnostics.from_stats(f.stats.cpu())
     assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
-    assert diag.token_count == int(d["out_token_count"]) == 32768
+    assert diag.token_count == int(d["out_token_count"]) == len(d["tokens"])
     assert diag.clipped_fraction == float(d["out_clipped_fraction"])
     np.testing.assert_allclose(f.calib.cpu().numpy(), d["out_calibration"], rtol=4.5e-16, atol=0)
     np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], atol=2e-3, rtol=1e-3)
