@@ -1,7 +1,7 @@
 """Is the bench step host-bound anywhere? Time the C2 stored-probabilities step eagerly and
 as a CUDA-graph replay (the step is sync-free and capturable), interleaved on one box.
 
-    python profiles/graph_vs_eager.py [--rounds 3] [--steps 4]
+    python profiles/graph_vs_eager.py [--rounds 3] [--steps 4] [--config c2]
 """
 import argparse
 import sys
@@ -18,9 +18,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--config", default="c2", choices=sorted(bench.CONFIGS))
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
-    cfg = bench.CONFIGS["c2"]
+    cfg = bench.CONFIGS[a.config]
     meta = bench.make_batch_host(cfg, 0, 1)
     H, W, batch, _ = bench.build_device_inputs(cfg, meta, dev, 0)
     icfg = IcePopConfig()
