@@ -323,8 +323,9 @@ int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N
 int icepop_set_cta_group(int32_t cta_group);
 
 /* Tile shape of the long-K plain GEMMs (K4, K5) on CTA pairs: 1 (default) = 256 x 512 tiles
- * (two N = 256 MMAs per k step into one TMEM accumulator), 0 = 256 x 256. Process-wide; the
- * ICEPOP_WIDE_TILES environment variable sets the initial value. */
+ * (two N = 256 MMAs per k step into one TMEM accumulator) unless the output is too small to
+ * fill the GPU with them (then 256 x 256), 2 = 256 x 512 always, 0 = 256 x 256 always.
+ * Process-wide; the ICEPOP_WIDE_TILES environment variable sets the initial value. */
 int icepop_set_wide_tiles(int32_t enable);
 
 /* Tile shape of K1 (the forward GEMM with the softmax epilogue) on CTA pairs: 0 (default) =

@@ -269,8 +269,8 @@ inline int bn_of(int epi) { return epi_dual(epi) ? 128 : BN_; }
 int g_wide_tiles = -1;
 
 bool wide_tiles() {
-  if (g_wide_tiles < 0) g_wide_tiles = env_int("ICEPOP_WIDE_TILES", 1) ? 1 : 0;
-  return g_wide_tiles == 1;
+  if (g_wide_tiles < 0) g_wide_tiles = std::min(env_int("ICEPOP_WIDE_TILES", 1), 2);
+  return g_wide_tiles >= 1;
 }
 
 // K1 (EPI_LSE) on 256 x 512 tiles: one TMEM accumulator released to the MMA warp in halves
@@ -286,6 +286,17 @@ bool k1_wide() {
 int k1_bn() { return k1_wide() ? BN_WIDE : BN_; }
 // Partial (max, sum, q) triples per token that K1 writes: one per tile half (umma_gemm.cuh epi_lse).
 int64_t k1_parts(int64_t V) { return 2 * ((V + k1_bn() - 1) / k1_bn()); }
+
+// A 512-wide tile does the work of two 256-wide ones ~5% cheaper (fewer operand bytes per
+// FLOP) but halves the tile count. On a small output (C1's dH: 32 wide tiles for 74 CTA
+// pairs) that leaves pairs idle, so the long-K GEMMs take wide tiles only when their wave
+// count costs no more than the narrow tiles' (weighted by that 5%).
+bool wide_pays(int64_t M, int64_t N, int64_t units) {
+  const int64_t m_t = (M + 2 * BM - 1) / (2 * BM);
+  const int64_t waves_w = (m_t * ((N + BN_WIDE - 1) / BN_WIDE) + units - 1) / units;
+  const int64_t waves_n = (m_t * ((N + BN_ - 1) / BN_) + units - 1) / units;
+  return 2 * waves_w * 95 <= waves_n * 100;
+}
 
 // Device-side block lists of a block-sparse GEMM (GemmShape::kb_map ...), or none.
 struct Sparse {
@@ -303,7 +314,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
     return fail(ICEPOP_EINVAL, "GEMM extent too large");
   const int cg = cta_group();
   const bool long_k = (K + BK - 1) / BK >= long_k_blocks();
-  const bool wide = (epi == EPI_STORE && cg == 2 && long_k && wide_tiles()) || (epi == EPI_LSE && k1_wide());
+  bool wide = (epi == EPI_STORE && cg == 2 && long_k && wide_tiles()) || (epi == EPI_LSE && k1_wide());
+  if (wide && epi == EPI_STORE && g_wide_tiles != 2) wide = wide_pays(M, N, num_sms() / cg);
   const int bn = wide ? BN_WIDE : bn_of(epi);
   if (epi_dual(epi) && !B2) return fail(ICEPOP_EINVAL, "dual-accumulator GEMM needs a second B operand");
   CUtensorMap ta, tb, tb2;
@@ -1353,7 +1365,7 @@ int icepop_set_cta_group(int32_t cta_group) {
 }
 
 int icepop_set_wide_tiles(int32_t enable) {
-  g_wide_tiles = enable ? 1 : 0;
+  g_wide_tiles = enable <= 0 ? 0 : (enable >= 2 ? 2 : 1);
   return ICEPOP_OK;
 }
 

@@ -63,11 +63,11 @@ def wide_tiles():
 
     lib = _lib.ensure_device(0)
 
-    def set_(on):
-        _lib.check(lib.icepop_set_wide_tiles(int(on)))
+    def set_(on):  # on: 512-wide tiles forced (2), not only where they fill the GPU (1)
+        _lib.check(lib.icepop_set_wide_tiles(2 if on else 0))
 
     yield set_
-    set_(True)
+    _lib.check(lib.icepop_set_wide_tiles(1))
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
@@ -90,3 +90,27 @@ def test_gemm_long_k_wide_tiles(cuda_device, wide_tiles, a_mn, b_mn, M, N, K):
     assert torch.equal(Cw, Cn)
     assert torch.equal(Cw_acc, Cw + 0.5)
     assert torch.equal(Cw_bf, Cw.to(torch.bfloat16))
+
+
+def test_small_long_k_output_takes_narrow_tiles_with_same_bits(cuda_device, wide_tiles):
+    """A long-K GEMM whose output is too small to fill the GPU with 256x512 tiles (C1's dH:
+    4,096 x 1,024 at K = 32,768) runs on 256x256 tiles by default; all three settings give the
+    same bits (fp32 accumulation order along K is the same for both tile widths)."""
+    from paper_2510_18855_b200 import _lib
+
+    lib = _lib.ensure_device(0)
+    M, N, K = 4096, 1024, 32768
+    g = torch.Generator(device=cuda_device).manual_seed(5)
+    A = torch.randn(M, K, device=cuda_device, generator=g).to(torch.bfloat16)
+    B = torch.randn(K, N, device=cuda_device, generator=g).to(torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for mode in (1, 2, 0):
+        _lib.check(lib.icepop_set_wide_tiles(mode))
+        C = torch.empty(M, N, device=cuda_device, dtype=torch.float32)
+        _lib.check(lib.icepop_gemm_bf16(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, 0, 1, 1, 0, st))
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = A.float() @ B.float()
+    assert float((outs[0] - ref).norm() / ref.norm()) < 1e-4  # fp32 summation order over K = 32,768

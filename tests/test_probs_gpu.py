@@ -241,7 +241,7 @@ def test_long_k_backward_wide_tiles(cuda_device, layout):
     try:
         _lib.check(lib.icepop_set_skip_inactive(0))  # keep dZ rows in token order for the reference below
         for wide in (1, 0):
-            _lib.check(lib.icepop_set_wide_tiles(wide))
+            _lib.check(lib.icepop_set_wide_tiles(2 * wide))  # 2: 512-wide tiles forced
             f = icepop_fwd(H, W, _batch(c, cuda_device), cfg, layout=layout, store_probs=True)
             gh, gw = icepop_bwd(H, W, _batch(c, cuda_device), f, cfg, layout=layout, grad_hidden_dtype=torch.float32)
             res[wide] = (gh, gw)
