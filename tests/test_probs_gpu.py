@@ -505,3 +505,45 @@ def test_k1_wide_tile_matches_default(cuda_device, V, layout):
     assert _rel(gh1.cpu().numpy(), gh0.cpu().numpy()) < 1e-4
     o = _oracle(c)
     assert _rel(gw1.cpu().numpy(), o["grad_weight"]) < 1e-2
+
+
+def test_fwd_bwd_chunk_allocation_fallback(cuda_device, monkeypatch):
+    """icepop_fwd_bwd's probabilities buffer: if the chunk the memory estimate picked does not
+    allocate, the chunk halves, the result equals that chunking, and the size that allocated
+    is remembered (later calls do not pay the failed allocation again)."""
+    import paper_2510_18855_b200.loss as L
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd_bwd
+
+    c = _case(n_seqs=6, seed=88, V=1000, lens=[3000, 2100, 1700, 900, 4000, 2500])
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    cfg = IcePopConfig()
+    ref, gh_ref, gw_ref = icepop_fwd_bwd(H, W, _batch(c, cuda_device), cfg, grad_hidden_dtype=torch.float32,
+                                         max_chunk_tokens=4096)
+    real_empty = torch.empty
+    calls = []
+
+    def fake_empty(*shape, **kw):
+        size = tuple(shape[0]) if len(shape) == 1 and isinstance(shape[0], tuple) else tuple(shape)
+        if kw.get("dtype") == torch.bfloat16 and len(size) == 2 and size[1] == 1000:
+            calls.append(size[0])
+            if size[0] > 4096:
+                raise torch.OutOfMemoryError("simulated")
+        return real_empty(*shape, **kw)
+
+    key = (cuda_device.index if cuda_device.index is not None else 0, 1000)
+    L._PROBS_CHUNK_OK.pop(key, None)
+    monkeypatch.setattr(L.torch, "empty", fake_empty)
+    try:
+        f, gh, gw = icepop_fwd_bwd(H, W, _batch(c, cuda_device), cfg, grad_hidden_dtype=torch.float32,
+                                   max_chunk_tokens=8192)
+        assert calls[:2] == [8192, 4096] and L._PROBS_CHUNK_OK[key] == 4096
+        calls.clear()
+        icepop_fwd_bwd(H, W, _batch(c, cuda_device), cfg, grad_hidden_dtype=torch.float32, max_chunk_tokens=8192)
+        assert calls[0] == 4096  # remembered: no failed attempt
+    finally:
+        monkeypatch.undo()
+        L._PROBS_CHUNK_OK.pop(key, None)
+    assert f.extras["chunks"] == ref.extras["chunks"]
+    for name in ("lse", "lp_cur", "kept", "coeff"):
+        assert torch.equal(getattr(f, name), getattr(ref, name)), name
+    assert torch.equal(gh, gh_ref) and torch.equal(gw, gw_ref)
