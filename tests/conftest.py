@@ -24,7 +24,7 @@ def golden_cases() -> list[str]:
     """The small/medium reference cases (c1_config0, BASELINE configs[0] at full size, has its
     own schema and tests)."""
     return sorted(p.stem for p in GOLDEN.glob("*.npz")
-                  if p.stem not in ("advantages", "c1_config0", "c2_slice", "c3_slice"))
+                  if p.stem not in ("advantages", "c1_config0", "c2_slice", "c3_slice", "c2_slice_kl"))
 
 
 def load_c1() -> tuple[dict, np.ndarray]:
@@ -43,7 +43,21 @@ C1_PROJ_SEED = 7
 
 
 # full-width slice fixtures (make_golden.py c2_slice_case): name -> (weight seed, hidden d)
-SLICES = {"c2_slice": (2511, 4096), "c3_slice": (2512, 8192)}
+SLICES = {"c2_slice": (2511, 4096), "c3_slice": (2512, 8192), "c2_slice_kl": (2511, 4096)}
+
+
+def slice_weight_ref(name: str):
+    """The reference policy of a KL slice fixture: bf16(W + N(0, 0.1)) with the fixture's
+    ref_seed, W the bf16-exact weights (make_golden.py c2_slice_case)."""
+    import torch
+
+    seed, d_hidden = SLICES[name]
+    with np.load(GOLDEN / f"{name}.npz") as z:
+        ref_seed = int(z["ref_seed"])
+    w = np.random.default_rng(seed).normal(0.0, 0.5, (d_hidden, 157184))
+    w = torch.from_numpy(w).to(torch.bfloat16).to(torch.float64).numpy()
+    w += np.random.default_rng(ref_seed).normal(0.0, 0.1, w.shape)
+    return torch.from_numpy(w).to(torch.bfloat16)
 
 
 @functools.lru_cache(maxsize=2)

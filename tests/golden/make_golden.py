@@ -280,7 +280,7 @@ def c2s_weights() -> np.ndarray:
 
 
 def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN, w_seed: int = C2S_W_SEED,
-                  w_scale: float = C2S_W_SCALE) -> None:
+                  w_scale: float = C2S_W_SCALE, kl_coeff: float = 0.0, ref_seed: int | None = None) -> None:
     """One GRPO group (8 rollouts x 4,096 tokens = 32,768 tokens) at BASELINE configs[1]'s full
     width (hidden 4,096, vocab 157,184) through the reference's own objective_and_grad (one
     pass, ~10 min on one core: a 4-hot gather and np.add.at over T x V per rollout). lp_train_old
@@ -310,8 +310,11 @@ def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN
     rewards = [float(x) for x in rng.normal(0.5, 0.5, C2S_SEQS)]
     group = PromptGroup(task=task, rollouts=rollouts, rewards=rewards,
                         advantages=[float(a) for a in group_advantages(rewards)])
-    cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C2S_SEQS)
-    out = objective_and_grad([group], theta, theta, None, cfg, MaskingBounds(0.5, 5.0), 1.0)
+    ref = None
+    if ref_seed is not None:  # KL-to-ref term (objective.py:254-263) against a perturbed reference policy
+        ref = PolicyParams(bf16_exact(theta.weights + np.random.default_rng(ref_seed).normal(0.0, 0.1, theta.weights.shape)))
+    cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C2S_SEQS, kl_coeff=kl_coeff)
+    out = objective_and_grad([group], theta, theta, ref, cfg, MaskingBounds(0.5, 5.0), 1.0)
     lp_written = np.asarray([rec.logp_train_cur for r in rollouts for rec in r.tokens])
     data = pack([group], d)
     proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((C2S_V, 4))
@@ -326,6 +329,9 @@ def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN
         out_token_count=np.asarray(out.token_count),
         out_grad_norm=np.asarray(np.linalg.norm(out.grad)),
         out_grad_proj=out.grad @ proj,
+        out_kl_to_ref=np.asarray(out.kl_to_ref),
+        kl_coeff=np.asarray(kl_coeff),
+        ref_seed=np.asarray(-1 if ref_seed is None else ref_seed),
     )
     np.savez_compressed(OUT / f"{name}.npz", **data)
     print(f"{name}: tokens={out.token_count} popped={int((~out.per_token_mask_kept).sum())} "
@@ -338,3 +344,5 @@ if __name__ == "__main__":
     c2_slice_case()
     # BASELINE configs[2]/[4] width (hidden 8,192), a shorter group (8 x 2,048 tokens)
     c2_slice_case("c3_slice", d=8192, seq_len=2048, w_seed=2512, w_scale=0.5)
+    # the KL-to-ref term (gamma = 0.4) at configs[1]'s width: the dual-accumulator GEMMs
+    c2_slice_case("c2_slice_kl", seq_len=2048, kl_coeff=0.4, ref_seed=77)

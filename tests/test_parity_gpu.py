@@ -231,3 +231,36 @@ def test_full_width_slice_matches_reference(cuda_device, name, store_probs):
     gp = (gw.double() @ proj).cpu().numpy()
     assert _rel(gp, d["out_grad_proj"]) < 1e-2
     assert float(torch.linalg.vector_norm(gw.double())) == pytest.approx(float(d["out_grad_norm"]), rel=1e-2)
+
+
+def test_full_width_kl_slice_matches_reference(cuda_device):
+    """The KL-to-ref term (gamma = 0.4, objective.py:254-263) at configs[1]'s width (8 x 2,048
+    tokens, hidden 4,096, vocab 157,184; reference policy = W + N(0, 0.1)) against the
+    reference's own objective_and_grad (tests/golden/c2_slice_kl.npz): the dual-accumulator
+    K1r/K3r GEMMs. Mask and counts bit-exact; kl_to_ref, objective, lp_cur and dW (norm and
+    projection) within the bf16 path's tolerances."""
+    from conftest import C1_PROJ_SEED, GOLDEN, load_slice, slice_weight_ref
+    from paper_2510_18855_b200.features import multihot
+    from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
+
+    if not (GOLDEN / "c2_slice_kl.npz").exists():
+        pytest.skip("c2_slice_kl.npz not generated")
+    d, w = load_slice("c2_slice_kl")
+    wr = slice_weight_ref("c2_slice_kl")
+    H = torch.from_numpy(multihot(d["feats"], w.shape[0])).to(torch.bfloat16).to(cuda_device)
+    W, Wr = w.to(cuda_device), wr.to(cuda_device)
+    batch = _batch(d, cuda_device)
+    cfg = IcePopConfig(kl_coeff=float(d["kl_coeff"]))
+    f = icepop_fwd(H, W, batch, cfg, layout="dv", weight_ref=Wr)
+    _, gw = icepop_bwd(H, W, batch, f, cfg, layout="dv", weight_ref=Wr, need_hidden=False)
+    finish(f.stats)
+    diag = Diagnostics.from_stats(f.stats.cpu())
+    assert np.array_equal(f.kept.cpu().numpy().astype(bool), d["out_kept"])
+    assert diag.token_count == int(d["out_token_count"]) == len(d["tokens"])
+    assert diag.clipped_fraction == float(d["out_clipped_fraction"])
+    np.testing.assert_allclose(f.lp_cur.cpu().numpy(), d["out_lp_cur"], atol=2e-3, rtol=1e-3)
+    assert diag.kl_to_ref == pytest.approx(float(d["out_kl_to_ref"]), rel=1e-2, abs=1e-5)
+    assert diag.objective_value == pytest.approx(float(d["out_objective"]), rel=1e-3, abs=1e-5)
+    proj = torch.from_numpy(np.random.default_rng(C1_PROJ_SEED).standard_normal((w.shape[1], 4))).to(cuda_device)
+    assert _rel((gw.double() @ proj).cpu().numpy(), d["out_grad_proj"]) < 1e-2
+    assert float(torch.linalg.vector_norm(gw.double())) == pytest.approx(float(d["out_grad_norm"]), rel=1e-2)
