@@ -24,7 +24,7 @@ def golden_cases() -> list[str]:
     """The small/medium reference cases (c1_config0, BASELINE configs[0] at full size, has its
     own schema and tests)."""
     return sorted(p.stem for p in GOLDEN.glob("*.npz")
-                  if p.stem not in ("advantages", "c1_config0", "c2_slice", "c3_slice", "c2_slice_kl"))
+                  if p.stem not in ("advantages", "c1_config0") and "slice" not in p.stem)
 
 
 def load_c1() -> tuple[dict, np.ndarray]:
@@ -43,7 +43,8 @@ C1_PROJ_SEED = 7
 
 
 # full-width slice fixtures (make_golden.py c2_slice_case): name -> (weight seed, hidden d)
-SLICES = {"c2_slice": (2511, 4096), "c3_slice": (2512, 8192), "c2_slice_kl": (2511, 4096)}
+SLICES = {"c2_slice": (2511, 4096), "c3_slice": (2512, 8192), "c2_slice_kl": (2511, 4096),
+          "c2_slice_tis": (2511, 4096)}
 
 
 def slice_weight_ref(name: str):

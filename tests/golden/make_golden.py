@@ -280,7 +280,8 @@ def c2s_weights() -> np.ndarray:
 
 
 def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN, w_seed: int = C2S_W_SEED,
-                  w_scale: float = C2S_W_SCALE, kl_coeff: float = 0.0, ref_seed: int | None = None) -> None:
+                  w_scale: float = C2S_W_SCALE, kl_coeff: float = 0.0, ref_seed: int | None = None,
+                  algo: Algo = Algo.ICEPOP, temperature: float = 1.0) -> None:
     """One GRPO group (8 rollouts x 4,096 tokens = 32,768 tokens) at BASELINE configs[1]'s full
     width (hidden 4,096, vocab 157,184) through the reference's own objective_and_grad (one
     pass, ~10 min on one core: a 4-hot gather and np.add.at over T x V per rollout). lp_train_old
@@ -298,8 +299,8 @@ def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN
         rollouts.append(Rollout(task=task, stream=np.random.default_rng(i), uid=i, group_uid=0, tokens=recs,
                                 terminal=True))
         feats = _rollout_feats(task, recs, d)
-        z = theta.weights[feats[:, 0]] + theta.weights[feats[:, 1]] + theta.weights[feats[:, 2]] + \
-            theta.weights[feats[:, 3]]
+        z = (theta.weights[feats[:, 0]] + theta.weights[feats[:, 1]] + theta.weights[feats[:, 2]] +
+             theta.weights[feats[:, 3]]) / temperature
         m = z.max(axis=1)
         lse = m + np.log(np.exp(z - m[:, None]).sum(axis=1))
         lp = z[np.arange(seq_len), toks_all[i]] - lse
@@ -313,8 +314,8 @@ def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN
     ref = None
     if ref_seed is not None:  # KL-to-ref term (objective.py:254-263) against a perturbed reference policy
         ref = PolicyParams(bf16_exact(theta.weights + np.random.default_rng(ref_seed).normal(0.0, 0.1, theta.weights.shape)))
-    cfg = ObjectiveConfig(algo=Algo.ICEPOP, group_size=C2S_SEQS, kl_coeff=kl_coeff)
-    out = objective_and_grad([group], theta, theta, ref, cfg, MaskingBounds(0.5, 5.0), 1.0)
+    cfg = ObjectiveConfig(algo=algo, group_size=C2S_SEQS, kl_coeff=kl_coeff)
+    out = objective_and_grad([group], theta, theta, ref, cfg, MaskingBounds(0.5, 5.0), temperature)
     lp_written = np.asarray([rec.logp_train_cur for r in rollouts for rec in r.tokens])
     data = pack([group], d)
     proj = np.random.default_rng(C1_PROJ_SEED).standard_normal((C2S_V, 4))
@@ -331,6 +332,8 @@ def c2_slice_case(name: str = "c2_slice", d: int = C2S_D, seq_len: int = C2S_LEN
         out_grad_proj=out.grad @ proj,
         out_kl_to_ref=np.asarray(out.kl_to_ref),
         kl_coeff=np.asarray(kl_coeff),
+        algo=np.asarray(algo.value),
+        temperature=np.asarray(temperature),
         ref_seed=np.asarray(-1 if ref_seed is None else ref_seed),
     )
     np.savez_compressed(OUT / f"{name}.npz", **data)
@@ -346,3 +349,5 @@ if __name__ == "__main__":
     c2_slice_case("c3_slice", d=8192, seq_len=2048, w_seed=2512, w_scale=0.5)
     # the KL-to-ref term (gamma = 0.4) at configs[1]'s width: the dual-accumulator GEMMs
     c2_slice_case("c2_slice_kl", seq_len=2048, kl_coeff=0.4, ref_seed=77)
+    # TIS at temperature 0.7, configs[1]'s width
+    c2_slice_case("c2_slice_tis", seq_len=2048, algo=Algo.TIS, temperature=0.7)

@@ -198,12 +198,13 @@ def test_config0_full_size_matches_reference(cuda_device, path):
 
 
 @pytest.mark.parametrize("store_probs", [True, False], ids=["probs", "recompute"])
-@pytest.mark.parametrize("name", ["c2_slice", "c3_slice"])
+@pytest.mark.parametrize("name", ["c2_slice", "c3_slice", "c2_slice_tis"])
 def test_full_width_slice_matches_reference(cuda_device, name, store_probs):
     """One GRPO group at BASELINE's full lm_head width against the reference's own
     objective_and_grad (H = the reference's 4-hot features, exact in bf16): c2_slice = 8 x 4,096
     tokens at hidden 4,096 (configs[1]), c3_slice = 8 x 2,048 tokens at hidden 8,192
-    (configs[2]-[4]), vocab 157,184. Mask and counts bit-exact; lp_cur / entropy / objective /
+    (configs[2]-[4]), c2_slice_tis = TIS at temperature 0.7, 8 x 2,048 tokens at hidden 4,096;
+    vocab 157,184. Mask and counts bit-exact; lp_cur / entropy / objective /
     dW (norm and a fixed projection) within the bf16 path's tolerances."""
     from conftest import C1_PROJ_SEED, GOLDEN, load_slice
     from paper_2510_18855_b200.features import multihot
@@ -215,7 +216,8 @@ def test_full_width_slice_matches_reference(cuda_device, name, store_probs):
     H = torch.from_numpy(multihot(d["feats"], w.shape[0])).to(torch.bfloat16).to(cuda_device)
     W = w.to(cuda_device)
     batch = _batch(d, cuda_device)
-    cfg = IcePopConfig()
+    cfg = IcePopConfig(algo=str(d["algo"]) if "algo" in d else "icepop",
+                       temperature=float(d["temperature"]) if "temperature" in d else 1.0)
     f = icepop_fwd(H, W, batch, cfg, layout="dv", store_probs=store_probs)
     _, gw = icepop_bwd(H, W, batch, f, cfg, layout="dv", need_hidden=False)
     finish(f.stats)
