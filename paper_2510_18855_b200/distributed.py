@@ -112,7 +112,9 @@ def stream_barrier(group=None, device=None) -> None:
     queued after it starts only when every rank has finished the work queued before it."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
-    t = torch.zeros(1, device=device if device is not None else torch.cuda.current_device())
+    if device is None:
+        device = "cpu" if dist.get_backend(group) == "gloo" else torch.cuda.current_device()
+    t = torch.zeros(1, device=device)
     dist.all_reduce(t, group=group)
 
 
@@ -160,11 +162,17 @@ class PeerSlots:
             t.slots[o] = p
         return t
 
-    def fold(self, out: torch.Tensor) -> torch.Tensor:
-        """out (fp32, shard_elems) = sum of this rank's slots over ranks 0..world-1."""
+    def fold(self, out: torch.Tensor, release: bool = True) -> torch.Tensor:
+        """out (fp32, shard_elems) = sum of this rank's slots over ranks 0..world-1.
+
+        With ``release`` (default) a second ``stream_barrier`` follows the fold: a peer's next
+        K5 (which stores into these slots) cannot start before every rank has folded, so the
+        slots are never overwritten while still being read (write-after-read across steps)."""
         if out.dtype != torch.float32 or out.numel() != self.shard_elems or not out.is_contiguous():
             raise ValueError("out must be a contiguous fp32 tensor of shard_rows * row_len elements")
         self._ops.fold(self.local, self.world, self.shard_elems, out)
+        if release and self.world > 1:
+            stream_barrier(self.group)
         return out
 
     def close(self) -> None:

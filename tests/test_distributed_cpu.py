@@ -211,3 +211,45 @@ def test_peer_slots_exchange_handles(world):
         assert (w, rk, sr) == (world, r, 5)
         assert slots[r] == 1000 + r
         assert [s for o, s in enumerate(slots) if o != r] == [5000 + 1000 + o for o in range(world) if o != r]
+
+
+class _RecordingPeerOps(_FakePeerOps):
+    """Fake ops whose fold logs this rank's event; the log is shared through a file."""
+
+    def __init__(self, rank, log):
+        super().__init__(rank)
+        self.log = log
+
+    def fold(self, local, world, shard_elems, out):
+        import time
+
+        time.sleep(0.3 * (world - 1 - self.rank))  # lower ranks fold late
+        with open(self.log, "a") as f:
+            f.write(f"fold {self.rank}\n")
+
+
+def _fold_release_fn(rank, world):
+    from paper_2510_18855_b200.distributed import PeerSlots
+
+    log = os.environ["ICEPOP_TEST_FOLD_LOG"]
+    ps = PeerSlots(shard_rows=5, row_len=8, _ops=_RecordingPeerOps(rank, log))
+    ps.fold(torch.empty(40, dtype=torch.float32))
+    # after fold returns, the next step's K5 may store into peers' slots: every rank must
+    # already have folded
+    with open(log, "a") as f:
+        f.write(f"next {rank}\n")
+    return True
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_slots_fold_releases_slots_only_after_every_rank_folded(world, tmp_path, monkeypatch):
+    """Write-after-read across steps: no rank leaves fold() (and so no rank's next K5 writes
+    into a peer slot) before every owner has finished reading its slots."""
+    log = tmp_path / "fold.log"
+    monkeypatch.setenv("ICEPOP_TEST_FOLD_LOG", str(log))
+    run_ranks(_fold_release_fn, world=world)
+    lines = log.read_text().split()
+    events = [(lines[i], int(lines[i + 1])) for i in range(0, len(lines), 2)]
+    last_fold = max(i for i, (e, _) in enumerate(events) if e == "fold")
+    first_next = min(i for i, (e, _) in enumerate(events) if e == "next")
+    assert last_fold < first_next, events
