@@ -510,9 +510,9 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
     bufs = [{k: torch.empty_like(v, device=dev) for k, v in host.items()} for _ in range(2)]
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     out_host = torch.empty(8, dtype=torch.float64).pin_memory()
-    # the first step's copy cannot overlap anything: time 8 to 16 steps so that this start-up
+    # the first step's copy cannot overlap anything: time 16 to 32 steps so that this start-up
     # exposure (~40 ms at C2) stays small (every step's copy is still inside the timed region)
-    steps = max(8, min(args.steps, 16))
+    steps = max(16, min(args.steps, 32))
     main = torch.cuda.current_stream(dev)
     copy_stream = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
