@@ -58,6 +58,16 @@ def rollout_feats(prompt_id: int, token_ids, n_features: int) -> np.ndarray:
     return feats
 
 
+def multihot_device(feats, n_features: int, dtype):
+    """`multihot` built on the GPU from the [N, 4] feature ids (a device int64 tensor): the
+    counts are small integers, so the float scatter-add is exact in any order."""
+    import torch
+
+    h = torch.zeros((feats.shape[0], n_features), dtype=torch.float32, device=feats.device)
+    h.scatter_add_(1, feats, torch.ones(feats.shape, dtype=torch.float32, device=feats.device))
+    return h.to(dtype)
+
+
 def multihot(feats: np.ndarray, n_features: int, dtype=np.float64) -> np.ndarray:
     """Dense H[t, f] = multiplicity of row f among the 4 feature rows of position t."""
     h = np.zeros((feats.shape[0], n_features), dtype=dtype)

@@ -226,7 +226,7 @@ def objective_and_grad(
     """
     import torch
 
-    from .features import multihot
+    from .features import multihot_device
     from .loss import Diagnostics, IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd, icepop_fwd_bwd
 
     if temperature <= 0:
@@ -245,8 +245,9 @@ def objective_and_grad(
         group_offsets=torch.from_numpy(p.go).to(dev),
         advantages=torch.from_numpy(p.adv).to(dev),
     )
+    feats = torch.from_numpy(np.ascontiguousarray(p.feats, dtype=np.int64)).to(dev)
     if precision == "fp64":
-        H = torch.from_numpy(multihot(p.feats, n_features)).to(dev)
+        H = multihot_device(feats, n_features, torch.float64)
         W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
         Wr = torch.from_numpy(np.ascontiguousarray(ref.weights, dtype=np.float64)).to(dev) if ref is not None else None
         fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
@@ -257,11 +258,13 @@ def objective_and_grad(
         nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
 
         def pad_bf16(w):
-            wn = np.zeros((nf_pad, vocab))
-            wn[:n_features] = w
-            return torch.from_numpy(wn).to(torch.bfloat16).to(dev)
+            # round on the host (torch's threaded cast), copy a quarter of the fp64 bytes
+            wb = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)).to(torch.bfloat16)
+            if nf_pad != n_features:
+                wb = torch.cat([wb, wb.new_zeros((nf_pad - n_features, vocab))])
+            return wb.to(dev)
 
-        H = torch.from_numpy(multihot(p.feats, nf_pad)).to(torch.bfloat16).to(dev)
+        H = multihot_device(feats, nf_pad, torch.bfloat16)
         W = pad_bf16(theta.weights)
         Wr = pad_bf16(ref.weights) if ref is not None else None
         # value and gradient together: stored probabilities (in token chunks if needed)
@@ -271,11 +274,12 @@ def objective_and_grad(
         raise ValueError("precision must be 'fp64' or 'bf16'")
     finish(fwd.stats)
     diag = Diagnostics.from_stats(fwd.stats.cpu())
+    grad_finite = bool(torch.isfinite(gw).all())
     grad = gw.to(torch.float64).cpu().numpy()
     lp_cur = fwd.lp_cur.cpu().numpy()
     for rec, value in zip(p.records, lp_cur):  # objective.py:224-225
         rec.logp_train_cur = float(value)
-    if not math.isfinite(diag.objective_value) or not np.isfinite(grad).all():
+    if not math.isfinite(diag.objective_value) or not grad_finite:
         raise NumericError("objective or gradient is not finite")
     kept = fwd.kept.cpu().numpy().astype(bool)
     return LossBreakdown(
