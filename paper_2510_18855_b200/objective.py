@@ -218,12 +218,22 @@ def objective_and_grad(
     *,
     precision: str | None = None,
     device=None,
+    grad_out: np.ndarray | None = None,
 ) -> LossBreakdown:
     """Objective value and its exact analytic ascent gradient w.r.t. theta, on the GPU.
 
     Same contract as objective.py:172-298, including the write-back of the recomputed
     lp_cur into every TokenRecord (objective.py:224-225).
+
+    ``grad_out`` (extension, keyword only): a C-contiguous float64 array shaped like
+    theta.weights that receives the gradient and is returned as ``LossBreakdown.grad``.
+    A trainer that reuses one buffer skips materialising a fresh 8*n_features*V-byte array per
+    call, which dominates the call at small batches.
     """
+    if grad_out is not None and (not isinstance(grad_out, np.ndarray) or grad_out.dtype != np.float64
+                                 or grad_out.shape != tuple(theta.weights.shape)
+                                 or not grad_out.flags.c_contiguous or not grad_out.flags.writeable):
+        raise ValueError("grad_out must be a writeable C-contiguous float64 array shaped like theta.weights")
     import torch
 
     from .features import multihot_device
@@ -275,7 +285,11 @@ def objective_and_grad(
     finish(fwd.stats)
     diag = Diagnostics.from_stats(fwd.stats.cpu())
     grad_finite = bool(torch.isfinite(gw).all())
-    grad = gw.to(torch.float64).cpu().numpy()
+    if grad_out is not None:
+        torch.from_numpy(grad_out).copy_(gw.to(torch.float64))
+        grad = grad_out
+    else:
+        grad = gw.to(torch.float64).cpu().numpy()
     lp_cur = fwd.lp_cur.cpu().numpy()
     for rec, value in zip(p.records, lp_cur):  # objective.py:224-225
         rec.logp_train_cur = float(value)

@@ -94,6 +94,17 @@ def main():
         kept_eq = np.array_equal(np.asarray(out.per_token_mask_kept), np.asarray(ref.per_token_mask_kept))
         j_rel = abs(out.objective_value - ref.objective_value) / max(abs(ref.objective_value), 1e-30)
         g_rel = float(np.linalg.norm(out.grad - ref.grad) / max(np.linalg.norm(ref.grad), 1e-30))
+        buf = np.empty_like(w)
+        tb = []
+        for _ in range(a.reps):
+            gs = copy.deepcopy(groups)
+            t0 = time.perf_counter()
+            dropin.objective_and_grad(gs, theta, theta, None, cfg, bounds, precision=precision, grad_out=buf)
+            tb.append(time.perf_counter() - t0)
+        tb.sort()
+        print(f"drop-in {precision} with a reused grad_out: {tb[len(tb) // 2] * 1e3:.1f} ms per call "
+              f"({t_ref / tb[len(tb) // 2]:.0f}x the reference); same grad bits as the fresh array: "
+              f"{np.array_equal(buf, out.grad)}")
         print(f"drop-in {precision}: {t * 1e3:.1f} ms per call (median of {a.reps}; min {ts[0] * 1e3:.1f}) = "
               f"{n_tok / t:.0f} tokens/s, {t_ref / t:.0f}x the reference; mask bit-exact {kept_eq}, "
               f"J rel {j_rel:.2e}, grad rel {g_rel:.2e}, token_count {out.token_count}, "

@@ -134,6 +134,25 @@ def test_dropin_bf16_matches_reference_golden(name):
     assert np.linalg.norm(out.grad - d["out_grad"]) / np.linalg.norm(d["out_grad"]) < 1e-2
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp64"])
+def test_dropin_grad_out_receives_the_same_gradient(precision):
+    """grad_out (keyword extension): the gradient lands in the caller's array, bit-identical to
+    the freshly allocated one, and LossBreakdown.grad is that array; a bad buffer is refused."""
+    O = _obj()
+    d = load_golden("medium_icepop")
+    cfg, bounds = cfg_of(d)
+    args = (Params(d["weight"], 1), Params(d["weight"], 0), None, cfg, bounds, d["temperature"])
+    fresh = O.objective_and_grad(groups_from_golden(d), *args, precision=precision)
+    buf = np.full(d["weight"].shape, np.nan)
+    out = O.objective_and_grad(groups_from_golden(d), *args, precision=precision, grad_out=buf)
+    assert out.grad is buf
+    assert np.array_equal(buf, fresh.grad)
+    assert out.objective_value == fresh.objective_value
+    for bad in (np.zeros(d["weight"].shape, np.float32), np.zeros((2, 3)), np.asfortranarray(buf)):
+        with pytest.raises(ValueError):
+            O.objective_and_grad(groups_from_golden(d), *args, precision=precision, grad_out=bad)
+
+
 # ------------------------------------------------------------------ reference semantics
 def test_degenerate_case_all_algorithms_bit_identical():
     """test_objective.py:133-146: calib == 1 and theta == theta_old -> algos agree bitwise."""
