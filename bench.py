@@ -3,6 +3,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
     torchrun --nproc-per-node N bench.py --gpus N ...        (token-sharded, weak scaling)
 
+`--gpus N` (N > 1) without torchrun starts the N ranks itself (torch.distributed.run on
+127.0.0.1, NCCL_DEBUG=INFO with the INIT subsystem so the communicator's nranks is logged) and
+refuses when fewer than N GPUs are visible. `--dry-run` runs the rank plumbing over gloo on the
+CPU (no GPU work, no throughput).
+
 A step = one IcePop forward (K0 advantages, K1 fused lm_head GEMM + online softmax, K2
 epilogue) + backward (bf16 dZ -- formed in place from the probabilities K1 stored when they
 fit in HBM ("stored-probabilities" mode, the default at C2), else recomputed by the K3 GEMM
@@ -137,6 +142,22 @@ def make_batch_host(cfg: dict, rank: int, world: int, zero_adv_frac: float = 0.0
     return dict(cu=cu, go=go, rewards=rewards, n_local=n_local, token_offset=rank * n_local)
 
 
+def sample_on_policy(H, W, g, rows: int = 4096):
+    """Sampled tokens y_t ~ softmax(H_t . W^T) (on-policy, as the rollout engine
+    draws them), by the Gumbel-max trick over row chunks of the logits (setup, untimed; cuBLAS
+    bf16 logits are exact enough to sample from)."""
+    import torch
+
+    out = torch.empty(H.shape[0], dtype=torch.int32, device=H.device)
+    for i in range(0, H.shape[0], rows):
+        z = (H[i:i + rows] @ W.T).float()
+        u = torch.rand(z.shape, device=H.device, generator=g).clamp_(min=1e-20)
+        z.sub_(u.log_().neg_().log_())  # z + Gumbel(0, 1)
+        out[i:i + rows] = z.argmax(dim=1).to(torch.int32)
+        del z, u
+    return out
+
+
 def build_device_inputs(cfg, meta, dev, rank):
     import torch
 
@@ -147,7 +168,7 @@ def build_device_inputs(cfg, meta, dev, rank):
     N, d, V = meta["n_local"], cfg["hidden"], cfg["vocab"]
     H = torch.randn(N, d, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
     W = (torch.randn(V, d, device=dev, generator=g, dtype=torch.float32) * (2.0 / np.sqrt(d))).to(torch.bfloat16)
-    tokens = torch.randint(0, V, (N,), device=dev, generator=g, dtype=torch.int32)
+    tokens = sample_on_policy(H, W, g)
     # setup forward (untimed): lp_theta(y) -> lp_old = lp + N(0, 0.1) exercises the clip
     # branch; lp_inf = lp_old - N(0, sigma) pops ~1.5 permille
     lib = _lib.ensure_device(dev.index)
@@ -361,6 +382,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
                    "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective,
                    "zero_adv_group_frac": args.zero_adv_frac},
+        "per_gpu_value": round(value / world, 1),
         "gpu_launches": launches_per_step * args.steps,
         "step_tflops_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12, 1),
         "step_frac_of_peak_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms / 1e3) / 1e12 / pk["tflops"], 4),
@@ -463,7 +485,7 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
         shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=d, vocab=V, n_seqs=batch.n_seqs,
                            n_groups=batch.n_groups, weight_layout=_lib.W_VD)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr(),
-                           probs=dz.data_ptr(), tile_max=tm.data_ptr())
+                           probs=dz.data_ptr(), tile_max=tm.data_ptr(), lp_cur=f.lp_cur.data_ptr())
         wsp = _sp_workspace(N, d, V, batch.n_seqs, dev)
         nbytes = 4 * N * d + 4 * N * tm.shape[1] + N
         if wsp is not None:
@@ -747,13 +769,93 @@ def main():
                     help="fraction of prompt groups with identical rewards (zero advantages)")
     ap.add_argument("--dw-collective", choices=["fused", "nccl"], default="fused",
                     help="N>1: dW reduce-scatter fused into K5 over NVLink, or NCCL all-reduce")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: launch the ranks over gloo and run the host-side plumbing (shards, "
+                         "stats all-reduce, max-over-ranks timing) without any GPU work")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))  # one process per GPU, as the driver's torchrun does
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to time a different "
+              "number of ranks than requested", file=sys.stderr)
+        sys.exit(2)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules ask for >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code. Refuses, never silently runs
+    fewer ranks, when fewer than N GPUs are visible (the reference arm needs no GPU; the gloo
+    dry run none either)."""
+    n = args.gpus
+    if args.impl == "ours" and not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}; refusing", file=sys.stderr)
+            return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the driver checks nranks=N in NCCL's init lines
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "4")
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """--dry-run: every rank joins a gloo group, takes its token shard of the config's batch,
+    all-reduces a stats vector (the fp64 statistics exchange) and the max of its host-timed
+    no-op step (the bench's max-over-ranks rule); rank 0 prints the line. No GPU work, no
+    throughput claim: it proves the launcher and the rank plumbing."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = dict(CONFIGS[args.config])
+    meta = make_batch_host(cfg, rank, world, args.zero_adv_frac)
+    stats = torch.zeros(8, dtype=torch.float64)
+    stats[2] = meta["n_local"]
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.all_reduce(stats)
+    ms = torch.tensor([1e3 * (time.perf_counter() - t0)], dtype=torch.float64)
+    ranks = torch.tensor([rank, meta["token_offset"], meta["n_local"]], dtype=torch.int64)
+    gathered = [torch.zeros_like(ranks) for _ in range(world)]
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_gather(gathered, ranks)
+    else:
+        gathered = [ranks]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": None, "unit": UNIT, "n_gpus": world,
+                          "ranks": [{"rank": int(g[0]), "token_offset": int(g[1]), "tokens": int(g[2])}
+                                    for g in gathered],
+                          "global_tokens": int(stats[2].item()), "ms_allreduce_max": round(float(ms.item()), 3),
+                          "config": {"workload": cfg["name"], "parallelism": f"dp{world} token-sharded",
+                                     "backend": "gloo"}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

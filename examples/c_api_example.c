@@ -148,6 +148,7 @@ int main(int argc, char** argv) {
   saved.coeff = d_coeff;
   saved.probs = d_probs;
   saved.tile_max = d_tmax;
+  saved.lp_cur = d_lp; /* the sampled token's exact term c (1 - exp(lp_cur)) */
   /* loss = -J: grad_scale = -1; the workspace lets the backward compact zero-coefficient rows */
   IK(icepop_bwd_bf16(&shape, &cfg, d_hid, d_w, NULL, &saved, -1.0, d_gh, 0, d_gw, 0, d_bws, bwd_bytes, st));
   IK(icepop_finish(d_stats, st));

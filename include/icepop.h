@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define ICEPOP_ABI_VERSION 3
+#define ICEPOP_ABI_VERSION 4
 
 enum icepop_status {
   ICEPOP_OK = 0,
@@ -196,14 +196,20 @@ typedef struct icepop_saved {
   const float* kl_w;      /* [n_tokens]                                                   */
   void* probs;            /* out->probs / out->tile_max of the forward, or NULL. CONSUMED: the */
   const float* tile_max;  /* backward may overwrite rows of probs (a second backward passes NULL) */
+  /* [n_tokens] out->lp_cur of the forward. Required with probs: the sampled token's term
+   * of dZ, c (1 - p_y), is formed from p_y = exp(lp_cur) in fp64 and enters the GEMMs as a
+   * one-hot term, with q_y zeroed in probs. Forming it by cancellation against the bf16
+   * q_y would lose 2^-9 p_y / (1 - p_y) of it: 12% on tokens with p_y = 0.98. */
+  const double* lp_cur;
 } icepop_saved;
 
 /* Backward: recompute logits tile by tile, dZ = grad_scale*coeff_t*(e_y - softmax(z_t))
  * [- grad_scale*kl_w_t*p*(log p - log p_ref - kl_t) when gamma > 0] (bf16 chunk), then
  * grad_hidden = dZ.W^T and grad_weight (+)= H^T.dZ on tcgen05. With saved->probs there is no
  * logit recompute (not with gamma > 0). Given its workspace (icepop_workspace_bytes with
- * max_chunk_tokens < 0) the backward is row-scaled: dH = s (Q.W) + c W[y] and
- * dW = Q^T.(s H) + scatter_y(c H), s = -c 2^(-lse2), c = grad_scale coeff. Rows with a
+ * max_chunk_tokens < 0) the backward is row-scaled: dH = s (Q.W) + c (1 - p_y) W[y] and
+ * dW = Q^T.(s H) + scatter_y(c (1 - p_y) H), s = -c 2^(-lse2), c = grad_scale coeff, with
+ * q_y zeroed in probs and p_y = exp(saved->lp_cur). Rows with a
  * reference R != 0 get their dZ formed in place in probs first. Blocks without an active row
  * are skipped. With a NULL or smaller workspace, dZ is formed in place for every row
  * instead; probs is consumed either way.
@@ -270,6 +276,13 @@ int icepop_kl_bf16(const icepop_shape* shape, double temperature, const void* hi
  * icepop_finish(stats) maps it to NumericError. lr <= 0 or beta outside [0,1) -> EINVAL. */
 int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, void* weight_bf16,
                           int64_t n, double lr, double beta, double* stats, void* stream);
+
+/* ---- diagnostics ----------------------------------------------------------------------- */
+/* Number of long-K GEMM launches on the current device whose wave barriers were abandoned
+ * because a unit waited longer than ICEPOP_WAVE_TIMEOUT_US (default 2000): a concurrent kernel
+ * held SMs, so part of the grid started late. The result is unaffected (the barrier only keeps
+ * operand slices in L2); the count says the GEMM ran without that alignment. Synchronous. */
+int icepop_wave_barrier_abandons(int64_t* count);
 
 /* ---- fp64 SIMT validation path ----------------------------------------------------- */
 /* Same semantics in fp64 on CUDA cores (still CUDA, no CPU fallback), so the

@@ -20,7 +20,7 @@ OK, EINVAL, ENUMERIC, ECUDA, EARCH = 0, 1, 2, 3, 4
 ALGO_ICEPOP, ALGO_GRPO, ALGO_TIS = 0, 1, 2
 W_DV, W_VD = 0, 1
 NSTATS = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 PROBS_SLAB = 64  # ICEPOP_PROBS_SLAB: vocab columns per tile_max entry
 
 
@@ -103,6 +103,7 @@ class Saved(ctypes.Structure):
         ("kl_w", _c_p),
         ("probs", _c_p),
         ("tile_max", _c_p),
+        ("lp_cur", _c_p),
     ]
 
 
@@ -178,6 +179,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "icepop_finish": (ctypes.c_int, [_c_p, _c_p]),
     "icepop_gemm_bf16": (ctypes.c_int, [_c_p, _c_p, _c_p, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _c_p]),
+    "icepop_wave_barrier_abandons": (ctypes.c_int, [_P(_i64)]),
     "icepop_set_cta_group": (ctypes.c_int, [_i32]),
     "icepop_set_wide_tiles": (ctypes.c_int, [_i32]),
     "icepop_set_k1_wide": (ctypes.c_int, [_i32]),
@@ -232,6 +234,14 @@ def ensure_device(device_index: int) -> ctypes.CDLL:
         check(lib.icepop_device_check(device_index))
         _device_ok.add(device_index)
     return lib
+
+
+def wave_barrier_abandons(device_index: int = 0) -> int:
+    """Long-K GEMM launches on this device whose wave barriers timed out (include/icepop.h)."""
+    lib = ensure_device(device_index)
+    n = _i64(0)
+    check(lib.icepop_wave_barrier_abandons(ctypes.byref(n)))
+    return int(n.value)
 
 
 def ptr(t) -> int | None:

@@ -8,7 +8,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstdarg>
+#include <map>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
@@ -131,12 +133,44 @@ constexpr int BN_WIDE = 512;
 
 int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
 
-// Dynamic tile scheduling: a pool of device counters (one per launch, zeroed stream-ordered
-// right before it). ICEPOP_SCHED=static selects the static round-robin schedule instead.
+// Scheduler counters (the dynamic schedule's tile counter, or the long-K waves' chunk counter
+// and abandon flag): a ring of N_COUNTERS pairs per (device, stream), one pair per launch,
+// zeroed stream-ordered right before it. Launches on one stream run in order, so a pair is
+// reused only after the launch that last used it has finished; launches on different streams
+// never share one. (Replays of one captured CUDA graph on two streams at once would: replay a
+// graph on one stream at a time.) ICEPOP_SCHED=static selects the static round-robin schedule.
 constexpr int N_COUNTERS = 256;
-int* g_counters[16] = {nullptr};
-std::atomic<unsigned> g_counter_next[16];
+struct CounterRing {
+  int32_t* base = nullptr;
+  unsigned next = 0;
+};
+std::map<std::pair<int, cudaStream_t>, CounterRing> g_rings;
+int32_t* g_diag[16] = {nullptr};  // per device: [0] launches whose wave barriers were abandoned
 std::mutex g_counter_mutex;
+
+int diag_ptr(int dev, int32_t** out) {
+  *out = nullptr;
+  if (dev < 0 || dev >= 16) return ICEPOP_OK;
+  std::lock_guard<std::mutex> lock(g_counter_mutex);
+  if (!g_diag[dev]) {
+    ICP_CUDA(cudaMalloc(&g_diag[dev], 4 * sizeof(int32_t)));
+    ICP_CUDA(cudaMemset(g_diag[dev], 0, 4 * sizeof(int32_t)));
+  }
+  *out = g_diag[dev];
+  return ICEPOP_OK;
+}
+
+// Longest a unit of a long-K GEMM waits at a wave barrier before abandoning the barriers of
+// its launch (ICEPOP_WAVE_TIMEOUT_US, default 2 ms; a barrier chunk takes ~50 us at C2).
+uint32_t wave_timeout_ns() {
+  static uint32_t v = 0;
+  if (v == 0) {
+    const char* e = getenv("ICEPOP_WAVE_TIMEOUT_US");
+    const long us = e ? std::max(1L, atol(e)) : 2000L;
+    v = (uint32_t)std::min<long>(us * 1000L, 4000000000L);
+  }
+  return v;
+}
 
 int dynamic_sched() {
   static int v = -1;
@@ -161,13 +195,14 @@ int tile_counter(cudaStream_t st, int32_t** out) {
   if (!dynamic_sched()) return ICEPOP_OK;
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return ICEPOP_OK;
+  int32_t* c = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_counter_mutex);
-    if (!g_counters[dev]) ICP_CUDA(cudaMalloc(&g_counters[dev], N_COUNTERS * sizeof(int)));
+    CounterRing& r = g_rings[std::make_pair(dev, st)];
+    if (!r.base) ICP_CUDA(cudaMalloc(&r.base, 2 * N_COUNTERS * sizeof(int32_t)));
+    c = r.base + 2 * (r.next++ % N_COUNTERS);
   }
-  int* c = g_counters[dev] + (g_counter_next[dev].fetch_add(1) % N_COUNTERS);
-  ICP_CUDA(cudaMemsetAsync(c, 0, sizeof(int), st));
+  ICP_CUDA(cudaMemsetAsync(c, 0, 2 * sizeof(int32_t), st));
   *out = c;
   return ICEPOP_OK;
 }
@@ -194,10 +229,8 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     ICP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_done.fetch_or(bit, std::memory_order_acq_rel);
   }
-  const int units = std::min(sh.num_tiles, num_sms() / CG);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)(units * CG));
   cfg.blockDim = dim3(gemm_threads(EPI));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -208,6 +241,24 @@ int launch_umma_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // Persistent grid: one unit (CTA pair) per pair of SMs, capped by the clusters an idle device
+  // holds at once (fewer under MPS or green contexts), so that no wave barrier waits for a
+  // unit that cannot be resident.
+  static std::atomic<int> max_units[16];
+  int cap = num_sms() / CG;
+  if (dev >= 0 && dev < 16) {
+    int mu = max_units[dev].load(std::memory_order_relaxed);
+    if (mu == 0) {
+      cfg.gridDim = dim3((unsigned)(cap * CG));
+      int n = 0;
+      mu = (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) ? n : cap;
+      (void)cudaGetLastError();
+      max_units[dev].store(mu, std::memory_order_relaxed);
+    }
+    cap = std::min(cap, mu);
+  }
+  const int units = std::max(1, std::min(sh.num_tiles, cap));
+  cfg.gridDim = dim3((unsigned)(units * CG));
   ICP_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tb2, tc, sh, ep));
   return ICEPOP_OK;
 }
@@ -355,9 +406,14 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.wave_counter = nullptr;
   static const int sync_kb = env_int("ICEPOP_SYNC_KB", 64);  // K5 at C2: 1,495 -> 1,529 TFLOP/s (64 ~ 256 > 16)
   sh.sync_kb = sync_kb;
+  sh.wave_timeout_ns = wave_timeout_ns();
+  sh.diag = nullptr;
   if (long_k) {
     ICP_TRY(tile_counter(st, &sh.wave_counter));
     sh.tile_counter = nullptr;
+    int dev = 0;
+    ICP_CUDA(cudaGetDevice(&dev));
+    ICP_TRY(diag_ptr(dev, &sh.diag));
   } else {
     ICP_TRY(tile_counter(st, &sh.tile_counter));
   }
@@ -883,6 +939,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     if (!sv.tile_max) return fail(ICEPOP_EINVAL, "saved->probs needs saved->tile_max");
     if (V % 8 != 0 || (reinterpret_cast<uintptr_t>(sv.probs) & 15u) != 0)
       return fail(ICEPOP_EINVAL, "saved->probs needs vocab %% 8 == 0 and 16-byte alignment");
+    if (!sv.lp_cur) return fail(ICEPOP_EINVAL, "saved->probs needs saved->lp_cur (the sampled token's exact term)");
   }
   // chunk = as many dZ rows as the workspace holds (all rows, or a multiple of 128)
   bool skip = skip_inactive() && !kl_grad;  // with gamma > 0 every row has a KL gradient
@@ -980,11 +1037,13 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
       if (scaled) {
         k_sp_prep<<<grid, SPP_THREADS, 0, st>>>(sv.tile_max, tm_ld, (int32_t)((V + 63) / 64), lse, coeff,
-                                                (float)grad_scale, reinterpret_cast<const uint4*>(hidden), d / 8,
-                                                sw.rscale, sw.ohc, sw.exc, reinterpret_cast<uint4*>(sw.hid_s), nc);
+                                                (float)grad_scale, sv.lp_cur, tokens, dzb, V,
+                                                reinterpret_cast<const uint4*>(hidden), d / 8, sw.rscale, sw.ohc,
+                                                sw.exc, reinterpret_cast<uint4*>(sw.hid_s), nc);
       }
       k_dz_probs<<<grid, DZP_THREADS, 0, st>>>(reinterpret_cast<uint4*>(dzb), sv.tile_max, tm_ld, lse, coeff,
-                                               (float)grad_scale, tokens, nc, V / 8, scaled ? sw.exc : nullptr);
+                                               (float)grad_scale, tokens, nc, V / 8, sv.lp_cur,
+                                               scaled ? sw.exc : nullptr);
       ICP_CUDA(cudaGetLastError());
     } else {
       ICP_TRY(launch_dz(shape, cfg->temperature, h, weight, kl_grad ? weight_ref : nullptr, cs, grad_scale, w.dz, V,
@@ -1355,6 +1414,18 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
     k_merge_err<<<1, 1, 0, st>>>(e, stats);
   }
   ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_wave_barrier_abandons(int64_t* count) {
+  if (!count) return fail(ICEPOP_EINVAL, "null out pointer");
+  int dev = 0;
+  ICP_CUDA(cudaGetDevice(&dev));
+  int32_t* d = nullptr;
+  ICP_TRY(diag_ptr(dev, &d));
+  int32_t h = 0;
+  if (d) ICP_CUDA(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  *count = h;
   return ICEPOP_OK;
 }
 

@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ pr
                                                           int32_t tm_ld, const float* __restrict__ lse,
                                                           const float* __restrict__ coeff, float coeff_scale,
                                                           const int32_t* __restrict__ tokens, int64_t n, int64_t v8,
+                                                          const double* __restrict__ lp_cur,
                                                           const uint8_t* __restrict__ only = nullptr) {
   for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
     if (only && !only[t]) continue;  // block-uniform: rows the GEMMs scale themselves stay as they are
@@ -500,6 +501,9 @@ __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ pr
     }
     const float lse2 = lse[t] * 1.4426950408889634f;  // log2(e)
     const int y = tokens[t];
+    // the sampled token's entry c (1 - p_y) from p_y = exp(lp_cur) in fp64: formed from the bf16
+    // q_y it would lose 2^-9 p_y / (1 - p_y) of its value to cancellation (objective.py:251-252)
+    const float dzy = (float)((double)cf * -expm1(lp_cur[t]));
     const float* tm = tile_max + t * tm_ld;
     constexpr int U = 4;
     for (int64_t k0 = threadIdx.x; k0 < v8; k0 += U * DZP_THREADS) {
@@ -523,8 +527,8 @@ __global__ void __launch_bounds__(DZP_THREADS) k_dz_probs(uint4* __restrict__ pr
         for (int i = 0; i < 4; ++i) {
           const float2 qq = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
           const int64_t c = k * 8 + 2 * i;
-          const float d0 = fmaf(qq.x, s, c == y ? cf : 0.f);
-          const float d1 = fmaf(qq.y, s, c + 1 == y ? cf : 0.f);
+          const float d0 = c == y ? dzy : qq.x * s;
+          const float d1 = c + 1 == y ? dzy : qq.y * s;
           const __nv_bfloat162 o = __floats2bfloat162_rn(d0, d1);
           w[i] = *reinterpret_cast<const uint32_t*>(&o);
         }
@@ -595,13 +599,21 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const int32_t* __res
 // Row-scaled stored-probabilities backward, per row t. q was stored as 2^(u - R_slab) with
 // R_slab = 0 except for slabs whose maximum left the finite range (exception rows, any R != 0).
 // For the other rows p = q 2^(-lse2) has one scale per row, so the GEMMs take it directly:
-//   dH = s (Q.W) + c W[y],  dW = Q^T.(s H) + scatter_y(c H),  s = -c 2^(-lse2), c = coeff * gs.
+//   dH = s (Q.W) + c (1 - p_y) W[y],  dW = Q^T.(s H) + scatter_y(c (1 - p_y) H),
+//   s = -c 2^(-lse2), c = coeff * gs,
+// with q_y set to 0 in probs here, so the sampled token's column enters only through the
+// one-hot term, whose 1 - p_y = -expm1(lp_cur) is fp64-exact (objective.py:251-252). Taking
+// it as c - c q_y 2^(-lse2) instead cancels: the bf16 q_y carries 2^-9 p_y of error against a
+// result of size 1 - p_y (12% on a token with p_y = 0.98, the common case in RL batches).
 // Exception rows get their dZ in place (k_dz_probs with `only`) and enter the GEMMs unscaled
-// (s = 1, c = 0). Writes s, c, the exception flag and H'[t] = bf16(s H[t]).
+// (s = 1, c = 0). Writes s, c (1 - p_y), the exception flag and H'[t] = bf16(s H[t]).
 constexpr int SPP_THREADS = 128;
 __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict__ tile_max, int32_t tm_ld,
                                                          int32_t n_slabs, const float* __restrict__ lse,
                                                          const float* __restrict__ coeff, float gs,
+                                                         const double* __restrict__ lp_cur,
+                                                         const int32_t* __restrict__ tokens,
+                                                         __nv_bfloat16* __restrict__ probs, int64_t vocab,
                                                          const uint4* __restrict__ hid, int64_t d8,
                                                          float* __restrict__ rscale, float* __restrict__ ohc,
                                                          uint8_t* __restrict__ exc, uint4* __restrict__ hid_s, int64_t n) {
@@ -614,8 +626,9 @@ __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict
     const float sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
     if (threadIdx.x == 0) {
       rscale[t] = sc;
-      ohc[t] = ex ? 0.f : cf;
+      ohc[t] = (ex || cf == 0.f) ? 0.f : (float)((double)cf * -expm1(lp_cur[t]));
       exc[t] = ex ? 1 : 0;
+      if (!ex) probs[t * vocab + tokens[t]] = __ushort_as_bfloat16((unsigned short)0);
     }
     const uint4* src = hid + t * d8;
     uint4* dst = hid_s + t * d8;

@@ -48,8 +48,12 @@ struct GemmShape {
   int32_t num_tiles;
   int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
-  int32_t* wave_counter;  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr
+  // static schedule with a grid barrier per wave (long-K GEMMs), or nullptr. wave_counter[0]
+  // counts issued k-chunks; wave_counter[1] is the abandon flag (see chunk_wait).
+  int32_t* wave_counter;
   int32_t sync_kb;        // waves: k-blocks per barrier chunk (0 = one barrier per wave)
+  uint32_t wave_timeout_ns;  // a barrier wait longer than this abandons the barriers of the launch
+  int32_t* diag;          // device diagnostics: diag[0] += 1 per abandoned launch (or nullptr)
   // Block sparsity (device lists, or null): the GEMM runs only k-blocks kb_map[0 .. *kb_cnt)
   // of K and m-tiles mt_map[0 .. *mt_cnt) of M; the skipped ones hold only zero rows.
   const int32_t* kb_map;
@@ -780,18 +784,26 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       // before every unit has issued those of chunk g-1 (one monotonic counter over the whole
       // launch; skb = k_blocks is a plain barrier per wave). This keeps the tiles of a wave
       // within ~2 chunks of each other in k, so the operand slices they share stay in L2 even
-      // when K is long (K5: K = tokens). The grid is sized so every unit is co-resident; the
-      // watchdog guards the spin.
+      // when K is long (K5: K = tokens). The barrier is a locality hint, not a correctness
+      // requirement: the grid is sized to fit an idle GPU, but a concurrent kernel (an NCCL
+      // kernel on a comm stream, another stream, an MPS neighbour) can hold SMs so that some
+      // units start only after others finish. A unit that waits longer than wave_timeout_ns
+      // (normally ~50 us per chunk) therefore sets the abandon flag, and from then on no unit
+      // of the launch waits: the GEMM completes with the same result, only without the L2
+      // alignment. It never spins forever.
       const int skb = (sh.sync_kb > 0 && sh.sync_kb < sh.k_blocks) ? sh.sync_kb : max(sh.k_blocks, 1);
       const int spt = max(1, (sh.k_blocks + skb - 1) / skb);  // chunks per tile
+      volatile int32_t* abandon = sh.wave_counter ? sh.wave_counter + 1 : nullptr;
       auto chunk_wait = [&](int g) {
         const int target = n_units * g;
+        if (*abandon) return;
         const uint64_t t0 = globaltimer_ns();
         while (ld_acquire_gpu(sh.wave_counter) < target) {
-          __nanosleep(128);
-          if (globaltimer_ns() - t0 > 20000000000ull) {
-            printf("icepop: wave barrier watchdog (block %d)\n", blockIdx.x);
-            __trap();
+          __nanosleep(256);
+          if (*abandon) return;
+          if (globaltimer_ns() - t0 > sh.wave_timeout_ns) {
+            if (atomicExch(const_cast<int32_t*>(abandon), 1) == 0 && sh.diag) atomicAdd(sh.diag, 1);
+            return;
           }
         }
       };

@@ -517,7 +517,7 @@ def icepop_bwd(
             ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
         saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                            lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
-                           probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
+                           probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max), lp_cur=_lib.ptr(fwd.lp_cur))
         _lib.check(lib.icepop_bwd_bf16(shape, c_cfg, hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
                                        float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
                                        _lib.ptr(gw), 1 if accumulate else 0, _lib.ptr(ws),
@@ -589,7 +589,7 @@ def icepop_bwd_reduce_scatter(
             scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                        lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
-                       probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max))
+                       probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max), lp_cur=_lib.ptr(fwd.lp_cur))
     _lib.check(lib.icepop_bwd_bf16_rs(shape, cfg.to_c(), hidden.data_ptr(), weight.data_ptr(), _lib.ptr(wr), saved,
                                       float(grad_scale), _lib.ptr(gh), 1 if gh_dtype == torch.float32 else 0,
                                       rs_target, _lib.ptr(scratch), _lib.ptr(ws), 0 if ws is None else ws.numel(),
@@ -791,13 +791,13 @@ def _setup_context(ctx, inputs, output):
     (hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, alpha, beta, clip_eps, tis_cap, temperature, algo, layout,
      token_offset, store_probs) = inputs
     loss, stats, lse, lp_cur, entropy, kept, coeff, probs, tile_max = output
-    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff, probs, tile_max)
+    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, probs, tile_max)
     ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset)
     ctx.probs_live = probs.numel() > 0  # consumed by the first backward (rows may become dZ)
 
 
 def _backward(ctx, grad_loss, *unused):
-    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, coeff, probs, tile_max = ctx.saved_tensors
+    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, probs, tile_max = ctx.saved_tensors
     alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset = ctx.cfg
     cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
     batch = PackedBatch(tokens, lp_old, lp_inf, cu, go, adv, token_offset=token_offset)
@@ -805,7 +805,7 @@ def _backward(ctx, grad_loss, *unused):
     scale = -grad_loss.to(torch.float64)
     if hidden.dtype == torch.bfloat16:
         c = (coeff * scale).to(torch.float32)
-        fwd = IcePopForward(lse, None, None, None, None, None, c, None)
+        fwd = IcePopForward(lse, lp_cur, None, None, None, None, c, None)
         if ctx.probs_live:  # a second backward (retain_graph) falls back to the recompute
             fwd.extras["probs"], fwd.extras["tile_max"] = probs, tile_max
             ctx.probs_live = False

@@ -35,6 +35,7 @@ def main():
     coeff = torch.randn(N, device=dev, generator=g) * 1e-4
     coeff[torch.rand(N, device=dev, generator=g) < a.inactive] = 0.0
     tokens = torch.randint(0, V, (N,), device=dev, generator=g, dtype=torch.int32)
+    lp_cur = torch.full((N,), -3.0, dtype=torch.float64, device=dev)
     H = torch.zeros((N, d), dtype=torch.bfloat16, device=dev)
     W = torch.zeros((V, d), dtype=torch.bfloat16, device=dev)
     shape = _lib.Shape(n_tokens=N, token_offset=0, hidden=d, vocab=V, n_seqs=1, n_groups=1, weight_layout=_lib.W_VD)
@@ -42,7 +43,7 @@ def main():
     _lib.check(lib.icepop_workspace_bytes(shape, -1, 0, None, b))
     ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
     saved = _lib.Saved(tokens=tokens.data_ptr(), lse=lse.data_ptr(), coeff=coeff.data_ptr(), probs=probs.data_ptr(),
-                       tile_max=tm.data_ptr())
+                       tile_max=tm.data_ptr(), lp_cur=lp_cur.data_ptr())
     st = torch.cuda.current_stream().cuda_stream
     active = int((coeff != 0).sum())
     for name, w in (("dZ pass", None), ("dZ pass + block lists", ws)):

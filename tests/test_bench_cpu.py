@@ -56,3 +56,49 @@ def test_reference_arm_line(capsys, monkeypatch):
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "tokens/s"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def _run_bench(*args, env_extra=None, timeout=240):
+    import os
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra or {})
+    return subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                          timeout=timeout, env=env, cwd=str(ROOT))
+
+
+def test_gpus_2_self_launches_two_gloo_ranks():
+    """`bench.py --gpus 2` without torchrun starts two ranks itself (gloo dry run on CPU): both
+    take their token shard, the stats all-reduce sums them, rank 0 alone prints."""
+    import json
+
+    r = _run_bench("--gpus", "2", "--dry-run", "--config", "c1")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["dry_run"] is True
+    assert [x["rank"] for x in line["ranks"]] == [0, 1]
+    assert line["ranks"][1]["token_offset"] == line["ranks"][0]["tokens"] == 4096
+    assert line["global_tokens"] == 2 * 4096
+
+
+def test_gpus_1_dry_run_is_one_rank():
+    import json
+
+    r = _run_bench("--gpus", "1", "--dry-run", "--config", "c1")
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and len(line["ranks"]) == 1
+
+
+def test_gpus_n_refuses_without_gpus():
+    """More ranks than visible GPUs: a clear refusal, never a silent 1-GPU run."""
+    r = _run_bench("--gpus", "2", "--steps", "1", "--warmup", "3", env_extra={"CUDA_VISIBLE_DEVICES": ""})
+    assert r.returncode == 2 and "refusing" in r.stderr
+
+
+def test_world_size_mismatch_refuses():
+    r = _run_bench("--gpus", "4", "--dry-run", env_extra={"WORLD_SIZE": "2", "RANK": "0"})
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr

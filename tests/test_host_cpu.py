@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
                          check=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}$", out, re.M), f"{name} not a defined text symbol"
-    assert lib.icepop_abi_version() == 3
+    assert lib.icepop_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_library_has_sm100a_tensor_core_code():
@@ -57,9 +57,9 @@ def test_ctypes_struct_layout_matches_c(tmp_path: Path):
     src = tmp_path / "layout.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "icepop.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(icepop_config), sizeof(icepop_shape),"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(icepop_config), sizeof(icepop_shape),"
         " sizeof(icepop_batch), sizeof(icepop_fwd_out), sizeof(icepop_f64_out), offsetof(icepop_shape, n_seqs),"
-        " offsetof(icepop_config, algo), sizeof(icepop_saved), offsetof(icepop_saved, tile_max));return 0;}\n")
+        " offsetof(icepop_config, algo), sizeof(icepop_saved), offsetof(icepop_saved, tile_max), offsetof(icepop_saved, lp_cur));return 0;}\n")
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
@@ -67,7 +67,7 @@ def test_ctypes_struct_layout_matches_c(tmp_path: Path):
 
     want = [ctypes.sizeof(_lib.Config), ctypes.sizeof(_lib.Shape), ctypes.sizeof(_lib.Batch),
             ctypes.sizeof(_lib.FwdOut), ctypes.sizeof(_lib.F64Out), _lib.Shape.n_seqs.offset,
-            _lib.Config.algo.offset, ctypes.sizeof(_lib.Saved), _lib.Saved.tile_max.offset]
+            _lib.Config.algo.offset, ctypes.sizeof(_lib.Saved), _lib.Saved.tile_max.offset, _lib.Saved.lp_cur.offset]
     assert got == want
 
 
