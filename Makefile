@@ -8,7 +8,13 @@ SRC := $(PKG)/csrc/icepop_abi.cu
 DEPS := $(wildcard $(PKG)/csrc/*.cuh) include/icepop.h
 LIB := $(PKG)/libicepop_b200.so
 
-all: $(LIB)
+TESTLIB := tests/native/libicepop_testhelpers.so
+
+all: $(LIB) $(TESTLIB)
+
+# test-only helpers (tests/native): never loaded by the product package
+$(TESTLIB): tests/native/occupy.cu
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
 
 $(LIB): $(SRC) $(DEPS)
 	$(NVCC) $(NVFLAGS) -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; false)
@@ -20,6 +26,6 @@ build:
 $(LIB): | build
 
 clean:
-	rm -f $(LIB) build/ptxas.log
+	rm -f $(LIB) $(TESTLIB) build/ptxas.log
 
 .PHONY: all clean

@@ -322,6 +322,32 @@ def run_ours(args):
     ms = float(t.item())
     diag = Diagnostics.from_stats(f.stats.cpu())
 
+    def timed_steps(step_fn, n, warm=2):
+        """Device time per step of step_fn (CUDA events on the torch stream, max over ranks)."""
+        for _ in range(warm):
+            step_fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(n):
+            step_fn()
+        a1.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([a0.elapsed_time(a1) / n], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    def record(ms_v, n, note, **extra):
+        r = {"value": round(N * world / (ms_v / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms_v, 3), "steps": n,
+             "step_tflops_alg": round(FLOP_PER_TOKEN(d, V) * N / (ms_v / 1e3) / 1e12, 1), "note": note}
+        r.update(extra)
+        return r
+
+    n_var = max(2, min(args.steps, 4))
+
     # ---------------- on-policy variant (extra line item; the headline is the general case)
     onp_res = None
     if not args.no_onpolicy:
@@ -337,26 +363,52 @@ def run_ours(args):
                 wait_grad(allreduce_grad(g))
             return f
 
-        for _ in range(2):
-            step_onp()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        o0.record()
-        n_onp = max(2, min(args.steps, 4))
-        for _ in range(n_onp):
-            step_onp()
-        o1.record()
-        torch.cuda.synchronize()
-        oms = o0.elapsed_time(o1) / n_onp
-        t2 = torch.tensor([oms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        oms = float(t2.item())
-        onp_res = {"value": round(N * world / (oms / 1e3), 1), "unit": UNIT, "ms_per_step": round(oms, 3),
-                   "steps": n_onp, "note": "theta == theta_old (the reference loop's own case, scheduler.py:540) "
-                   "with lp_train_old recorded by icepop_logprob_bf16: GEMM-free exact forward + full backward"}
+        onp_res = record(timed_steps(step_onp, n_var), n_var,
+                         "theta == theta_old (the reference loop's own case, scheduler.py:540) with lp_train_old "
+                         "recorded by icepop_logprob_bf16: GEMM-free exact forward + full backward")
+
+    # ---------------- recompute variant: the north star's "logits never written to HBM" mode
+    rec_res = None
+    if not args.no_recompute and sp:
+        def step_rec():
+            f = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=False)
+            _, g = icepop_bwd(H, W, batch, f, icfg, layout="vd", grad_scale=-1.0)
+            if world > 1:
+                allreduce_stats(f.stats)
+                wait_grad(allreduce_grad(g))
+            return f
+
+        rms = timed_steps(step_rec, n_var)
+        rk = kernel_times(H, W, batch, icfg, meta, cfg, min(chunk, N), dev, False) if not args.no_kernel_timing else {}
+        rec_res = record(rms, n_var, "logits never stored: K1 writes only per-row statistics, K3 recomputes the "
+                         "logits tile by tile into bf16 dZ chunks (8.d.V executed FLOPs per token instead of 6)",
+                         kernels_ms={k: round(v["ms"], 3) for k, v in rk.items()},
+                         executed_tflops=round(8.0 * d * V * N / (rms / 1e3) / 1e12, 1))
+
+    # ---------------- the reference loop's call pattern: ref passed, gamma = 0 (scheduler.py:530-542)
+    ref_res = None
+    if not args.no_ref_diag and sp:
+        gr = torch.Generator(device=dev).manual_seed(77)
+        Wr = (W.float() + 0.01 * torch.randn(W.shape, device=dev, generator=gr)).to(torch.bfloat16)
+
+        def step_ref():
+            f = icepop_fwd(H, W, batch, icfg, layout="vd", weight_ref=Wr, store_probs=sp)
+            _, g = icepop_bwd(H, W, batch, f, icfg, layout="vd", grad_scale=-1.0, weight_ref=Wr)
+            if world > 1:
+                allreduce_stats(f.stats)
+                wait_grad(allreduce_grad(g))
+            return f
+
+        f0 = icepop_fwd(H, W, batch, icfg, layout="vd", weight_ref=Wr, store_probs=sp)
+        ref_mode = "stored-probabilities" if "probs" in f0.extras else "recompute"
+        del f0
+        rfms = timed_steps(step_ref, n_var)
+        ref_res = record(rfms, n_var, "KL-to-ref diagnostic with gamma = 0, as train_loop calls objective_and_grad "
+                         "(ref=params.copy(), scheduler.py:530-542): dual-accumulator forward (z and z_ref share "
+                         "every hidden tile) that also stores the probabilities, so the backward is the "
+                         "headline's; 8.d.V executed FLOPs per token",
+                         dz_mode=ref_mode, executed_tflops=round(8.0 * d * V * N / (rfms / 1e3) / 1e12, 1))
+        del Wr
 
     # ---------------- per-kernel timing pass (same work, events between launches)
     kern = (kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp or bool(sp_chunk))
@@ -420,6 +472,13 @@ def run_ours(args):
         line["e2e"] = e2e
     if onp_res:
         line["on_policy"] = onp_res
+    if rec_res:
+        line["recompute"] = rec_res
+    if ref_res:
+        if kern:  # the headline plus one extra forward GEMM (the KL diagnostic's z_ref)
+            ref_res["target_ms"] = round(ms + kern["K1_fwd_lse+K2"]["ms"], 3)
+        line["ref_diag"] = ref_res
+    line["wave_barrier_abandons"] = _lib.wave_barrier_abandons(local)
     if clocks:
         line["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -763,6 +822,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--no-onpolicy", action="store_true")
+    ap.add_argument("--no-recompute", action="store_true", help="skip the recompute-mode sub-record")
+    ap.add_argument("--no-ref-diag", action="store_true", help="skip the ref-passed (gamma = 0) sub-record")
     ap.add_argument("--seqs", type=int, default=0,
                     help="override the config's sequences per rank (e.g. the C5 sweep: 16/32/64/128/256)")
     ap.add_argument("--zero-adv-frac", type=float, default=0.0,

@@ -134,29 +134,42 @@ constexpr int BN_WIDE = 512;
 int g_cta_group = 0;  // 0 = not yet read from ICEPOP_CTA_GROUP (default 2)
 
 // Scheduler counters (the dynamic schedule's tile counter, or the long-K waves' chunk counter
-// and abandon flag): a ring of N_COUNTERS pairs per (device, stream), one pair per launch,
-// zeroed stream-ordered right before it. Launches on one stream run in order, so a pair is
-// reused only after the launch that last used it has finished; launches on different streams
-// never share one. (Replays of one captured CUDA graph on two streams at once would: replay a
-// graph on one stream at a time.) ICEPOP_SCHED=static selects the static round-robin schedule.
+// and abandon flag): one pair per launch, zeroed stream-ordered right before it, from a ring of
+// N_COUNTERS pairs per stream. Launches on one stream run in order, so a pair is reused only
+// after the launch that last used it has finished; streams get their own rings (N_RINGS per
+// device, assigned in order of first use and reused modulo N_RINGS beyond that). Replays of one
+// captured CUDA graph on two streams at once would share pairs: replay a graph on one stream at
+// a time. The pool is allocated once per device (icepop_device_check, or the first launch), so
+// no allocation happens inside a stream capture.
 constexpr int N_COUNTERS = 256;
-struct CounterRing {
-  int32_t* base = nullptr;
-  unsigned next = 0;
+constexpr int N_RINGS = 64;
+struct DevicePool {
+  int32_t* counters = nullptr;  // [N_RINGS][N_COUNTERS][2]
+  int32_t* diag = nullptr;      // [4]: [0] launches whose wave barriers were abandoned
+  unsigned next[N_RINGS] = {0};
+  int n_streams = 0;
+  std::map<cudaStream_t, int> ring_of;
 };
-std::map<std::pair<int, cudaStream_t>, CounterRing> g_rings;
-int32_t* g_diag[16] = {nullptr};  // per device: [0] launches whose wave barriers were abandoned
+DevicePool g_pool[16];
 std::mutex g_counter_mutex;
 
-int diag_ptr(int dev, int32_t** out) {
-  *out = nullptr;
-  if (dev < 0 || dev >= 16) return ICEPOP_OK;
+int ensure_pool(int dev) {
+  if (dev < 0 || dev >= 16) return fail(ICEPOP_EINVAL, "device index %d out of range", dev);
   std::lock_guard<std::mutex> lock(g_counter_mutex);
-  if (!g_diag[dev]) {
-    ICP_CUDA(cudaMalloc(&g_diag[dev], 4 * sizeof(int32_t)));
-    ICP_CUDA(cudaMemset(g_diag[dev], 0, 4 * sizeof(int32_t)));
+  DevicePool& p = g_pool[dev];
+  if (!p.counters) {
+    int32_t* buf = nullptr;
+    ICP_CUDA(cudaMalloc(&buf, (2 * N_RINGS * N_COUNTERS + 4) * sizeof(int32_t)));
+    ICP_CUDA(cudaMemset(buf, 0, (2 * N_RINGS * N_COUNTERS + 4) * sizeof(int32_t)));
+    p.counters = buf;
+    p.diag = buf + 2 * N_RINGS * N_COUNTERS;
   }
-  *out = g_diag[dev];
+  return ICEPOP_OK;
+}
+
+int diag_ptr(int dev, int32_t** out) {
+  ICP_TRY(ensure_pool(dev));
+  *out = g_pool[dev].diag;
   return ICEPOP_OK;
 }
 
@@ -195,12 +208,20 @@ int tile_counter(cudaStream_t st, int32_t** out) {
   if (!dynamic_sched()) return ICEPOP_OK;
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
+  ICP_TRY(ensure_pool(dev));
   int32_t* c = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_counter_mutex);
-    CounterRing& r = g_rings[std::make_pair(dev, st)];
-    if (!r.base) ICP_CUDA(cudaMalloc(&r.base, 2 * N_COUNTERS * sizeof(int32_t)));
-    c = r.base + 2 * (r.next++ % N_COUNTERS);
+    DevicePool& p = g_pool[dev];
+    auto it = p.ring_of.find(st);
+    int ring;
+    if (it == p.ring_of.end()) {
+      ring = p.n_streams++ % N_RINGS;
+      p.ring_of.emplace(st, ring);
+    } else {
+      ring = it->second;
+    }
+    c = p.counters + 2 * (ring * N_COUNTERS + (int)(p.next[ring]++ % N_COUNTERS));
   }
   ICP_CUDA(cudaMemsetAsync(c, 0, 2 * sizeof(int32_t), st));
   *out = c;
@@ -378,7 +399,8 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   // [zero_rows_to, N] and EPI_LSE's stored probabilities [M, N]
   CUtensorMap tc = tb;
   if (epi == EPI_DZ) ICP_TRY(encode_2d(&tc, ep.dz, (uint64_t)N, (uint64_t)ep.zero_rows_to, (uint64_t)ep.ldz, 64, 32));
-  if (epi == EPI_LSE && ep.probs) ICP_TRY(encode_2d(&tc, ep.probs, (uint64_t)N, (uint64_t)M, (uint64_t)N, 64, 32));
+  if ((epi == EPI_LSE || epi == EPI_LSE_REF) && ep.probs)
+    ICP_TRY(encode_2d(&tc, ep.probs, (uint64_t)N, (uint64_t)M, (uint64_t)N, 64, 32));
   GemmShape sh;
   sh.M = (int)M;
   sh.N = (int)N;
@@ -724,7 +746,12 @@ int icepop_device_check(int device) {
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, umma_gemm_kernel<BN_, false, false, EPI_LSE, 2>);
   if (e != cudaSuccess) return fail(ICEPOP_EARCH, "sm_100a kernels not loadable: %s", cudaGetErrorString(e));
-  return ICEPOP_OK;
+  int cur = 0;
+  ICP_CUDA(cudaGetDevice(&cur));
+  ICP_CUDA(cudaSetDevice(device));
+  const int rc = ensure_pool(device);  // scheduler counters: allocated here, never inside a capture
+  cudaSetDevice(cur);
+  return rc;
 }
 
 int icepop_group_advantages(const double* rewards, const int32_t* group_offsets, int32_t n_groups, int32_t n_seqs,
@@ -762,7 +789,10 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
   if (out->probs) {
-    if (ref) return fail(ICEPOP_EINVAL, "stored probabilities are not supported with weight_ref");
+    // with gamma > 0 the backward needs the KL term's gradient, which the recompute forms
+    if (ref && cfg->kl_coeff > 0.0)
+      return fail(ICEPOP_EINVAL, "stored probabilities with weight_ref need kl_coeff == 0 (the KL term then "
+                                 "enters J only)");
     if (!out->tile_max) return fail(ICEPOP_EINVAL, "stored probabilities need out->tile_max");
     if (V % 8 != 0) return fail(ICEPOP_EINVAL, "stored probabilities need vocab %% 8 == 0");
     if (((reinterpret_cast<uintptr_t>(out->probs) | reinterpret_cast<uintptr_t>(out->tile_max)) & 15u) != 0)
@@ -1394,15 +1424,11 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
   if (velocity && !(beta >= 0.0 && beta < 1.0)) return fail(ICEPOP_EINVAL, "momentum beta must be in [0, 1)");
   if (!weight || !grad || n < 0) return fail(ICEPOP_EINVAL, "null weight/grad");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static unsigned* err[16] = {nullptr};  // one error word per device
   int dev = 0;
   ICP_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return fail(ICEPOP_EINVAL, "device index out of range");
-  {
-    std::lock_guard<std::mutex> lock(g_counter_mutex);
-    if (!err[dev]) ICP_CUDA(cudaMalloc(&err[dev], sizeof(unsigned)));
-  }
-  unsigned* e = err[dev];
+  int32_t* dg = nullptr;
+  ICP_TRY(diag_ptr(dev, &dg));
+  unsigned* e = reinterpret_cast<unsigned*>(dg + 2);  // the device pool's error word for this call
   ICP_CUDA(cudaMemsetAsync(e, 0, sizeof(unsigned), st));
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   if (n > 0)

@@ -154,7 +154,7 @@ struct EpiParams {
 //         each CTA stages its own 128 rows of A and half (BN/2 rows) of B, so the B operand
 //         is read from L2 once per pair instead of once per CTA.
 // Epilogues that stage bf16 tiles in smem for TMA stores: K3's dZ and K1's stored probabilities.
-__host__ __device__ constexpr bool epi_staging(int epi) { return epi == EPI_DZ || epi == EPI_LSE; }
+__host__ __device__ constexpr bool epi_staging(int epi) { return epi == EPI_DZ || epi == EPI_LSE || epi == EPI_LSE_REF; }
 
 template <int BN, int CG, bool DUAL = false, bool EPI_STAGING = false>
 struct GemmCfg {
@@ -560,60 +560,94 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
 // 1 = TMEM column + BN), the ref online (max, sum) and the cross term
 // x = sum_j 2^(u_j - mx) (u_j - ur_j), u = z log2(e): after the merge,
 // sum_v p_v (z_v - zr_v) = ln2 * X / S and kl = that - lse + lse_ref (objective.py:257-258).
+// In stored-probabilities mode (ep.probs; gamma = 0, where the KL term is a diagnostic only, as
+// in train_loop's own call, scheduler.py:530-542) it also writes q = 2^(u - R) per 64-column
+// slab and the slab references R exactly as epi_lse does, so the backward is the stored mode's
+// and the call executes one extra forward GEMM (z_ref) instead of a forward plus a recompute.
 template <int BN>
-__device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
-                                            int n_blk, int row, uint32_t taddr) {
+__device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
+                                            uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
+                                            int quarter, uint32_t taddr) {
+  static_assert(BN % 64 == 0, "64-column slabs");
   const int m = m0 + row;
   const bool row_ok = m < sh.M;
   const int y = (row_ok && ep.targets) ? __ldg(ep.targets + m) : -1;
+  const int row0 = m0 + quarter * 32;
+  const bool warp_rows = row0 < sh.M;  // warp-uniform
+  const bool store = ep.probs != nullptr;
   float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_x = 0.f;
   float ref_m = -1e30f, ref_s = 0.f;
+  float refs[BN / 64];
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    float v[32], w[32];
-    tmem_ld32(taddr + c * 32, v);
-    tmem_ld32(taddr + BN + c * 32, w);
-    const int col0 = n0 + c * 32;
+  for (int sl = 0; sl < BN / 64; ++sl) {
+    float v[64], w[64];
+    tmem_ld32(taddr + sl * 64, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld32(taddr + sl * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+    tmem_ld32(taddr + BN + sl * 64, *reinterpret_cast<float(*)[32]>(w));
+    tmem_ld32(taddr + BN + sl * 64 + 32, *reinterpret_cast<float(*)[32]>(w + 32));
+    refs[sl] = 0.f;
+    const int col0 = n0 + sl * 64;
     if (col0 >= sh.N) continue;  // warp-uniform
     const int rel = y - col0;
-    if ((unsigned)rel < 32u) {
+    if ((unsigned)rel < 64u) {
       float zt = 0.f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) zt = (j == rel) ? v[j] : zt;
+      for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
       if (row_ok) ep.ztok[m] = zt * ep.inv_t;
     }
-    float cm = -1e30f, cr = -1e30f;
+    float smx = -1e30f;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < 64; ++j) {
       const bool ok = col0 + j < sh.N;
       v[j] = ok ? v[j] * ep.scale_log2 : -1e30f;
       w[j] = ok ? w[j] * ep.scale_log2 : -1e30f;
-      cm = fmaxf(cm, v[j]);
-      cr = fmaxf(cr, w[j]);
+      smx = fmaxf(smx, v[j]);
     }
-    const float nm = fmaxf(run_m, cm);
-    const float a = fast_exp2(run_m - nm);
-    run_q = a * (run_q + (run_m - nm) * run_s);
-    run_s = a * run_s;
-    run_x = a * run_x;
-    const float nr = fmaxf(ref_m, cr);
-    ref_s *= fast_exp2(ref_m - nr);
-    float s = 0.f, q = 0.f, x = 0.f, sr = 0.f;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float d = v[j] - nm;
-      const float e = fast_exp2(d);
-      s += e;
-      q = fmaf(e, d, q);
-      x = fmaf(e, v[j] - w[j], x);
-      sr += fast_exp2(w[j] - nr);
+    for (int hh = 0; hh < 2; ++hh) {
+      const float* vh = v + 32 * hh;
+      const float* wh = w + 32 * hh;
+      float cm = -1e30f, cr = -1e30f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        cm = fmaxf(cm, vh[j]);
+        cr = fmaxf(cr, wh[j]);
+      }
+      const float nm = fmaxf(run_m, cm);
+      const float a = fast_exp2(run_m - nm);
+      run_q = a * (run_q + (run_m - nm) * run_s);
+      run_s = a * run_s;
+      run_x = a * run_x;
+      const float nr = fmaxf(ref_m, cr);
+      ref_s *= fast_exp2(ref_m - nr);
+      float sm = 0.f, q = 0.f, x = 0.f, sr = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float d = vh[j] - nm;
+        const float e = fast_exp2(d);
+        sm += e;
+        q = fmaf(e, d, q);
+        x = fmaf(e, vh[j] - wh[j], x);
+        sr += fast_exp2(wh[j] - nr);
+      }
+      run_s += sm;
+      run_q += q;
+      run_x += x;
+      run_m = nm;
+      ref_s += sr;
+      ref_m = nr;
     }
-    run_s += s;
-    run_q += q;
-    run_x += x;
-    run_m = nm;
-    ref_s += sr;
-    ref_m = nr;
+    if (store) {
+      // q = 2^(u - R), R = 0 while the slab maximum lies within +-PROBS_REF_RANGE (epi_lse)
+      const float R = fabsf(smx) <= PROBS_REF_RANGE ? 0.f : smx;
+      refs[sl] = R;
+      if (warp_rows) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16x2(fast_exp2(v[2 * j] - R), fast_exp2(v[2 * j + 1] - R));
+        stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
+      }
+    }
   }
   if (row_ok) {
     float* p = ep.part + (int64_t)n_blk * 6 * sh.M + m;
@@ -623,6 +657,14 @@ __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams
     p[3 * (int64_t)sh.M] = ref_m;
     p[4 * (int64_t)sh.M] = ref_s;
     p[5 * (int64_t)sh.M] = run_x;
+    if (store) {
+      float* tm = ep.tile_max + (int64_t)m * ep.tm_ld;
+#pragma unroll
+      for (int sl = 0; sl < BN / 64; ++sl)
+        if (n0 / 64 + sl < ep.tm_ld) tm[n0 / 64 + sl] = refs[sl];
+      if (n0 + BN >= sh.N)  // the last tile zeroes the row's padding entries
+        for (int k = n0 / 64 + BN / 64; k < ep.tm_ld; ++k) tm[k] = 0.f;
+    }
   }
 }
 
@@ -1009,7 +1051,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         else
           epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       }
-      if constexpr (EPI == EPI_LSE_REF) epi_lse_ref<BN>(sh, ep, m0, n_blk * BN, n_blk, row, taddr);
+      if constexpr (EPI == EPI_LSE_REF)
+        epi_lse_ref<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
+                        quarter, taddr);
       if constexpr (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
       tc_fence_before();
       __syncwarp();

@@ -114,6 +114,10 @@ def stream_barrier(group=None, device=None) -> None:
         return
     if device is None:
         device = "cpu" if dist.get_backend(group) == "gloo" else torch.cuda.current_device()
+    if str(device) == "cpu" and torch.cuda.is_available() and torch.cuda.is_initialized():
+        # a CPU collective does not wait for the CUDA stream: drain it first, so the barrier
+        # still means "this rank's queued device work (e.g. the fold reading the slots) is done"
+        torch.cuda.current_stream().synchronize()
     t = torch.zeros(1, device=device)
     dist.all_reduce(t, group=group)
 

@@ -22,6 +22,7 @@ rank's partial sums (include/icepop.h ``enum icepop_stat``) -- sum them across r
 
 from __future__ import annotations
 
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -47,10 +48,13 @@ STORE_PROBS = os.environ.get("ICEPOP_STORE_PROBS", "auto")
 STORE_PROBS_FRACTION = 0.6
 
 
-def _resolve_store_probs(store_probs, n: int, v: int, device, with_ref: bool) -> bool:
+def _resolve_store_probs(store_probs, n: int, v: int, device, kl_grad: bool) -> bool:
+    """Whether the forward stores the probabilities. Never with the KL-to-ref gradient
+    (gamma > 0: the recompute forms it); with a reference policy and gamma = 0 the KL term is a
+    diagnostic of the forward only, so the probabilities are stored as usual."""
     if store_probs is None:
         store_probs = {"auto": None, "1": True, "0": False}.get(STORE_PROBS.lower(), None)
-    if store_probs is False or with_ref or v % 8 != 0 or n == 0:
+    if store_probs is False or kl_grad or v % 8 != 0 or n == 0:
         return False
     if store_probs is True:
         return True
@@ -245,12 +249,31 @@ def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _on_device(fn):
+    """Run an entry point with its tensors' device current: the library launches on the current
+    CUDA device, so a call on cuda:1 tensors while cuda:0 is current must switch first (the
+    stream passed is always the tensors' device's current stream)."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        t = args[0] if args else next(iter(kwargs.values()), None)
+        if isinstance(t, PackedBatch):
+            t = t.tokens
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            with torch.cuda.device(t.device):
+                return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapper
+
+
 def _lib_for(t: torch.Tensor):
     if t.device.type != "cuda":
         raise RuntimeError("libicepop_b200 runs on CUDA tensors only (no CPU fallback)")
     return _lib.ensure_device(t.device.index if t.device.index is not None else torch.cuda.current_device())
 
 
+@_on_device
 def icepop_fwd(
     hidden: torch.Tensor,
     weight: torch.Tensor,
@@ -300,16 +323,17 @@ def icepop_fwd(
             lse_ref = torch.empty(n, dtype=torch.float32, device=dev)
             kl_w = torch.empty(n, dtype=torch.float32, device=dev)
         probs = tile_max = None
+        kl_grad = wr is not None and cfg.kl_coeff > 0.0
         if probs_buffers is not None:
             pb, tb = probs_buffers
             tm_ld = _lib.tile_max_ld(shape.vocab)
             if (pb.dtype != torch.bfloat16 or pb.dim() != 2 or pb.shape[0] < n or pb.shape[1] != shape.vocab
                     or tb.dtype != torch.float32 or tb.dim() != 2 or tb.shape[0] < n or tb.shape[1] != tm_ld
-                    or not pb.is_contiguous() or not tb.is_contiguous() or wr is not None):
+                    or not pb.is_contiguous() or not tb.is_contiguous() or kl_grad):
                 raise ValueError("probs_buffers must be contiguous (bf16 [>=N, V], f32 [>=N, tile_max_ld(V)]) "
-                                 "and cannot be combined with weight_ref")
+                                 "and cannot be combined with the KL gradient (weight_ref with kl_coeff > 0)")
             probs, tile_max = pb[:n], tb[:n]
-        elif _resolve_store_probs(store_probs, n, shape.vocab, dev, wr is not None):
+        elif _resolve_store_probs(store_probs, n, shape.vocab, dev, kl_grad):
             try:
                 probs = torch.empty((n, shape.vocab), dtype=torch.bfloat16, device=dev)
                 tile_max = torch.empty((n, _lib.tile_max_ld(shape.vocab)), dtype=torch.float32, device=dev)
@@ -376,6 +400,7 @@ def icepop_fwd(
     raise ValueError(f"unsupported dtype {hidden.dtype}: use bfloat16 (tensor cores) or float64 (validation)")
 
 
+@_on_device
 def icepop_logprob(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor, layout: str = "vd",
                    temperature: float = 1.0) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """log pi(y_t), lse_t and entropy_t with the K1 kernel (the train engine's lp recording,
@@ -401,6 +426,7 @@ def icepop_logprob(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Ten
     return lp, lse, ent
 
 
+@_on_device
 def icepop_fwd_onpolicy(batch: PackedBatch, lse_old: torch.Tensor, entropy_old: torch.Tensor | None,
                         cfg: IcePopConfig = IcePopConfig(), hidden_dim: int = 8, vocab: int = 8) -> IcePopForward:
     """Forward when theta == theta_old and batch.lp_train_old came from :func:`icepop_logprob`
@@ -428,6 +454,7 @@ def icepop_fwd_onpolicy(batch: PackedBatch, lse_old: torch.Tensor, entropy_old: 
     return f
 
 
+@_on_device
 def discrepancy(hidden: torch.Tensor, weight_p: torch.Tensor, weight_q: torch.Tensor, layout: str = "vd",
                 temperature: float = 1.0) -> tuple[torch.Tensor, torch.Tensor]:
     """delta = mean_t KL(pi_p(.|t) || pi_q(.|t)) over the rows of `hidden` (the probe
@@ -468,6 +495,7 @@ def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chu
     return bwd_b.value
 
 
+@_on_device
 def icepop_bwd(
     hidden: torch.Tensor,
     weight: torch.Tensor,
@@ -551,6 +579,7 @@ def icepop_bwd(
     raise ValueError(f"unsupported dtype {hidden.dtype}")
 
 
+@_on_device
 def icepop_bwd_reduce_scatter(
     hidden: torch.Tensor,
     weight: torch.Tensor,
@@ -613,6 +642,7 @@ def probs_chunk_tokens(n: int, vocab: int, device) -> int:
     return rows // 4096 * 4096
 
 
+@_on_device
 def icepop_fwd_bwd(
     hidden: torch.Tensor,
     weight: torch.Tensor,
@@ -638,7 +668,8 @@ def icepop_fwd_bwd(
     """
     n = hidden.shape[0]
     v = weight.shape[1] if layout == "dv" else weight.shape[0]
-    usable = hidden.dtype == torch.bfloat16 and weight_ref is None and v % 8 == 0 and n > 0 and hidden.is_cuda
+    kl_grad = weight_ref is not None and cfg.kl_coeff > 0.0
+    usable = hidden.dtype == torch.bfloat16 and not kl_grad and v % 8 == 0 and n > 0 and hidden.is_cuda
     chunk = 0
     if usable:
         chunk = probs_chunk_tokens(n, v, hidden.device)
@@ -650,9 +681,9 @@ def icepop_fwd_bwd(
                             weight_ref, grad_hidden_dtype)
         return f, gh, gw
     if chunk >= n:
-        f = icepop_fwd(hidden, weight, batch, cfg, layout, store_probs=True)
+        f = icepop_fwd(hidden, weight, batch, cfg, layout, weight_ref=weight_ref, store_probs=True)
         gh, gw = icepop_bwd(hidden, weight, batch, f, cfg, layout, grad_scale, need_hidden, True, grad_weight,
-                            grad_hidden_dtype=grad_hidden_dtype)
+                            weight_ref, grad_hidden_dtype=grad_hidden_dtype)
         return f, gh, gw
     dev = hidden.device
     gw = grad_weight if grad_weight is not None else torch.zeros(tuple(weight.shape), dtype=torch.float32, device=dev)
@@ -684,9 +715,9 @@ def icepop_fwd_bwd(
         sub = PackedBatch(batch.tokens[s0:e0], batch.lp_train_old[s0:e0], batch.lp_infer_old[s0:e0],
                           batch.cu_seqlens, batch.group_offsets, batch.advantages, batch.rewards,
                           token_offset=batch.token_offset + s0)
-        f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, probs_buffers=bufs)
+        f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, weight_ref=weight_ref, probs_buffers=bufs)
         ghc, _ = icepop_bwd(hidden[s0:e0], weight, sub, f, cfg, layout, grad_scale, need_hidden, True, gw,
-                            grad_hidden_dtype=grad_hidden_dtype, workspace=ws)
+                            weight_ref, grad_hidden_dtype=grad_hidden_dtype, workspace=ws)
         if gh is not None:
             gh[s0:e0] = ghc
         stats[: _lib.STAT_ERRORS] += f.stats[: _lib.STAT_ERRORS]
@@ -694,11 +725,13 @@ def icepop_fwd_bwd(
         parts.append(f)
     cat = lambda name: torch.cat([getattr(p, name) for p in parts])  # noqa: E731
     out = IcePopForward(cat("lse"), cat("lp_cur"), cat("entropy"), cat("kept"), cat("calib"), cat("surrogate"),
-                        cat("coeff"), stats)
+                        cat("coeff"), stats, kl=cat("kl") if weight_ref is not None else None,
+                        lse_ref=cat("lse_ref") if weight_ref is not None else None)
     out.extras["chunks"] = len(parts)
     return out, gh, gw
 
 
+@_on_device
 def finish(stats: torch.Tensor) -> None:
     """One host sync; raise NumericError/ValueError from the device error word."""
     lib = _lib.load()
@@ -856,6 +889,7 @@ def icepop_loss(
     return loss, dict(stats=stats, lse=lse, lp_cur=lp_cur, entropy=entropy, kept=kept, coeff=coeff)
 
 
+@_on_device
 def group_advantages(rewards: torch.Tensor, group_offsets: torch.Tensor) -> torch.Tensor:
     """K0 on device: per-group z-scored rewards (objective.py:153-159), bit-identical to numpy."""
     lib = _lib_for(rewards)

@@ -16,8 +16,10 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .loss import _on_device
 
 
+@_on_device
 def sgd_update_(weight: torch.Tensor, grad: torch.Tensor, lr: float, velocity: torch.Tensor | None = None,
                 beta: float = 0.9, weight_bf16: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
     """In place: v = beta v + g (if velocity) else v = g; weight += lr v (gradient ASCENT)."""

@@ -297,11 +297,14 @@ def test_skip_inactive_all_rows_inactive(cuda_device):
     assert torch.count_nonzero(gh) == 0 and torch.count_nonzero(gw) == 0
 
 
-@pytest.mark.parametrize("kl_coeff", [0.0, 0.4])
+@pytest.mark.parametrize("kl_coeff,store_probs", [(0.0, False), (0.0, True), (0.4, None)],
+                         ids=["gamma0-recompute", "gamma0-probs", "gamma0.4"])
 @pytest.mark.parametrize("layout", ["vd", "dv"])
-def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff):
+def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff, store_probs):
     """KL-to-ref on tensor cores (objective.py:254-263): dual-accumulator GEMMs; the KL
-    diagnostic always, its gradient when gamma > 0."""
+    diagnostic always, its gradient when gamma > 0. With gamma = 0 (train_loop's own call,
+    scheduler.py:530-542) the dual forward also stores the probabilities and the backward is
+    the stored mode's."""
     from paper_2510_18855_b200.loss import Diagnostics, IcePopConfig, finish, icepop_bwd, icepop_fwd
 
     c = _case(seed=31, layout=layout, V=1000)
@@ -310,7 +313,8 @@ def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff):
     cfg = IcePopConfig(kl_coeff=kl_coeff)
     H, W, Wrd = c["H"].to(cuda_device), c["W"].to(cuda_device), Wr.to(cuda_device)
     b = _batch(c, cuda_device)
-    f = icepop_fwd(H, W, b, cfg, layout=layout, weight_ref=Wrd)
+    f = icepop_fwd(H, W, b, cfg, layout=layout, weight_ref=Wrd, store_probs=store_probs)
+    assert ("probs" in f.extras) == bool(store_probs)
     gh, gw = icepop_bwd(H, W, b, f, cfg, layout=layout, weight_ref=Wrd, grad_hidden_dtype=torch.float32)
     finish(f.stats)
     from oracle.icepop_oracle import icepop_dense
@@ -324,6 +328,28 @@ def test_kl_to_ref_bf16_vs_oracle(cuda_device, cta_group, layout, kl_coeff):
     assert d.objective_value == pytest.approx(o["objective"], rel=2e-3, abs=1e-5)
     assert _rel(gw.cpu().numpy(), o["grad_weight"]) < 1e-2
     assert _rel(gh.cpu().numpy(), o["grad_hidden"]) < 1e-2
+
+
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_kl_forward_statistics_identical_with_stored_probs(cuda_device, cta_group, layout):
+    """The dual forward's statistics (lse, lp_cur, entropy, kl, mask, coefficients, stats) are
+    the same bits whether or not it also stores the probabilities; the stored q and slab
+    references match the plain forward's (same q = 2^(u - R) rule)."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    c = _case(seed=32, layout=layout, V=1000)
+    rng = np.random.default_rng(8)
+    Wr = torch.from_numpy(c["W"].double().numpy() + rng.normal(0, 0.05, tuple(c["W"].shape))).to(torch.bfloat16)
+    H, W, Wrd = c["H"].to(cuda_device), c["W"].to(cuda_device), Wr.to(cuda_device)
+    a = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, weight_ref=Wrd, store_probs=True)
+    b = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, weight_ref=Wrd, store_probs=False)
+    p = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, store_probs=True)
+    for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff", "stats", "kl", "lse_ref"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    nslab = -(-1000 // 64)
+    assert torch.equal(a.extras["tile_max"][:, :nslab], p.extras["tile_max"][:, :nslab])
+    qa, qp = a.extras["probs"].float(), p.extras["probs"].float()
+    assert torch.allclose(qa, qp, rtol=2.0 ** -7, atol=1e-30)  # at most one bf16 step apart (exp2 rounding)
 
 
 def test_on_policy_forward_equals_full_forward(cuda_device):

@@ -140,17 +140,20 @@ def test_autograd_retain_graph_second_backward(cuda_device):
     assert _rel(W.grad.float().cpu().numpy(), g1[1].cpu().numpy()) < 1e-2
 
 
-def test_auto_mode_skips_probs_with_weight_ref(cuda_device):
-    """weight_ref (KL term): the forward keeps the recompute mode even when asked."""
+def test_probs_with_weight_ref_only_without_kl_gradient(cuda_device):
+    """weight_ref with gamma > 0 (the KL gradient): the forward keeps the recompute mode even
+    when asked; with gamma = 0 (a forward-only diagnostic) it stores the probabilities."""
     from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
 
     c = _case(seed=56, V=1000)
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
-    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), weight_ref=W.clone(), store_probs=True)
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(kl_coeff=0.3), weight_ref=W.clone(), store_probs=True)
     assert "probs" not in f.extras
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), weight_ref=W.clone(), store_probs=True)
+    assert "probs" in f.extras
 
 
-def _c_fwd(c, dev, probs, tile_max, weight_ref=None):
+def _c_fwd(c, dev, probs, tile_max, weight_ref=None, kl_coeff=0.0):
     from paper_2510_18855_b200 import _lib
     from paper_2510_18855_b200.loss import IcePopConfig, _shape
 
@@ -170,7 +173,7 @@ def _c_fwd(c, dev, probs, tile_max, weight_ref=None):
     out = _lib.FwdOut(stats=stats.data_ptr(), kl=_lib.ptr(kl[0]), lse_ref=_lib.ptr(kl[1]), kl_w=_lib.ptr(kl[2]),
                       probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max),
                       **{k: v.data_ptr() for k, v in outs.items()})
-    rc = lib.icepop_fwd_bf16(shape, IcePopConfig().to_c(), H.data_ptr(), W.data_ptr(), _lib.ptr(weight_ref),
+    rc = lib.icepop_fwd_bf16(shape, IcePopConfig(kl_coeff=kl_coeff).to_c(), H.data_ptr(), W.data_ptr(), _lib.ptr(weight_ref),
                              b.to_c(), out, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream)
     return rc, shape, b, outs
 
@@ -186,8 +189,8 @@ def test_abi_rejects_invalid_probs_arguments(cuda_device):
     tm = torch.empty((N, _lib.tile_max_ld(1000)), dtype=torch.float32, device=cuda_device)
     rc, *_ = _c_fwd(c, cuda_device, probs, None)
     assert rc == _lib.EINVAL  # tile_max missing
-    rc, *_ = _c_fwd(c, cuda_device, probs, tm, weight_ref=c["W"].to(cuda_device))
-    assert rc == _lib.EINVAL  # no stored probabilities with the KL term
+    rc, *_ = _c_fwd(c, cuda_device, probs, tm, weight_ref=c["W"].to(cuda_device), kl_coeff=0.3)
+    assert rc == _lib.EINVAL  # no stored probabilities with the KL gradient (gamma > 0)
     flat = torch.empty(N * 1000 + 8, dtype=torch.bfloat16, device=cuda_device)
     rc, *_ = _c_fwd(c, cuda_device, flat[1:1 + N * 1000], tm)
     assert rc == _lib.EINVAL  # probs not 16-byte aligned
