@@ -171,6 +171,14 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
                     const void* weight, const void* weight_ref, const icepop_batch* batch,
                     const icepop_fwd_out* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The IcePop epilogue alone (K2 + the stats reduction), re-run over the K1 partials that the
+ * last icepop_fwd_bf16 call left in `workspace` (same shape, same weight_ref-ness `with_ref`,
+ * same temperature): other bounds, algorithm, clip epsilon or advantages without another GEMM
+ * (e.g. a mask-bound sweep). Writes the same outputs as the forward except probs / tile_max. */
+int icepop_fwd_epilogue_bf16(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch,
+                             int32_t with_ref, const icepop_fwd_out* out, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* On-policy forward (theta == theta_old, as in the reference's own loop, scheduler.py:540-541,
  * with lp_train_old recorded by icepop_logprob_bf16 under the same weights): then
  * lp_cur == lp_train_old exactly and r == 1 (objective.py:240), so no GEMM runs -- the IcePop
@@ -347,6 +355,13 @@ int icepop_set_wide_tiles(int32_t enable);
  * The stored probabilities and slab references are the same bits either way; the statistics
  * differ only by the summation grouping. Process-wide; ICEPOP_K1_WIDE sets the initial value. */
 int icepop_set_k1_wide(int32_t enable);
+
+/* K1 run length: the consecutive vocabulary tiles one CTA pair processes for one block of
+ * tokens, merging the softmax statistics in registers and writing one partial per run (K2
+ * merges ceil(V / (256 run)) partials per token instead of ceil(V / 256)). 0 (default) =
+ * automatic (16, shorter when the problem has too few tiles to keep every pair busy), else 1..64.
+ * Process-wide; ICEPOP_K1_RUN sets the initial value. */
+int icepop_set_k1_run(int32_t run);
 
 /* Backward row skipping: rows whose gradient coefficient is exactly zero (popped tokens,
  * clip-inactive tokens, zero-advantage sequences; objective.py:250) contribute nothing to

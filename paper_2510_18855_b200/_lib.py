@@ -143,6 +143,10 @@ SIGNATURES: dict[str, tuple] = {
         ctypes.c_int,
         [_P(Shape), _P(Config), _c_p, _c_p, _c_p, _P(Batch), _P(FwdOut), _c_p, _sz, _c_p],
     ),
+    "icepop_fwd_epilogue_bf16": (
+        ctypes.c_int,
+        [_P(Shape), _P(Config), _P(Batch), _i32, _P(FwdOut), _c_p, _sz, _c_p],
+    ),
     "icepop_fwd_onpolicy": (
         ctypes.c_int,
         [_P(Shape), _P(Config), _P(Batch), _c_p, _c_p, _P(FwdOut), _c_p, _sz, _c_p],
@@ -184,6 +188,7 @@ SIGNATURES: dict[str, tuple] = {
     "icepop_set_wide_tiles": (ctypes.c_int, [_i32]),
     "icepop_set_k1_wide": (ctypes.c_int, [_i32]),
     "icepop_set_skip_inactive": (ctypes.c_int, [_i32]),
+    "icepop_set_k1_run": (ctypes.c_int, [_i32]),
 }
 
 _lib: ctypes.CDLL | None = None

@@ -356,8 +356,33 @@ bool k1_wide() {
 
 // Column tile of K1.
 int k1_bn() { return k1_wide() ? BN_WIDE : BN_; }
-// Partial (max, sum, q) triples per token that K1 writes: one per tile half (umma_gemm.cuh epi_lse).
-int64_t k1_parts(int64_t V) { return 2 * ((V + k1_bn() - 1) / k1_bn()); }
+
+// K1's run length: the n-tiles a unit processes back to back for one m-block, merging the
+// softmax statistics in registers and writing one partial per run (umma_gemm.cuh epi_lse). 16
+// cuts the partials K1 writes and K2 reads from 2 * ceil(V/256) * 12 bytes per token (3.9 GB at
+// C2) to 2 * ceil(V/4096) * 12 (0.25 GB); small problems take shorter runs so that every unit
+// still gets >= 16 runs (the last run's imbalance stays small). ICEPOP_K1_RUN overrides.
+int g_k1_run = -1;  // 0 = automatic; ICEPOP_K1_RUN / icepop_set_k1_run
+
+int k1_run_len(int64_t n_tokens, int64_t V, int64_t d) {
+  if ((d + BK - 1) / BK >= long_k_blocks()) return 1;  // a long-K K1 runs static waves, tile by tile
+  if (g_k1_run < 0) g_k1_run = env_int("ICEPOP_K1_RUN", 0);
+  if (g_k1_run > 0) return std::min(g_k1_run, 64);
+  const int cg = cta_group();
+  const int64_t m_t = (std::max<int64_t>(n_tokens, 1) + BM * cg - 1) / (BM * cg);
+  const int64_t n_t = (V + k1_bn() - 1) / k1_bn();
+  const int64_t units = std::max(1, num_sms() / cg);
+  int r = 16;
+  while (r > 1 && m_t * ((n_t + r - 1) / r) < 16 * units) r /= 2;
+  return r;
+}
+
+// Partial (max, sum, q) triples per token that K1 writes: one per run and tile half.
+int64_t k1_parts(int64_t n_tokens, int64_t V, int64_t d) {
+  const int64_t n_t = (V + k1_bn() - 1) / k1_bn();
+  const int r = k1_run_len(n_tokens, V, d);
+  return 2 * ((n_t + r - 1) / r);
+}
 
 // A 512-wide tile does the work of two 256-wide ones ~5% cheaper (fewer operand bytes per
 // FLOP) but halves the tile count. On a small output (C1's dH: 32 wide tiles for 74 CTA
@@ -409,7 +434,9 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   sh.n_tiles = (int)((N + bn - 1) / bn);
   sh.k_blocks = (int)((K + BK - 1) / BK);
   if ((int64_t)sh.m_tiles * sh.n_tiles > INT32_MAX) return fail(ICEPOP_EINVAL, "too many tiles");
-  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+  // runs of n-tiles: K1 only (its epilogue merges statistics across a run); never with waves
+  sh.run_len = (epi == EPI_LSE && !long_k) ? k1_run_len(M, N, K) : 1;
+  sh.num_tiles = sh.m_tiles * n_chunks(sh);
   sh.group_m = group_m_for(epi, sh.m_tiles, sh.n_tiles, cg, long_k, K, num_sms() / cg);
   sh.ext_dev = ext.dim ? ext.dev : nullptr;
   sh.ext_base = ext.base;
@@ -609,8 +636,8 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
   memset(&w, 0, sizeof(w));
   const int64_t n = std::max<int64_t>(s->n_tokens, 1);
   if (!bwd) {  // the backward reads none of the forward's scratch
-    // K1: two partials per 256-column tile (the most any K1 tile width writes); KL: one per 128
-    const int64_t n_parts = ref ? (s->vocab + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : 2 * ((s->vocab + BN_ - 1) / BN_);
+    // K1: two partials per run (k1_parts); KL: one per 128-column tile
+    const int64_t n_parts = ref ? (s->vocab + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : k1_parts(n, s->vocab, s->hidden);
     w.part = c.take<float>((size_t)n_parts * (ref ? 6 : 3) * n);
     w.ztok = c.take<float>((size_t)n);
     w.adv = c.take<double>((size_t)s->n_seqs);
@@ -728,6 +755,38 @@ icepop_saved offset_saved(const icepop_saved& s, int64_t o) {
   return r;
 }
 
+// K2 (merge of K1's partials + the IcePop epilogue) and the fixed-order stats reduction, from
+// the forward workspace `w` (partials, ztok, token-check error word).
+int run_k2(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch, const icepop_fwd_out* out,
+           const BF16Workspace& w, bool ref, const double* adv, cudaStream_t st) {
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  TokenArgs a;
+  fill_token_args(a, shape, cfg, batch, adv);
+  if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
+  a.part = w.part;
+  a.n_parts = (int32_t)(ref ? (V + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : k1_parts(N, V, d));
+  a.part_rows = ref ? 6 : 3;
+  a.kl_f = ref ? out->kl : nullptr;
+  a.lse_ref_f = ref ? out->lse_ref : nullptr;
+  a.kl_w_f = ref ? out->kl_w : nullptr;
+  a.ztok = w.ztok;
+  a.lse_f = out->lse;
+  a.lp_cur = out->lp_cur;
+  a.entropy_f = out->entropy;
+  a.kept = out->kept;
+  a.calib = out->calib;
+  a.surrogate = out->surrogate;
+  a.coeff_f = out->coeff;
+  a.block_stats = w.block_stats;
+  const int grid = token_grid(N);
+  k2_icepop_tokens<0><<<grid, TOK_THREADS, 0, st>>>(a);
+  ICP_CUDA(cudaGetLastError());
+  k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
+  k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -736,6 +795,12 @@ extern "C" {
 int icepop_abi_version(void) { return ICEPOP_ABI_VERSION; }
 
 const char* icepop_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"
+
+static int preload_kernels();
+
+extern "C" {
 
 int icepop_device_check(int device) {
   cudaDeviceProp p;
@@ -749,7 +814,8 @@ int icepop_device_check(int device) {
   int cur = 0;
   ICP_CUDA(cudaGetDevice(&cur));
   ICP_CUDA(cudaSetDevice(device));
-  const int rc = ensure_pool(device);  // scheduler counters: allocated here, never inside a capture
+  int rc = ensure_pool(device);  // scheduler counters: allocated here, never inside a capture
+  if (rc == ICEPOP_OK) rc = preload_kernels();
   cudaSetDevice(cur);
   return rc;
 }
@@ -819,32 +885,23 @@ int icepop_fwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
     ICP_TRY(run_umma(ref ? EPI_LSE_REF : EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st,
                      Extent(), ref ? weight_ref : nullptr));
   }
-  // K2: merge + IcePop epilogue
-  TokenArgs a;
-  fill_token_args(a, shape, cfg, batch, adv);
-  if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
-  a.part = w.part;
-  a.n_parts = (int32_t)(ref ? (V + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : k1_parts(V));
-  a.part_rows = ref ? 6 : 3;
-  a.kl_f = ref ? out->kl : nullptr;
-  a.lse_ref_f = ref ? out->lse_ref : nullptr;
-  a.kl_w_f = ref ? out->kl_w : nullptr;
-  a.ztok = w.ztok;
-  a.lse_f = out->lse;
-  a.lp_cur = out->lp_cur;
-  a.entropy_f = out->entropy;
-  a.kept = out->kept;
-  a.calib = out->calib;
-  a.surrogate = out->surrogate;
-  a.coeff_f = out->coeff;
-  a.block_stats = w.block_stats;
-  const int grid = token_grid(N);
-  k2_icepop_tokens<0><<<grid, TOK_THREADS, 0, st>>>(a);
-  ICP_CUDA(cudaGetLastError());
-  k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
-  k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
-  ICP_CUDA(cudaGetLastError());
-  return ICEPOP_OK;
+  return run_k2(shape, cfg, batch, out, w, ref, adv, st);
+}
+
+int icepop_fwd_epilogue_bf16(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch,
+                             int32_t with_ref, const icepop_fwd_out* out, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  ICP_TRY(check_shape(shape, true));
+  ICP_TRY(check_config(cfg));
+  if (!batch || !out || !out->stats) return fail(ICEPOP_EINVAL, "null batch/out/stats");
+  const bool ref = with_ref != 0;
+  BF16Workspace w = carve_bf16(shape, workspace, 0, false, ref);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ICEPOP_EINVAL, "forward workspace too small: need %zu bytes", w.bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double* adv = nullptr;
+  ICP_TRY(prepare_advantages(shape, batch, w.adv, &adv, st));
+  return run_k2(shape, cfg, batch, out, w, ref, adv, st);
 }
 
 int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, const icepop_batch* batch,
@@ -927,7 +984,7 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   ep.ztok = w.ztok;
   const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
   ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
-  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)k1_parts(V), w.ztok, N, lse, lp,
+  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)k1_parts(N, V, d), w.ztok, N, lse, lp,
                                                           entropy);
   ICP_CUDA(cudaGetLastError());
   return ICEPOP_OK;
@@ -1471,6 +1528,12 @@ int icepop_set_k1_wide(int32_t enable) {
   return ICEPOP_OK;
 }
 
+int icepop_set_k1_run(int32_t run) {
+  if (run < 0 || run > 64) return fail(ICEPOP_EINVAL, "k1 run length must be in [0, 64] (0 = automatic)");
+  g_k1_run = run;
+  return ICEPOP_OK;
+}
+
 int icepop_set_skip_inactive(int32_t enable) {
   g_skip_inactive = enable ? 1 : 0;
   return ICEPOP_OK;
@@ -1495,3 +1558,90 @@ int icepop_gemm_bf16(const void* A, const void* B, void* C, int64_t M, int64_t N
 }
 
 }  // extern "C"
+
+// Load every kernel now (cudaFuncGetAttributes forces it under CUDA's lazy loading), not at its
+// first launch: loading a function waits for the kernels running on the device, so a first
+// launch behind a kernel that spins on another stream -- an NCCL kernel waiting on its peers --
+// would wait for it and could deadlock.
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+static cudaError_t touch_gemm() {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, umma_gemm_kernel<BN, A_MN, B_MN, EPI, CG>);
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+static int touch_epi() {  // the instantiations launch_umma can select
+  constexpr int BN = epi_dual(EPI) ? 128 : BN_;
+  cudaError_t e = touch_gemm<BN, A_MN, B_MN, EPI, 2>();
+  if (e == cudaSuccess) e = touch_gemm<BN, A_MN, B_MN, EPI, 1>();
+  if constexpr (EPI == EPI_STORE || EPI == EPI_LSE)
+    if (e == cudaSuccess) e = touch_gemm<BN_WIDE, A_MN, B_MN, EPI, 2>();
+  if (e != cudaSuccess) return fail(ICEPOP_ECUDA, "kernel load failed: %s", cudaGetErrorString(e));
+  return ICEPOP_OK;
+}
+
+template <class K>
+static int touch(K k) {
+  cudaFuncAttributes fa;
+  const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+  if (e != cudaSuccess) return fail(ICEPOP_ECUDA, "kernel load failed: %s", cudaGetErrorString(e));
+  return ICEPOP_OK;
+}
+
+static int preload_kernels() {
+  ICP_TRY((touch_epi<false, false, EPI_STORE>()));
+  ICP_TRY((touch_epi<false, true, EPI_STORE>()));
+  ICP_TRY((touch_epi<true, false, EPI_STORE>()));
+  ICP_TRY((touch_epi<true, true, EPI_STORE>()));
+  ICP_TRY((touch_epi<false, false, EPI_LSE>()));
+  ICP_TRY((touch_epi<false, true, EPI_LSE>()));
+  ICP_TRY((touch_epi<false, false, EPI_DZ>()));
+  ICP_TRY((touch_epi<false, true, EPI_DZ>()));
+  ICP_TRY((touch_epi<false, false, EPI_LSE_REF>()));
+  ICP_TRY((touch_epi<false, true, EPI_LSE_REF>()));
+  ICP_TRY((touch_epi<false, false, EPI_DZ_REF>()));
+  ICP_TRY((touch_epi<false, true, EPI_DZ_REF>()));
+  ICP_TRY(touch(k0_group_advantages));
+  ICP_TRY(touch(k2_icepop_tokens<0>));
+  ICP_TRY(touch(k2_icepop_tokens<1>));
+  ICP_TRY(touch(k2_icepop_tokens<2>));
+  ICP_TRY(touch(k_finalize_stats));
+  ICP_TRY(touch(k_merge_err));
+  ICP_TRY(touch(k_check_tokens));
+  ICP_TRY(touch(k_logprob_finish));
+  ICP_TRY(touch(k_kl_finish));
+  ICP_TRY(touch(k_sum_blocks));
+  ICP_TRY(touch(k_sgd_update));
+  ICP_TRY(touch(k_rs_fold));
+  ICP_TRY(touch(k_active_count));
+  ICP_TRY(touch(k_active_scan));
+  ICP_TRY(touch(k_active_scatter));
+  ICP_TRY(touch(k_gather_active));
+  ICP_TRY(touch(k_dz_probs));
+  ICP_TRY(touch(k_block_flags));
+  ICP_TRY(touch(k_block_lists));
+  ICP_TRY(touch(k_sp_prep));
+  ICP_TRY(touch(k_iota));
+  ICP_TRY(touch(k_onehot_scatter));
+  // CUB's radix sort (the one-hot scatter's order): run a small and a large sort once so that
+  // both of its dispatch paths (single tile, one-sweep) are loaded
+  const int n_big = 1 << 20;
+  int32_t* buf = nullptr;
+  size_t tb_small = 0, tb_big = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb_small, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, 64, 0, 18);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb_big, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n_big, 0, 18);
+  const size_t tb = std::max(tb_small, tb_big);
+  ICP_CUDA(cudaMalloc(&buf, 4 * (size_t)n_big * sizeof(int32_t) + tb));
+  ICP_CUDA(cudaMemset(buf, 0, 4 * (size_t)n_big * sizeof(int32_t)));
+  void* tmp = buf + 4 * (size_t)n_big;
+  for (int n : {64, n_big}) {
+    size_t t = tb;
+    ICP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, buf, buf + n_big, buf + 2 * n_big, buf + 3 * n_big, n, 0, 18,
+                                             (cudaStream_t)0));
+  }
+  ICP_CUDA(cudaDeviceSynchronize());
+  ICP_CUDA(cudaFree(buf));
+  return ICEPOP_OK;
+}

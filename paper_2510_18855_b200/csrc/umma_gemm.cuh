@@ -45,6 +45,11 @@ __host__ __device__ constexpr bool epi_dual(int epi) { return epi == EPI_LSE_REF
 struct GemmShape {
   int32_t M, N, K;
   int32_t m_tiles, n_tiles, k_blocks;
+  // Scheduling items: a RUN is run_len consecutive n-tiles of one m-block (fewer at the ragged
+  // end), handed to one unit as a whole, so an epilogue can carry per-row state across the run
+  // (K1 merges its softmax statistics over the run and writes one partial per run instead of
+  // one per tile). num_tiles counts runs (= tiles when run_len == 1).
+  int32_t run_len;
   int32_t num_tiles;
   int32_t group_m;       // raster: GROUP_M m-tiles walk the n dimension together (L2 reuse)
   int32_t* tile_counter;  // dynamic schedule: zeroed before launch; nullptr = static round robin
@@ -70,6 +75,10 @@ struct GemmShape {
   int32_t dz_tma_store;   // EPI_DZ: stage dZ tiles in smem and write them with TMA (else direct stores)
 };
 
+__host__ __device__ __forceinline__ int n_chunks(const GemmShape& sh) {
+  return (sh.n_tiles + sh.run_len - 1) / sh.run_len;
+}
+
 // Resolve a device-side extent into the shape every role of the kernel uses.
 __device__ __forceinline__ void resolve_extent(GemmShape& sh, int tile_m, int bn) {
   if (!sh.ext_dev) return;
@@ -83,7 +92,7 @@ __device__ __forceinline__ void resolve_extent(GemmShape& sh, int tile_m, int bn
     if (sh.k_blocks == 0 && !sh.keep_empty) sh.m_tiles = 0;  // nothing to accumulate
   }
   (void)bn;
-  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+  sh.num_tiles = sh.m_tiles * n_chunks(sh);
 }
 
 // Apply the device-side block lists (block-sparse backward): fewer m-tiles / k-blocks.
@@ -93,7 +102,7 @@ __device__ __forceinline__ void resolve_sparsity(GemmShape& sh) {
     sh.k_blocks = max(0, min(*sh.kb_cnt, sh.k_blocks));
     if (sh.k_blocks == 0 && !sh.keep_empty) sh.m_tiles = 0;
   }
-  sh.num_tiles = sh.m_tiles * sh.n_tiles;
+  sh.num_tiles = sh.m_tiles * n_chunks(sh);
 }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
@@ -182,14 +191,18 @@ struct GemmCfg {
   static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 256;
 };
 
-__device__ __forceinline__ void tile_coords(const GemmShape& sh, int tile, int& m_blk, int& n_blk) {
-  const int group = sh.group_m * sh.n_tiles;
-  const int g = tile / group;
+// Run `run` -> its m-block, first n-tile and tile count. Raster: group_m m-blocks walk the n
+// dimension together in chunks of run_len n-tiles (L2 reuse of both operands).
+__device__ __forceinline__ void run_coords(const GemmShape& sh, int run, int& m_blk, int& n_first, int& count) {
+  const int nc = n_chunks(sh);
+  const int group = sh.group_m * nc;
+  const int g = run / group;
   const int first_m = g * sh.group_m;
   const int gm = min(sh.m_tiles - first_m, sh.group_m);
-  const int r = tile - g * group;
+  const int r = run - g * group;
   m_blk = first_m + r % gm;
-  n_blk = r / gm;
+  n_first = (r / gm) * sh.run_len;
+  count = min(sh.run_len, sh.n_tiles - n_first);
   if (sh.mt_map) m_blk = __ldg(sh.mt_map + m_blk);
 }
 
@@ -399,10 +412,14 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
 // MMAs once TMEM columns [0, 256) are read, so both warps of a quarter first read two slabs of
 // that half each (then arrive on `half_bar`) and only then two of the second half: `half` then
 // selects slabs {2 half, 2 half + 1, 4 + 2 half, 5 + 2 half}, output slabs 4 half .. 4 half + 3.
+// Runs: (run_m, run_s, run_q) is this warp's running triple over the tiles of the current run
+// (reset by the caller at the run's first tile); the run's last tile writes it as partial
+// 2 part_idx + half, part_idx = the run's n-chunk. One partial per run instead of per tile.
 template <int BN, int CG>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
-                                        uint8_t* stage1, int m0, int n0, int n_blk, int half, int row, int lane,
-                                        int quarter, uint32_t taddr, uint32_t half_bar) {
+                                        uint8_t* stage1, int m0, int n0, int part_idx, bool last, int half, int row,
+                                        int lane, int quarter, uint32_t taddr, uint32_t half_bar, float& run_m,
+                                        float& run_s, float& run_q) {
   static_assert(BN == 256 || BN == 512, "64-column slabs, four or eight per tile");
   constexpr int NH = BN / 128;  // slabs per warp
   const int m = m0 + row;
@@ -411,7 +428,6 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
   const int row0 = m0 + quarter * 32;
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
-  float run_m = -1e30f, run_s = 0.f, run_q = 0.f;
   float refs[NH];
   int ebuf = 0;
 #pragma unroll
@@ -457,10 +473,12 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
     __syncwarp();  // the next slab's tcgen05.ld is warp-collective (.sync.aligned)
   }
   if (row_ok) {
-    float* p = ep.part + (int64_t)(2 * n_blk + half) * 3 * sh.M + m;
-    p[0] = run_m;
-    p[sh.M] = run_s;
-    p[2 * (int64_t)sh.M] = run_q;
+    if (last) {
+      float* p = ep.part + (int64_t)(2 * part_idx + half) * 3 * sh.M + m;
+      p[0] = run_m;
+      p[sh.M] = run_s;
+      p[2 * (int64_t)sh.M] = run_q;
+    }
     if (store) {
       // references in output-column order: TMEM slabs c, c+1 (c even) hold output slabs k, k+1
       float* tm = ep.tile_max + (int64_t)m * ep.tm_ld + n0 / 64;
@@ -800,12 +818,13 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  // Tile sequence of this unit. Static: unit, unit + n_units, ... Dynamic: the leader's MMA
-  // thread claims tiles from a global counter (one tile of prefetch) and publishes tile j in
-  // ring slot j % RING -- locally with st.shared + arrive, to the peer CTA with st.async
-  // (complete_tx on the peer's rfull barrier, armed by the peer's producer). Tile j+2 is
-  // published only after the MMA has waited for the epilogues of tile j-2, so a slot is never
-  // overwritten while a role of either CTA may still read it. -1 ends the sequence.
+  // Run sequence of this unit (a run is run_len tiles; run_len = 1 for every GEMM but K1).
+  // Static: unit, unit + n_units, ... Dynamic: the leader's MMA thread claims runs from a
+  // global counter (one run of prefetch) and publishes run j in ring slot j % RING -- locally
+  // with st.shared + arrive, to the peer CTA with st.async (complete_tx on the peer's rfull
+  // barrier, armed by the peer's producer). Run j+2 is published only after the MMA has waited
+  // for the epilogue of the tile two accumulators back (a tile of run j-1 or earlier), so a slot
+  // is never overwritten while a role of either CTA may still read it. -1 ends the sequence.
   auto ring_get = [&](int j, bool arm) -> int {
     if (!dynamic) {
       const int t = unit + j * n_units;
@@ -859,10 +878,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           chunk_wait(j * spt);
           atomicAdd(sh.wave_counter, 1);
         }
-        int m_blk, n_blk;
-        tile_coords(sh, tile, m_blk, n_blk);
+        int m_blk, n_first, n_count;
+        run_coords(sh, tile, m_blk, n_first, n_count);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
-        const int n0 = n_blk * BN + (int)rank * B_ROWS;
+        for (int tt = 0; tt < n_count; ++tt) {
+        const int n0 = (n_first + tt) * BN + (int)rank * B_ROWS;
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
           const int kc = (sh.kb_map ? __ldg(sh.kb_map + kb) : kb) * BK;  // k coordinate of this block
@@ -913,6 +933,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (waves && rank == 0 && (kb % skb == skb - 1 || kb == sh.k_blocks - 1)) atomicAdd(sh.wave_counter, 1);
         }
+        }
       }
     }
   } else if (warp == 1) {
@@ -943,12 +964,18 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int j = 0; cur >= 0; ++j) {
+        int m_blk_r, n_first_r, n_count;
+        run_coords(sh, cur, m_blk_r, n_first_r, n_count);
+        (void)m_blk_r;
+        (void)n_first_r;
+        int nxt2 = -1;
+        for (int tt = 0; tt < n_count; ++tt) {
         // SPLIT: wait only for the epilogue to have read TMEM columns [0, BN/2) (thalf)
         mbar_wait(SPLIT ? thalf0 : tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
-        int nxt2 = -1;
-        if (dynamic) {
-          // epilogues of tile j-2 are done -> ring slot (j+2) % RING is free
+        if (dynamic && tt == 0) {
+          // the epilogue is done with the tile two accumulators back (run j-1 or earlier), so
+          // every role has read run j-2's ring slot -> slot (j+2) % RING is free
           nxt2 = (nxt1 >= 0 && claimed < sh.num_tiles) ? claimed : -1;
           publish(j + 2, nxt2);
           claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
@@ -1012,6 +1039,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         // accumulator ready for the epilogue warps (of both CTAs)
         if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
         if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+        }
         if (dynamic) {
           cur = nxt1;
           nxt1 = nxt2;
@@ -1034,16 +1062,21 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     for (int j = 0;; ++j) {
       const int tile = ring_get(j, false);
       if (tile < 0) break;
-      int m_blk, n_blk;
-      tile_coords(sh, tile, m_blk, n_blk);
+      int m_blk, n_first, n_count;
+      run_coords(sh, tile, m_blk, n_first, n_count);
       const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
+      float run_m = -1e30f, run_s = 0.f, run_q = 0.f;  // EPI_LSE: this warp's triple over the run
+      (void)run_m; (void)run_s; (void)run_q;
+      for (int tt = 0; tt < n_count; ++tt) {
+      const int n_blk = n_first + tt;
       mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
       if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
       if constexpr (EPI == EPI_LSE)
-        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN, n_blk, ehalf, row,
-                        lane, quarter, taddr, SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u);
+        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN,
+                        n_first / sh.run_len, tt == n_count - 1, ehalf, row, lane, quarter, taddr,
+                        SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q);
       if constexpr (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
           epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
@@ -1061,6 +1094,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         mbar_arrive_tmem_free(CG == 2 ? mapa_shared(tempty0 + 8 * acc, 0) : tempty0 + 8 * acc);
       }
       if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+      }
     }
     if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
     if (STAGING && lane == 0) bulk_wait<0>();  // all staged tile stores complete

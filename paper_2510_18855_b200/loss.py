@@ -283,8 +283,13 @@ def icepop_fwd(
     weight_ref: torch.Tensor | None = None,
     store_probs: bool | None = None,
     probs_buffers: tuple[torch.Tensor, torch.Tensor] | None = None,
+    keep_workspace: bool = False,
 ) -> IcePopForward:
     """Forward of the IcePop objective on this rank's tokens (objective.py:215-278).
+
+    ``keep_workspace`` (bf16): keep K1's per-row partials in ``extras`` so that
+    :func:`icepop_epilogue` can re-run the IcePop epilogue (other bounds, algorithm, clip
+    epsilon or advantages) without another GEMM.
 
     ``store_probs`` (bf16 path): keep the bf16 probabilities for the backward (True / False /
     None = ``ICEPOP_STORE_PROBS``, default "auto": when they fit in device memory).
@@ -365,6 +370,9 @@ def icepop_fwd(
         f.extras["kl_w"] = kl_w
         if probs is not None:
             f.extras["probs"], f.extras["tile_max"] = probs, tile_max
+        if keep_workspace:
+            f.extras["fwd_workspace"] = (ws, shape, wr is not None)
+            f.extras["temperature"] = cfg.temperature
         return f
     if hidden.dtype == torch.float64:
         if weight.dtype != torch.float64:
@@ -398,6 +406,40 @@ def icepop_fwd(
                                       out, ws.data_ptr(), ws.numel(), st))
         return IcePopForward(lse, lp_cur, entropy, kept, calib, surrogate, coeff, stats, kl=kl, lse_ref=lse_ref)
     raise ValueError(f"unsupported dtype {hidden.dtype}: use bfloat16 (tensor cores) or float64 (validation)")
+
+
+@_on_device
+def icepop_epilogue(batch: PackedBatch, fwd: IcePopForward, cfg: IcePopConfig = IcePopConfig()) -> IcePopForward:
+    """Re-run the IcePop epilogue (K2: log-softmax merge, mask, ratio, clip, surrogate,
+    coefficients, statistics) over the K1 partials a ``keep_workspace=True`` forward kept, with
+    another config / batch metadata (same tokens, weights and temperature). Returns new outputs;
+    no GEMM runs. include/icepop.h icepop_fwd_epilogue_bf16."""
+    if "fwd_workspace" not in fwd.extras:
+        raise ValueError("the forward must be run with keep_workspace=True")
+    ws, shape, with_ref = fwd.extras["fwd_workspace"]
+    if cfg.temperature != fwd.extras.get("temperature", cfg.temperature):
+        raise ValueError("the epilogue cannot change the temperature (the partials are of z / T)")
+    lib = _lib_for(ws)
+    batch.validate()
+    n = int(shape.n_tokens)
+    if batch.tokens.numel() != n:
+        raise ValueError("batch does not match the forward's token count")
+    dev = ws.device
+    e = lambda dt: torch.empty(n, dtype=dt, device=dev)  # noqa: E731
+    out = IcePopForward(e(torch.float32), e(torch.float64), e(torch.float32), e(torch.uint8), e(torch.float64),
+                        e(torch.float64), e(torch.float32), torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev))
+    if with_ref:
+        out.kl, out.lse_ref = e(torch.float32), e(torch.float32)
+        out.extras["kl_w"] = e(torch.float32)
+    sh = _lib.Shape(n_tokens=n, token_offset=batch.token_offset, hidden=shape.hidden, vocab=shape.vocab,
+                    n_seqs=batch.n_seqs, n_groups=batch.n_groups, weight_layout=shape.weight_layout)
+    c_out = _lib.FwdOut(lse=out.lse.data_ptr(), lp_cur=out.lp_cur.data_ptr(), entropy=out.entropy.data_ptr(),
+                        kept=out.kept.data_ptr(), calib=out.calib.data_ptr(), surrogate=out.surrogate.data_ptr(),
+                        coeff=out.coeff.data_ptr(), stats=out.stats.data_ptr(), kl=_lib.ptr(out.kl),
+                        lse_ref=_lib.ptr(out.lse_ref), kl_w=_lib.ptr(out.extras.get("kl_w")))
+    _lib.check(lib.icepop_fwd_epilogue_bf16(sh, cfg.to_c(), batch.to_c(), 1 if with_ref else 0, c_out, ws.data_ptr(),
+                                            ws.numel(), _stream(dev)))
+    return out
 
 
 @_on_device

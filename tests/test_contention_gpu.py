@@ -46,6 +46,14 @@ def test_long_k_gemm_completes_while_sms_are_held(cuda_device, a_mn, b_mn):
     flag = torch.zeros(1, dtype=torch.int32, device=cuda_device)
     status = torch.zeros(1, dtype=torch.int32, device=cuda_device)
     started = torch.zeros(1, dtype=torch.int32, device=cuda_device)
+    # load the helper kernels first: a kernel's first launch (CUDA lazy loading) waits for the
+    # kernels already running, here the holder (the library preloads its own kernels)
+    assert h.th_set_flag(status.data_ptr(), None, torch.cuda.current_stream().cuda_stream) == 0
+    assert h.th_hold_sms(1, 1024, status.data_ptr(), 0, started.data_ptr(), started.data_ptr(), None,
+                         torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    status.zero_()
+    started.zero_()
     torch.cuda.synchronize()
     before = _lib.wave_barrier_abandons(0)
     # non-default streams on both sides: the legacy default stream would serialise the flag

@@ -504,3 +504,53 @@ def test_fused_reduce_scatter_emulated_ranks(cuda_device, monkeypatch, layout, w
     torch.cuda.synchronize()
     assert torch.isfinite(gw).all()
     assert _rel(gw.cpu().numpy(), gw_ref.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("run", [1, 3, 16])
+@pytest.mark.parametrize("layout", ["vd", "dv"])
+def test_k1_runs_merge_statistics(cuda_device, cta_group, layout, run):
+    """K1 runs (icepop_set_k1_run): a CTA pair merges the softmax statistics of `run`
+    consecutive vocabulary tiles in registers and writes one partial per run. The forward's
+    per-token outputs agree with single-tile partials to fp32 rounding and with the oracle;
+    the stored probabilities are the same bits."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_fwd
+
+    lib = _lib.ensure_device(0)
+    c = _case(seed=33, layout=layout, V=4096 + 40, d=256, n_seqs=6, lens=[700, 650, 300, 900, 128, 500])
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    try:
+        _lib.check(lib.icepop_set_k1_run(1))
+        a = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, store_probs=True)
+        _lib.check(lib.icepop_set_k1_run(run))
+        b = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), layout=layout, store_probs=True)
+    finally:
+        _lib.check(lib.icepop_set_k1_run(0))
+    assert torch.equal(a.extras["probs"], b.extras["probs"]) and torch.equal(a.extras["tile_max"], b.extras["tile_max"])
+    assert torch.equal(a.kept, b.kept)
+    torch.testing.assert_close(a.lse, b.lse, rtol=2e-6, atol=2e-6)
+    torch.testing.assert_close(a.entropy, b.entropy, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(a.lp_cur, b.lp_cur, rtol=0, atol=3e-5)
+    o = _oracle(c)
+    np.testing.assert_allclose(b.lp_cur.cpu().numpy(), o["lp_cur"], atol=2e-3, rtol=1e-3)
+    np.testing.assert_allclose(b.entropy.cpu().numpy(), o["entropy"], atol=2e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("with_ref", [False, True])
+def test_epilogue_rerun_equals_full_forward(cuda_device, with_ref):
+    """icepop_epilogue re-runs K2 over the K1 partials of a keep_workspace forward with another
+    config: the same bits as a full forward with that config (no GEMM)."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_epilogue, icepop_fwd
+
+    c = _case(seed=34, V=1000)
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    Wr = (W.float() + 0.05 * torch.randn_like(W.float())).to(torch.bfloat16) if with_ref else None
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), weight_ref=Wr, store_probs=False,
+                   keep_workspace=True)
+    for cfg in (IcePopConfig(alpha=0.8, beta=1.25), IcePopConfig(algo="tis", tis_cap=1.5, clip_eps=0.1)):
+        e = icepop_epilogue(_batch(c, cuda_device), f, cfg)
+        g = icepop_fwd(H, W, _batch(c, cuda_device), cfg, weight_ref=Wr, store_probs=False)
+        for name in ("lse", "lp_cur", "entropy", "kept", "calib", "surrogate", "coeff", "stats"):
+            assert torch.equal(getattr(e, name), getattr(g, name)), name
+        if with_ref:
+            assert torch.equal(e.kl, g.kl)
