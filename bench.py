@@ -459,6 +459,16 @@ def run_ours(args):
                             else None}
         line["kernels_tflops"] = {k: round(v["flop"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in kern.items()
                                   if v["flop"]}
+        if "K2_epilogue" in kern:  # the north star's bandwidth-bound IcePop epilogue
+            kz = kern["K2_epilogue"]
+            gbs = kz["bytes"] / (kz["ms"] / 1e3) / 1e9
+            line["roofline_epilogue"] = {
+                "bound": "hbm", "kernel": "K2 k2_icepop_tokens + k_finalize_stats", "achieved": round(gbs, 1),
+                "peak": pk["hbm"], "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4), "ms": round(kz["ms"], 4),
+                "bytes_per_launch": kz["bytes"], "partials_per_token": kz["n_partials_per_token"],
+                "bytes_note": "per token: K1's partials (12 B each, one per run of 2 vocabulary tiles) + tokens, "
+                              "ztok, lp_old, lp_inf (24 B) + lse, lp_cur, entropy, kept, calib, surrogate, coeff (37 B)"}
+            line["kernels_ms"]["K1_fwd_lse"] = round(kern["K1_fwd_lse+K2"]["ms"] - kz["ms"], 3)
         if "bwd_prep" in kern:  # the HBM-bound part of the stored-probabilities backward
             kz = kern["bwd_prep"]
             gbs = kz["bytes"] / (kz["ms"] / 1e3) / 1e9
@@ -488,6 +498,15 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _k1_parts(n: int, v: int, d: int, sms: int = 148) -> int:
+    """K1 partials per token (icepop_abi.cu k1_parts with the automatic run length)."""
+    m_t, n_t, units = -(-n // 256), -(-v // 256), sms // 2
+    r = 2
+    while r > 1 and m_t * -(-n_t // r) < 16 * units:
+        r //= 2
+    return -(-n_t // r)
 
 
 def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
@@ -526,10 +545,20 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
 
     def fwd():
         holder.clear()
-        holder["f"] = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=sp)
+        holder["f"] = icepop_fwd(H, W, batch, icfg, layout="vd", store_probs=sp, keep_workspace=True)
 
     timed("K1_fwd_lse+K2", fwd, 2.0 * N * d * V)
     f = holder["f"]
+    # K2 alone (the IcePop epilogue over K1's run partials, re-run from the forward's workspace):
+    # its HBM bytes per token are the partials (one per run of 2 vocabulary tiles, 12 B each) plus
+    # the per-token inputs (tokens, ztok, lp_old, lp_inf: 24 B) and outputs (lse, lp_cur,
+    # entropy, kept, calib, surrogate, coeff: 37 B)
+    from paper_2510_18855_b200.loss import icepop_epilogue
+
+    n_parts = _k1_parts(N, V, d)
+    timed("K2_epilogue", lambda: icepop_epilogue(batch, f, icfg), 0.0, reps=5,
+          nbytes=N * (12 * n_parts + 24 + 37))
+    res["K2_epilogue"]["n_partials_per_token"] = n_parts
     s = st.cuda_stream
     if sp:
         # the stored-probabilities backward with null gradients and its workspace runs only its

@@ -277,6 +277,22 @@ int icepop_kl_bf16(const icepop_shape* shape, double temperature, const void* hi
                    const void* weight_p, const void* weight_q, float* kl, float* lse_p, float* lse_q,
                    double* mean_kl, void* workspace, size_t workspace_bytes, void* stream);
 
+/* delta_and_gap (discrepancy.py:132-141) against caller-supplied inference-engine logits:
+ * infer_logits [n_tokens, vocab] row-major, already divided by the temperature (the
+ * reference perturbs the scaled train logits, policy.py:341-347); the train logits are
+ * H.W / temperature from the lm_head GEMM. Per row: kl_rows[t] = KL(p_infer || p_train),
+ * gap_rows[t] = max_v |p_infer - p_train|; *delta = mean_t kl_rows, *max_gap = max_t gap_rows
+ * (device scalars; any output may be NULL). fp64 arithmetic after the GEMM, fixed-order
+ * reductions. n_tokens == 0 -> EINVAL (an empty probe set). Workspace:
+ * icepop_delta_gap_workspace_bytes (f64 != 0 for the fp64 variant). */
+int icepop_delta_gap_workspace_bytes(const icepop_shape* shape, int32_t f64, size_t* bytes);
+int icepop_delta_gap_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                          const float* infer_logits, double* kl_rows, double* gap_rows, double* delta,
+                          double* max_gap, void* workspace, size_t workspace_bytes, void* stream);
+int icepop_delta_gap_f64(const icepop_shape* shape, double temperature, const double* hidden, const double* weight,
+                         const double* infer_logits, double* kl_rows, double* gap_rows, double* delta,
+                         double* max_gap, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- optimizer step (objective.py:301-326) --------------------------------- */
 /* Gradient ascent on an fp32 master copy: v = beta v + g (velocity != NULL) or v = g;
  * w += lr v; weight_bf16 (may be NULL) receives the bf16 copy the GEMMs read. Non-finite
@@ -285,9 +301,17 @@ int icepop_kl_bf16(const icepop_shape* shape, double temperature, const void* hi
 int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, void* weight_bf16,
                           int64_t n, double lr, double beta, double* stats, void* stream);
 
+/* The reference's own fp64 ascent step, bit for bit (objective.py:301-326; numpy rounds the
+ * product and the sum separately): v_out = beta velocity + grad when velocity != NULL (then
+ * the step is v_out) else the step is grad; weight_out = weight + lr step. Outputs may alias
+ * their inputs. Non-finite weights set ICEPOP_ERR_NONFINITE in stats (may be NULL; map with
+ * icepop_finish). lr <= 0 or beta outside [0, 1) -> EINVAL. */
+int icepop_sgd_update_f64(double* weight_out, const double* weight, const double* grad, const double* velocity,
+                          double* velocity_out, int64_t n, double lr, double beta, double* stats, void* stream);
+
 /* ---- diagnostics ----------------------------------------------------------------------- */
 /* Number of long-K GEMM launches on the current device whose wave barriers were abandoned
- * because a unit waited longer than ICEPOP_WAVE_TIMEOUT_US (default 2000): a concurrent kernel
+ * because a unit waited longer than ICEPOP_WAVE_TIMEOUT_US (default 10000): a concurrent kernel
  * held SMs, so part of the grid started late. The result is unaffected (the barrier only keeps
  * operand slices in L2); the count says the GEMM ran without that alignment. Synchronous. */
 int icepop_wave_barrier_abandons(int64_t* count);

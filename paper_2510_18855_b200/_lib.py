@@ -171,7 +171,13 @@ SIGNATURES: dict[str, tuple] = {
     "icepop_peer_close": (ctypes.c_int, [_c_p]),
     "icepop_dz_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _P(Saved), _f64, _c_p, _i64, _c_p]),
     "icepop_kl_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz, _c_p]),
+    "icepop_delta_gap_workspace_bytes": (ctypes.c_int, [_P(Shape), _i32, _P(_sz)]),
+    "icepop_delta_gap_bf16": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,
+                                             _c_p]),
+    "icepop_delta_gap_f64": (ctypes.c_int, [_P(Shape), _f64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _sz,
+                                            _c_p]),
     "icepop_sgd_update_f32": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _i64, _f64, _f64, _c_p, _c_p]),
+    "icepop_sgd_update_f64": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _i64, _f64, _f64, _c_p, _c_p]),
     "icepop_workspace_bytes_f64": (ctypes.c_int, [_P(Shape), _i32, _P(_sz)]),
     "icepop_fwd_f64": (
         ctypes.c_int,

@@ -174,12 +174,12 @@ int diag_ptr(int dev, int32_t** out) {
 }
 
 // Longest a unit of a long-K GEMM waits at a wave barrier before abandoning the barriers of
-// its launch (ICEPOP_WAVE_TIMEOUT_US, default 2 ms; a barrier chunk takes ~50 us at C2).
+// its launch (ICEPOP_WAVE_TIMEOUT_US, default 10 ms; a barrier chunk takes ~50 us at C2).
 uint32_t wave_timeout_ns() {
   static uint32_t v = 0;
   if (v == 0) {
     const char* e = getenv("ICEPOP_WAVE_TIMEOUT_US");
-    const long us = e ? std::max(1L, atol(e)) : 2000L;
+    const long us = e ? std::max(1L, atol(e)) : 10000L;
     v = (uint32_t)std::min<long>(us * 1000L, 4000000000L);
   }
   return v;
@@ -358,10 +358,13 @@ bool k1_wide() {
 int k1_bn() { return k1_wide() ? BN_WIDE : BN_; }
 
 // K1's run length: the n-tiles a unit processes back to back for one m-block, merging the
-// softmax statistics in registers and writing one partial per run (umma_gemm.cuh epi_lse). 16
-// cuts the partials K1 writes and K2 reads from 2 * ceil(V/256) * 12 bytes per token (3.9 GB at
-// C2) to 2 * ceil(V/4096) * 12 (0.25 GB); small problems take shorter runs so that every unit
-// still gets >= 16 runs (the last run's imbalance stays small). ICEPOP_K1_RUN overrides.
+// softmax statistics in registers (and the two column halves through shared memory) and writing
+// one partial per row and run (umma_gemm.cuh epi_lse). Runs of 2 cut the partials K1 writes and
+// K2 reads from 2 * ceil(V/256) * 12 bytes per token (3.9 GB at C2) to ceil(V/512) * 12 (0.97
+// GB). Longer runs cost K1 time at C2 (measured, profiles/r02_k1_run_ab.log: 1, 2 -> 250.6,
+// 251.0 ms; 4 -> 252.4; 8 -> 257.1; 16 -> 272.5 ms, one box): a pair that stays on one m-block
+// for many tiles loosens the raster's sharing of each weight tile. Small problems take runs of
+// 1 when fewer than 16 runs per unit would remain. ICEPOP_K1_RUN / icepop_set_k1_run override.
 int g_k1_run = -1;  // 0 = automatic; ICEPOP_K1_RUN / icepop_set_k1_run
 
 int k1_run_len(int64_t n_tokens, int64_t V, int64_t d) {
@@ -372,16 +375,16 @@ int k1_run_len(int64_t n_tokens, int64_t V, int64_t d) {
   const int64_t m_t = (std::max<int64_t>(n_tokens, 1) + BM * cg - 1) / (BM * cg);
   const int64_t n_t = (V + k1_bn() - 1) / k1_bn();
   const int64_t units = std::max(1, num_sms() / cg);
-  int r = 16;
+  int r = 2;
   while (r > 1 && m_t * ((n_t + r - 1) / r) < 16 * units) r /= 2;
   return r;
 }
 
-// Partial (max, sum, q) triples per token that K1 writes: one per run and tile half.
+// Partial (max, sum, q) triples per token that K1 writes: one per run.
 int64_t k1_parts(int64_t n_tokens, int64_t V, int64_t d) {
   const int64_t n_t = (V + k1_bn() - 1) / k1_bn();
   const int r = k1_run_len(n_tokens, V, d);
-  return 2 * ((n_t + r - 1) / r);
+  return (n_t + r - 1) / r;
 }
 
 // A 512-wide tile does the work of two 256-wide ones ~5% cheaper (fewer operand bytes per
@@ -1500,6 +1503,101 @@ int icepop_sgd_update_f32(float* weight, const float* grad, float* velocity, voi
   return ICEPOP_OK;
 }
 
+int icepop_delta_gap_workspace_bytes(const icepop_shape* shape, int32_t f64, size_t* bytes) {
+  ICP_TRY(check_shape(shape, !f64));
+  if (!bytes) return fail(ICEPOP_EINVAL, "null out pointer");
+  Carver c(nullptr);
+  const size_t n = (size_t)std::max<int64_t>(shape->n_tokens, 1);
+  c.take<uint8_t>(n * (size_t)shape->vocab * (f64 ? 8 : 4));  // train logits
+  c.take<double>(2 * n);                                       // kl / gap rows when not requested
+  *bytes = align_up(c.off, 256);
+  return ICEPOP_OK;
+}
+
+// delta and max token gap (discrepancy.py:132-141) given the inference engine's logits: the train
+// logits come from the lm_head GEMM (tcgen05 for bf16, SIMT for fp64), the rest from one fp64 row
+// kernel and a fixed-order finish.
+static int delta_gap_impl(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                          const void* infer_logits, bool f64, double* kl_rows, double* gap_rows, double* delta,
+                          double* max_gap, void* workspace, size_t workspace_bytes, void* stream) {
+  ICP_TRY(check_shape(shape, !f64));
+  if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
+  if (!hidden || !weight || !infer_logits) return fail(ICEPOP_EINVAL, "null argument");
+  const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
+  if (N == 0) return fail(ICEPOP_EINVAL, "probe set must be non-empty");  // discrepancy.py:136-137
+  size_t need = 0;
+  ICP_TRY(icepop_delta_gap_workspace_bytes(shape, f64 ? 1 : 0, &need));
+  if (!workspace || workspace_bytes < need) return fail(ICEPOP_EINVAL, "workspace too small: need %zu bytes", need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver c(workspace);
+  void* z = c.take<uint8_t>((size_t)N * V * (f64 ? 8 : 4));
+  double* rows = c.take<double>(2 * (size_t)N);
+  double* kl = kl_rows ? kl_rows : rows;
+  double* gap = gap_rows ? gap_rows : rows + N;
+  const bool dv = shape->weight_layout == ICEPOP_W_DV;
+  const int grid = (int)std::min<int64_t>(N, (int64_t)num_sms() * 8);
+  if (f64) {
+    ICP_TRY(logits_f64(shape, static_cast<const double*>(hidden), static_cast<const double*>(weight),
+                       static_cast<double*>(z), st));
+    k_delta_gap_rows<double, double><<<grid, DG_THREADS, 0, st>>>(
+        static_cast<const double*>(z), static_cast<const double*>(infer_logits), N, V, 1.0 / temperature, kl, gap);
+  } else {
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.out = z;
+    ep.ldo = V;
+    ep.out_f32 = 1;
+    ep.vec_ok = (V % 8 == 0) ? 1 : 0;
+    ICP_TRY(run_umma(EPI_STORE, hidden, d, false, weight, dv ? V : d, dv, N, V, d, ep, st));
+    k_delta_gap_rows<float, float><<<grid, DG_THREADS, 0, st>>>(
+        static_cast<const float*>(z), static_cast<const float*>(infer_logits), N, V, 1.0 / temperature, kl, gap);
+  }
+  ICP_CUDA(cudaGetLastError());
+  k_delta_gap_finish<<<1, DG_THREADS, 0, st>>>(kl, gap, N, delta, max_gap);
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
+int icepop_delta_gap_bf16(const icepop_shape* shape, double temperature, const void* hidden, const void* weight,
+                          const float* infer_logits, double* kl_rows, double* gap_rows, double* delta,
+                          double* max_gap, void* workspace, size_t workspace_bytes, void* stream) {
+  return delta_gap_impl(shape, temperature, hidden, weight, infer_logits, false, kl_rows, gap_rows, delta, max_gap,
+                        workspace, workspace_bytes, stream);
+}
+
+int icepop_delta_gap_f64(const icepop_shape* shape, double temperature, const double* hidden, const double* weight,
+                         const double* infer_logits, double* kl_rows, double* gap_rows, double* delta,
+                         double* max_gap, void* workspace, size_t workspace_bytes, void* stream) {
+  return delta_gap_impl(shape, temperature, hidden, weight, infer_logits, true, kl_rows, gap_rows, delta, max_gap,
+                        workspace, workspace_bytes, stream);
+}
+
+int icepop_sgd_update_f64(double* weight_out, const double* weight, const double* grad, const double* velocity,
+                          double* velocity_out, int64_t n, double lr, double beta, double* stats, void* stream) {
+  // objective.py:301-326: lr <= 0 -> ValueError, beta outside [0, 1) -> ValueError
+  if (!(lr > 0.0)) return fail(ICEPOP_EINVAL, "learning rate must be positive");
+  if (velocity && !(beta >= 0.0 && beta < 1.0)) return fail(ICEPOP_EINVAL, "momentum beta must be in [0, 1)");
+  if (!weight_out || !weight || !grad || n < 0 || (velocity && !velocity_out))
+    return fail(ICEPOP_EINVAL, "null weight/grad/velocity_out");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  ICP_CUDA(cudaGetDevice(&dev));
+  int32_t* dg = nullptr;
+  ICP_TRY(diag_ptr(dev, &dg));
+  unsigned* e = reinterpret_cast<unsigned*>(dg + 3);
+  ICP_CUDA(cudaMemsetAsync(e, 0, sizeof(unsigned), st));
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  if (n > 0)
+    k_sgd_update_f64<<<std::max(grid, 1), 256, 0, st>>>(weight_out, weight, grad, velocity, velocity_out, n, lr,
+                                                         beta, e);
+  if (stats) {
+    ICP_CUDA(cudaMemsetAsync(stats, 0, sizeof(double) * ICEPOP_NSTATS, st));
+    k_merge_err<<<1, 1, 0, st>>>(e, stats);
+  }
+  ICP_CUDA(cudaGetLastError());
+  return ICEPOP_OK;
+}
+
 int icepop_wave_barrier_abandons(int64_t* count) {
   if (!count) return fail(ICEPOP_EINVAL, "null out pointer");
   int dev = 0;
@@ -1612,6 +1710,10 @@ static int preload_kernels() {
   ICP_TRY(touch(k_kl_finish));
   ICP_TRY(touch(k_sum_blocks));
   ICP_TRY(touch(k_sgd_update));
+  ICP_TRY(touch(k_sgd_update_f64));
+  ICP_TRY(touch(k_delta_gap_rows<float, float>));
+  ICP_TRY(touch(k_delta_gap_rows<double, double>));
+  ICP_TRY(touch(k_delta_gap_finish));
   ICP_TRY(touch(k_rs_fold));
   ICP_TRY(touch(k_active_count));
   ICP_TRY(touch(k_active_scan));

@@ -345,6 +345,85 @@ __global__ void k_sum_blocks(const double* __restrict__ block_sums, int nb, doub
   }
 }
 
+// delta and max token gap per probe row (discrepancy.py:132-141): with p the inference engine's
+// distribution softmax(zi) and q the training engine's softmax(zt) (both already divided by T):
+//   kl_t = sum_v p_v (log p_v - log q_v),  gap_t = max_v |p_v - q_v|.
+// One block per row, fp64 arithmetic, fixed-order block reductions (deterministic). zt is
+// read as TZ (the train logits the GEMM wrote, scaled here by inv_t), zi as TI.
+constexpr int DG_THREADS = 256;
+
+template <class T>
+__device__ __forceinline__ double block_reduce_dg(double v, bool is_max, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, x) : v + x;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = sh[0];
+  for (int w = 1; w < DG_THREADS / 32; ++w) r = is_max ? fmax(r, sh[w]) : r + sh[w];
+  return r;
+}
+
+template <class TZ, class TI>
+__global__ void __launch_bounds__(DG_THREADS) k_delta_gap_rows(const TZ* __restrict__ zt, const TI* __restrict__ zi,
+                                                               int64_t n, int64_t V, double inv_t,
+                                                               double* __restrict__ kl, double* __restrict__ gap) {
+  __shared__ double sh[DG_THREADS / 32];
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    const TZ* a = zt + t * V;
+    const TI* b = zi + t * V;
+    double ma = -INFINITY, mb = -INFINITY;
+    for (int64_t v = threadIdx.x; v < V; v += DG_THREADS) {
+      ma = fmax(ma, (double)a[v] * inv_t);
+      mb = fmax(mb, (double)b[v]);
+    }
+    ma = block_reduce_dg<double>(ma, true, sh);
+    mb = block_reduce_dg<double>(mb, true, sh);
+    double sa = 0.0, sb = 0.0;
+    for (int64_t v = threadIdx.x; v < V; v += DG_THREADS) {
+      sa += exp((double)a[v] * inv_t - ma);
+      sb += exp((double)b[v] - mb);
+    }
+    sa = block_reduce_dg<double>(sa, false, sh);
+    sb = block_reduce_dg<double>(sb, false, sh);
+    const double lsa = ma + log(sa), lsb = mb + log(sb);
+    double k = 0.0, g = 0.0;
+    for (int64_t v = threadIdx.x; v < V; v += DG_THREADS) {
+      const double lq = (double)a[v] * inv_t - lsa, lp = (double)b[v] - lsb;
+      const double p = exp(lp);
+      k += p * (lp - lq);
+      g = fmax(g, fabs(p - exp(lq)));
+    }
+    k = block_reduce_dg<double>(k, false, sh);
+    g = block_reduce_dg<double>(g, true, sh);
+    if (threadIdx.x == 0) {
+      kl[t] = k;
+      gap[t] = g;
+    }
+  }
+}
+
+// delta = mean_t kl_t (fixed order), max_gap = max_t gap_t: one block.
+__global__ void k_delta_gap_finish(const double* __restrict__ kl, const double* __restrict__ gap, int64_t n,
+                                   double* __restrict__ delta, double* __restrict__ max_gap) {
+  __shared__ double sh[DG_THREADS / 32];
+  double s = 0.0, m = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += DG_THREADS) {
+    s += kl[t];
+    m = fmax(m, gap[t]);
+  }
+  s = block_reduce_dg<double>(s, false, sh);
+  m = block_reduce_dg<double>(m, true, sh);
+  if (threadIdx.x == 0) {
+    if (delta) *delta = s / (double)n;
+    if (max_gap) *max_gap = m;
+  }
+}
+
 // ------------------------------------------------------------------ optimizer step (f-2)
 // Gradient ASCENT as the reference (objective.py:301-326): v = beta v + g (momentum) or v = g,
 // w += lr v; non-finite weights set the error word; optional bf16 copy of w for the GEMMs.
@@ -361,6 +440,27 @@ __global__ void k_sgd_update(float* __restrict__ w, const float* __restrict__ g,
     const float nw = fmaf(lr, step, w[i]);
     w[i] = nw;
     if (w_bf16) w_bf16[i] = __float2bfloat16_rn(nw);
+    bad |= !isfinite(nw);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, ICEPOP_ERR_NONFINITE);
+}
+
+// The reference's own update in fp64 (objective.py:301-326), bit for bit: numpy rounds
+// lr * step and the sum separately (no FMA), and the momentum step v' = beta v + g likewise.
+// w_out / v_out may alias w / v (in-place update); non-finite results set the error word.
+__global__ void k_sgd_update_f64(double* __restrict__ w_out, const double* __restrict__ w,
+                                 const double* __restrict__ g, const double* __restrict__ v,
+                                 double* __restrict__ v_out, int64_t n, double lr, double beta,
+                                 unsigned* __restrict__ err) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double step = g[i];
+    if (v) {
+      step = __dadd_rn(__dmul_rn(beta, v[i]), step);  // objective.py:323
+      v_out[i] = step;
+    }
+    const double nw = __dadd_rn(w[i], __dmul_rn(lr, step));  // objective.py:307
+    w_out[i] = nw;
     bad |= !isfinite(nw);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, ICEPOP_ERR_NONFINITE);

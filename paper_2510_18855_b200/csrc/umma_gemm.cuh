@@ -188,7 +188,9 @@ struct GemmCfg {
   // buffers, EPI_LSE 8 warps x 1 buffer
   static constexpr int EPI_BUF_BYTES = 32 * 128;
   static constexpr int EPI_STAGE_BYTES = EPI_STAGING ? 8 * EPI_BUF_BYTES : 0;
-  static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 256;
+  // K1's half-merge exchange (one (max, sum, q) triple per TMEM lane), after the barrier block
+  static constexpr int XCH_BYTES = EPI_STAGING ? BM * 3 * 4 : 0;
+  static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + EPI_STAGE_BYTES + 256 + XCH_BYTES;
 };
 
 // Run `run` -> its m-block, first n-tile and tile count. Raster: group_m m-blocks walk the n
@@ -413,13 +415,15 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
 // that half each (then arrive on `half_bar`) and only then two of the second half: `half` then
 // selects slabs {2 half, 2 half + 1, 4 + 2 half, 5 + 2 half}, output slabs 4 half .. 4 half + 3.
 // Runs: (run_m, run_s, run_q) is this warp's running triple over the tiles of the current run
-// (reset by the caller at the run's first tile); the run's last tile writes it as partial
-// 2 part_idx + half, part_idx = the run's n-chunk. One partial per run instead of per tile.
+// (reset by the caller at the run's first tile). At the run's last tile the two warps of a TMEM
+// lane quarter merge their triples through `xch` (the second-half warp hands its triple over
+// between two named barriers) and the first-half warp writes partial part_idx = the run's
+// n-chunk: one partial per row and run instead of two per tile.
 template <int BN, int CG>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
                                         uint8_t* stage1, int m0, int n0, int part_idx, bool last, int half, int row,
                                         int lane, int quarter, uint32_t taddr, uint32_t half_bar, float& run_m,
-                                        float& run_s, float& run_q) {
+                                        float& run_s, float& run_q, float* xch) {
   static_assert(BN == 256 || BN == 512, "64-column slabs, four or eight per tile");
   constexpr int NH = BN / 128;  // slabs per warp
   const int m = m0 + row;
@@ -472,13 +476,26 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
     }
     __syncwarp();  // the next slab's tcgen05.ld is warp-collective (.sync.aligned)
   }
-  if (row_ok) {
-    if (last) {
-      float* p = ep.part + (int64_t)(2 * part_idx + half) * 3 * sh.M + m;
-      p[0] = run_m;
-      p[sh.M] = run_s;
-      p[2 * (int64_t)sh.M] = run_q;
+  if (last) {  // warp-uniform: both warps of the quarter reach it on the same tile
+    float* x = xch + (quarter * 32 + lane) * 3;
+    if (half == 1) {
+      x[0] = run_m;
+      x[1] = run_s;
+      x[2] = run_q;
     }
+    named_bar_sync(1 + quarter, 64);
+    if (half == 0 && row_ok) {
+      const float m2 = x[0], s2 = x[1], q2 = x[2];
+      const float nm = fmaxf(run_m, m2);
+      const float a = fast_exp2(run_m - nm), b = fast_exp2(m2 - nm);
+      float* p = ep.part + (int64_t)part_idx * 3 * sh.M + m;
+      p[0] = nm;
+      p[sh.M] = fmaf(a, run_s, b * s2);
+      p[2 * (int64_t)sh.M] = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(m2 - nm, s2, q2));
+    }
+    named_bar_sync(1 + quarter, 64);  // the exchange slot is free for the next run
+  }
+  if (row_ok) {
     if (store) {
       // references in output-column order: TMEM slabs c, c+1 (c even) hold output slabs k, k+1
       float* tm = ep.tile_max + (int64_t)m * ep.tm_ld + n0 / 64;
@@ -765,6 +782,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   // barrier block: full[S] empty[S] tfull[2] tempty[2] rfull[RING] | tmem_holder | ring[RING]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::RING);
   int32_t* ring = reinterpret_cast<int32_t*>(tmem_holder + 1);
+  float* xch = reinterpret_cast<float*>(sEpi + Cfg::EPI_STAGE_BYTES + 256);  // XCH_BYTES (K1)
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * STAGES);
@@ -1076,7 +1094,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       if constexpr (EPI == EPI_LSE)
         epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN,
                         n_first / sh.run_len, tt == n_count - 1, ehalf, row, lane, quarter, taddr,
-                        SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q);
+                        SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q, xch);
       if constexpr (EPI == EPI_DZ) {
         if (sh.dz_tma_store)
           epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,

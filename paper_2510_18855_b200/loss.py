@@ -524,6 +524,45 @@ def discrepancy(hidden: torch.Tensor, weight_p: torch.Tensor, weight_q: torch.Te
     return mean, kl
 
 
+@_on_device
+def delta_and_gap(hidden: torch.Tensor, weight: torch.Tensor, infer_logits: torch.Tensor, layout: str = "vd",
+                  temperature: float = 1.0):
+    """delta = mean_t KL(p_infer,t || p_train,t) and max_token_gap = max_{t,v} |p_infer - p_train|
+    over the probe rows of `hidden` (discrepancy.py:132-141), given the inference engine's logits
+    `infer_logits` [n, V] (already divided by the temperature, as the reference perturbs the
+    scaled train logits). The train logits are H.W / temperature from the lm_head GEMM.
+
+    bf16 hidden / weight with fp32 infer_logits (tensor cores), or all fp64 (SIMT, for the
+    reference's exact tests). Returns (delta, max_gap) as device fp64 scalars and the per-row
+    (kl, gap) fp64 vectors. include/icepop.h icepop_delta_gap_*."""
+    lib = _lib_for(hidden)
+    f64 = hidden.dtype == torch.float64
+    if f64:
+        if weight.dtype != torch.float64 or infer_logits.dtype != torch.float64:
+            raise ValueError("the fp64 probe needs fp64 hidden, weight and infer_logits")
+    elif hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16 or infer_logits.dtype != torch.float32:
+        raise ValueError("the probe runs on bf16 hidden/weight with fp32 infer_logits (or all fp64)")
+    hidden, weight, infer_logits = hidden.contiguous(), weight.contiguous(), infer_logits.contiguous()
+    n, d = hidden.shape
+    v = weight.shape[1] if layout == "dv" else weight.shape[0]
+    if tuple(infer_logits.shape) != (n, v):
+        raise ValueError(f"infer_logits must be [{n}, {v}]")
+    shape = _lib.Shape(n_tokens=n, token_offset=0, hidden=d, vocab=v, n_seqs=1, n_groups=1,
+                       weight_layout=LAYOUTS[layout])
+    dev = hidden.device
+    nb = _lib._sz()
+    _lib.check(lib.icepop_delta_gap_workspace_bytes(shape, 1 if f64 else 0, nb))
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=dev)
+    kl = torch.empty(n, dtype=torch.float64, device=dev)
+    gap = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    fn = lib.icepop_delta_gap_f64 if f64 else lib.icepop_delta_gap_bf16
+    _lib.check(fn(shape, float(temperature), hidden.data_ptr(), weight.data_ptr(), infer_logits.data_ptr(),
+                  kl.data_ptr(), gap.data_ptr(), out.data_ptr(), out.data_ptr() + 8, ws.data_ptr(), ws.numel(),
+                  _stream(dev)))
+    return out[0], out[1], kl, gap
+
+
 def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chunk_bytes: int | None = None) -> int:
     """Backward workspace for a dZ chunk of at most `chunk_bytes` (default DZ_CHUNK_BYTES)."""
     lib = _lib.load()

@@ -312,30 +312,113 @@ def objective_and_grad(
     )
 
 
+def _device_step(weights: np.ndarray, grad: np.ndarray, lr: float, velocity: np.ndarray | None = None,
+                 beta: float = 0.0):
+    """One fp64 ascent step on the GPU (icepop_sgd_update_f64, the reference's rounding bit for
+    bit): returns (new weights, new velocity or None) as host arrays."""
+    import torch
+
+    from . import _lib
+    from .loss import _stream
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.ensure_device(dev.index)
+    w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
+    g = torch.from_numpy(np.ascontiguousarray(grad, dtype=np.float64)).to(dev)
+    v = torch.from_numpy(np.ascontiguousarray(velocity, dtype=np.float64)).to(dev) if velocity is not None else None
+    stats = torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev)
+    _lib.check(lib.icepop_sgd_update_f64(w.data_ptr(), w.data_ptr(), g.data_ptr(), _lib.ptr(v), _lib.ptr(v), w.numel(),
+                                         float(lr), float(beta), stats.data_ptr(), _stream(dev)))
+    err = int(stats[_lib.STAT_ERRORS].item())
+    if err & 4:
+        raise NumericError("parameter update produced non-finite weights")  # objective.py:309-310
+    return w.cpu().numpy(), (v.cpu().numpy() if v is not None else None)
+
+
 def sgd_update(theta, grad: np.ndarray, lr: float):
-    """objective.py:301-311 (host update; the fused device update is SURVEY 8f-2)."""
+    """objective.py:301-311 on the device: gradient ascent w + lr g in fp64 with numpy's
+    rounding (the same bits), version_id + 1, NumericError on non-finite weights."""
     if lr <= 0:
         raise ValueError("learning rate must be positive")
-    if grad.shape != theta.weights.shape:
+    if np.shape(grad) != theta.weights.shape:
         raise ValueError("gradient shape does not match parameters")
-    with np.errstate(over="ignore"):
-        weights = theta.weights + lr * grad
-    if not np.isfinite(weights).all():
-        raise NumericError("parameter update produced non-finite weights")
+    weights, _ = _device_step(theta.weights, grad, lr)
     return type(theta)(weights=weights, version_id=theta.version_id + 1)
 
 
 def momentum_update(theta, grad, velocity, lr: float, beta: float = 0.9):
-    """objective.py:314-326."""
+    """objective.py:314-326 on the device: v' = beta v + g, then the ascent step with v'
+    (one kernel); returns (new params, v')."""
     if not 0.0 <= beta < 1.0:
         raise ValueError("momentum beta must be in [0, 1)")
-    new_velocity = beta * velocity + grad
-    return sgd_update(theta, new_velocity, lr), new_velocity
+    if np.shape(velocity) != np.shape(grad):
+        raise ValueError("velocity shape does not match the gradient")
+    if lr <= 0:
+        raise ValueError("learning rate must be positive")
+    if np.shape(grad) != theta.weights.shape:
+        raise ValueError("gradient shape does not match parameters")
+    weights, new_velocity = _device_step(theta.weights, grad, lr, velocity, beta)
+    return type(theta)(weights=weights, version_id=theta.version_id + 1), new_velocity
+
+
+def delta_and_gap(params, probes, infer, temperature: float = 1.0, *, precision: str | None = None):
+    """discrepancy.py:132-141 on the device: (mean over the probes of KL(p_infer || p_train),
+    max |p_infer - p_train|).
+
+    The inference engine's logits are the reference's own simulation of that engine
+    (mismatchlab.policy.perturb_logits of the scaled train logits with noise_keys, policy.py:
+    269-277, 341-347): the noise model is the engine's, not part of the path, and is not ported
+    (SURVEY.md 8f-1), so this drop-in needs mismatchlab. The train logits (multi-hot H . W, the
+    feature rows restated in features.py), the log-softmaxes, the KL and the gap run on the
+    GPU (loss.delta_and_gap; fp64 by default like the objective, so the reference's exact and
+    finite-difference tests hold)."""
+    import torch
+    from mismatchlab.policy import noise_keys, perturb_logits  # type: ignore  (the engine simulator)
+
+    from .features import feature_rows, multihot_device
+    from .loss import delta_and_gap as _device_delta_gap
+
+    if not probes:
+        raise ValueError("probe set must be non-empty")  # discrepancy.py:136-137
+    if temperature <= 0:
+        raise ValueError("temperature must be positive")
+    precision = precision or _DEFAULT_PRECISION
+    n_features, vocab = params.weights.shape
+    feats = np.empty((len(probes), 4), dtype=np.int64)
+    kf = np.empty(len(probes), dtype=np.uint64)
+    kv = np.empty(len(probes), dtype=np.uint64)
+    for i, ctx in enumerate(probes):
+        prev, last = ctx.window()
+        feats[i] = feature_rows(ctx.prompt_id, prev, last, n_features)
+        kf[i], kv[i] = noise_keys(infer, params.version_id, ctx.prompt_id, prev, last)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fd = torch.from_numpy(feats).to(dev)
+    W64 = torch.from_numpy(np.ascontiguousarray(params.weights, dtype=np.float64)).to(dev)
+    H64 = multihot_device(fd, n_features, torch.float64)
+    train = (H64 @ W64 / temperature).cpu().numpy()  # the simulator's input (the engine perturbs it)
+    infer_logits = perturb_logits(train, kf, kv, infer.mismatch_scale)
+    if precision == "fp64":
+        d, g, _, _ = _device_delta_gap(H64, W64, torch.from_numpy(np.ascontiguousarray(infer_logits)).to(dev),
+                                       layout="dv", temperature=temperature)
+    elif precision == "bf16":
+        nf_pad = (n_features + 7) // 8 * 8
+        Wb = torch.zeros((nf_pad, vocab), dtype=torch.bfloat16, device=dev)
+        Wb[:n_features] = W64.to(torch.bfloat16)
+        d, g, _, _ = _device_delta_gap(multihot_device(fd, nf_pad, torch.bfloat16), Wb,
+                                       torch.from_numpy(infer_logits.astype(np.float32)).to(dev), layout="dv",
+                                       temperature=temperature)
+    else:
+        raise ValueError("precision must be 'fp64' or 'bf16'")
+    out = torch.stack([d, g]).cpu().numpy()
+    return float(out[0]), float(out[1])
 
 
 def install(precision: str | None = None) -> None:
-    """Rebind mismatchlab's objective_and_grad to this drop-in."""
+    """Rebind mismatchlab's objective_and_grad and the update step that follows
+    it (sgd_update / momentum_update, scheduler.py:551-555) to this drop-in, in every module
+    that binds the names (objective.py, scheduler.py:29-40, __init__.py:32-34)."""
     import mismatchlab  # type: ignore
+    import mismatchlab.discrepancy  # type: ignore
     import mismatchlab.objective  # type: ignore
     import mismatchlab.scheduler  # type: ignore
 
@@ -343,10 +426,16 @@ def install(precision: str | None = None) -> None:
         set_default_precision(precision)
     for mod in (mismatchlab, mismatchlab.objective, mismatchlab.scheduler):
         mod.objective_and_grad = objective_and_grad
+        mod.sgd_update = sgd_update
+        mod.momentum_update = momentum_update
+    # the discrepancy probe: measure() (discrepancy.py:144-161, called by train_loop) looks the
+    # name up in its own module
+    for mod in (mismatchlab, mismatchlab.discrepancy):
+        mod.delta_and_gap = delta_and_gap
 
 
 __all__ = [
     "Algo", "LossBreakdown", "MaskingBounds", "ObjectiveConfig", "PromptGroup", "TokenRecord", "empty_breakdown",
-    "group_advantages", "install", "mask", "momentum_update", "objective_and_grad", "set_default_precision",
-    "sgd_update",
+    "delta_and_gap", "group_advantages", "install", "mask", "momentum_update", "objective_and_grad",
+    "set_default_precision", "sgd_update",
 ]

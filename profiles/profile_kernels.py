@@ -63,6 +63,7 @@ def main():
         saved = _lib.Saved(tokens=tokens.data_ptr(), lse=f.lse.data_ptr(), coeff=f.coeff.data_ptr())
         if sp:  # the stored-probabilities backward with null gradients = the dZ pass alone
             saved.probs, saved.tile_max = f.extras["probs"].data_ptr(), f.extras["tile_max"].data_ptr()
+            saved.lp_cur = f.lp_cur.data_ptr()
             _lib.check(lib.icepop_bwd_bf16(shape, IcePopConfig().to_c(), H.data_ptr(), W.data_ptr(), None, saved,
                                            -1.0, None, 0, None, 0, None, 0, st))
         else:

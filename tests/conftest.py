@@ -107,3 +107,29 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+REF_INSTALL = ROOT / "baseline" / "_ref"
+_BOUND = ("objective_and_grad", "sgd_update", "momentum_update", "delta_and_gap")
+
+
+@pytest.fixture
+def mismatchlab_ref():
+    """The unmodified reference (the baseline/_ref install, which travels to the GPU box), with
+    every name the drop-in's install() rebinds restored afterwards."""
+    if not (REF_INSTALL / "mismatchlab").exists():
+        pytest.skip("the reference install (baseline/_ref) is not present")
+    if str(REF_INSTALL) not in sys.path:
+        sys.path.insert(0, str(REF_INSTALL))
+    import mismatchlab
+    import mismatchlab.discrepancy
+    import mismatchlab.objective
+    import mismatchlab.scheduler
+
+    mods = (mismatchlab, mismatchlab.objective, mismatchlab.scheduler, mismatchlab.discrepancy)
+    saved = {(m, n): getattr(m, n) for m in mods for n in _BOUND if hasattr(m, n)}
+    try:
+        yield mismatchlab
+    finally:
+        for (m, n), f in saved.items():
+            setattr(m, n, f)

@@ -72,4 +72,4 @@ def test_long_k_gemm_completes_while_sms_are_held(cuda_device, a_mn, b_mn):
     assert _lib.wave_barrier_abandons(0) > before
     ref = (A.float().T if a_mn else A.float()) @ (B.float() if b_mn else B.float().T)
     err = float((C - ref).norm() / ref.norm())
-    assert err < 1e-5, err
+    assert err < 1e-4, err  # fp32 accumulation over K = 32,768 in both

@@ -253,3 +253,62 @@ def test_peer_slots_fold_releases_slots_only_after_every_rank_folded(world, tmp_
     last_fold = max(i for i, (e, _) in enumerate(events) if e == "fold")
     first_next = min(i for i, (e, _) in enumerate(events) if e == "next")
     assert last_fold < first_next, events
+
+
+class _FoldingPeerOps(_FakePeerOps):
+    """Fake ops whose fold writes the owner's summed dW shard (what the CUDA fold of the slots
+    K5 filled would produce): the sum over ranks of each rank's seeded partial dW."""
+
+    def __init__(self, rank, world, shape):
+        super().__init__(rank)
+        self.world, self.shape = world, shape
+
+    def fold(self, local, world, shard_elems, out):
+        full = sum(_partial_dw(r, self.shape) for r in range(world)).reshape(-1)
+        lo = self.rank * shard_elems
+        part = full[lo:lo + shard_elems]
+        out.zero_()
+        out[:part.numel()] = part
+
+
+def _partial_dw(rank, shape):
+    return torch.randn(shape, generator=torch.Generator().manual_seed(100 + rank))
+
+
+def _composed_fn(rank, world):
+    from paper_2510_18855_b200.optim import ShardedAscent
+
+    shape = (37, 16)  # 37 dW rows: the last shard is ragged
+    w0 = torch.randn(shape, generator=torch.Generator().manual_seed(7))
+    weight = w0.to(torch.bfloat16)
+    lr, beta = 0.25, 0.5
+
+    def ref_update(m, g, v, out):  # objective.py:314-326 in torch (stand-in for the CUDA kernel)
+        v.mul_(beta).add_(g)
+        m.add_(lr * v)
+        out.copy_(m.to(torch.bfloat16))
+
+    opt = ShardedAscent(weight, lr, beta=beta, _ops=_FoldingPeerOps(rank, world, shape), _update_fn=ref_update)
+    assert opt.world == world and opt.rank == rank
+    opt.step()
+    opt.step()  # velocity carries over: v2 = beta v1 + g
+    return weight.float().numpy(), w0.numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ascent_composed_step_gloo(world):
+    """ShardedAscent.step over gloo: each rank folds its shard of the summed dW (the fused
+    reduce-scatter's slots), runs the momentum update on its fp32 master shard, and the bf16
+    shards are all-gathered into every rank's replicated weight; two steps equal two unsharded
+    momentum steps on the summed dW."""
+    out = run_ranks(_composed_fn, world=world)
+    shape = (37, 16)
+    g = sum(_partial_dw(r, shape) for r in range(world))
+    w = torch.from_numpy(out[0][1]).to(torch.bfloat16).float()  # the master starts from the bf16 weight
+    v = torch.zeros(shape)
+    for _ in range(2):
+        v = 0.5 * v + g
+        w = w + 0.25 * v
+    want = w.to(torch.bfloat16).float().numpy()
+    for wb, _ in out:
+        np.testing.assert_array_equal(wb, want)
