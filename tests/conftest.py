@@ -24,7 +24,8 @@ def golden_cases() -> list[str]:
     """The small/medium reference cases (c1_config0, BASELINE configs[0] at full size, has its
     own schema and tests)."""
     return sorted(p.stem for p in GOLDEN.glob("*.npz")
-                  if p.stem not in ("advantages", "c1_config0") and "slice" not in p.stem)
+                  if p.stem not in ("advantages", "c1_config0", "updates", "discrepancy", "lp_record")
+                  and "slice" not in p.stem)
 
 
 def load_c1() -> tuple[dict, np.ndarray]:
