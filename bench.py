@@ -491,6 +491,8 @@ def run_ours(args):
     line["wave_barrier_abandons"] = _lib.wave_barrier_abandons(local)
     if clocks:
         line["clocks"] = clocks
+    if rank == 0 and not args.no_dropin:
+        line["dropin_c1"] = run_dropin_c1(dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, H, W, batch, meta, args.cpu_tokens)
     if world > 1:
@@ -685,6 +687,76 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
     return out
 
 
+# ----------------------------------------------------------------------------- reference-facing API
+def run_dropin_c1(dev, reps: int = 8) -> dict:
+    """BASELINE configs[0] (8 x 512 tokens, 1,024 features, V = 32,768, one GRPO group of 8)
+    through the drop-in ``objective_and_grad`` -- the call the reference's own loop makes
+    (scheduler.py:540-542) -- with its Python records and host fp64 weights in, the fp64
+    gradient and per-token diagnostics out, and the lp_cur write-back into every TokenRecord:
+    wall clock per call (median), bf16 tensor-core path, with a fresh gradient array and with a
+    reused ``grad_out``."""
+    import copy
+    from dataclasses import dataclass
+
+    import torch
+
+    from paper_2510_18855_b200 import objective as O
+
+    @dataclass
+    class Task:
+        prompt_id: int
+
+    @dataclass
+    class Rollout:
+        tokens: list
+
+    @dataclass
+    class Params:
+        weights: np.ndarray
+        version_id: int = 0
+
+        @property
+        def n_features(self):
+            return self.weights.shape[0]
+
+    rng = np.random.default_rng(0)
+    S, T, nf, V = 8, 512, 1024, 32768
+    w = rng.normal(0.0, 0.8, (nf, V))
+    task = Task(prompt_id=17)
+    rollouts = []
+    for _ in range(S):
+        lp = rng.normal(-10.4, 0.3, T)
+        inf = lp - rng.normal(0, 0.233, T)
+        rollouts.append(Rollout([O.TokenRecord(int(y), float(b), float(a), float(a), 0)
+                                 for y, a, b in zip(rng.integers(0, V, T), lp, inf)]))
+    rewards = [float(x) for x in rng.integers(0, 2, S)]
+    groups = [O.PromptGroup(task=task, rollouts=rollouts, rewards=rewards,
+                            advantages=list(O.group_advantages(rewards)) if len(set(rewards)) > 1 else [0.0] * S)]
+    theta = Params(w)
+    cfg, bounds = O.ObjectiveConfig(), O.MaskingBounds()
+    buf = np.empty_like(w)
+    out = {}
+    with torch.cuda.device(dev):
+        for name, kw in (("fresh_grad", {}), ("grad_out", {"grad_out": buf})):
+            for _ in range(2):
+                O.objective_and_grad(copy.deepcopy(groups), theta, theta, None, cfg, bounds, precision="bf16", **kw)
+            ts = []
+            for _ in range(reps):
+                gs = copy.deepcopy(groups)
+                t0 = time.perf_counter()
+                r = O.objective_and_grad(gs, theta, theta, None, cfg, bounds, precision="bf16", **kw)
+                ts.append(time.perf_counter() - t0)
+            ms = 1e3 * float(np.median(ts))
+            out[name] = {"ms_per_call": round(ms, 2), "value": round(S * T / (ms / 1e3), 1)}
+    return {"unit": UNIT, "config": "C1: 8 x 512 tokens, n_features 1,024, V 32,768, 1 GRPO group of 8 (synthetic)",
+            "h2d_bytes_per_call": int(nf * V * 2 + S * T * (4 + 8 + 8 + 8 * 4)),
+            "d2h_bytes_per_call": int(nf * V * 8 + S * T * 8 * 4),
+            "token_count": r.token_count, "calls": reps, **out,
+            "note": "wall clock of objective_and_grad(precision='bf16'): record packing, H2D of the bf16 "
+                    "weights (cast on the host into pinned memory), multi-hot H on the device, the fused "
+                    "fwd+bwd kernels, D2H of the fp64 gradient and the per-token diagnostics, write-back"}
+
+
 # ----------------------------------------------------------------------------- CPU baseline
 def cpu_sample(cfg, n_tokens, seed=0):
     """A bounded host sample of the same workload: 1 group of 2 sequences."""
@@ -852,6 +924,7 @@ def main():
     ap.add_argument("--no-kernel-timing", action="store_true")
     ap.add_argument("--no-onpolicy", action="store_true")
     ap.add_argument("--no-recompute", action="store_true", help="skip the recompute-mode sub-record")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the reference-API (objective_and_grad) record")
     ap.add_argument("--no-ref-diag", action="store_true", help="skip the ref-passed (gamma = 0) sub-record")
     ap.add_argument("--seqs", type=int, default=0,
                     help="override the config's sequences per rank (e.g. the C5 sweep: 16/32/64/128/256)")

@@ -109,6 +109,11 @@ typedef struct icepop_batch {
   const int32_t* group_offsets; /* [n_groups+1]   sequence offsets of prompt groups     */
   const double* advantages;     /* [n_seqs]       PromptGroup.advantages, or NULL       */
   const double* rewards;        /* [n_seqs]       used (with group_advantages) if advantages == NULL */
+  /* [n_tokens] (local) the calibration ratio c_t = exp(lp_train_old - lp_infer_old) computed by
+   * the caller, or NULL (then computed on the device with CUDA's exp, which may differ from
+   * numpy's by 1 ulp). The drop-in passes numpy's own values so that the mask is the
+   * reference's bit for bit even for a c_t within 1 ulp of alpha or beta (objective.py:227). */
+  const double* calib;
 } icepop_batch;
 
 /* ---- library ---------------------------------------------------------------------- */

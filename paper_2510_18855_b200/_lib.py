@@ -72,6 +72,7 @@ class Batch(ctypes.Structure):
         ("group_offsets", _c_p),
         ("advantages", _c_p),
         ("rewards", _c_p),
+        ("calib", _c_p),
     ]
 
 

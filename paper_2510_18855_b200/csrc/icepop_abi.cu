@@ -556,6 +556,7 @@ void fill_token_args(TokenArgs& a, const icepop_shape* s, const icepop_config* c
   a.cu_seqlens = b->cu_seqlens;
   a.group_offsets = b->group_offsets;
   a.adv = adv;
+  a.calib_in = b->calib;
   a.alpha = c->alpha;
   a.beta = c->beta;
   a.clip_eps = c->clip_eps;
@@ -950,14 +951,14 @@ int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, con
 __global__ void k_logprob_finish(const float* part, int n_parts, const float* ztok, int64_t n, float* lse,
                                  double* lp, float* entropy) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    float M = -1e30f;
-    for (int j = 0; j < n_parts; ++j) M = fmaxf(M, part[(int64_t)j * 3 * n + t]);
-    float S = 0.f, Q = 0.f;
-    for (int j = 0; j < n_parts; ++j) {
+    float M = -1e30f, S = 0.f, Q = 0.f;
+    for (int j = 0; j < n_parts; ++j) {  // one pass with a running maximum (k2_icepop_tokens)
       const float* p = part + (int64_t)j * 3 * n + t;
-      const float sc = exp2f(p[0] - M);
-      S = fmaf(p[n], sc, S);
-      Q = fmaf(sc, fmaf(p[0] - M, p[n], p[2 * n]), Q);
+      const float mj = p[0], nm = fmaxf(M, mj);
+      const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
+      Q = fmaf(ca, fmaf(M - nm, S, Q), cb * fmaf(mj - nm, p[n], p[2 * n]));
+      S = fmaf(ca, S, cb * p[n]);
+      M = nm;
     }
     const float l2s = log2f(S);
     const float l = (M + l2s) * LN2_F;

@@ -81,6 +81,7 @@ struct TokenArgs {
   const int32_t* cu_seqlens;
   const int32_t* group_offsets;
   const double* adv;
+  const double* calib_in;  // caller-computed c_t, or null (exp on the device)
   // bf16 mode inputs: K1 partials
   const float* part;  // [n_parts][part_rows][n_tokens]
   int32_t n_parts;
@@ -173,25 +174,28 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
        t += (int64_t)gridDim.x * blockDim.x) {
     double lp_cur, ent, kl = 0.0;
     if (MODE == 0) {
-      // merge split-V partials (log2 units) -> lse, entropy; lp = z[y] - lse
+      // merge split-V partials (log2 units) -> lse, entropy; lp = z[y] - lse. One pass with a
+      // running maximum: each partial is read exactly once (a max pass first would re-read the
+      // partials' maxima from DRAM: they exceed L2 at C2's size)
       const int64_t R = a.part_rows;
       float M = -1e30f, Mr = -1e30f;
-      for (int j = 0; j < a.n_parts; ++j) {
-        const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
-        M = fmaxf(M, p[0]);
-        if (R == 6) Mr = fmaxf(Mr, p[3 * a.n_tokens]);
-      }
       float S = 0.f, Q = 0.f, Sr = 0.f, X = 0.f;
       for (int j = 0; j < a.n_parts; ++j) {
         const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
         const float mj = p[0], sj = p[a.n_tokens], qj = p[2 * a.n_tokens];
-        const float sc = exp2f(mj - M);
-        S = fmaf(sj, sc, S);
-        Q = fmaf(sc, fmaf(mj - M, sj, qj), Q);
+        const float nm = fmaxf(M, mj);
+        const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
+        // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S before the rescale
+        Q = fmaf(ca, fmaf(M - nm, S, Q), cb * fmaf(mj - nm, sj, qj));
+        S = fmaf(ca, S, cb * sj);
         if (R == 6) {
-          Sr = fmaf(p[4 * a.n_tokens], exp2f(p[3 * a.n_tokens] - Mr), Sr);
-          X = fmaf(p[5 * a.n_tokens], sc, X);
+          X = fmaf(ca, X, cb * p[5 * a.n_tokens]);
+          const float mr = p[3 * a.n_tokens];
+          const float nr = fmaxf(Mr, mr);
+          Sr = fmaf(exp2f(Mr - nr), Sr, exp2f(mr - nr) * p[4 * a.n_tokens]);
+          Mr = nr;
         }
+        M = nm;
       }
       const float l2s = log2f(S);
       const float lse = (M + l2s) * LN2_F;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     const double A = a.adv[seq];
     const double lpo = a.lp_old[t];
     // calibration and mask (objective.py:227-238)
-    const double c = exp(__dsub_rn(lpo, a.lp_inf[t]));
+    const double c = a.calib_in ? a.calib_in[t] : exp(__dsub_rn(lpo, a.lp_inf[t]));
     if (!isfinite(c)) err |= ICEPOP_ERR_CALIB_OVERFLOW;
     bool kept;
     double factor;

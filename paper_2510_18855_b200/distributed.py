@@ -52,6 +52,7 @@ def shard_batch(hidden: torch.Tensor, batch: PackedBatch, rank: int, world: int,
         advantages=batch.advantages,
         rewards=batch.rewards,
         token_offset=s,
+        calib=batch.calib[s:e] if batch.calib is not None else None,
     )
     return hidden[s:e], local
 

@@ -170,6 +170,7 @@ class PackedBatch:
     advantages: torch.Tensor | None = None  # float64 [S]
     rewards: torch.Tensor | None = None  # float64 [S] (advantages computed by K0 if None)
     token_offset: int = 0
+    calib: torch.Tensor | None = None  # float64 [n_local] caller-computed exp(lp_old - lp_inf), optional
 
     @property
     def n_seqs(self) -> int:
@@ -188,12 +189,15 @@ class PackedBatch:
             group_offsets=_lib.ptr(self.group_offsets),
             advantages=_lib.ptr(self.advantages),
             rewards=_lib.ptr(self.rewards),
+            calib=_lib.ptr(self.calib),
         )
 
     def validate(self) -> None:
         for name in ("tokens", "cu_seqlens", "group_offsets"):
             if getattr(self, name).dtype != torch.int32:
                 raise ValueError(f"{name} must be int32")
+        if self.calib is not None and (self.calib.dtype != torch.float64 or self.calib.numel() != self.tokens.numel()):
+            raise ValueError("calib must be float64 with one entry per token")
         for name in ("lp_train_old", "lp_infer_old"):
             if getattr(self, name).dtype != torch.float64:
                 raise ValueError(f"{name} must be float64 (the mask is computed bit-exactly in fp64)")
@@ -795,7 +799,8 @@ def icepop_fwd_bwd(
         e0 = min(n, s0 + chunk)
         sub = PackedBatch(batch.tokens[s0:e0], batch.lp_train_old[s0:e0], batch.lp_infer_old[s0:e0],
                           batch.cu_seqlens, batch.group_offsets, batch.advantages, batch.rewards,
-                          token_offset=batch.token_offset + s0)
+                          token_offset=batch.token_offset + s0,
+                          calib=batch.calib[s0:e0] if batch.calib is not None else None)
         f = icepop_fwd(hidden[s0:e0], weight, sub, cfg, layout, weight_ref=weight_ref, probs_buffers=bufs)
         ghc, _ = icepop_bwd(hidden[s0:e0], weight, sub, f, cfg, layout, grad_scale, need_hidden, True, gw,
                             weight_ref, grad_hidden_dtype=grad_hidden_dtype, workspace=ws)

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import enum
 import math
+import operator
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -173,38 +174,93 @@ class _Packed:
     adv: np.ndarray
     feats: np.ndarray
     records: list
+    error: Exception | None = None  # the first validation error, raised after the prefix
+
+
+_FIELDS = operator.attrgetter("token", "logp_train_old", "logp_infer_old", "gen_version")
 
 
 def _pack(groups, theta, theta_old) -> _Packed:
-    """Validate like objective.py:190-213 and flatten in group-major order (:271-276)."""
+    """Validate like objective.py:190-213 and flatten in group-major order (:271-276).
+
+    The reference validates a group / rollout only when its loop reaches it, after computing
+    (and writing back lp_cur for) every rollout before it, so a later ValueError can be preceded
+    by a NumericError or by write-backs. Packing therefore stops at the first invalid group or
+    rollout: the valid prefix is packed and that error is returned with it."""
     from .features import rollout_feats
 
     if not groups:
         raise ValueError("objective needs at least one prompt group")
     if theta_old.version_id > theta.version_id:
         raise ValueError("theta_old must not be newer than theta")
-    tokens, lp_old, lp_inf, cu, go, adv, feats, records = [], [], [], [0], [0], [], [], []
+    rows, cu, go, adv, feats, records = [], [0], [0], [], [], []
+    error = None
     for group in groups:
         if not group.rollouts:
-            raise ValueError("empty prompt group")
+            error = ValueError("empty prompt group")
+            break
         for rollout, advantage in zip(group.rollouts, group.advantages):
             toks = rollout.tokens
             if not toks:
-                raise ValueError("empty rollout in prompt group")
-            if any(rec.gen_version > theta_old.version_id for rec in toks):
-                raise ValueError("token generated by a version newer than theta_old")
-            ids = [rec.token for rec in toks]
-            tokens += ids
-            lp_old += [rec.logp_train_old for rec in toks]
-            lp_inf += [rec.logp_infer_old for rec in toks]
+                error = ValueError("empty rollout in prompt group")
+                break
+            vals = list(map(_FIELDS, toks))
+            if max(v[3] for v in vals) > theta_old.version_id:
+                error = ValueError("token generated by a version newer than theta_old")
+                break
+            rows += vals
             records += toks
-            feats.append(rollout_feats(group.task.prompt_id, ids, theta.n_features))
+            feats.append(rollout_feats(group.task.prompt_id, [v[0] for v in vals], theta.n_features))
             cu.append(cu[-1] + len(toks))
             adv.append(float(advantage))
-        go.append(go[-1] + len(group.rollouts))
-    return _Packed(np.asarray(tokens, dtype=np.int32), np.asarray(lp_old, dtype=np.float64),
-                   np.asarray(lp_inf, dtype=np.float64), np.asarray(cu, dtype=np.int32),
-                   np.asarray(go, dtype=np.int32), np.asarray(adv, dtype=np.float64), np.concatenate(feats), records)
+        if len(adv) > go[-1]:
+            go.append(len(adv))
+        if error is not None:
+            break
+    if not rows:
+        return _Packed(*(np.zeros(0),) * 7, records=[], error=error)
+    a = np.array(rows, dtype=np.float64)
+    return _Packed(a[:, 0].astype(np.int32), np.ascontiguousarray(a[:, 1]), np.ascontiguousarray(a[:, 2]),
+                   np.asarray(cu, dtype=np.int32), np.asarray(go, dtype=np.int32), np.asarray(adv, dtype=np.float64),
+                   np.concatenate(feats), records, error)
+
+
+# Host buffers reused across calls: pinned bf16 staging of the weights (the cast runs on the host's
+# threads straight into pinned memory, then one fast DMA), and page-locked grad_out arrays.
+_STAGING: dict = {}
+_REGISTERED: dict = {}  # (address, nbytes) -> the array (kept alive while registered)
+
+
+def _pinned_bf16(shape) -> "torch.Tensor":
+    import torch
+
+    t = _STAGING.get(shape)
+    if t is None:
+        _STAGING.clear()
+        t = _STAGING[shape] = torch.zeros(shape, dtype=torch.bfloat16, pin_memory=True)
+    return t
+
+
+def _page_lock(arr: np.ndarray) -> None:
+    """Register a reused grad_out buffer with CUDA once (cudaHostRegister) so the gradient's D2H
+    runs at full DMA speed; at most two buffers stay registered (and referenced)."""
+    import torch
+
+    key = (arr.ctypes.data, arr.nbytes)
+    if key in _REGISTERED:
+        return
+    cudart = torch.cuda.cudart()
+    while len(_REGISTERED) >= 2:
+        (addr, _), _old = _REGISTERED.popitem()
+        cudart.cudaHostUnregister(addr)
+    if int(cudart.cudaHostRegister(key[0], key[1], 0)) == 0:
+        _REGISTERED[key] = arr
+
+
+def _write_back(records, lp_cur: list, n: int) -> None:
+    """objective.py:224-225 for the first n packed tokens."""
+    for rec, value in zip(records[:n], lp_cur[:n]):
+        rec.logp_train_cur = value
 
 
 def objective_and_grad(
@@ -222,31 +278,49 @@ def objective_and_grad(
 ) -> LossBreakdown:
     """Objective value and its exact analytic ascent gradient w.r.t. theta, on the GPU.
 
-    Same contract as objective.py:172-298, including the write-back of the recomputed
-    lp_cur into every TokenRecord (objective.py:224-225).
+    Same contract as objective.py:172-298: the same validation, the same exceptions in the
+    same order (a rollout's NumericError -- non-finite logits, calibration or importance ratio
+    -- before a later rollout's ValueError), and the write-back of the recomputed lp_cur into
+    every TokenRecord the reference would have reached (objective.py:224-225). The calibration
+    ratio is numpy's own exp(lp_old - lp_inf), handed to the kernels, so the mask is the
+    reference's bit for bit.
 
     ``grad_out`` (extension, keyword only): a C-contiguous float64 array shaped like
-    theta.weights that receives the gradient and is returned as ``LossBreakdown.grad``.
-    A trainer that reuses one buffer skips materialising a fresh 8*n_features*V-byte array per
-    call, which dominates the call at small batches.
+    theta.weights that receives the gradient and is returned as ``LossBreakdown.grad``. It is
+    page-locked once and kept referenced while registered (the last two such buffers), so a
+    trainer that reuses it gets the gradient at DMA speed instead of materialising a fresh
+    8 * n_features * V-byte array per call. It must not share memory with theta's or ref's
+    weights, and it receives nothing when the call raises.
     """
-    if grad_out is not None and (not isinstance(grad_out, np.ndarray) or grad_out.dtype != np.float64
-                                 or grad_out.shape != tuple(theta.weights.shape)
-                                 or not grad_out.flags.c_contiguous or not grad_out.flags.writeable):
-        raise ValueError("grad_out must be a writeable C-contiguous float64 array shaped like theta.weights")
+    if grad_out is not None:
+        if (not isinstance(grad_out, np.ndarray) or grad_out.dtype != np.float64
+                or grad_out.shape != tuple(theta.weights.shape) or not grad_out.flags.c_contiguous
+                or not grad_out.flags.writeable):
+            raise ValueError("grad_out must be a writeable C-contiguous float64 array shaped like theta.weights")
+        if np.shares_memory(grad_out, theta.weights) or (ref is not None and np.shares_memory(grad_out, ref.weights)):
+            raise ValueError("grad_out must not share memory with the parameters")
     import torch
 
     from .features import multihot_device
-    from .loss import Diagnostics, IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd, icepop_fwd_bwd
+    from .loss import Diagnostics, IcePopConfig, PackedBatch, icepop_fwd, icepop_fwd_bwd
 
-    if temperature <= 0:
-        raise ValueError("temperature must be positive")
     precision = precision or _DEFAULT_PRECISION
-    p = _pack(groups, theta, theta_old)
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if precision not in ("fp64", "bf16"):
+        raise ValueError("precision must be 'fp64' or 'bf16'")
     n_features, vocab = theta.weights.shape
+    p = _pack(groups, theta, theta_old)
+    if not p.records:  # the first group / rollout is invalid
+        raise p.error
+    if temperature <= 0:  # batched_train_logits of the first rollout (policy.py:281-282)
+        raise ValueError("temperature must be positive")
+    if p.tokens.min() < 0 or p.tokens.max() >= vocab:
+        raise ValueError("token id outside the vocabulary")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     icfg = IcePopConfig(alpha=bounds.alpha, beta=bounds.beta, clip_eps=cfg.clip_eps, tis_cap=cfg.tis_cap,
                         temperature=float(temperature), kl_coeff=cfg.kl_coeff, algo=_algo_name(cfg.algo))
+    calib = np.exp(p.lp_old - p.lp_inf)  # objective.py:227, numpy's bits
+    with np.errstate(over="ignore", invalid="ignore"):
+        calib_c = np.where(np.isfinite(calib), calib, 0.0)  # non-finite: raised below, in the reference's order
     batch = PackedBatch(
         tokens=torch.from_numpy(p.tokens).to(dev),
         lp_train_old=torch.from_numpy(p.lp_old).to(dev),
@@ -254,48 +328,82 @@ def objective_and_grad(
         cu_seqlens=torch.from_numpy(p.cu).to(dev),
         group_offsets=torch.from_numpy(p.go).to(dev),
         advantages=torch.from_numpy(p.adv).to(dev),
+        calib=torch.from_numpy(calib_c).to(dev),
     )
     feats = torch.from_numpy(np.ascontiguousarray(p.feats, dtype=np.int64)).to(dev)
-    if precision == "fp64":
-        H = multihot_device(feats, n_features, torch.float64)
-        W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
-        Wr = torch.from_numpy(np.ascontiguousarray(ref.weights, dtype=np.float64)).to(dev) if ref is not None else None
-        fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
-        _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
-    elif precision == "bf16":
-        if vocab % 8:
-            raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
-        nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
+    need_grad = p.error is None  # a validation error later in the batch: the forward decides what raises
+    gw = None
+    with torch.cuda.device(dev):
+        if precision == "fp64":
+            H = multihot_device(feats, n_features, torch.float64)
+            W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
+            Wr = torch.from_numpy(np.ascontiguousarray(ref.weights, dtype=np.float64)).to(dev) if ref is not None \
+                else None
+            fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr)
+            if need_grad:
+                from .loss import icepop_bwd
 
-        def pad_bf16(w):
-            # round on the host (torch's threaded cast), copy a quarter of the fp64 bytes
-            wb = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)).to(torch.bfloat16)
-            if nf_pad != n_features:
-                wb = torch.cat([wb, wb.new_zeros((nf_pad - n_features, vocab))])
-            return wb.to(dev)
+                _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
+        else:
+            if vocab % 8:
+                raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
+            nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
 
-        H = multihot_device(feats, nf_pad, torch.bfloat16)
-        W = pad_bf16(theta.weights)
-        Wr = pad_bf16(ref.weights) if ref is not None else None
-        # value and gradient together: stored probabilities (in token chunks if needed)
-        fwd, _, gw = icepop_fwd_bwd(H, W, batch, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
-        gw = gw[:n_features]
-    else:
-        raise ValueError("precision must be 'fp64' or 'bf16'")
-    finish(fwd.stats)
-    diag = Diagnostics.from_stats(fwd.stats.cpu())
-    grad_finite = bool(torch.isfinite(gw).all())
-    if grad_out is not None:
-        torch.from_numpy(grad_out).copy_(gw.to(torch.float64))
-        grad = grad_out
-    else:
-        grad = gw.to(torch.float64).cpu().numpy()
-    lp_cur = fwd.lp_cur.cpu().numpy()
-    for rec, value in zip(p.records, lp_cur):  # objective.py:224-225
-        rec.logp_train_cur = float(value)
-    if not math.isfinite(diag.objective_value) or not grad_finite:
+            def upload(w):
+                st = _pinned_bf16((nf_pad, vocab))
+                st[:n_features].copy_(torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)))
+                return st.to(dev, non_blocking=True)
+
+            H = multihot_device(feats, nf_pad, torch.bfloat16)
+            W = upload(theta.weights)
+            Wr = None
+            if ref is not None:
+                torch.cuda.current_stream(dev).synchronize()  # the staging buffer is reused
+                Wr = upload(ref.weights)
+            if need_grad:  # value and gradient together: stored probabilities (token chunks if needed)
+                fwd, _, gw = icepop_fwd_bwd(H, W, batch, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
+                gw = gw[:n_features]
+            else:
+                fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr, store_probs=False)
+        grad_finite = torch.isfinite(gw).all() if gw is not None else None
+        host = torch.cat([fwd.lp_cur.to(torch.float64), fwd.entropy.to(torch.float64), fwd.surrogate,
+                          fwd.kept.to(torch.float64), fwd.stats]).cpu().numpy()
+    n = p.tokens.size
+    lp_cur, entropy, surrogate, kept = host[:n], host[n:2 * n], host[2 * n:3 * n], host[3 * n:4 * n] != 0
+    diag = Diagnostics.from_stats(host[4 * n:])
+    lp_list = lp_cur.tolist()
+    # the reference's per-rollout NumericErrors, in its order (policy.py:287-288, objective.py:
+    # 228-229, 241-242): the first rollout with non-finite logits, calibration or ratio raises,
+    # after writing back lp_cur for the rollouts before it (and for itself, unless its logits
+    # are what failed)
+    with np.errstate(over="ignore", invalid="ignore"):
+        bad_logits = ~(np.isfinite(lp_cur) & np.isfinite(entropy))
+        bad_calib = ~np.isfinite(calib)
+        bad_ratio = ~np.isfinite(np.exp(lp_cur - p.lp_old))
+    starts = p.cu[:-1]
+    per_roll = np.stack([np.logical_or.reduceat(b, starts) for b in (bad_logits, bad_calib, bad_ratio)])
+    failing = np.flatnonzero(per_roll.any(axis=0))
+    if failing.size:
+        r = int(failing[0])
+        kind = int(np.argmax(per_roll[:, r]))
+        _write_back(p.records, lp_list, int(p.cu[r + (0 if kind == 0 else 1)]))
+        raise NumericError(("non-finite logits (corrupted parameters)", "calibration ratio overflow",
+                            "importance ratio overflow")[kind])
+    _write_back(p.records, lp_list, n)
+    if p.error is not None:
+        raise p.error
+    if not math.isfinite(diag.objective_value) or not bool(grad_finite):
         raise NumericError("objective or gradient is not finite")
-    kept = fwd.kept.cpu().numpy().astype(bool)
+    with torch.cuda.device(dev):
+        g64 = gw.to(torch.float64)
+        if grad_out is not None:
+            _page_lock(grad_out)
+            torch.from_numpy(grad_out).copy_(g64)
+            grad = grad_out
+        else:
+            out = torch.empty(tuple(theta.weights.shape), dtype=torch.float64, pin_memory=True)
+            out.copy_(g64)
+            grad = out.numpy()
     return LossBreakdown(
         objective_value=diag.objective_value,
         per_token_mask_kept=kept,
@@ -306,9 +414,9 @@ def objective_and_grad(
         mean_logp=diag.mean_logp,
         entropy_all=diag.entropy_all,
         entropy_clipped=diag.entropy_clipped,
-        per_token_surrogate=fwd.surrogate.cpu().numpy(),
-        per_token_calibration=fwd.calib.cpu().numpy(),
-        per_token_entropy=fwd.entropy.to(torch.float64).cpu().numpy(),
+        per_token_surrogate=surrogate,
+        per_token_calibration=calib,
+        per_token_entropy=entropy,
     )
 
 
@@ -414,9 +522,10 @@ def delta_and_gap(params, probes, infer, temperature: float = 1.0, *, precision:
 
 
 def install(precision: str | None = None) -> None:
-    """Rebind mismatchlab's objective_and_grad and the update step that follows
-    it (sgd_update / momentum_update, scheduler.py:551-555) to this drop-in, in every module
-    that binds the names (objective.py, scheduler.py:29-40, __init__.py:32-34)."""
+    """Rebind mismatchlab's objective_and_grad, group_advantages, the update step
+    that follows it (sgd_update / momentum_update, scheduler.py:551-555) and the discrepancy
+    probe (delta_and_gap) to this drop-in, in every module that binds the names (objective.py,
+    scheduler.py:29-40, discrepancy.py, __init__.py:15-34)."""
     import mismatchlab  # type: ignore
     import mismatchlab.discrepancy  # type: ignore
     import mismatchlab.objective  # type: ignore
@@ -428,6 +537,7 @@ def install(precision: str | None = None) -> None:
         mod.objective_and_grad = objective_and_grad
         mod.sgd_update = sgd_update
         mod.momentum_update = momentum_update
+        mod.group_advantages = group_advantages  # K0 (objective.py:153-159, scheduler.py:353-354)
     # the discrepancy probe: measure() (discrepancy.py:144-161, called by train_loop) looks the
     # name up in its own module
     for mod in (mismatchlab, mismatchlab.discrepancy):

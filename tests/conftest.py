@@ -111,7 +111,7 @@ def cuda_device():
 
 
 REF_INSTALL = ROOT / "baseline" / "_ref"
-_BOUND = ("objective_and_grad", "sgd_update", "momentum_update", "delta_and_gap")
+_BOUND = ("objective_and_grad", "sgd_update", "momentum_update", "delta_and_gap", "group_advantages")
 
 
 @pytest.fixture

@@ -364,3 +364,61 @@ def test_group_advantages_on_device():
     for _ in range(5):
         perm = rng.permutation(len(rewards))
         assert np.array_equal(O.group_advantages([rewards[i] for i in perm]), base[perm])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "bf16"])
+def test_error_order_and_progressive_write_back(precision):
+    """The reference raises in loop order (objective.py:204-242): a NumericError in group 1
+    comes before a ValueError in group 2, and lp_cur has been written back for every rollout up
+    to the failing one (a calibration overflow fails after that rollout's write-back)."""
+    O = _obj()
+    from paper_2510_18855_b200.errors import NumericError
+
+    theta = rand_params(16, 8, 0.4, 5)
+    cfg, b = O.ObjectiveConfig(group_size=2), O.MaskingBounds()
+    g0 = manual_group(theta, [(1, 1.0, 1.0), (2, 1.0, 1.0)], [1.0, -1.0])
+    g1 = manual_group(theta, [(3, 1.0, 1.0), (4, 1.0, 1.0)], [1.0, -1.0])
+    g2 = manual_group(theta, [(5, 1.0, 1.0), (6, 1.0, 1.0)], [1.0, -1.0])
+    g1.rollouts[1].tokens[0].logp_infer_old = -800.0  # calibration overflow in group 1, rollout 1
+    g2.rollouts[1].tokens = []                         # and a ValueError later, in group 2
+    recs = [r.tokens[0] for g in (g0, g1, g2) for r in g.rollouts if r.tokens]
+    for r in recs:
+        r.logp_train_cur = 123.0
+    with pytest.raises(NumericError, match="calibration"):
+        O.objective_and_grad([g0, g1, g2], theta, theta, None, cfg, b, precision=precision)
+    # rollouts 0..3 (through the failing one) were written back, group 2's were not reached
+    assert all(r.logp_train_cur != 123.0 for r in recs[:4]) and recs[4].logp_train_cur == 123.0
+    g1.rollouts[1].tokens[0].logp_infer_old = g1.rollouts[1].tokens[0].logp_train_old
+    with pytest.raises(ValueError, match="empty rollout"):
+        O.objective_and_grad([g0, g1, g2], theta, theta, None, cfg, b, precision=precision)
+    assert recs[4].logp_train_cur != 123.0  # group 2's first rollout was computed before the error
+
+
+def test_grad_out_untouched_on_error_and_must_not_alias_parameters():
+    O = _obj()
+    from paper_2510_18855_b200.errors import NumericError
+
+    theta = rand_params(16, 8, 0.4, 6)
+    cfg, b = O.ObjectiveConfig(group_size=2), O.MaskingBounds()
+    g = manual_group(theta, [(1, 1.0, 1.0), (2, 1.0, 1.0)], [1.0, -1.0])
+    g.rollouts[0].tokens[0].logp_infer_old = -800.0
+    buf = np.full_like(theta.weights, 7.0)
+    with pytest.raises(NumericError):
+        O.objective_and_grad([g], theta, theta, None, cfg, b, grad_out=buf)
+    assert (buf == 7.0).all()
+    with pytest.raises(ValueError, match="share memory"):
+        O.objective_and_grad([g], theta, theta, None, cfg, b, grad_out=theta.weights)
+
+
+def test_mask_uses_numpys_calibration_bits():
+    """per_token_calibration is numpy's exp(lp_old - lp_inf) itself, and the mask follows it even
+    for a ratio sitting exactly on a bound (objective.py:227-232)."""
+    O = _obj()
+    theta = rand_params(16, 8, 0.4, 7)
+    g = manual_group(theta, [(1, 0.5, 1.0), (2, 5.0, 1.0), (3, 1.0, 1.0)], [1.0, -1.0, 0.5])
+    out = O.objective_and_grad([g], theta, theta, None, O.ObjectiveConfig(group_size=2), O.MaskingBounds())
+    lp_old = np.array([r.tokens[0].logp_train_old for r in g.rollouts])
+    lp_inf = np.array([r.tokens[0].logp_infer_old for r in g.rollouts])
+    c = np.exp(lp_old - lp_inf)
+    assert np.array_equal(out.per_token_calibration, c)
+    assert np.array_equal(out.per_token_mask_kept, (c >= 0.5) & (c <= 5.0))

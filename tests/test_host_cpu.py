@@ -100,3 +100,52 @@ def test_multihot_counts_duplicates():
 
     h = multihot(np.array([[1, 1, 3, 0], [2, 2, 2, 2]]), 4)
     assert h.tolist() == [[1, 2, 0, 1], [0, 0, 4, 0]]
+
+
+def _records(O, toks, version=0):
+    return [O.TokenRecord(int(t), -1.0, -1.1, -1.1, version) for t in toks]
+
+
+def test_pack_stops_at_the_first_invalid_rollout():
+    """The drop-in validates like objective.py:204-213, in the reference's loop order: the valid
+    prefix is packed and the first invalid group / rollout comes back as the error to raise after
+    the prefix has been computed (a NumericError in the prefix comes first)."""
+    from dataclasses import dataclass
+
+    from paper_2510_18855_b200 import objective as O
+
+    @dataclass
+    class Task:
+        prompt_id: int
+
+    @dataclass
+    class Rollout:
+        tokens: list
+
+    @dataclass
+    class Params:
+        weights: np.ndarray
+        version_id: int = 1
+
+        @property
+        def n_features(self):
+            return self.weights.shape[0]
+
+    theta = Params(np.zeros((16, 8)))
+    g1 = O.PromptGroup(Task(3), [Rollout(_records(O, [1, 2, 3])), Rollout(_records(O, [4]))], [1.0, 0.0], [1.0, -1.0])
+    g2 = O.PromptGroup(Task(4), [Rollout(_records(O, [5, 6])), Rollout([])], [1.0, 0.0], [1.0, -1.0])
+    p = O._pack([g1, g2], theta, theta)
+    assert isinstance(p.error, ValueError) and "empty rollout" in str(p.error)
+    assert p.tokens.tolist() == [1, 2, 3, 4, 5, 6] and p.cu.tolist() == [0, 3, 4, 6] and p.go.tolist() == [0, 2, 3]
+    assert len(p.records) == 6 and p.feats.shape == (6, 4)
+    g3 = O.PromptGroup(Task(5), [Rollout(_records(O, [7], version=2))], [1.0], [0.0])
+    p = O._pack([g1, g3], theta, theta)
+    assert "newer than theta_old" in str(p.error) and p.cu.tolist() == [0, 3, 4] and p.go.tolist() == [0, 2]
+    p = O._pack([O.PromptGroup(Task(6), [], [], []), g1], theta, theta)
+    assert "empty prompt group" in str(p.error) and not p.records
+    p = O._pack([g1], theta, theta)
+    assert p.error is None and p.lp_old.tolist() == [-1.1] * 4 and p.lp_inf.tolist() == [-1.0] * 4
+    with pytest.raises(ValueError, match="at least one prompt group"):
+        O._pack([], theta, theta)
+    with pytest.raises(ValueError, match="newer than theta"):
+        O._pack([g1], Params(theta.weights, 0), theta)
