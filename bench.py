@@ -446,14 +446,17 @@ def run_ours(args):
         # (its share of the step equals each backward GEMM's); per-kernel figures follow.
         dom = "K1_fwd_lse+K2"
         ach = kern[dom]["flop"] / (kern[dom]["ms"] / 1e3) / 1e12
-        traffic = None
+        # DRAM bytes per launch from the committed ncu capture of this kernel at this config (ncu
+        # cannot run inside the timed bench); `traffic_measured` says which capture
+        traffic = traffic_src = None
         tj = ROOT / "profiles" / "ncu_traffic.json"
         if tj.exists():
             t = json.loads(tj.read_text()).get(args.config, {}).get(dom)
             traffic = t["dram_bytes_per_launch"] if t else None
+            traffic_src = t.get("measured") if t else None
         line["roofline"] = {"bound": "tensor", "kernel": dom, "achieved": round(ach, 1), "peak": pk["tflops"],
                             "unit": "TFLOP/s", "frac": round(ach / pk["tflops"], 4), "traffic": traffic,
-                            "traffic_unit": "bytes/launch (ncu dram read+write)",
+                            "traffic_unit": "bytes/launch (ncu dram read+write)", "traffic_measured": traffic_src,
                             "flop_per_launch": kern[dom]["flop"], "peak_kind": "burst (%s)" % pk["source"],
                             "frac_of_sustained": round(ach / pk["tflops_sustained"], 4) if pk["tflops_sustained"]
                             else None}

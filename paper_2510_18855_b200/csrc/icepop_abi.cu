@@ -420,8 +420,11 @@ int run_umma(int epi, const void* A, int64_t lda, bool a_mn, const void* B, int6
   if (epi_dual(epi) && !B2) return fail(ICEPOP_EINVAL, "dual-accumulator GEMM needs a second B operand");
   CUtensorMap ta, tb, tb2;
   ICP_TRY(operand_map(&ta, A, M, K, lda, a_mn, BM));
-  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, bn / cg));
-  if (B2) ICP_TRY(operand_map(&tb2, B2, N, K, ldb, b_mn, bn / cg));
+  // B box rows: a CTA stages bn / cg rows of B; the dual-accumulator tiles stage bn rows of W
+  // and of W_ref (the leader / the peer, or one CTA both: umma_gemm.cuh GemmCfg)
+  const int b_box = epi_dual(epi) ? bn : bn / cg;
+  ICP_TRY(operand_map(&tb, B, N, K, ldb, b_mn, b_box));
+  if (B2) ICP_TRY(operand_map(&tb2, B2, N, K, ldb, b_mn, b_box));
   else tb2 = tb;
   // bf16 store map of the staging epilogues (32 rows x 64 cols boxes, SW128): EPI_DZ's dZ
   // [zero_rows_to, N] and EPI_LSE's stored probabilities [M, N]
@@ -1523,9 +1526,9 @@ static int delta_gap_impl(const icepop_shape* shape, double temperature, const v
                           double* max_gap, void* workspace, size_t workspace_bytes, void* stream) {
   ICP_TRY(check_shape(shape, !f64));
   if (!(temperature > 0.0)) return fail(ICEPOP_EINVAL, "temperature must be positive");
-  if (!hidden || !weight || !infer_logits) return fail(ICEPOP_EINVAL, "null argument");
   const int64_t N = shape->n_tokens, d = shape->hidden, V = shape->vocab;
   if (N == 0) return fail(ICEPOP_EINVAL, "probe set must be non-empty");  // discrepancy.py:136-137
+  if (!hidden || !weight || !infer_logits) return fail(ICEPOP_EINVAL, "null argument");
   size_t need = 0;
   ICP_TRY(icepop_delta_gap_workspace_bytes(shape, f64 ? 1 : 0, &need));
   if (!workspace || workspace_bytes < need) return fail(ICEPOP_EINVAL, "workspace too small: need %zu bytes", need);

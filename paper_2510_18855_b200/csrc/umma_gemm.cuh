@@ -165,12 +165,17 @@ struct EpiParams {
 // Epilogues that stage bf16 tiles in smem for TMA stores: K3's dZ and K1's stored probabilities.
 __host__ __device__ constexpr bool epi_staging(int epi) { return epi == EPI_DZ || epi == EPI_LSE || epi == EPI_LSE_REF; }
 
+// DUAL (the KL-to-ref variants): the vocabulary tile is BN = 128 wide and its B operand is the
+// concatenation [W rows n0..n0+127 ; W_ref rows n0..n0+127], so ONE N = 256 MMA per k16 step
+// writes z to accumulator columns [0, 128) and z_ref to [128, 256) -- the smem traffic per FLOP
+// of a plain 256-wide tile (two N = 128 MMAs would read the A tile twice). With CTA pairs the
+// leader stages the W half and the peer the W_ref half; a single CTA stages both.
 template <int BN, int CG, bool DUAL = false, bool EPI_STAGING = false>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / CG) * BK * 2;
-  static constexpr int B2_BYTES = DUAL ? B_BYTES : 0;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + B2_BYTES;
+  static constexpr int B_ROWS_CTA = DUAL ? (CG == 2 ? BN : 2 * BN) : BN / CG;  // B rows this CTA stages
+  static constexpr int B_BYTES = B_ROWS_CTA * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (220 * 1024 / STAGE_BYTES) < 6 ? (220 * 1024 / STAGE_BYTES) : 6;
   static constexpr int NACC = DUAL ? 2 : 1;              // accumulators per tile
   // double-buffered accumulators while they fit the 512 TMEM columns; 512-wide tiles (long-K
@@ -180,7 +185,7 @@ struct GemmCfg {
   // MMAs per k16 step: N <= 256 per tcgen05.mma, so a 512-wide tile issues two, the second
   // reading B at +B_SUB_BYTES (its rows in each CTA's slab) into TMEM columns [256, 512)
   static constexpr int NSUB = BN > 256 ? BN / 256 : 1;
-  static constexpr int N_MMA = BN / NSUB;
+  static constexpr int N_MMA = DUAL ? 2 * BN : BN / NSUB;
   static constexpr int B_SUB_BYTES = (N_MMA / CG) * 128;  // K-major: rows x 128 B; MN-major: boxes x 8 KB
   static constexpr int TILE_M = BM * CG;
   static constexpr int RING = 4;  // tile-index ring (dynamic scheduler -> all roles of the pair)
@@ -770,13 +775,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   resolve_extent(sh, Cfg::TILE_M, BN);
   resolve_sparsity(sh);
   constexpr int STAGES = Cfg::STAGES;
-  constexpr int B_ROWS = BN / CG;  // rows of B staged by this CTA
+  constexpr int B_ROWS = BN / CG;  // rows of B staged by this CTA (DUAL: BN rows of W or W_ref each)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint8_t* sB2 = sB + STAGES * Cfg::B_BYTES;  // DUAL only
   uint8_t* sEpi = smem + STAGES * Cfg::STAGE_BYTES;  // STAGING only (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + Cfg::EPI_STAGE_BYTES);
   // barrier block: full[S] empty[S] tfull[2] tempty[2] rfull[RING] | tmem_holder | ring[RING]
@@ -900,7 +904,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         run_coords(sh, tile, m_blk, n_first, n_count);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
         for (int tt = 0; tt < n_count; ++tt) {
-        const int n0 = (n_first + tt) * BN + (int)rank * B_ROWS;
+        const int n0 = (n_first + tt) * BN + (DUAL ? 0 : (int)rank * B_ROWS);
         for (int kb = 0; kb < sh.k_blocks; ++kb) {
           if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
           const int kc = (sh.kb_map ? __ldg(sh.kb_map + kb) : kb) * BK;  // k coordinate of this block
@@ -908,8 +912,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           const uint32_t fb_local = full0 + 8 * stage;
           const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
-          const uint32_t b2_dst = smem_u32(sB2 + stage * Cfg::B_BYTES);
-          (void)b2_dst;
           if (CG == 1) {
             mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
             if (!A_MN) {
@@ -918,14 +920,16 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #pragma unroll
               for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kc);
             }
+            // DUAL: the W_ref rows follow the W rows (K-major: BN rows x 128 B; MN-major: BN/64 boxes)
+            constexpr uint32_t b2_off = B_MN ? (BN / 64) * (BK * 128) : BN * 128;
             if (!B_MN) {
               tma_load_2d(b_dst, &tmB, fb_local, kc, n0);
-              if (DUAL) tma_load_2d(b2_dst, &tmB2, fb_local, kc, n0);
+              if (DUAL) tma_load_2d(b_dst + b2_off, &tmB2, fb_local, kc, n0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
+              for (int j2 = 0; j2 < (DUAL ? BN : B_ROWS) / 64; ++j2) {
                 tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kc);
-                if (DUAL) tma_load_2d(b2_dst + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kc);
+                if (DUAL) tma_load_2d(b_dst + b2_off + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kc);
               }
             }
           } else {
@@ -937,15 +941,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #pragma unroll
               for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kc);
             }
+            // DUAL: the leader stages the tile's W rows, the peer the same rows of W_ref
+            const CUtensorMap* tb = (DUAL && rank == 1) ? &tmB2 : &tmB;
             if (!B_MN) {
-              tma_load_2d_cg2(b_dst, &tmB, fb, kc, n0);
-              if (DUAL) tma_load_2d_cg2(b2_dst, &tmB2, fb, kc, n0);
+              tma_load_2d_cg2(b_dst, tb, fb, kc, n0);
             } else {
 #pragma unroll
-              for (int j2 = 0; j2 < B_ROWS / 64; ++j2) {
-                tma_load_2d_cg2(b_dst + j2 * (BK * 128), &tmB, fb, n0 + 64 * j2, kc);
-                if (DUAL) tma_load_2d_cg2(b2_dst + j2 * (BK * 128), &tmB2, fb, n0 + 64 * j2, kc);
-              }
+              for (int j2 = 0; j2 < Cfg::B_ROWS_CTA / 64; ++j2)
+                tma_load_2d_cg2(b_dst + j2 * (BK * 128), tb, fb, n0 + 64 * j2, kc);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -1003,8 +1006,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         auto issue = [&](int kb, int st, int h0, int h1) {
           const uint32_t a_base = smem_u32(sA + st * Cfg::A_BYTES);
           const uint32_t b_base = smem_u32(sB + st * Cfg::B_BYTES);
-          const uint32_t b2_base = smem_u32(sB2 + st * Cfg::B_BYTES);
-          (void)b2_base;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
@@ -1019,12 +1020,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
               const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
               if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
               else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
-            }
-            if (DUAL) {
-              const uint64_t bd2 = B_MN ? sdesc_sw128(b2_base + kk * 2048, BK * 128, 1024)
-                                        : sdesc_sw128(b2_base + kk * 32, 16, 1024);
-              if (CG == 2) umma_bf16_cg2(d_tmem + BN, ad, bd2, idesc, accum);
-              else umma_bf16(d_tmem + BN, ad, bd2, idesc, accum);
             }
           }
         };

@@ -852,11 +852,21 @@ class Diagnostics:
         )
 
 
-# --------------------------------------------------------------------------- custom op
+# --------------------------------------------------------------------------- custom ops
+# Two torch.library ops: the forward (pure) and the backward, which declares that it overwrites
+# the stored probabilities (its dZ is formed in place in them), so functionalization and
+# torch.compile see the mutation. The probabilities travel to the backward as a ctx attribute,
+# not a saved tensor: they are consumed (and freed) by the first backward; a second one
+# (retain_graph) recomputes the logits.
+def _cfg_of(alpha, beta, clip_eps, tis_cap, temperature, kl_coeff, algo) -> IcePopConfig:
+    return IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, kl_coeff, {v: k for k, v in ALGOS.items()}[algo])
+
+
 @torch.library.custom_op("icepop_b200::icepop_loss", mutates_args=())
 def _icepop_loss_op(
     hidden: torch.Tensor,
     weight: torch.Tensor,
+    weight_ref: torch.Tensor | None,
     tokens: torch.Tensor,
     lp_train_old: torch.Tensor,
     lp_infer_old: torch.Tensor,
@@ -868,77 +878,147 @@ def _icepop_loss_op(
     clip_eps: float,
     tis_cap: float,
     temperature: float,
+    kl_coeff: float,
     algo: int,
     layout: int,
     token_offset: int,
     store_probs: bool,
 ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor,
-           torch.Tensor, torch.Tensor]:
-    cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
+           torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    cfg = _cfg_of(alpha, beta, clip_eps, tis_cap, temperature, kl_coeff, algo)
     batch = PackedBatch(tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages,
                         token_offset=token_offset)
     sp = store_probs and hidden.dtype == torch.bfloat16
-    f = icepop_fwd(hidden, weight, batch, cfg, "dv" if layout == _lib.W_DV else "vd", store_probs=sp)
+    f = icepop_fwd(hidden, weight, batch, cfg, "dv" if layout == _lib.W_DV else "vd", weight_ref=weight_ref,
+                   store_probs=sp)
     loss = -f.stats[_lib.STAT_OBJECTIVE]
+    empty = lambda dt: hidden.new_empty((0,), dtype=dt)  # noqa: E731  outputs must be fresh tensors
     probs = f.extras.get("probs")
     tile_max = f.extras.get("tile_max")
-    if probs is None:  # outputs must be fresh tensors of the shapes the fake promises
-        probs = hidden.new_empty((0,), dtype=torch.bfloat16)
-        tile_max = hidden.new_empty((0,), dtype=torch.float32)
-    return loss, f.stats, f.lse, f.lp_cur, f.entropy, f.kept, f.coeff.to(torch.float64), probs, tile_max
+    if probs is None:
+        probs, tile_max = empty(torch.bfloat16), empty(torch.float32)
+    kl = f.kl if weight_ref is not None else empty(f.lse.dtype)
+    lse_ref = f.lse_ref if weight_ref is not None else empty(f.lse.dtype)
+    kl_w = f.extras.get("kl_w")
+    if kl_w is None:
+        kl_w = empty(torch.float32)
+    return (loss, f.stats, f.lse, f.lp_cur, f.entropy, f.kept, f.coeff.to(torch.float64), kl, lse_ref, kl_w, probs,
+            tile_max)
 
 
 @_icepop_loss_op.register_fake
-def _(hidden, weight, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages, alpha, beta,
-      clip_eps, tis_cap, temperature, algo, layout, token_offset, store_probs):
+def _(hidden, weight, weight_ref, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages, alpha,
+      beta, clip_eps, tis_cap, temperature, kl_coeff, algo, layout, token_offset, store_probs):
     n = hidden.shape[0]
-    f64 = dict(dtype=torch.float64, device=hidden.device)
-    # lse / entropy are f32 on the bf16 path and f64 on the validation path
-    f32 = dict(dtype=torch.float64 if hidden.dtype == torch.float64 else torch.float32, device=hidden.device)
+    dev = hidden.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    # lse / entropy / kl are f32 on the bf16 path and f64 on the validation path
+    fx = dict(dtype=torch.float64 if hidden.dtype == torch.float64 else torch.float32, device=dev)
     v = weight.shape[1] if layout == _lib.W_DV else weight.shape[0]
-    sp = store_probs and hidden.dtype == torch.bfloat16
-    probs_shape = (n, v) if sp else (0,)
-    tm_shape = (n, _lib.tile_max_ld(v)) if sp else (0,)
-    return (hidden.new_empty((), dtype=torch.float64), hidden.new_empty((_lib.NSTATS,), **{"dtype": torch.float64}),
-            torch.empty(n, **f32), torch.empty(n, **f64), torch.empty(n, **f32),
-            torch.empty(n, dtype=torch.uint8, device=hidden.device), torch.empty(n, **f64),
-            torch.empty(probs_shape, dtype=torch.bfloat16, device=hidden.device),
-            torch.empty(tm_shape, dtype=torch.float32, device=hidden.device))
+    sp = store_probs and hidden.dtype == torch.bfloat16 and not (weight_ref is not None and kl_coeff > 0)
+    ref = weight_ref is not None
+    kl_w_n = n if ref and hidden.dtype == torch.bfloat16 else 0
+    return (hidden.new_empty((), dtype=torch.float64), torch.empty(_lib.NSTATS, **f64), torch.empty(n, **fx),
+            torch.empty(n, **f64), torch.empty(n, **fx), torch.empty(n, dtype=torch.uint8, device=dev),
+            torch.empty(n, **f64), torch.empty(n if ref else 0, **fx), torch.empty(n if ref else 0, **fx),
+            torch.empty(kl_w_n, dtype=torch.float32, device=dev),
+            torch.empty((n, v) if sp else (0,), dtype=torch.bfloat16, device=dev),
+            torch.empty((n, _lib.tile_max_ld(v)) if sp else (0,), dtype=torch.float32, device=dev))
+
+
+@torch.library.custom_op("icepop_b200::icepop_loss_backward", mutates_args=("probs",))
+def _icepop_loss_backward_op(
+    grad_loss: torch.Tensor,
+    hidden: torch.Tensor,
+    weight: torch.Tensor,
+    weight_ref: torch.Tensor | None,
+    tokens: torch.Tensor,
+    lp_train_old: torch.Tensor,
+    lp_infer_old: torch.Tensor,
+    cu_seqlens: torch.Tensor,
+    group_offsets: torch.Tensor,
+    advantages: torch.Tensor,
+    lse: torch.Tensor,
+    lp_cur: torch.Tensor,
+    coeff: torch.Tensor,
+    kl: torch.Tensor,
+    lse_ref: torch.Tensor,
+    kl_w: torch.Tensor,
+    probs: torch.Tensor,
+    tile_max: torch.Tensor,
+    alpha: float,
+    beta: float,
+    clip_eps: float,
+    tis_cap: float,
+    temperature: float,
+    kl_coeff: float,
+    algo: int,
+    layout: int,
+    token_offset: int,
+    need_hidden: bool,
+    need_weight: bool,
+) -> tuple[torch.Tensor, torch.Tensor]:
+    """d(loss)/d(hidden), d(loss)/d(weight) for loss = -J (grad_loss scales them on the device,
+    no host sync). Overwrites `probs` (when non-empty) with dZ rows."""
+    cfg = _cfg_of(alpha, beta, clip_eps, tis_cap, temperature, kl_coeff, algo)
+    batch = PackedBatch(tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets, advantages,
+                        token_offset=token_offset)
+    scale = -grad_loss.to(torch.float64)
+    ref = weight_ref is not None
+    if hidden.dtype == torch.bfloat16:
+        fwd = IcePopForward(lse, lp_cur, None, None, None, None, (coeff * scale).to(torch.float32), None,
+                            kl=kl if ref else None, lse_ref=lse_ref if ref else None)
+        if ref:  # the KL gradient's coefficient carries the same scale
+            fwd.extras["kl_w"] = (kl_w.to(torch.float64) * scale).to(torch.float32)
+        if probs.numel():
+            fwd.extras["probs"], fwd.extras["tile_max"] = probs, tile_max
+    else:
+        fwd = IcePopForward(lse, torch.empty_like(lse, dtype=torch.float64), torch.empty_like(lse, dtype=torch.float64),
+                            None, None, None, coeff * scale, torch.zeros(_lib.NSTATS, dtype=torch.float64,
+                                                                         device=lse.device),
+                            kl=kl if ref else None, lse_ref=lse_ref if ref else None)
+    lay = "dv" if layout == _lib.W_DV else "vd"
+    # the fp64 path takes the KL gradient's scale through grad_scale (its kl_w is formed inside)
+    gscale = 1.0 if hidden.dtype == torch.bfloat16 or not ref or kl_coeff == 0.0 else None
+    if gscale is None:  # fp64 with the KL gradient: one host read of grad_loss (validation path)
+        gscale = float(-grad_loss.item())
+        fwd.coeff = coeff
+    gh, gw = icepop_bwd(hidden, weight, batch, fwd, cfg, lay, gscale, need_hidden, need_weight, weight_ref=weight_ref)
+    gh = gh.to(hidden.dtype) if gh is not None else hidden.new_empty((0,))
+    gw = gw.to(weight.dtype) if gw is not None else weight.new_empty((0,))
+    return gh, gw
+
+
+@_icepop_loss_backward_op.register_fake
+def _(grad_loss, hidden, weight, weight_ref, tokens, lp_train_old, lp_infer_old, cu_seqlens, group_offsets,
+      advantages, lse, lp_cur, coeff, kl, lse_ref, kl_w, probs, tile_max, alpha, beta, clip_eps, tis_cap,
+      temperature, kl_coeff, algo, layout, token_offset, need_hidden, need_weight):
+    return (torch.empty_like(hidden) if need_hidden else hidden.new_empty((0,)),
+            torch.empty_like(weight) if need_weight else weight.new_empty((0,)))
 
 
 def _setup_context(ctx, inputs, output):
-    (hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, alpha, beta, clip_eps, tis_cap, temperature, algo, layout,
-     token_offset, store_probs) = inputs
-    loss, stats, lse, lp_cur, entropy, kept, coeff, probs, tile_max = output
-    ctx.save_for_backward(hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, probs, tile_max)
-    ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset)
-    ctx.probs_live = probs.numel() > 0  # consumed by the first backward (rows may become dZ)
+    (hidden, weight, weight_ref, tokens, lp_old, lp_inf, cu, go, adv, alpha, beta, clip_eps, tis_cap, temperature,
+     kl_coeff, algo, layout, token_offset, store_probs) = inputs
+    loss, stats, lse, lp_cur, entropy, kept, coeff, kl, lse_ref, kl_w, probs, tile_max = output
+    ctx.save_for_backward(hidden, weight, weight_ref, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, kl,
+                          lse_ref, kl_w)
+    ctx.cfg = (alpha, beta, clip_eps, tis_cap, temperature, kl_coeff, algo, layout, token_offset)
+    # consumed by the first backward (its rows become dZ); not a saved tensor, so the declared
+    # in-place write does not trip autograd's version check, and the memory is released after
+    ctx.probs = (probs, tile_max) if probs.numel() else None
 
 
 def _backward(ctx, grad_loss, *unused):
-    hidden, weight, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, probs, tile_max = ctx.saved_tensors
-    alpha, beta, clip_eps, tis_cap, temperature, algo, layout, token_offset = ctx.cfg
-    cfg = IcePopConfig(alpha, beta, clip_eps, tis_cap, temperature, 0.0, {v: k for k, v in ALGOS.items()}[algo])
-    batch = PackedBatch(tokens, lp_old, lp_inf, cu, go, adv, token_offset=token_offset)
-    # loss = -J: scale the per-token coefficients on device (no host sync for grad_loss)
-    scale = -grad_loss.to(torch.float64)
-    if hidden.dtype == torch.bfloat16:
-        c = (coeff * scale).to(torch.float32)
-        fwd = IcePopForward(lse, lp_cur, None, None, None, None, c, None)
-        if ctx.probs_live:  # a second backward (retain_graph) falls back to the recompute
-            fwd.extras["probs"], fwd.extras["tile_max"] = probs, tile_max
-            ctx.probs_live = False
-    else:
-        fwd = IcePopForward(lse, torch.empty_like(lse, dtype=torch.float64),
-                            torch.empty_like(lse, dtype=torch.float64), None, None, None, coeff * scale,
-                            torch.zeros(_lib.NSTATS, dtype=torch.float64, device=lse.device))
-    lay = "dv" if layout == _lib.W_DV else "vd"
-    gh, gw = icepop_bwd(hidden, weight, batch, fwd, cfg, lay, 1.0, ctx.needs_input_grad[0], ctx.needs_input_grad[1])
-    if gw is not None:
-        gw = gw.to(weight.dtype)
-    if gh is not None:
-        gh = gh.to(hidden.dtype)
-    return (gh, gw) + (None,) * 15
+    hidden, weight, weight_ref, tokens, lp_old, lp_inf, cu, go, adv, lse, lp_cur, coeff, kl, lse_ref, kl_w = \
+        ctx.saved_tensors
+    probs, tile_max = ctx.probs if ctx.probs is not None else (hidden.new_empty((0,), dtype=torch.bfloat16),
+                                                                hidden.new_empty((0,), dtype=torch.float32))
+    ctx.probs = None  # a second backward (retain_graph) recomputes
+    gh, gw = _icepop_loss_backward_op(grad_loss, hidden, weight, weight_ref, tokens, lp_old, lp_inf, cu, go, adv, lse,
+                                      lp_cur, coeff, kl, lse_ref, kl_w, probs, tile_max, *ctx.cfg,
+                                      ctx.needs_input_grad[0], ctx.needs_input_grad[1])
+    return (gh if ctx.needs_input_grad[0] else None, gw if ctx.needs_input_grad[1] else None) + (None,) * 17
 
 
 _icepop_loss_op.register_autograd(_backward, setup_context=_setup_context)
@@ -951,28 +1031,34 @@ def icepop_loss(
     cfg: IcePopConfig = IcePopConfig(),
     layout: str = "vd",
     store_probs: bool | None = None,
+    weight_ref: torch.Tensor | None = None,
 ):
     """Differentiable IcePop loss (= -J on this rank's tokens) and per-token aux.
 
-    Returns ``(loss, aux)`` with aux = dict(stats, lse, lp_cur, entropy, kept, coeff).
-    ``batch.advantages`` must be given (compute them with K0 via
-    :func:`group_advantages` when starting from rewards). ``store_probs``: as in
-    :func:`icepop_fwd` (the probabilities live until the first backward consumes them).
+    Returns ``(loss, aux)`` with aux = dict(stats, lse, lp_cur, entropy, kept, coeff[, kl]).
+    ``batch.advantages`` must be given (compute them with K0 via :func:`group_advantages` when
+    starting from rewards). ``store_probs``: as in :func:`icepop_fwd` (the probabilities live
+    until the first backward consumes them). ``weight_ref`` with ``cfg.kl_coeff`` adds the
+    KL-to-ref term (objective.py:254-263; a frozen reference: it receives no gradient).
     """
     if batch.advantages is None:
         raise ValueError("icepop_loss needs batch.advantages (see group_advantages)")
-    if cfg.kl_coeff != 0.0:
-        raise ValueError("icepop_loss: kl_coeff must be 0 (KL-to-ref is the fp64 functional path)")
     if layout not in LAYOUTS:
         raise ValueError(f"weight layout must be 'dv' or 'vd', got {layout!r}")
     v = weight.shape[1] if layout == "dv" else weight.shape[0]
+    kl_grad = weight_ref is not None and cfg.kl_coeff > 0.0
     sp = hidden.is_cuda and hidden.dtype == torch.bfloat16 and _resolve_store_probs(
-        store_probs, hidden.shape[0], v, hidden.device, False)
-    loss, stats, lse, lp_cur, entropy, kept, coeff, _probs, _tile_max = _icepop_loss_op(
-        hidden, weight, batch.tokens, batch.lp_train_old, batch.lp_infer_old, batch.cu_seqlens,
+        store_probs, hidden.shape[0], v, hidden.device, kl_grad)
+    wr = weight_ref.detach() if weight_ref is not None else None
+    (loss, stats, lse, lp_cur, entropy, kept, coeff, kl, _lse_ref, _kl_w, _probs, _tile_max) = _icepop_loss_op(
+        hidden, weight, wr, batch.tokens, batch.lp_train_old, batch.lp_infer_old, batch.cu_seqlens,
         batch.group_offsets, batch.advantages, cfg.alpha, cfg.beta, cfg.clip_eps, cfg.tis_cap, cfg.temperature,
-        ALGOS[cfg.algo], LAYOUTS[layout], batch.token_offset, bool(sp))
-    return loss, dict(stats=stats, lse=lse, lp_cur=lp_cur, entropy=entropy, kept=kept, coeff=coeff)
+        cfg.kl_coeff if weight_ref is not None else 0.0, ALGOS[cfg.algo], LAYOUTS[layout], batch.token_offset,
+        bool(sp))
+    aux = dict(stats=stats, lse=lse, lp_cur=lp_cur, entropy=entropy, kept=kept, coeff=coeff)
+    if weight_ref is not None:
+        aux["kl"] = kl
+    return loss, aux
 
 
 @_on_device

@@ -554,3 +554,49 @@ def test_epilogue_rerun_equals_full_forward(cuda_device, with_ref):
             assert torch.equal(getattr(e, name), getattr(g, name)), name
         if with_ref:
             assert torch.equal(e.kl, g.kl)
+
+
+@pytest.mark.parametrize("kl_coeff", [0.0, 0.3])
+def test_custom_op_kl_to_ref_autograd(cuda_device, kl_coeff):
+    """icepop_loss with weight_ref: the KL diagnostic (gamma = 0) and its gradient (gamma > 0)
+    through the custom ops equal the functional path's -2 dJ (objective.py:254-263)."""
+    from paper_2510_18855_b200.loss import IcePopConfig, icepop_bwd, icepop_fwd, icepop_loss
+
+    c = _case(seed=35, V=1000)
+    rng = np.random.default_rng(9)
+    Wr = torch.from_numpy(c["W"].double().numpy() + rng.normal(0, 0.05, tuple(c["W"].shape))).to(torch.bfloat16)
+    Wr = Wr.to(cuda_device)
+    cfg = IcePopConfig(kl_coeff=kl_coeff)
+    H = c["H"].to(cuda_device).requires_grad_(True)
+    W = c["W"].to(cuda_device).requires_grad_(True)
+    b = _batch(c, cuda_device)
+    loss, aux = icepop_loss(H, W, b, cfg, weight_ref=Wr)
+    (2.0 * loss).backward()
+    f = icepop_fwd(H.detach(), W.detach(), b, cfg, weight_ref=Wr)
+    gh, gw = icepop_bwd(H.detach(), W.detach(), b, f, cfg, grad_scale=-2.0, weight_ref=Wr,
+                        grad_hidden_dtype=torch.float32)
+    assert loss.item() == pytest.approx(-f.stats[0].item(), rel=1e-12)
+    assert torch.equal(aux["kl"], f.kl)
+    assert _rel(H.grad.float().cpu().numpy(), gh.cpu().numpy()) < 1e-2
+    assert _rel(W.grad.float().cpu().numpy(), gw.cpu().numpy()) < 1e-2
+
+
+@pytest.mark.parametrize("store_probs", [True, False])
+def test_custom_ops_pass_opcheck(cuda_device, store_probs):
+    """torch.library.opcheck: the ops' schemas (the backward's declared write to the stored
+    probabilities), fake-tensor shapes and autograd registration are consistent."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import _icepop_loss_backward_op, _icepop_loss_op
+
+    c = _case(seed=36, V=512, d=128, n_seqs=3, lens=[100, 60, 90])
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    b = _batch(c, cuda_device)
+    args = (H, W, None, b.tokens, b.lp_train_old, b.lp_infer_old, b.cu_seqlens, b.group_offsets, b.advantages,
+            0.5, 5.0, 0.2, 2.0, 1.0, 0.0, 0, _lib.W_VD, 0, store_probs)
+    torch.library.opcheck(_icepop_loss_op, args, test_utils=("test_schema", "test_faketensor"))
+    out = _icepop_loss_op(*args)
+    (_, _, lse, lp_cur, _, _, coeff, kl, lse_ref, kl_w, probs, tile_max) = out
+    bargs = (torch.ones((), dtype=torch.float64, device=cuda_device), H, W, None, b.tokens, b.lp_train_old,
+             b.lp_infer_old, b.cu_seqlens, b.group_offsets, b.advantages, lse, lp_cur, coeff, kl, lse_ref, kl_w,
+             probs, tile_max, 0.5, 5.0, 0.2, 2.0, 1.0, 0.0, 0, _lib.W_VD, 0, True, True)
+    torch.library.opcheck(_icepop_loss_backward_op, bargs, test_utils=("test_schema", "test_faketensor"))
