@@ -489,8 +489,11 @@ def icepop_fwd_onpolicy(batch: PackedBatch, lse_old: torch.Tensor, entropy_old: 
                       torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev),
                       torch.empty(n, dtype=torch.float32, device=dev),
                       torch.empty(_lib.NSTATS, dtype=torch.float64, device=dev))
-    fb = _lib._sz()
-    _lib.check(lib.icepop_workspace_bytes(shape, 0, 0, fb, None))
+    fb = _lib._sz()  # (the workspace query wants the bf16 path's multiples of 8; the size only grows)
+    ws_shape = _lib.Shape(n_tokens=n, token_offset=batch.token_offset, hidden=-(-hidden_dim // 8) * 8,
+                          vocab=-(-vocab // 8) * 8, n_seqs=batch.n_seqs, n_groups=batch.n_groups,
+                          weight_layout=_lib.W_VD)
+    _lib.check(lib.icepop_workspace_bytes(ws_shape, 0, 0, fb, None))
     ws = torch.empty(max(fb.value, 1), dtype=torch.uint8, device=dev)
     out = _lib.FwdOut(lse=f.lse.data_ptr(), lp_cur=f.lp_cur.data_ptr(), entropy=f.entropy.data_ptr(),
                       kept=f.kept.data_ptr(), calib=f.calib.data_ptr(), surrogate=f.surrogate.data_ptr(),

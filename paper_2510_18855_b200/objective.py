@@ -21,6 +21,7 @@ scheduler.py:38 and __init__.py:33).
 from __future__ import annotations
 
 import enum
+import functools
 import math
 import operator
 from dataclasses import dataclass, field
@@ -123,6 +124,7 @@ except Exception:  # noqa: BLE001
 
 
 _DEFAULT_PRECISION = "fp64"
+_LAST_PATH = ""  # "full" or "onpolicy": the forward the last objective_and_grad call ran (tests)
 
 
 def set_default_precision(precision: str) -> None:
@@ -333,8 +335,28 @@ def objective_and_grad(
     feats = torch.from_numpy(np.ascontiguousarray(p.feats, dtype=np.int64)).to(dev)
     need_grad = p.error is None  # a validation error later in the batch: the forward decides what raises
     gw = None
+    # theta is theta_old with every lp_train_old recorded by record_train_logprobs under theta:
+    # the exact on-policy forward (no forward GEMM; r == 1 bit for bit, as in the reference's loop)
+    stash = _onpolicy_stash(p.records, theta, theta_old, temperature, precision) \
+        if need_grad and ref is None and precision == "bf16" else None
+    global _LAST_PATH
+    _LAST_PATH = "onpolicy" if stash is not None else "full"
     with torch.cuda.device(dev):
-        if precision == "fp64":
+        if stash is not None:
+            from .loss import icepop_bwd, icepop_fwd_onpolicy
+
+            if vocab % 8:
+                raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
+            nf = (n_features + 7) // 8 * 8
+            H = multihot_device(feats, nf, torch.bfloat16)
+            W = torch.zeros((nf, vocab), dtype=torch.bfloat16, device=dev)
+            W[:n_features] = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
+            st = torch.from_numpy(stash).to(dev)
+            fwd = icepop_fwd_onpolicy(batch, st[:, 0].to(torch.float32), st[:, 1].to(torch.float32), icfg,
+                                      hidden_dim=nf, vocab=vocab)
+            _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False)
+            gw = gw[:n_features]
+        elif precision == "fp64":
             H = multihot_device(feats, n_features, torch.float64)
             W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
             Wr = torch.from_numpy(np.ascontiguousarray(ref.weights, dtype=np.float64)).to(dev) if ref is not None \
@@ -469,6 +491,84 @@ def momentum_update(theta, grad, velocity, lr: float, beta: float = 0.9):
     return type(theta)(weights=weights, version_id=theta.version_id + 1), new_velocity
 
 
+def _record_key(params, temperature: float, precision: str) -> tuple:
+    return (id(params.weights), params.version_id, float(temperature), precision)
+
+
+def record_train_logprobs(groups, params, temperature: float = 1.0, *, precision: str | None = None) -> int:
+    """The training engine's old-logprob recording (scheduler.py:296-311) as ONE
+    batched device forward -- the lm_head GEMM with the online log-softmax, no objective -- over
+    every token generated by `params`' version (gen_version == params.version_id; tokens of
+    older versions keep the values recorded when they were generated, as in the reference's
+    partial rollouts). Writes TokenRecord.logp_train_old and logp_train_cur (the reference
+    initialises both to the same value) and keeps the row's lse and entropy with the record, so
+    objective_and_grad with theta is theta_old -- the reference loop's own call,
+    scheduler.py:540-541 -- runs the exact on-policy forward (lp_cur == lp_train_old bit for bit,
+    no forward GEMM: icepop_fwd_onpolicy). Returns the number of tokens recorded."""
+    import torch
+
+    from .features import multihot_device, rollout_feats
+    from .loss import IcePopConfig, PackedBatch, icepop_fwd
+
+    precision = precision or _DEFAULT_PRECISION
+    n_features, vocab = params.weights.shape
+    recs, feats = [], []
+    for group in groups:
+        for rollout in group.rollouts:
+            toks = rollout.tokens
+            if not toks:
+                continue
+            f = rollout_feats(group.task.prompt_id, [r.token for r in toks], n_features)
+            keep = [i for i, r in enumerate(toks) if r.gen_version == params.version_id]
+            recs += [toks[i] for i in keep]
+            feats.append(f[keep])
+    if not recs:
+        return 0
+    n = len(recs)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fd = torch.from_numpy(np.ascontiguousarray(np.concatenate(feats), dtype=np.int64)).to(dev)
+    zeros = torch.zeros(n, dtype=torch.float64, device=dev)
+    batch = PackedBatch(torch.tensor([r.token for r in recs], dtype=torch.int32, device=dev), zeros, zeros,
+                        torch.tensor([0, n], dtype=torch.int32, device=dev),
+                        torch.tensor([0, 1], dtype=torch.int32, device=dev),
+                        torch.zeros(1, dtype=torch.float64, device=dev))
+    cfg = IcePopConfig(temperature=float(temperature))
+    if precision == "fp64":
+        H = multihot_device(fd, n_features, torch.float64)
+        W = torch.from_numpy(np.ascontiguousarray(params.weights, dtype=np.float64)).to(dev)
+    elif precision == "bf16":
+        nf_pad = (n_features + 7) // 8 * 8
+        H = multihot_device(fd, nf_pad, torch.bfloat16)
+        W = torch.zeros((nf_pad, vocab), dtype=torch.bfloat16, device=dev)
+        W[:n_features] = torch.from_numpy(np.ascontiguousarray(params.weights, dtype=np.float64)).to(dev)
+    else:
+        raise ValueError("precision must be 'fp64' or 'bf16'")
+    f = icepop_fwd(H, W, batch, cfg, layout="dv", store_probs=False)
+    lp = f.lp_cur.cpu().tolist()
+    lse = f.lse.to(torch.float64).cpu().tolist()
+    ent = f.entropy.to(torch.float64).cpu().tolist()
+    key = _record_key(params, temperature, precision)
+    for rec, a, b, c in zip(recs, lp, lse, ent):
+        rec.logp_train_old = rec.logp_train_cur = a
+        rec._icepop_record = (key, a, b, c)
+    return n
+
+
+def _onpolicy_stash(records, theta, theta_old, temperature: float, precision: str):
+    """(lse, entropy) per record when every record was recorded by record_train_logprobs under
+    theta (== theta_old) and still holds that logp_train_old; else None."""
+    if theta is not theta_old and (theta.weights is not theta_old.weights or theta.version_id != theta_old.version_id):
+        return None
+    key = _record_key(theta, temperature, precision)
+    out = []
+    for rec in records:
+        st = getattr(rec, "_icepop_record", None)
+        if st is None or st[0] != key or st[1] != rec.logp_train_old:
+            return None
+        out.append((st[2], st[3]))
+    return np.asarray(out, dtype=np.float64)
+
+
 def delta_and_gap(params, probes, infer, temperature: float = 1.0, *, precision: str | None = None):
     """discrepancy.py:132-141 on the device: (mean over the probes of KL(p_infer || p_train),
     max |p_infer - p_train|).
@@ -521,11 +621,32 @@ def delta_and_gap(params, probes, infer, temperature: float = 1.0, *, precision:
     return float(out[0]), float(out[1])
 
 
-def install(precision: str | None = None) -> None:
+def _recording(step):
+    """Wrap a scheduler iteration (run_iteration / run_iteration_baseline): after the reference
+    generates and completes its groups, re-record the fresh tokens' logp_train_old in one batched
+    device forward (record_train_logprobs), so the loop's objective_and_grad(groups, params,
+    params, ...) takes the exact on-policy path."""
+
+    @functools.wraps(step)
+    def wrapper(state, params, cfg, group_cfg, *args, **kwargs):
+        report, groups = step(state, params, cfg, group_cfg, *args, **kwargs)
+        if groups:
+            record_train_logprobs(groups, params, state.temperature)
+        return report, groups
+
+    wrapper.__wrapped_step__ = step
+    return wrapper
+
+
+def install(precision: str | None = None, *, record: bool = False) -> None:
     """Rebind mismatchlab's objective_and_grad, group_advantages, the update step
     that follows it (sgd_update / momentum_update, scheduler.py:551-555) and the discrepancy
     probe (delta_and_gap) to this drop-in, in every module that binds the names (objective.py,
-    scheduler.py:29-40, discrepancy.py, __init__.py:15-34)."""
+    scheduler.py:29-40, discrepancy.py, __init__.py:15-34). ``record=True`` also re-records the
+    fresh tokens' logp_train_old of every train_loop iteration on the device; a
+    later objective_and_grad(groups, params, params, None, ...) on those groups runs the exact
+    on-policy forward (bf16 precision; train_loop itself always passes a reference policy for
+    the KL diagnostic, which needs the forward GEMM)."""
     import mismatchlab  # type: ignore
     import mismatchlab.discrepancy  # type: ignore
     import mismatchlab.objective  # type: ignore
@@ -542,10 +663,15 @@ def install(precision: str | None = None) -> None:
     # name up in its own module
     for mod in (mismatchlab, mismatchlab.discrepancy):
         mod.delta_and_gap = delta_and_gap
+    if record:  # the old-logprob recording of train_loop's iterations on the device (8f-1)
+        for name in ("run_iteration", "run_iteration_baseline"):
+            step = getattr(mismatchlab.scheduler, name)
+            if not hasattr(step, "__wrapped_step__"):
+                setattr(mismatchlab.scheduler, name, _recording(step))
 
 
 __all__ = [
     "Algo", "LossBreakdown", "MaskingBounds", "ObjectiveConfig", "PromptGroup", "TokenRecord", "empty_breakdown",
     "delta_and_gap", "group_advantages", "install", "mask", "momentum_update", "objective_and_grad",
-    "set_default_precision", "sgd_update",
+    "record_train_logprobs", "set_default_precision", "sgd_update",
 ]

@@ -128,7 +128,8 @@ def mismatchlab_ref():
     import mismatchlab.scheduler
 
     mods = (mismatchlab, mismatchlab.objective, mismatchlab.scheduler, mismatchlab.discrepancy)
-    saved = {(m, n): getattr(m, n) for m in mods for n in _BOUND if hasattr(m, n)}
+    saved = {(m, n): getattr(m, n) for m in mods for n in _BOUND + ("run_iteration", "run_iteration_baseline")
+             if hasattr(m, n)}
     try:
         yield mismatchlab
     finally:
