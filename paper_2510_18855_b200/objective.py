@@ -320,9 +320,9 @@ def objective_and_grad(
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     icfg = IcePopConfig(alpha=bounds.alpha, beta=bounds.beta, clip_eps=cfg.clip_eps, tis_cap=cfg.tis_cap,
                         temperature=float(temperature), kl_coeff=cfg.kl_coeff, algo=_algo_name(cfg.algo))
-    calib = np.exp(p.lp_old - p.lp_inf)  # objective.py:227, numpy's bits
-    with np.errstate(over="ignore", invalid="ignore"):
-        calib_c = np.where(np.isfinite(calib), calib, 0.0)  # non-finite: raised below, in the reference's order
+    with np.errstate(over="ignore", invalid="ignore"):  # a non-finite ratio raises below, in the reference's order
+        calib = np.exp(p.lp_old - p.lp_inf)  # objective.py:227, numpy's bits
+        calib_c = np.where(np.isfinite(calib), calib, 0.0)
     batch = PackedBatch(
         tokens=torch.from_numpy(p.tokens).to(dev),
         lp_train_old=torch.from_numpy(p.lp_old).to(dev),
