@@ -904,56 +904,56 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         run_coords(sh, tile, m_blk, n_first, n_count);
         const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
         for (int tt = 0; tt < n_count; ++tt) {
-        const int n0 = (n_first + tt) * BN + (DUAL ? 0 : (int)rank * B_ROWS);
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
-          if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
-          const int kc = (sh.kb_map ? __ldg(sh.kb_map + kb) : kb) * BK;  // k coordinate of this block
-          mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          const uint32_t fb_local = full0 + 8 * stage;
-          const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
-          if (CG == 1) {
-            mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
-            if (!A_MN) {
-              tma_load_2d(a_dst, &tmA, fb_local, kc, m0);
-            } else {
+          const int n0 = (n_first + tt) * BN + (DUAL ? 0 : (int)rank * B_ROWS);
+          for (int kb = 0; kb < sh.k_blocks; ++kb) {
+            if (waves && rank == 0 && kb % skb == 0) chunk_wait(j * spt + kb / skb);
+            const int kc = (sh.kb_map ? __ldg(sh.kb_map + kb) : kb) * BK;  // k coordinate of this block
+            mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            const uint32_t fb_local = full0 + 8 * stage;
+            const uint32_t a_dst = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b_dst = smem_u32(sB + stage * Cfg::B_BYTES);
+            if (CG == 1) {
+              mbar_arrive_expect_tx(fb_local, Cfg::STAGE_BYTES);
+              if (!A_MN) {
+                tma_load_2d(a_dst, &tmA, fb_local, kc, m0);
+              } else {
 #pragma unroll
-              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kc);
-            }
-            // DUAL: the W_ref rows follow the W rows (K-major: BN rows x 128 B; MN-major: BN/64 boxes)
-            constexpr uint32_t b2_off = B_MN ? (BN / 64) * (BK * 128) : BN * 128;
-            if (!B_MN) {
-              tma_load_2d(b_dst, &tmB, fb_local, kc, n0);
-              if (DUAL) tma_load_2d(b_dst + b2_off, &tmB2, fb_local, kc, n0);
-            } else {
+                for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d(a_dst + j2 * (BK * 128), &tmA, fb_local, m0 + 64 * j2, kc);
+              }
+              // DUAL: the W_ref rows follow the W rows (K-major: BN rows x 128 B; MN-major: BN/64 boxes)
+              constexpr uint32_t b2_off = B_MN ? (BN / 64) * (BK * 128) : BN * 128;
+              if (!B_MN) {
+                tma_load_2d(b_dst, &tmB, fb_local, kc, n0);
+                if (DUAL) tma_load_2d(b_dst + b2_off, &tmB2, fb_local, kc, n0);
+              } else {
 #pragma unroll
-              for (int j2 = 0; j2 < (DUAL ? BN : B_ROWS) / 64; ++j2) {
-                tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kc);
-                if (DUAL) tma_load_2d(b_dst + b2_off + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kc);
+                for (int j2 = 0; j2 < (DUAL ? BN : B_ROWS) / 64; ++j2) {
+                  tma_load_2d(b_dst + j2 * (BK * 128), &tmB, fb_local, n0 + 64 * j2, kc);
+                  if (DUAL) tma_load_2d(b_dst + b2_off + j2 * (BK * 128), &tmB2, fb_local, n0 + 64 * j2, kc);
+                }
+              }
+            } else {
+              const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
+              if (rank == 0) mbar_arrive_expect_tx(fb_local, CG * Cfg::STAGE_BYTES);
+              if (!A_MN) {
+                tma_load_2d_cg2(a_dst, &tmA, fb, kc, m0);
+              } else {
+#pragma unroll
+                for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kc);
+              }
+              // DUAL: the leader stages the tile's W rows, the peer the same rows of W_ref
+              const CUtensorMap* tb = (DUAL && rank == 1) ? &tmB2 : &tmB;
+              if (!B_MN) {
+                tma_load_2d_cg2(b_dst, tb, fb, kc, n0);
+              } else {
+#pragma unroll
+                for (int j2 = 0; j2 < Cfg::B_ROWS_CTA / 64; ++j2)
+                  tma_load_2d_cg2(b_dst + j2 * (BK * 128), tb, fb, n0 + 64 * j2, kc);
               }
             }
-          } else {
-            const uint32_t fb = mapa_shared(fb_local, 0);  // the leader's barrier counts both halves
-            if (rank == 0) mbar_arrive_expect_tx(fb_local, CG * Cfg::STAGE_BYTES);
-            if (!A_MN) {
-              tma_load_2d_cg2(a_dst, &tmA, fb, kc, m0);
-            } else {
-#pragma unroll
-              for (int j2 = 0; j2 < BM / 64; ++j2) tma_load_2d_cg2(a_dst + j2 * (BK * 128), &tmA, fb, m0 + 64 * j2, kc);
-            }
-            // DUAL: the leader stages the tile's W rows, the peer the same rows of W_ref
-            const CUtensorMap* tb = (DUAL && rank == 1) ? &tmB2 : &tmB;
-            if (!B_MN) {
-              tma_load_2d_cg2(b_dst, tb, fb, kc, n0);
-            } else {
-#pragma unroll
-              for (int j2 = 0; j2 < Cfg::B_ROWS_CTA / 64; ++j2)
-                tma_load_2d_cg2(b_dst + j2 * (BK * 128), tb, fb, n0 + 64 * j2, kc);
-            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            if (waves && rank == 0 && (kb % skb == skb - 1 || kb == sh.k_blocks - 1)) atomicAdd(sh.wave_counter, 1);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (waves && rank == 0 && (kb % skb == skb - 1 || kb == sh.k_blocks - 1)) atomicAdd(sh.wave_counter, 1);
-        }
         }
       }
     }
@@ -991,67 +991,67 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         (void)n_first_r;
         int nxt2 = -1;
         for (int tt = 0; tt < n_count; ++tt) {
-        // SPLIT: wait only for the epilogue to have read TMEM columns [0, BN/2) (thalf)
-        mbar_wait(SPLIT ? thalf0 : tempty0 + 8 * acc, acc_phase ^ 1);
-        tc_fence_after();
-        if (dynamic && tt == 0) {
-          // the epilogue is done with the tile two accumulators back (run j-1 or earlier), so
-          // every role has read run j-2's ring slot -> slot (j+2) % RING is free
-          nxt2 = (nxt1 >= 0 && claimed < sh.num_tiles) ? claimed : -1;
-          publish(j + 2, nxt2);
-          claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
-        }
-        const uint32_t d_tmem = tmem_base + acc * BN * Cfg::NACC;
-        // MMAs of k-block kb on smem stage st for sub-tiles [h0, h1)
-        auto issue = [&](int kb, int st, int h0, int h1) {
-          const uint32_t a_base = smem_u32(sA + st * Cfg::A_BYTES);
-          const uint32_t b_base = smem_u32(sB + st * Cfg::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
-                                     : sdesc_sw128(a_base + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
-                                     : sdesc_sw128(b_base + kk * 32, 16, 1024);
-            const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-#pragma unroll
-            for (int h = 0; h < Cfg::NSUB; ++h) {
-              if (h < h0 || h >= h1) continue;
-              // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
-              const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
-              if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
-              else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
-            }
-          }
-        };
-        // SPLIT: the first-half MMAs of the first `pre` k-blocks run while the epilogue still
-        // reads the previous tile's second half; their stages stay full until the second-half
-        // MMAs (issued once the whole accumulator is free) have read them too.
-        const int pre = SPLIT ? min(STAGES, sh.k_blocks) : 0;
-        if (SPLIT) {
-          int st2 = stage;
-          uint32_t ph2 = phase;
-          for (int kb = 0; kb < pre; ++kb) {
-            mbar_wait(full0 + 8 * st2, ph2);
-            tc_fence_after();
-            issue(kb, st2, 0, 1);
-            if (++st2 == STAGES) { st2 = 0; ph2 ^= 1; }
-          }
-          mbar_wait(tempty0, acc_phase ^ 1);
+          // SPLIT: wait only for the epilogue to have read TMEM columns [0, BN/2) (thalf)
+          mbar_wait(SPLIT ? thalf0 : tempty0 + 8 * acc, acc_phase ^ 1);
           tc_fence_after();
-        }
-        for (int kb = 0; kb < sh.k_blocks; ++kb) {
-          if (kb >= pre) {
-            mbar_wait(full0 + 8 * stage, phase);
+          if (dynamic && tt == 0) {
+            // the epilogue is done with the tile two accumulators back (run j-1 or earlier), so
+            // every role has read run j-2's ring slot -> slot (j+2) % RING is free
+            nxt2 = (nxt1 >= 0 && claimed < sh.num_tiles) ? claimed : -1;
+            publish(j + 2, nxt2);
+            claimed = nxt2 >= 0 ? claim() : sh.num_tiles;
+          }
+          const uint32_t d_tmem = tmem_base + acc * BN * Cfg::NACC;
+          // MMAs of k-block kb on smem stage st for sub-tiles [h0, h1)
+          auto issue = [&](int kb, int st, int h0, int h1) {
+            const uint32_t a_base = smem_u32(sA + st * Cfg::A_BYTES);
+            const uint32_t b_base = smem_u32(sB + st * Cfg::B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = A_MN ? sdesc_sw128(a_base + kk * 2048, BK * 128, 1024)
+                                       : sdesc_sw128(a_base + kk * 32, 16, 1024);
+              const uint64_t bd = B_MN ? sdesc_sw128(b_base + kk * 2048, BK * 128, 1024)
+                                       : sdesc_sw128(b_base + kk * 32, 16, 1024);
+              const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+#pragma unroll
+              for (int h = 0; h < Cfg::NSUB; ++h) {
+                if (h < h0 || h >= h1) continue;
+                // +h * B_SUB_BYTES in the start-address field (>> 4) of the descriptor
+                const uint64_t bdh = bd + (uint64_t)((h * Cfg::B_SUB_BYTES) >> 4);
+                if (CG == 2) umma_bf16_cg2(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
+                else umma_bf16(d_tmem + h * Cfg::N_MMA, ad, bdh, idesc, accum);
+              }
+            }
+          };
+          // SPLIT: the first-half MMAs of the first `pre` k-blocks run while the epilogue still
+          // reads the previous tile's second half; their stages stay full until the second-half
+          // MMAs (issued once the whole accumulator is free) have read them too.
+          const int pre = SPLIT ? min(STAGES, sh.k_blocks) : 0;
+          if (SPLIT) {
+            int st2 = stage;
+            uint32_t ph2 = phase;
+            for (int kb = 0; kb < pre; ++kb) {
+              mbar_wait(full0 + 8 * st2, ph2);
+              tc_fence_after();
+              issue(kb, st2, 0, 1);
+              if (++st2 == STAGES) { st2 = 0; ph2 ^= 1; }
+            }
+            mbar_wait(tempty0, acc_phase ^ 1);
             tc_fence_after();
           }
-          issue(kb, stage, kb < pre ? 1 : 0, Cfg::NSUB);
-          // frees the smem slot (in both CTAs) when these MMAs finish
-          if (CG == 2) umma_commit_cg2(empty0 + 8 * stage, 0x3); else umma_commit(empty0 + 8 * stage);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        // accumulator ready for the epilogue warps (of both CTAs)
-        if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
-        if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+          for (int kb = 0; kb < sh.k_blocks; ++kb) {
+            if (kb >= pre) {
+              mbar_wait(full0 + 8 * stage, phase);
+              tc_fence_after();
+            }
+            issue(kb, stage, kb < pre ? 1 : 0, Cfg::NSUB);
+            // frees the smem slot (in both CTAs) when these MMAs finish
+            if (CG == 2) umma_commit_cg2(empty0 + 8 * stage, 0x3); else umma_commit(empty0 + 8 * stage);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          // accumulator ready for the epilogue warps (of both CTAs)
+          if (CG == 2) umma_commit_cg2(tfull0 + 8 * acc, 0x3); else umma_commit(tfull0 + 8 * acc);
+          if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
         }
         if (dynamic) {
           cur = nxt1;
@@ -1081,32 +1081,32 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       float run_m = -1e30f, run_s = 0.f, run_q = 0.f;  // EPI_LSE: this warp's triple over the run
       (void)run_m; (void)run_s; (void)run_q;
       for (int tt = 0; tt < n_count; ++tt) {
-      const int n_blk = n_first + tt;
-      mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
-      if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
-      if constexpr (EPI == EPI_LSE)
-        epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN,
-                        n_first / sh.run_len, tt == n_count - 1, ehalf, row, lane, quarter, taddr,
-                        SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q, xch);
-      if constexpr (EPI == EPI_DZ) {
-        if (sh.dz_tma_store)
-          epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
-                         quarter, taddr);
-        else
-          epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
-      }
-      if constexpr (EPI == EPI_LSE_REF)
-        epi_lse_ref<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
-                        quarter, taddr);
-      if constexpr (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_tmem_free(CG == 2 ? mapa_shared(tempty0 + 8 * acc, 0) : tempty0 + 8 * acc);
-      }
-      if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+        const int n_blk = n_first + tt;
+        mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN * Cfg::NACC;
+        if constexpr (EPI == EPI_STORE) epi_store<BN, CG>(sh, ep, m0, n_blk * BN, row, taddr);
+        if constexpr (EPI == EPI_LSE)
+          epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN,
+                          n_first / sh.run_len, tt == n_count - 1, ehalf, row, lane, quarter, taddr,
+                          SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q, xch);
+        if constexpr (EPI == EPI_DZ) {
+          if (sh.dz_tma_store)
+            epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
+                           quarter, taddr);
+          else
+            epi_dz<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+        }
+        if constexpr (EPI == EPI_LSE_REF)
+          epi_lse_ref<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, n_blk, row, lane,
+                          quarter, taddr);
+        if constexpr (EPI == EPI_DZ_REF) epi_dz_ref<BN>(sh, ep, m0, n_blk * BN, row, taddr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_tmem_free(CG == 2 ? mapa_shared(tempty0 + 8 * acc, 0) : tempty0 + 8 * acc);
+        }
+        if (++acc == Cfg::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
       }
     }
     if (EPI == EPI_STORE && ep.rs_world > 0) __threadfence_system();  // peer stores visible system-wide
