@@ -206,9 +206,11 @@ def test_abi_rejects_invalid_probs_arguments(cuda_device):
     assert rc == _lib.EINVAL
 
 
-def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group):
+@pytest.mark.parametrize("with_ref", [False, True], ids=["K1", "K1-dual"])
+def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group, with_ref):
     """The TMA stores of q are clipped to [N, V]: guard bands around the buffer stay intact
-    (N = 1,111 rows is not a multiple of 32 or 128; V = 1,000 ends mid 64-column slab)."""
+    (N = 1,111 rows is not a multiple of 32 or 128; V = 1,000 ends mid 64-column slab), for K1
+    and for the dual-accumulator forward (weight_ref with gamma = 0) that also stores them."""
     from paper_2510_18855_b200 import _lib
 
     c = _case(seed=58, V=1000, lens=[500, 411, 200], n_seqs=3)
@@ -219,7 +221,7 @@ def test_clipped_probability_stores_stay_in_bounds(cuda_device, cta_group):
     L = _lib.tile_max_ld(V)
     tm_buf = torch.full((N * L + 2 * 64,), 777.0, dtype=torch.float32, device=cuda_device)
     tm = tm_buf[64:64 + N * L].view(N, L)
-    rc, *_ = _c_fwd(c, cuda_device, probs, tm)
+    rc, *_ = _c_fwd(c, cuda_device, probs, tm, weight_ref=c["W"].to(cuda_device) if with_ref else None)
     assert rc == _lib.OK
     torch.cuda.synchronize()
     assert torch.all(buf[:G] == 12345.0) and torch.all(buf[G + N * V:] == 12345.0)
