@@ -265,6 +265,43 @@ def _write_back(records, lp_cur: list, n: int) -> None:
         rec.logp_train_cur = value
 
 
+# Vocabulary padding of the bf16 path: its TMA tensors need rows of a multiple of 16 bytes, so a
+# vocabulary that is not a multiple of 8 is padded with columns whose logits are -1e4 (one extra
+# always-on feature row carries that value into the padded columns only): they get probability
+# exactly 0 in fp32, so no statistic, mask or gradient of a real column changes, and the padded
+# rows / columns of the gradient are dropped.
+_PAD_LOGIT = -1.0e4
+
+
+def _bf16_shapes(n_features: int, vocab: int) -> tuple[int, int, bool]:
+    """(feature rows, vocabulary columns, padded) of the bf16 operands."""
+    pad = vocab % 8 != 0
+    return (n_features + (1 if pad else 0) + 7) // 8 * 8, (vocab + 7) // 8 * 8, pad
+
+
+def _bf16_hidden(feats, n_features: int, vocab: int):
+    """Multi-hot H of the bf16 path (features.multihot_device), plus the padding feature."""
+    import torch
+
+    from .features import multihot_device
+
+    nf_pad, _, pad = _bf16_shapes(n_features, vocab)
+    H = multihot_device(feats, nf_pad, torch.bfloat16)
+    if pad:
+        H[:, n_features] = 1.0
+    return H
+
+
+def _bf16_weight_into(dst, w: np.ndarray, n_features: int, vocab: int):
+    """Write weights [n_features, vocab] (fp64, host) into a zeroed bf16 buffer [nf_pad, v_pad]."""
+    import torch
+
+    dst[:n_features, :vocab].copy_(torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)))
+    if vocab % 8:
+        dst[n_features, vocab:] = _PAD_LOGIT
+    return dst
+
+
 def objective_and_grad(
     groups,
     theta,
@@ -345,17 +382,15 @@ def objective_and_grad(
         if stash is not None:
             from .loss import icepop_bwd, icepop_fwd_onpolicy
 
-            if vocab % 8:
-                raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
-            nf = (n_features + 7) // 8 * 8
-            H = multihot_device(feats, nf, torch.bfloat16)
-            W = torch.zeros((nf, vocab), dtype=torch.bfloat16, device=dev)
-            W[:n_features] = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
+            nf, vp, _ = _bf16_shapes(n_features, vocab)
+            H = _bf16_hidden(feats, n_features, vocab)
+            W = _bf16_weight_into(torch.zeros((nf, vp), dtype=torch.bfloat16, device=dev), theta.weights,
+                                  n_features, vocab)
             st = torch.from_numpy(stash).to(dev)
             fwd = icepop_fwd_onpolicy(batch, st[:, 0].to(torch.float32), st[:, 1].to(torch.float32), icfg,
-                                      hidden_dim=nf, vocab=vocab)
+                                      hidden_dim=nf, vocab=vp)
             _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False)
-            gw = gw[:n_features]
+            gw = gw[:n_features, :vocab]
         elif precision == "fp64":
             H = multihot_device(feats, n_features, torch.float64)
             W = torch.from_numpy(np.ascontiguousarray(theta.weights, dtype=np.float64)).to(dev)
@@ -367,16 +402,13 @@ def objective_and_grad(
 
                 _, gw = icepop_bwd(H, W, batch, fwd, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
         else:
-            if vocab % 8:
-                raise ValueError("the bf16 path needs a vocabulary size that is a multiple of 8")
-            nf_pad = (n_features + 7) // 8 * 8  # zero feature rows are inert
+            nf_pad, v_pad, _ = _bf16_shapes(n_features, vocab)  # zero feature rows are inert
 
             def upload(w):
-                st = _pinned_bf16((nf_pad, vocab))
-                st[:n_features].copy_(torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)))
-                return st.to(dev, non_blocking=True)
+                return _bf16_weight_into(_pinned_bf16((nf_pad, v_pad)), w, n_features, vocab).to(dev,
+                                                                                                 non_blocking=True)
 
-            H = multihot_device(feats, nf_pad, torch.bfloat16)
+            H = _bf16_hidden(feats, n_features, vocab)
             W = upload(theta.weights)
             Wr = None
             if ref is not None:
@@ -384,7 +416,7 @@ def objective_and_grad(
                 Wr = upload(ref.weights)
             if need_grad:  # value and gradient together: stored probabilities (token chunks if needed)
                 fwd, _, gw = icepop_fwd_bwd(H, W, batch, icfg, layout="dv", need_hidden=False, weight_ref=Wr)
-                gw = gw[:n_features]
+                gw = gw[:n_features, :vocab]
             else:
                 fwd = icepop_fwd(H, W, batch, icfg, layout="dv", weight_ref=Wr, store_probs=False)
         grad_finite = torch.isfinite(gw).all() if gw is not None else None
@@ -537,10 +569,10 @@ def record_train_logprobs(groups, params, temperature: float = 1.0, *, precision
         H = multihot_device(fd, n_features, torch.float64)
         W = torch.from_numpy(np.ascontiguousarray(params.weights, dtype=np.float64)).to(dev)
     elif precision == "bf16":
-        nf_pad = (n_features + 7) // 8 * 8
-        H = multihot_device(fd, nf_pad, torch.bfloat16)
-        W = torch.zeros((nf_pad, vocab), dtype=torch.bfloat16, device=dev)
-        W[:n_features] = torch.from_numpy(np.ascontiguousarray(params.weights, dtype=np.float64)).to(dev)
+        nf_pad, v_pad, _ = _bf16_shapes(n_features, vocab)
+        H = _bf16_hidden(fd, n_features, vocab)
+        W = _bf16_weight_into(torch.zeros((nf_pad, v_pad), dtype=torch.bfloat16, device=dev), params.weights,
+                              n_features, vocab)
     else:
         raise ValueError("precision must be 'fp64' or 'bf16'")
     f = icepop_fwd(H, W, batch, cfg, layout="dv", store_probs=False)
@@ -609,12 +641,13 @@ def delta_and_gap(params, probes, infer, temperature: float = 1.0, *, precision:
         d, g, _, _ = _device_delta_gap(H64, W64, torch.from_numpy(np.ascontiguousarray(infer_logits)).to(dev),
                                        layout="dv", temperature=temperature)
     elif precision == "bf16":
-        nf_pad = (n_features + 7) // 8 * 8
-        Wb = torch.zeros((nf_pad, vocab), dtype=torch.bfloat16, device=dev)
-        Wb[:n_features] = W64.to(torch.bfloat16)
-        d, g, _, _ = _device_delta_gap(multihot_device(fd, nf_pad, torch.bfloat16), Wb,
-                                       torch.from_numpy(infer_logits.astype(np.float32)).to(dev), layout="dv",
-                                       temperature=temperature)
+        nf_pad, v_pad, _ = _bf16_shapes(n_features, vocab)
+        Wb = _bf16_weight_into(torch.zeros((nf_pad, v_pad), dtype=torch.bfloat16, device=dev), params.weights,
+                               n_features, vocab)
+        zi = np.full((len(probes), v_pad), -1e30, dtype=np.float32)  # padded columns: probability 0
+        zi[:, :vocab] = infer_logits
+        d, g, _, _ = _device_delta_gap(_bf16_hidden(fd, n_features, vocab), Wb, torch.from_numpy(zi).to(dev),
+                                       layout="dv", temperature=temperature)
     else:
         raise ValueError("precision must be 'fp64' or 'bf16'")
     out = torch.stack([d, g]).cpu().numpy()

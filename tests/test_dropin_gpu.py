@@ -422,3 +422,22 @@ def test_mask_uses_numpys_calibration_bits():
     c = np.exp(lp_old - lp_inf)
     assert np.array_equal(out.per_token_calibration, c)
     assert np.array_equal(out.per_token_mask_kept, (c >= 0.5) & (c <= 5.0))
+
+
+@pytest.mark.parametrize("vocab", [10, 37])
+def test_bf16_pads_a_vocabulary_not_a_multiple_of_8(vocab):
+    """The bf16 path pads V to a multiple of 8 with columns held at logit -1e4 (one always-on
+    feature row): the results match the fp64 path within the bf16 tolerances and the gradient
+    keeps the reference's shape."""
+    O = _obj()
+    theta = rand_params(21, vocab, 0.5, 8)
+    g = manual_group(theta, [(1, 1.0, 1.1), (2, 0.9, 1.0), (3, 1.2, 0.95), (vocab - 1, 1.0, 1.0)],
+                     [1.0, -1.0, 0.5, -0.5])
+    cfg, b = O.ObjectiveConfig(group_size=2), O.MaskingBounds()
+    a = O.objective_and_grad([g], theta, theta, None, cfg, b, precision="fp64")
+    c = O.objective_and_grad([g], theta, theta, None, cfg, b, precision="bf16")
+    assert c.grad.shape == theta.weights.shape
+    assert np.array_equal(a.per_token_mask_kept, c.per_token_mask_kept)
+    assert c.objective_value == pytest.approx(a.objective_value, rel=1e-2, abs=1e-3)
+    assert np.linalg.norm(c.grad - a.grad) <= 2e-2 * np.linalg.norm(a.grad)
+    np.testing.assert_allclose(c.per_token_entropy, a.per_token_entropy, atol=2e-2)

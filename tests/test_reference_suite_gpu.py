@@ -25,17 +25,25 @@ ROOT = Path(__file__).resolve().parents[1]
 SUITE = ROOT / "baseline" / "_ref_tests"
 
 
+# On the bf16 tensor-core path the tests that resolve the weights below bf16's resolution cannot
+# hold (the finite differences use h = 1e-6; an exactly-zero delta needs the
+# inference logits in the train logits' own rounding): they are deselected, everything else runs.
+BF16_DESELECT = "not finite_differences and not zero_scale_gives_exactly_zero_delta"
+
+
+@pytest.mark.parametrize("precision", ["fp64", "bf16"])
 @pytest.mark.parametrize("module", ["test_objective.py", "test_discrepancy.py", "test_scheduler.py"])
-def test_reference_suite_passes_unchanged(cuda_device, module):
+def test_reference_suite_passes_unchanged(cuda_device, module, precision):
     if not (SUITE / module).exists() or not (ROOT / "baseline" / "_ref" / "mismatchlab").exists():
         pytest.skip("the reference's tests / install are not present (run __graft_entry__.build() where "
                     "/root/reference exists)")
-    env = dict(os.environ, ICEPOP_DROPIN_PRECISION="fp64", PYTHONDONTWRITEBYTECODE="1")
+    env = dict(os.environ, ICEPOP_DROPIN_PRECISION=precision, PYTHONDONTWRITEBYTECODE="1")
+    sel = ["-k", BF16_DESELECT] if precision == "bf16" else []
     r = subprocess.run([sys.executable, "-m", "pytest", str(SUITE / module), "-q", "-p", "no:cacheprovider",
-                        "--rootdir", str(SUITE)], capture_output=True, text=True, cwd=str(SUITE), env=env,
+                        "--rootdir", str(SUITE), *sel], capture_output=True, text=True, cwd=str(SUITE), env=env,
                        timeout=1200)
     tail = r.stdout[-3000:] + r.stderr[-2000:]
     assert r.returncode == 0, tail
     m = re.search(r"(\d+) passed", r.stdout)
     assert m and int(m.group(1)) > 0, tail
-    print(f"{module}: {m.group(0)} under install()")
+    print(f"{module} [{precision}]: {m.group(0)} under install()")
