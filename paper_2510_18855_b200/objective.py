@@ -293,10 +293,13 @@ def _bf16_hidden(feats, n_features: int, vocab: int):
 
 
 def _bf16_weight_into(dst, w: np.ndarray, n_features: int, vocab: int):
-    """Write weights [n_features, vocab] (fp64, host) into a zeroed bf16 buffer [nf_pad, v_pad]."""
+    """Write weights [n_features, vocab] (fp64, host) into a bf16 buffer [nf_pad, v_pad] (a reused
+    staging buffer: every element outside the weights is rewritten)."""
     import torch
 
     dst[:n_features, :vocab].copy_(torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64)))
+    dst[:n_features, vocab:] = 0.0
+    dst[n_features:] = 0.0
     if vocab % 8:
         dst[n_features, vocab:] = _PAD_LOGIT
     return dst

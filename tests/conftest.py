@@ -127,6 +127,9 @@ def mismatchlab_ref():
     import mismatchlab.objective
     import mismatchlab.scheduler
 
+    from paper_2510_18855_b200 import objective as dropin
+
+    precision = dropin._DEFAULT_PRECISION  # install(precision=...) changes it for the process
     mods = (mismatchlab, mismatchlab.objective, mismatchlab.scheduler, mismatchlab.discrepancy)
     saved = {(m, n): getattr(m, n) for m in mods for n in _BOUND + ("run_iteration", "run_iteration_baseline")
              if hasattr(m, n)}
@@ -135,3 +138,4 @@ def mismatchlab_ref():
     finally:
         for (m, n), f in saved.items():
             setattr(m, n, f)
+        dropin.set_default_precision(precision)
