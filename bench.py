@@ -905,9 +905,14 @@ def run_reference(args):
     rng = np.random.default_rng(123)
     W64 = (rng.standard_normal((cfg["vocab"], cfg["hidden"]), dtype=np.float32) * (2.0 / np.sqrt(cfg["hidden"]))
            ).astype(np.float64)
-    n_tok = args.cpu_tokens or sample_tokens(cfg, W64, 12.0)  # 8 calls of ~12 s at the defaults
+    # Each timed step is one call on a token sample sized so the whole run takes ~2.5 minutes
+    # (8-30 s per step): the larger the sample, the better the call's fixed part (the fp64 V x d
+    # gradient buffer the reference allocates per call, ~3 s at C2) is amortised, as it would be
+    # over a full batch. Warm-up steps only warm BLAS threads and the buffers: small samples.
+    target_s = min(30.0, max(8.0, 150.0 / max(args.steps, 1)))
+    n_tok = args.cpu_tokens or sample_tokens(cfg, W64, target_s)
     for i in range(args.warmup):
-        time_oracle(cfg, n_tok, W64, seed=i)
+        time_oracle(cfg, min(n_tok, 64), W64, seed=i)
     tot_t, tot_n = 0.0, 0
     for i in range(args.steps):
         dt, n = time_oracle(cfg, n_tok, W64, seed=100 + i)
