@@ -241,7 +241,7 @@ int icepop_bwd_bf16(const icepop_shape* shape, const icepop_config* cfg, const v
  * V (DV). icepop_bwd_bf16_rs is icepop_bwd_bf16 whose last K5 epilogue stores each dW row
  * (+ this rank's earlier-chunk partial, kept in grad_weight_scratch) straight into the owner's
  * slot at row rank*shard_rows + (r - o*shard_rows) -- the transfer overlaps the GEMM tile by
- * tile. After a cross-rank barrier each owner calls icepop_rs_fold on its own slot buffer:
+ * tile; the row-scaled backward then adds its one-hot part into the touched rows of those slots. After a cross-rank barrier each owner calls icepop_rs_fold on its own slot buffer:
  * out = sum over ranks in rank order (deterministic). */
 typedef struct icepop_rs_target {
   int32_t world;      /* 1..8 */

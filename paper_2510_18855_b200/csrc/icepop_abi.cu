@@ -1052,7 +1052,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
   if (sp) {
     if (workspace && workspace_bytes >= carve_sparse(shape, nullptr).bytes) {
       sw = carve_sparse(shape, workspace);
-      scaled = !rs || grad_weight;  // the fused reduce-scatter takes the one-hot part as acc_src
+      scaled = true;  // (with the fused reduce-scatter the one-hot part goes straight to the slots)
       sparse = skip;
     }
     skip = false;
@@ -1174,13 +1174,26 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       // row-scaled stored probabilities: dW = Q^T.(s H) + scatter_y(c H); the one-hot part
       // is scattered after K5 into grad_weight, or (fused reduce-scatter) first into the local
       // scratch that K5's epilogue adds to every row it sends
-      auto onehot_scatter = [&](float* dst) -> int {
+      auto onehot_scatter = [&](float* dw, const icepop_rs_target* to) -> int {
         k_iota<<<(int)std::min<int64_t>((nc + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(sw.iota, nc);
         size_t tb = sw.sort_bytes;
         ICP_CUDA(cub::DeviceRadixSort::SortPairs(sw.sort_tmp, tb, tokens, sw.keys, sw.iota, sw.vals, (int)nc, 0,
                                                  sort_key_bits(V), st));
+        OneHotDst od;
+        memset(&od, 0, sizeof(od));
+        od.dw = dw;
+        od.sy = dv ? 1 : d;
+        od.sc = dv ? V : 1;
+        od.rows_are_y = dv ? 0 : 1;
+        if (to) {
+          od.rs_world = to->world;
+          od.rs_rank = to->rank;
+          od.shard_rows = to->shard_rows;
+          od.row_len = dv ? V : d;
+          for (int o = 0; o < to->world; ++o) od.slots[o] = to->slots[o];
+        }
         k_onehot_scatter<<<(int)std::min<int64_t>(nc, (int64_t)num_sms() * 8), OHS_THREADS, 0, st>>>(
-            sw.keys, sw.vals, nc, sw.ohc, reinterpret_cast<const uint4*>(hidden), d / 8, dst, dv ? 1 : d, dv ? V : 1);
+            sw.keys, sw.vals, nc, sw.ohc, reinterpret_cast<const uint4*>(hidden), d / 8, od);
         ICP_CUDA(cudaGetLastError());
         return ICEPOP_OK;
       };
@@ -1201,11 +1214,6 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.acc_src = (n_chunks > 1) ? grad_weight : nullptr;
         ew.out = nullptr;
         ext_k.dim = skip ? 2 : 0;
-        if (scaled) {
-          ICP_CUDA(cudaMemsetAsync(grad_weight, 0, sizeof(float) * d * V, st));
-          ICP_TRY(onehot_scatter(grad_weight));
-          ew.acc_src = grad_weight;
-        }
       }
       if (scaled) h = sw.hid_s;
       // an empty K extent must still store (zeros, or the local partial to the peers) when
@@ -1225,7 +1233,9 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
         ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
       }
-      if (scaled && !(rs && last)) ICP_TRY(onehot_scatter(grad_weight));
+      // the one-hot part after K5 stored dW: into grad_weight, or (fused reduce-scatter) straight
+      // into the owners' slots, sparse read-modify-writes of the rows the batch's tokens touch
+      if (scaled) ICP_TRY(onehot_scatter(grad_weight, rs && last ? rs : nullptr));
     }
   }
   return ICEPOP_OK;

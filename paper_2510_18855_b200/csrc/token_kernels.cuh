@@ -755,15 +755,37 @@ __global__ void k_iota(int32_t* __restrict__ out, int64_t n) {
     out[i] = (int32_t)i;
 }
 
+// Destination of the one-hot part of dW: element (vocabulary row y, hidden column col) of dW lives
+// at dw + y * sy + col * sc in the weight's layout ([V,d]: sy = d, sc = 1; [d,V]: sy = 1, sc = V)
+// -- or, with the fused reduce-scatter (rs_world > 0), in the slot its owner keeps for this rank:
+// dW row r (= y for [V,d], = col for [d,V]) is owned by o = r / shard_rows and sits at row
+// rank * shard_rows + r - o * shard_rows of slots[o] (row length row_len).
+struct OneHotDst {
+  float* dw;
+  int64_t sy, sc;
+  int32_t rs_world, rs_rank;
+  int64_t shard_rows, row_len;
+  int32_t rows_are_y;  // [V,d]: dW rows are vocabulary rows
+  float* slots[8];
+
+  __device__ __forceinline__ float* at(int64_t y, int64_t col) const {
+    if (rs_world == 0) return dw + y * sy + col * sc;
+    const int64_t r = rows_are_y ? y : col, c = rows_are_y ? col : y;
+    const int64_t o = r / shard_rows;
+    return slots[o] + ((int64_t)rs_rank * shard_rows + r - o * shard_rows) * row_len + c;
+  }
+};
+
 // One-hot part of dW: dW[y, :] += sum over tokens t with y_t = y of c_t H[t, :], in increasing t
 // (the token indices are radix-sorted by y, a stable sort), one block per run of equal y that
-// starts in its stride: deterministic, no atomics. dW element (y, col) at y * sy + col * sc.
+// starts in its stride: deterministic, no atomics. With the fused reduce-scatter it adds into the
+// owners' slots (over NVLink) after K5 stored there, so no dense local dW has to be built.
 constexpr int OHS_THREADS = 256;
 __global__ void __launch_bounds__(OHS_THREADS) k_onehot_scatter(const int32_t* __restrict__ ys,
                                                                 const int32_t* __restrict__ ts, int64_t n,
                                                                 const float* __restrict__ ohc,
                                                                 const uint4* __restrict__ hid, int64_t d8,
-                                                                float* __restrict__ dw, int64_t sy, int64_t sc) {
+                                                                const OneHotDst dst) {
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     const int32_t y = ys[i];
     if (i > 0 && ys[i - 1] == y) continue;  // not the start of a run (block-uniform)
@@ -787,9 +809,8 @@ __global__ void __launch_bounds__(OHS_THREADS) k_onehot_scatter(const int32_t* _
         }
       }
       if (!any) continue;
-      float* dst = dw + (int64_t)y * sy + k * 8 * sc;
-      if (sc == 1) {
-        float4* d4 = reinterpret_cast<float4*>(dst);
+      if (dst.rows_are_y) {  // 8 consecutive columns of one dW row: two 16-byte read-modify-writes
+        float4* d4 = reinterpret_cast<float4*>(dst.at(y, k * 8));
         float4 a = d4[0], b = d4[1];
         a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
         b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
@@ -797,7 +818,7 @@ __global__ void __launch_bounds__(OHS_THREADS) k_onehot_scatter(const int32_t* _
         d4[1] = b;
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dst[j * sc] += acc[j];
+        for (int j = 0; j < 8; ++j) *dst.at(y, k * 8 + j) += acc[j];
       }
     }
   }

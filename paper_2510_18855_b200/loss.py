@@ -700,10 +700,8 @@ def icepop_bwd_reduce_scatter(
         ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
         single_chunk = ws.numel() >= bwd_workspace_bytes(n, d, v, shape.n_seqs, 2 * n * v)
         scratch = None if single_chunk else torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
-    else:
+    else:  # stored probabilities: one chunk; the one-hot part of dW goes straight to the slots
         ws = _sp_workspace(n, d, v, shape.n_seqs, dev)
-        if ws is not None:  # the row-scaled backward sends the one-hot part of dW from this scratch
-            scratch = torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     saved = _lib.Saved(tokens=batch.tokens.data_ptr(), lse=fwd.lse.data_ptr(), coeff=fwd.coeff.data_ptr(),
                        lse_ref=_lib.ptr(fwd.lse_ref), kl=_lib.ptr(fwd.kl), kl_w=_lib.ptr(fwd.extras.get("kl_w")),
                        probs=_lib.ptr(probs), tile_max=_lib.ptr(tile_max), lp_cur=_lib.ptr(fwd.lp_cur))
