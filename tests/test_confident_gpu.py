@@ -89,6 +89,8 @@ def _compare(c, dev):
         ew = _row_err(_vocab_rows(gw, c["layout"]), gref)[live]
         res[mode] = dict(h_med=float(np.median(eh)), h_p95=float(np.quantile(eh, 0.95)),
                          w_med=float(np.median(ew)), w_max=float(ew.max()))
+    print(f"V={c['W'].numel() // c['H'].shape[1]} {c['layout']}: {int(conf.sum())} confident rows; "
+          f"stored {res[True]}, recompute {res[False]}")
     return res
 
 

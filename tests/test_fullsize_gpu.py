@@ -289,6 +289,7 @@ def test_c2_confident_tokens_full_size(cuda_device):
         ew = ((gw - gw_r).norm(dim=1) / wn.clamp_min(1e-30))[cols].cpu()
         out[mode] = dict(h_med=float(eh.median()), h_p95=float(eh.quantile(0.95)), w_med=float(ew.median()),
                          w_max=float(ew.max()))
+    print(f"confident rows {int(live.sum())}: stored {out[True]}, recompute {out[False]}")
     for k in out[True]:
         assert out[True][k] <= 2.0 * out[False][k] + 1e-4, (k, out)
     assert out[True]["h_med"] < 1e-2, out
