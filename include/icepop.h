@@ -209,10 +209,13 @@ typedef struct icepop_saved {
   const float* kl_w;      /* [n_tokens]                                                   */
   void* probs;            /* out->probs / out->tile_max of the forward, or NULL. CONSUMED: the */
   const float* tile_max;  /* backward may overwrite rows of probs (a second backward passes NULL) */
-  /* [n_tokens] out->lp_cur of the forward. Required with probs: the sampled token's term
-   * of dZ, c (1 - p_y), is formed from p_y = exp(lp_cur) in fp64 and enters the GEMMs as a
-   * one-hot term, with q_y zeroed in probs. Forming it by cancellation against the bf16
-   * q_y would lose 2^-9 p_y / (1 - p_y) of it: 12% on tokens with p_y = 0.98. */
+  /* [n_tokens] out->lp_cur of the forward. The sampled token's term of dZ, c (1 - p_y), is
+   * formed as c * -expm1(lp_cur) in fp64: with probs it enters the GEMMs as a one-hot term
+   * (q_y zeroed in probs), in the recompute mode it is K3's y entry. Required with probs;
+   * recommended always: forming it by cancellation, c - c p_y, loses 2^-9 p_y / (1 - p_y) of
+   * it against the bf16 q_y (12% on tokens with p_y = 0.98) and the absolute precision of the
+   * fp32 logits against the recomputed p_y. The forward keeps 1 - p_y to fp32 relative
+   * precision in lp_cur (log1p of the probability mass of the other tokens). */
   const double* lp_cur;
 } icepop_saved;
 

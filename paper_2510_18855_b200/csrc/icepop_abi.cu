@@ -618,6 +618,7 @@ struct BF16Workspace {
   int32_t* tok_act;
   float* lse_act;
   float* coeff_act;
+  double* lp_act;
   __nv_bfloat16* dz;
   int64_t chunk;
   size_t bytes;
@@ -661,6 +662,7 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
     w.tok_act = c.take<int32_t>((size_t)n);
     w.lse_act = c.take<float>((size_t)n);
     w.coeff_act = c.take<float>((size_t)n);
+    w.lp_act = c.take<double>((size_t)n);
   }
   w.dz = c.take<__nv_bfloat16>((size_t)chunk * (size_t)s->vocab);
   w.chunk = chunk;
@@ -739,6 +741,7 @@ int launch_dz(const icepop_shape* shape, double temperature, const void* h, cons
   ep.targets = sv.tokens;
   ep.lse = sv.lse;
   ep.coeff = sv.coeff;
+  ep.lp_cur = sv.lp_cur;
   ep.lse_ref = sv.lse_ref;
   ep.kl = sv.kl;
   ep.kl_w = sv.kl_w;
@@ -756,6 +759,7 @@ icepop_saved offset_saved(const icepop_saved& s, int64_t o) {
   r.tokens = s.tokens + o;
   r.lse = s.lse + o;
   r.coeff = s.coeff + o;
+  if (s.lp_cur) r.lp_cur = s.lp_cur + o;
   if (s.lse_ref) r.lse_ref = s.lse_ref + o;
   if (s.kl) r.kl = s.kl + o;
   if (s.kl_w) r.kl_w = s.kl_w + o;
@@ -963,10 +967,15 @@ __global__ void k_logprob_finish(const float* part, int n_parts, const float* zt
       S = fmaf(ca, S, cb * p[n]);
       M = nm;
     }
+    // the partials leave the sampled token out (k2_icepop_tokens): add it back, log1p when confident
+    const float zy = ztok[t];
+    const float ey = exp2f(zy * LOG2E_TOK - M);
+    const float Sx = S;
+    S += ey;
     const float l2s = log2f(S);
     const float l = (M + l2s) * LN2_F;
     if (lse) lse[t] = l;
-    if (lp) lp[t] = (double)(ztok[t] - l);
+    if (lp) lp[t] = ey > 0.5f * S ? (double)log1pf(-Sx / S) : (double)(zy - l);
     if (entropy) entropy[t] = (l2s - Q / S) * LN2_F;
   }
 }
@@ -1089,7 +1098,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     const int gg = (int)std::min<int64_t>((N * d8 + 255) / 256, (int64_t)num_sms() * 16);
     k_gather_active<<<gg, 256, 0, st>>>(w.idx, w.n_active, reinterpret_cast<const uint4*>(hidden), d8, tokens, lse,
                                         coeff, reinterpret_cast<uint4*>(w.hid_act), w.tok_act, w.lse_act,
-                                        w.coeff_act, N);
+                                        w.coeff_act, sv.lp_cur, w.lp_act, N);
     ICP_CUDA(cudaGetLastError());
     if (grad_hidden) ICP_CUDA(cudaMemsetAsync(grad_hidden, 0, (size_t)N * d * gh_esz, st));
     hsrc = w.hid_act;
@@ -1119,6 +1128,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       cs.tokens = tok_src + c0;
       cs.lse = lse_src + c0;
       cs.coeff = coeff_src + c0;
+      cs.lp_cur = sv.lp_cur ? w.lp_act + c0 : nullptr;
     }
     if (sp) {
       const int32_t tm_ld = (int32_t)(4 * ((V + BN_ - 1) / BN_));

@@ -19,6 +19,7 @@ namespace icp {
 
 constexpr int TOK_THREADS = 256;
 constexpr float LN2_F = 0.69314718055994531f;
+constexpr float LOG2E_TOK = 1.4426950408889634f;
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum)
 // for contiguous data, over f(i) for i in [0, n). Reproducing its association order
@@ -197,10 +198,18 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
         }
         M = nm;
       }
+      // K1's run partials (R == 3) leave the sampled token out of S: add 2^(u_y - M) back for the
+      // log-sum-exp, and take a confident token's log-prob as log1p(-S_{v != y} / S), which keeps
+      // 1 - p_y (the backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is
+      // to 1; z_y - lse would leave only the absolute precision of lse (~1e-6 for |z| ~ 10)
+      const float zy = a.ztok[t];
+      const float ey = R == 3 ? exp2f(zy * LOG2E_TOK - M) : 0.f;
+      const float Sx = S;
+      S += ey;
       const float l2s = log2f(S);
       const float lse = (M + l2s) * LN2_F;
       const float entf = (l2s - Q / S) * LN2_F;
-      lp_cur = (double)(a.ztok[t] - lse);
+      lp_cur = (R == 3 && ey > 0.5f * S) ? (double)log1pf(-Sx / S) : (double)(zy - lse);
       ent = (double)entf;
       if (a.lse_f) a.lse_f[t] = lse;
       if (a.entropy_f) a.entropy_f[t] = entf;
@@ -549,12 +558,14 @@ __global__ void __launch_bounds__(COMPACT_BLOCK) k_active_scatter(const float* _
 }
 
 // Gather active rows: hid_act[i] = hid[idx[i]] (bf16 rows of d elements, d % 8 == 0) and the
-// per-row scalars; rows [n_active, rows_cap) are zero-filled up to the next multiple of 256.
+// per-row scalars (lp_cur when given); rows [n_active, rows_cap) are zero-filled up to the next
+// multiple of 256.
 __global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_active,
                                 const uint4* __restrict__ hid, int64_t d8, const int32_t* __restrict__ tok,
                                 const float* __restrict__ lse, const float* __restrict__ coeff,
                                 uint4* __restrict__ hid_act, int32_t* __restrict__ tok_act,
-                                float* __restrict__ lse_act, float* __restrict__ coeff_act, int64_t rows_cap) {
+                                float* __restrict__ lse_act, float* __restrict__ coeff_act,
+                                const double* __restrict__ lp, double* __restrict__ lp_act, int64_t rows_cap) {
   const int na = *n_active;
   const int64_t rows_r = ((int64_t)na + 255) / 256 * 256;
   const int64_t rows = rows_cap < rows_r ? rows_cap : rows_r;
@@ -568,6 +579,7 @@ __global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* 
         tok_act[r] = tok[src];
         lse_act[r] = lse[src];
         coeff_act[r] = coeff[src];
+        if (lp) lp_act[r] = lp[src];
       }
     } else {
       hid_act[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -575,6 +587,7 @@ __global__ void k_gather_active(const int32_t* __restrict__ idx, const int32_t* 
         tok_act[r] = 0;
         lse_act[r] = 0.f;
         coeff_act[r] = 0.f;
+        if (lp) lp_act[r] = 0.0;
       }
     }
   }

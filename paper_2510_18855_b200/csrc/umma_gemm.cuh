@@ -126,6 +126,8 @@ struct EpiParams {
   float* ztok;             // EPI_LSE: [M] z[y] (natural units), written by the owning tile
   const float* lse;        // EPI_DZ: [M] natural units
   const float* coeff;      // EPI_DZ: [M]
+  const double* lp_cur;    // EPI_DZ / EPI_DZ_REF: [M] log p_y, or null: the sampled entry is c (1 - p_y)
+                           // with 1 - p_y = -expm1(lp_cur) instead of c - c p_y (cancellation)
   float coeff_scale;       // EPI_DZ: grad_scale
   __nv_bfloat16* dz;       // EPI_DZ: [M, ldz]
   int64_t ldz;
@@ -358,10 +360,12 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
 
 // One 64-column slab of K1's epilogue (FULL: all 64 columns < N, else the first `valid`):
 // slab maximum mx (log2 units), reference R, partial sums (s, q) against mx as two float2 lanes,
-// and the packed bf16 q = 2^(u - R).
-template <bool FULL>
+// and the packed bf16 q = 2^(u - R). EXCL (the rare slab holding some lane's sampled token, at
+// column `rel`): s leaves that column out, so that K2 holds sum_{v != y} exactly and 1 - p_y is
+// not formed by cancellation (K2 adds 2^(u_y - M) back for the log-sum-exp); q keeps it.
+template <bool FULL, bool EXCL>
 __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_log2, float& mx, float& ref,
-                                         float2& sum2, float2& q2, uint32_t (&pk)[32]) {
+                                         float2& sum2, float2& q2, uint32_t (&pk)[32], int rel) {
   if (!FULL) {
 #pragma unroll
     for (int j = 0; j < 64; ++j) v[j] = j < valid ? v[j] : -1e30f;
@@ -390,11 +394,12 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
     const float2 d = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nmx);
     // every third pair of a full slab on the FMA pipe (masked columns need the MUFU's exact 0)
     const float2 e = (FULL && j % 3 == 2) ? exp2_fma2(d) : make_float2(fast_exp2(d.x), fast_exp2(d.y));
+    const float2 es = EXCL ? make_float2(2 * j == rel ? 0.f : e.x, 2 * j + 1 == rel ? 0.f : e.y) : e;
     if (j & 1) {
-      sb = __fadd2_rn(sb, e);
+      sb = __fadd2_rn(sb, es);
       qb = __ffma2_rn(e, d, qb);
     } else {
-      sa = __fadd2_rn(sa, e);
+      sa = __fadd2_rn(sa, es);
       qa = __ffma2_rn(e, d, qa);
     }
     const float2 p = __fmul2_rn(e, qs2);
@@ -406,9 +411,10 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
 
 // K1 epilogue: log-sum-exp statistics of half of this tile's BN columns (`half`: TMEM columns
 // [half BN/2, (half+1) BN/2)) for one row, in log2 units,
-//   mx = max_j u_j,  s = sum_j 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
-// so that lse = ln2 (mx + log2 s) and entropy = ln2 (log2 s - q / s) after the merge (K2); the
-// half's triple is partial 2 n_blk + half. One TMEM pass in 64-column slabs: each slab's
+//   mx = max_j u_j,  s = sum_{j != y} 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
+// so that, with S the merged s plus K2's 2^(u_y - M), lse = ln2 (M + log2 S), entropy =
+// ln2 (log2 S - Q / S) and 1 - p_y = s / S without cancellation (K2); the halves' triples are
+// merged per run (below). One TMEM pass in 64-column slabs: each slab's
 // (max, sum, q) is taken against the slab's own maximum and merged online. In
 // stored-probabilities mode (ep.probs) the slab also emits q[m, v] = 2^(u_v - R) as bf16 (TMA
 // stores, clipped to M rows / N columns) and tile_max[m, v / 64] = R, the slab's reference: 0
@@ -456,7 +462,8 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
     const int col0 = tile_col<BN, CG>(n0, c * 64);
     if (col0 < sh.N) {  // warp-uniform
       const int rel = y - col0;
-      if (__any_sync(0xffffffffu, (unsigned)rel < 64u)) {  // some row's sampled token is in this slab (rare)
+      const bool y_slab = __any_sync(0xffffffffu, (unsigned)rel < 64u);  // some row's sampled token (rare)
+      if (y_slab) {
         float zt = 0.f;
 #pragma unroll
         for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
@@ -465,10 +472,14 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
       float mx, ref;
       float2 sum2, q2;
       uint32_t pk[32];
-      // the ragged last slab (columns past N take no part) is a separate, warp-uniform path so
-      // the common one carries no per-column predicates
-      if (col0 + 64 <= sh.N) lse_slab<true>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk);
-      else lse_slab<false>(v, sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk);
+      // the ragged last slab (columns past N take no part) and the slab with a sampled token
+      // are separate, warp-uniform paths so the common one carries no per-column predicates
+      if (col0 + 64 <= sh.N) {
+        if (y_slab) lse_slab<true, true>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, rel);
+        else lse_slab<true, false>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, -1);
+      } else {
+        lse_slab<false, true>(v, sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk, rel);
+      }
       if (store && warp_rows) stage_store_slab<1>(tmC, stage1, ebuf, pk, col0, row0, lane);
       const float s = sum2.x + sum2.y, q = q2.x + q2.y;
       refs[i] = ref;
@@ -514,6 +525,16 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
   }
 }
 
+// The sampled token's dZ entry c (1 - p_y) from the forward's lp_cur (fp64 -expm1, exact however
+// close p_y is to 1), or NAN when lp_cur is not given (then dz_entry forms c - c p_y).
+__device__ __forceinline__ float sampled_dz(const EpiParams& ep, int m, bool live, float cf) {
+  return (live && ep.lp_cur) ? (float)((double)cf * -expm1(__ldg(ep.lp_cur + m))) : __int_as_float(0x7fc00000);
+}
+
+__device__ __forceinline__ float dz_entry(float cf, float p, bool is_y, float dzy) {
+  return is_y ? (dzy == dzy ? dzy : fmaf(-cf, p, cf)) : -cf * p;
+}
+
 // dZ = coeff_scale * c_t * (e_{y_t} - softmax(z_t)) for this tile -> bf16.
 template <int BN>
 __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
@@ -526,6 +547,7 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
   const float lse2 = live ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
   const float cf = live ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
   const int y = live ? __ldg(ep.targets + m) : -1;
+  const float dzy = sampled_dz(ep, m, live, cf);
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
@@ -537,8 +559,8 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
     for (int j = 0; j < 16; ++j) {
       const float p0 = fast_exp2(fmaf(v[2 * j], ep.scale_log2, -lse2));
       const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
-      const float d0 = fmaf(-cf, p0, (col0 + 2 * j == y) ? cf : 0.f);
-      const float d1 = fmaf(-cf, p1, (col0 + 2 * j + 1 == y) ? cf : 0.f);
+      const float d0 = dz_entry(cf, p0, col0 + 2 * j == y, dzy);
+      const float d1 = dz_entry(cf, p1, col0 + 2 * j + 1 == y, dzy);
       pk[j] = live ? pack_bf16x2(d0, d1) : 0u;
     }
     __nv_bfloat16* dst = ep.dz + (int64_t)m * ep.ldz + col0;
@@ -571,6 +593,7 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
   const float lse2 = live ? __ldg(ep.lse + m) * LOG2E_F : 0.f;
   const float cf = live ? __ldg(ep.coeff + m) * ep.coeff_scale : 0.f;
   const int y = live ? __ldg(ep.targets + m) : -1;
+  const float dzy = sampled_dz(ep, m, live, cf);
   const int row0 = m0 + quarter * 32;  // first row of this warp's slab
   const bool warp_rows = row0 < ep.zero_rows_to;  // warp-uniform: any of its rows inside the map
 #pragma unroll 1
@@ -587,10 +610,10 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
       const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
       const float q0 = fast_exp2(fmaf(w[2 * j], ep.scale_log2, -lse2));
       const float q1 = fast_exp2(fmaf(w[2 * j + 1], ep.scale_log2, -lse2));
-      pk[j] = live ? pack_bf16x2(fmaf(-cf, p0, (col0 + 2 * j == y) ? cf : 0.f),
-                                 fmaf(-cf, p1, (col0 + 2 * j + 1 == y) ? cf : 0.f)) : 0u;
-      pk[16 + j] = live ? pack_bf16x2(fmaf(-cf, q0, (col0 + 32 + 2 * j == y) ? cf : 0.f),
-                                      fmaf(-cf, q1, (col0 + 32 + 2 * j + 1 == y) ? cf : 0.f)) : 0u;
+      pk[j] = live ? pack_bf16x2(dz_entry(cf, p0, col0 + 2 * j == y, dzy),
+                                 dz_entry(cf, p1, col0 + 2 * j + 1 == y, dzy)) : 0u;
+      pk[16 + j] = live ? pack_bf16x2(dz_entry(cf, q0, col0 + 32 + 2 * j == y, dzy),
+                                      dz_entry(cf, q1, col0 + 32 + 2 * j + 1 == y, dzy)) : 0u;
     }
     stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
   }
@@ -721,6 +744,7 @@ __device__ __forceinline__ void epi_dz_ref(const GemmShape& sh, const EpiParams&
   const float kw = row_ok ? __ldg(ep.kl_w + m) * ep.coeff_scale : 0.f;
   const float kl = row_ok ? __ldg(ep.kl + m) : 0.f;
   const int y = row_ok ? __ldg(ep.targets + m) : -1;
+  const float dzy = sampled_dz(ep, m, row_ok, cf);
   constexpr float LN2 = 0.69314718055994531f;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
@@ -739,7 +763,7 @@ __device__ __forceinline__ void epi_dz_ref(const GemmShape& sh, const EpiParams&
         const float lpr2 = fmaf(w[2 * j + h], ep.scale_log2, -lser2);  // log2 p_ref
         const float p = fast_exp2(lp2);
         const float diff = (lp2 - lpr2) * LN2 - kl;
-        d[h] = fmaf(-cf, p, (col0 + 2 * j + h == y) ? cf : 0.f) - kw * p * diff;
+        d[h] = dz_entry(cf, p, col0 + 2 * j + h == y, dzy) - kw * p * diff;
       }
       pk[j] = pack_bf16x2(d[0], d[1]);
     }
