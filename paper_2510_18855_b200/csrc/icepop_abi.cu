@@ -958,18 +958,20 @@ int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, con
 __global__ void k_logprob_finish(const float* part, int n_parts, const float* ztok, int64_t n, float* lse,
                                  double* lp, float* entropy) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    float M = -1e30f, S = 0.f, Q = 0.f;
+    const float zy = ztok[t], uy = zy * LOG2E_TOK;
+    float M = -1e30f, S = 0.f, Q = 0.f, Ey = 0.f;
     for (int j = 0; j < n_parts; ++j) {  // one pass with a running maximum (k2_icepop_tokens)
       const float* p = part + (int64_t)j * 3 * n + t;
-      const float mj = p[0], nm = fmaxf(M, mj);
+      const float mj = p[0], sr = p[n], sj = fabsf(sr), nm = fmaxf(M, mj);
+      const float eyj = signbit(sr) ? exp2f(uy - mj) : 0.f;  // the partial holding the token
       const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
-      Q = fmaf(ca, fmaf(M - nm, S, Q), cb * fmaf(mj - nm, p[n], p[2 * n]));
-      S = fmaf(ca, S, cb * p[n]);
+      Q = fmaf(ca, fmaf(M - nm, S + Ey, Q), cb * fmaf(mj - nm, sj + eyj, p[2 * n]));
+      S = fmaf(ca, S, cb * sj);
+      Ey = fmaf(ca, Ey, cb * eyj);
       M = nm;
     }
     // the partials leave the sampled token out (k2_icepop_tokens): add it back, log1p when confident
-    const float zy = ztok[t];
-    const float ey = exp2f(zy * LOG2E_TOK - M);
+    const float ey = exp2f(uy - M);
     const float Sx = S;
     S += ey;
     const float l2s = log2f(S);

@@ -179,16 +179,22 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
       // running maximum: each partial is read exactly once (a max pass first would re-read the
       // partials' maxima from DRAM: they exceed L2 at C2's size)
       const int64_t R = a.part_rows;
+      const float uy = a.ztok[t] * LOG2E_TOK;
       float M = -1e30f, Mr = -1e30f;
-      float S = 0.f, Q = 0.f, Sr = 0.f, X = 0.f;
+      float S = 0.f, Q = 0.f, Sr = 0.f, X = 0.f, Ey = 0.f;
       for (int j = 0; j < a.n_parts; ++j) {
         const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
-        const float mj = p[0], sj = p[a.n_tokens], qj = p[2 * a.n_tokens];
+        const float mj = p[0], sr = p[a.n_tokens], qj = p[2 * a.n_tokens];
+        // R == 3: the partial holding the sampled token flags it in the sign bit of its s (which
+        // leaves the token out); its 2^(u_y - mj) joins the full sum Q is rebased with
+        const float sj = fabsf(sr);
+        const float eyj = (R == 3 && signbit(sr)) ? exp2f(uy - mj) : 0.f;
         const float nm = fmaxf(M, mj);
         const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
-        // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S before the rescale
-        Q = fmaf(ca, fmaf(M - nm, S, Q), cb * fmaf(mj - nm, sj, qj));
+        // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S_full before the rescale
+        Q = fmaf(ca, fmaf(M - nm, S + Ey, Q), cb * fmaf(mj - nm, sj + eyj, qj));
         S = fmaf(ca, S, cb * sj);
+        Ey = fmaf(ca, Ey, cb * eyj);
         if (R == 6) {
           X = fmaf(ca, X, cb * p[5 * a.n_tokens]);
           const float mr = p[3 * a.n_tokens];
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
       // 1 - p_y (the backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is
       // to 1; z_y - lse would leave only the absolute precision of lse (~1e-6 for |z| ~ 10)
       const float zy = a.ztok[t];
-      const float ey = R == 3 ? exp2f(zy * LOG2E_TOK - M) : 0.f;
+      const float ey = R == 3 ? exp2f(uy - M) : 0.f;
       const float Sx = S;
       S += ey;
       const float l2s = log2f(S);

@@ -362,10 +362,11 @@ __device__ __forceinline__ void stage_store_slab(const CUtensorMap* tmC, uint8_t
 // slab maximum mx (log2 units), reference R, partial sums (s, q) against mx as two float2 lanes,
 // and the packed bf16 q = 2^(u - R). EXCL (the rare slab holding some lane's sampled token, at
 // column `rel`): s leaves that column out, so that K2 holds sum_{v != y} exactly and 1 - p_y is
-// not formed by cancellation (K2 adds 2^(u_y - M) back for the log-sum-exp); q keeps it.
+// not formed by cancellation (K2 adds 2^(u_y - M) back for the log-sum-exp); q keeps it, and
+// ey = 2^(u_y - mx) is returned (0 for lanes whose token is elsewhere) for the merges' rebasing.
 template <bool FULL, bool EXCL>
 __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_log2, float& mx, float& ref,
-                                         float2& sum2, float2& q2, uint32_t (&pk)[32], int rel) {
+                                         float2& sum2, float2& q2, uint32_t (&pk)[32], int rel, float& ey) {
   if (!FULL) {
 #pragma unroll
     for (int j = 0; j < 64; ++j) v[j] = j < valid ? v[j] : -1e30f;
@@ -388,6 +389,7 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
   const float2 sc2 = make_float2(scale_log2, scale_log2);
   const float2 nmx = make_float2(-mx, -mx);
   float2 sa = make_float2(0.f, 0.f), sb = sa, qa = sa, qb = sa;
+  ey = 0.f;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     // masked columns: d ~ -1e30 -> e = 0 and e * d = -0
@@ -395,6 +397,7 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
     // every third pair of a full slab on the FMA pipe (masked columns need the MUFU's exact 0)
     const float2 e = (FULL && j % 3 == 2) ? exp2_fma2(d) : make_float2(fast_exp2(d.x), fast_exp2(d.y));
     const float2 es = EXCL ? make_float2(2 * j == rel ? 0.f : e.x, 2 * j + 1 == rel ? 0.f : e.y) : e;
+    if (EXCL) ey = 2 * j == rel ? e.x : (2 * j + 1 == rel ? e.y : ey);
     if (j & 1) {
       sb = __fadd2_rn(sb, es);
       qb = __ffma2_rn(e, d, qb);
@@ -414,7 +417,10 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
 //   mx = max_j u_j,  s = sum_{j != y} 2^(u_j - mx),  q = sum_j 2^(u_j - mx) (u_j - mx),  u = z log2(e),
 // so that, with S the merged s plus K2's 2^(u_y - M), lse = ln2 (M + log2 S), entropy =
 // ln2 (log2 S - Q / S) and 1 - p_y = s / S without cancellation (K2); the halves' triples are
-// merged per run (below). One TMEM pass in 64-column slabs: each slab's
+// merged per run (below). Rebasing q to a new maximum needs the FULL sum (s + 2^(u_y - mx) when
+// the sampled token is in the range): the warp carries run_ey = 2^(u_y - run_m) (0 until it
+// meets the token), and a partial holding the token stores its s with the sign bit set, so the
+// next merge (half merge, K2) knows to add 2^(u_y - m) (u_y = ztok log2 e) before rebasing. One TMEM pass in 64-column slabs: each slab's
 // (max, sum, q) is taken against the slab's own maximum and merged online. In
 // stored-probabilities mode (ep.probs) the slab also emits q[m, v] = 2^(u_v - R) as bf16 (TMA
 // stores, clipped to M rows / N columns) and tile_max[m, v / 64] = R, the slab's reference: 0
@@ -434,7 +440,7 @@ template <int BN, int CG>
 __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
                                         uint8_t* stage1, int m0, int n0, int part_idx, bool last, int half, int row,
                                         int lane, int quarter, uint32_t taddr, uint32_t half_bar, float& run_m,
-                                        float& run_s, float& run_q, float* xch) {
+                                        float& run_s, float& run_q, float& run_ey, float* xch) {
   static_assert(BN == 256 || BN == 512, "64-column slabs, four or eight per tile");
   constexpr int NH = BN / 128;  // slabs per warp
   const int m = m0 + row;
@@ -469,45 +475,50 @@ __device__ __forceinline__ void epi_lse(const GemmShape& sh, const EpiParams& ep
         for (int j = 0; j < 64; ++j) zt = (j == rel) ? v[j] : zt;
         if (row_ok && (unsigned)rel < 64u) ep.ztok[m] = zt * ep.inv_t;
       }
-      float mx, ref;
+      float mx, ref, ey;
       float2 sum2, q2;
       uint32_t pk[32];
       // the ragged last slab (columns past N take no part) and the slab with a sampled token
       // are separate, warp-uniform paths so the common one carries no per-column predicates
       if (col0 + 64 <= sh.N) {
-        if (y_slab) lse_slab<true, true>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, rel);
-        else lse_slab<true, false>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, -1);
+        if (y_slab) lse_slab<true, true>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, rel, ey);
+        else lse_slab<true, false>(v, 64, ep.scale_log2, mx, ref, sum2, q2, pk, -1, ey);
       } else {
-        lse_slab<false, true>(v, sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk, rel);
+        lse_slab<false, true>(v, sh.N - col0, ep.scale_log2, mx, ref, sum2, q2, pk, rel, ey);
       }
       if (store && warp_rows) stage_store_slab<1>(tmC, stage1, ebuf, pk, col0, row0, lane);
       const float s = sum2.x + sum2.y, q = q2.x + q2.y;
       refs[i] = ref;
-      // merge the slab into the warp's running (max, sum, q)
+      // merge the slab into the warp's running (max, sum, q, ey); q rebases with the full sums
       const float nm = fmaxf(run_m, mx);
       const float a = fast_exp2(run_m - nm), b = fast_exp2(mx - nm);
-      run_q = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(mx - nm, s, q));
+      run_q = fmaf(a, fmaf(run_m - nm, run_s + run_ey, run_q), b * fmaf(mx - nm, s + ey, q));
       run_s = fmaf(a, run_s, b * s);
+      run_ey = fmaf(a, run_ey, b * ey);
       run_m = nm;
     }
     __syncwarp();  // the next slab's tcgen05.ld is warp-collective (.sync.aligned)
   }
   if (last) {  // warp-uniform: both warps of the quarter reach it on the same tile
+    // the second-half warp's s carries its has-the-token flag in the sign bit (-0 for s = 0)
     float* x = xch + (quarter * 32 + lane) * 3;
     if (half == 1) {
       x[0] = run_m;
-      x[1] = run_s;
+      x[1] = run_ey > 0.f ? -run_s : run_s;
       x[2] = run_q;
     }
-    named_bar_sync(1 + quarter, 64);
+    named_bar_sync(1 + quarter, 64);  // also orders ep.ztok[m] (either warp's store) before the read
     if (half == 0 && row_ok) {
-      const float m2 = x[0], s2 = x[1], q2 = x[2];
+      const float m2 = x[0], s2r = x[1], q2 = x[2];
+      const float s2 = fabsf(s2r);
+      const float ey2 = signbit(s2r) ? exp2f(ep.ztok[m] * LOG2E_F - m2) : 0.f;
       const float nm = fmaxf(run_m, m2);
       const float a = fast_exp2(run_m - nm), b = fast_exp2(m2 - nm);
+      const float ps = fmaf(a, run_s, b * s2);
       float* p = ep.part + (int64_t)part_idx * 3 * sh.M + m;
       p[0] = nm;
-      p[sh.M] = fmaf(a, run_s, b * s2);
-      p[2 * (int64_t)sh.M] = fmaf(a, fmaf(run_m - nm, run_s, run_q), b * fmaf(m2 - nm, s2, q2));
+      p[sh.M] = (run_ey > 0.f || ey2 > 0.f) ? -ps : ps;
+      p[2 * (int64_t)sh.M] = fmaf(a, fmaf(run_m - nm, run_s + run_ey, run_q), b * fmaf(m2 - nm, s2 + ey2, q2));
     }
     named_bar_sync(1 + quarter, 64);  // the exchange slot is free for the next run
   }
@@ -1102,8 +1113,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       int m_blk, n_first, n_count;
       run_coords(sh, tile, m_blk, n_first, n_count);
       const int m0 = m_blk * Cfg::TILE_M + (int)rank * BM;
-      float run_m = -1e30f, run_s = 0.f, run_q = 0.f;  // EPI_LSE: this warp's triple over the run
-      (void)run_m; (void)run_s; (void)run_q;
+      float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_ey = 0.f;  // EPI_LSE: this warp's run state
+      (void)run_m; (void)run_s; (void)run_q; (void)run_ey;
       for (int tt = 0; tt < n_count; ++tt) {
         const int n_blk = n_first + tt;
         mbar_wait_sleep(tfull0 + 8 * acc, acc_phase, sh.epi_sleep_ns);
@@ -1113,7 +1124,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         if constexpr (EPI == EPI_LSE)
           epi_lse<BN, CG>(sh, ep, &tmC, sEpi + (warp - 2) * Cfg::EPI_BUF_BYTES, m0, n_blk * BN,
                           n_first / sh.run_len, tt == n_count - 1, ehalf, row, lane, quarter, taddr,
-                          SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q, xch);
+                          SPLIT ? (CG == 2 ? mapa_shared(thalf0, 0) : thalf0) : 0u, run_m, run_s, run_q, run_ey, xch);
         if constexpr (EPI == EPI_DZ) {
           if (sh.dz_tma_store)
             epi_dz_tma<BN>(sh, ep, &tmC, sEpi + quarter * 2 * Cfg::EPI_BUF_BYTES, ebuf, m0, n_blk * BN, row, lane,
