@@ -148,3 +148,58 @@ def test_stored_backward_requires_lp_cur(cuda_device):
     rc = lib.icepop_bwd_bf16(shape, IcePopConfig().to_c(), H.data_ptr(), W.data_ptr(), None, saved, 1.0, None, 0,
                              gw.data_ptr(), 0, None, 0, torch.cuda.current_stream().cuda_stream)
     assert rc == _lib.EINVAL and "lp_cur" in _lib.last_error()
+
+
+def _one_minus_py(c):
+    """fp64 1 - p_y = sum_{v != y} p_v of the bf16 inputs (no cancellation)."""
+    Hd, Wd = c["H"].double().numpy(), c["W"].double().numpy()
+    z = Hd @ (Wd.T if c["layout"] == "vd" else Wd)
+    z -= z.max(1, keepdims=True)
+    e = np.exp(z)
+    rows = np.arange(len(z))
+    ey = e[rows, c["tokens"]].copy()
+    e[rows, c["tokens"]] = 0.0
+    other = e.sum(1)
+    return other / (other + ey)
+
+
+@pytest.mark.parametrize("run", [1, 2, 16])
+@pytest.mark.parametrize("case", ["v1000_std16", "full_width_std14"])
+def test_confident_lp_keeps_one_minus_py(cuda_device, case, run):
+    """lp_cur of a confident token keeps 1 - p_y = -expm1(lp_cur) to fp32 RELATIVE precision:
+    K1's slab sums leave the sampled token out and K2 takes lp = log1p(-S_{v != y} / S) (with
+    z_y - lse, lse's absolute rounding ~1e-6 would swamp 1 - p_y ~ 1e-6). Checked for the
+    forward (K2) and the lp recording (icepop_logprob), at K1 run lengths 1 / 2 / 16 (the
+    token's partial is flagged and merged at every level: slab, run, column half, K2), against
+    fp64 on the same bf16 inputs, down to 1 - p_y ~ 4e-13. Bound: median relative error of
+    1 - p_y <= 2e-5 and 99th percentile <= 2e-4 on rows with p_y > 0.9 (fp32 logits from a bf16
+    GEMM; measured 3.4e-6 / 1.9e-5, profiles/r02_confident_lp.log)."""
+    from paper_2510_18855_b200 import _lib
+    from paper_2510_18855_b200.loss import IcePopConfig, PackedBatch, icepop_fwd, icepop_logprob
+
+    if case == "v1000_std16":
+        c = _peaked_case(seed=75, N=1024, d=256, V=1000, layout="vd", sigma_logit=16.0)
+    else:
+        c = _peaked_case(seed=76, N=512, d=256, V=157184, layout="dv", sigma_logit=14.0)
+    q = _one_minus_py(c)
+    conf = c["py"] > 0.9
+    assert conf.sum() >= 50 and (q[conf] < 1e-4).sum() >= 5, "needs confident rows, some with 1 - p_y < 1e-4"
+    dev = cuda_device
+    b = PackedBatch(torch.from_numpy(c["tokens"]).to(dev), torch.from_numpy(c["lp_old"]).to(dev),
+                    torch.from_numpy(c["lp_inf"]).to(dev), torch.from_numpy(c["cu"]).to(dev),
+                    torch.from_numpy(c["go"]).to(dev), torch.from_numpy(c["adv"]).to(dev))
+    H, W = c["H"].to(dev), c["W"].to(dev)
+    lib = _lib.ensure_device(0)
+    try:
+        _lib.check(lib.icepop_set_k1_run(run))
+        f = icepop_fwd(H, W, b, IcePopConfig(), layout=c["layout"], store_probs=False)
+        lp_rec, _, _ = icepop_logprob(H, W, b.tokens, layout=c["layout"])
+    finally:
+        _lib.check(lib.icepop_set_k1_run(0))
+    for name, lp in (("forward", f.lp_cur), ("recording", lp_rec)):
+        g = -np.expm1(lp.cpu().numpy())
+        rel = np.abs(g - q)[conf] / q[conf]
+        med, p99 = float(np.median(rel)), float(np.quantile(rel, 0.99))
+        print(f"{case} run={run} {name}: {int(conf.sum())} confident rows, min 1-p_y {q[conf].min():.2e}, "
+              f"rel err of 1-p_y median {med:.2e} p99 {p99:.2e}")
+        assert med <= 2e-5 and p99 <= 2e-4, (name, med, p99)
