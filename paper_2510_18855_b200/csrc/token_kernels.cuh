@@ -185,10 +185,10 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
       for (int j = 0; j < a.n_parts; ++j) {
         const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
         const float mj = p[0], sr = p[a.n_tokens], qj = p[2 * a.n_tokens];
-        // R == 3: the partial holding the sampled token flags it in the sign bit of its s (which
-        // leaves the token out); its 2^(u_y - mj) joins the full sum Q is rebased with
+        // the partial holding the sampled token flags it in the sign bit of its s (which leaves
+        // the token out); its 2^(u_y - mj) joins the full sum Q is rebased with
         const float sj = fabsf(sr);
-        const float eyj = (R == 3 && signbit(sr)) ? exp2f(uy - mj) : 0.f;
+        const float eyj = signbit(sr) ? exp2f(uy - mj) : 0.f;
         const float nm = fmaxf(M, mj);
         const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
         // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S_full before the rescale
@@ -204,18 +204,18 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
         }
         M = nm;
       }
-      // K1's run partials (R == 3) leave the sampled token out of S: add 2^(u_y - M) back for the
-      // log-sum-exp, and take a confident token's log-prob as log1p(-S_{v != y} / S), which keeps
-      // 1 - p_y (the backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is
-      // to 1; z_y - lse would leave only the absolute precision of lse (~1e-6 for |z| ~ 10)
+      // K1's partials leave the sampled token out of S: add 2^(u_y - M) back for the log-sum-exp,
+      // and take a confident token's log-prob as log1p(-S_{v != y} / S), which keeps 1 - p_y (the
+      // backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is to 1;
+      // z_y - lse would leave only the absolute precision of lse (~1e-6 for |z| ~ 10)
       const float zy = a.ztok[t];
-      const float ey = R == 3 ? exp2f(uy - M) : 0.f;
+      const float ey = exp2f(uy - M);
       const float Sx = S;
       S += ey;
       const float l2s = log2f(S);
       const float lse = (M + l2s) * LN2_F;
       const float entf = (l2s - Q / S) * LN2_F;
-      lp_cur = (R == 3 && ey > 0.5f * S) ? (double)log1pf(-Sx / S) : (double)(zy - lse);
+      lp_cur = ey > 0.5f * S ? (double)log1pf(-Sx / S) : (double)(zy - lse);
       ent = (double)entf;
       if (a.lse_f) a.lse_f[t] = lse;
       if (a.entropy_f) a.entropy_f[t] = entf;

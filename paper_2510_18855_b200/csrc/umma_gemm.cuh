@@ -630,6 +630,29 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
   }
 }
 
+// One 32-column chunk of epi_lse_ref against the running maxima nm (z) and nr (z_ref): sums
+// s (leaving out column ry, the lane's sampled token, when EXCL: its e is returned in ey),
+// q = sum e d, x = sum e (u - ur), sr = sum 2^(ur - nr).
+template <bool EXCL>
+__device__ __forceinline__ void ref_chunk32(const float* vh, const float* wh, float nm, float nr, int ry, float& sm,
+                                            float& q, float& x, float& sr, float& ey) {
+  sm = 0.f, q = 0.f, x = 0.f, sr = 0.f, ey = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float d = vh[j] - nm;
+    const float e = fast_exp2(d);
+    if (EXCL) {
+      sm += j == ry ? 0.f : e;
+      ey = j == ry ? e : ey;
+    } else {
+      sm += e;
+    }
+    q = fmaf(e, d, q);
+    x = fmaf(e, vh[j] - wh[j], x);
+    sr += fast_exp2(wh[j] - nr);
+  }
+}
+
 // KL-to-ref forward epilogue: as epi_lse for z (accumulator 0) plus, for z_ref (accumulator
 // 1 = TMEM column + BN), the ref online (max, sum) and the cross term
 // x = sum_j 2^(u_j - mx) (u_j - ur_j), u = z log2(e): after the merge,
@@ -638,6 +661,8 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
 // in train_loop's own call, scheduler.py:530-542) it also writes q = 2^(u - R) per 64-column
 // slab and the slab references R exactly as epi_lse does, so the backward is the stored mode's
 // and the call executes one extra forward GEMM (z_ref) instead of a forward plus a recompute.
+// As in epi_lse, s leaves the sampled token out (run_ey carries it for rebasing q) and a
+// partial holding the token sets the sign bit of its s.
 template <int BN>
 __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams& ep, const CUtensorMap* tmC,
                                             uint8_t* stage2, int& ebuf, int m0, int n0, int n_blk, int row, int lane,
@@ -649,7 +674,7 @@ __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams
   const int row0 = m0 + quarter * 32;
   const bool warp_rows = row0 < sh.M;  // warp-uniform
   const bool store = ep.probs != nullptr;
-  float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_x = 0.f;
+  float run_m = -1e30f, run_s = 0.f, run_q = 0.f, run_x = 0.f, run_ey = 0.f;
   float ref_m = -1e30f, ref_s = 0.f;
   float refs[BN / 64];
 #pragma unroll 1
@@ -689,22 +714,18 @@ __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams
       }
       const float nm = fmaxf(run_m, cm);
       const float a = fast_exp2(run_m - nm);
-      run_q = a * (run_q + (run_m - nm) * run_s);
+      run_q = a * (run_q + (run_m - nm) * (run_s + run_ey));  // rebased with the full sum
       run_s = a * run_s;
+      run_ey = a * run_ey;
       run_x = a * run_x;
       const float nr = fmaxf(ref_m, cr);
       ref_s *= fast_exp2(ref_m - nr);
-      float sm = 0.f, q = 0.f, x = 0.f, sr = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float d = vh[j] - nm;
-        const float e = fast_exp2(d);
-        sm += e;
-        q = fmaf(e, d, q);
-        x = fmaf(e, vh[j] - wh[j], x);
-        sr += fast_exp2(wh[j] - nr);
-      }
+      const int ry = rel - 32 * hh;
+      float sm, q, x, sr, eyc;
+      if (__any_sync(0xffffffffu, (unsigned)ry < 32u)) ref_chunk32<true>(vh, wh, nm, nr, ry, sm, q, x, sr, eyc);
+      else ref_chunk32<false>(vh, wh, nm, nr, -1, sm, q, x, sr, eyc);
       run_s += sm;
+      run_ey += eyc;
       run_q += q;
       run_x += x;
       run_m = nm;
@@ -726,7 +747,7 @@ __device__ __forceinline__ void epi_lse_ref(const GemmShape& sh, const EpiParams
   if (row_ok) {
     float* p = ep.part + (int64_t)n_blk * 6 * sh.M + m;
     p[0] = run_m;
-    p[sh.M] = run_s;
+    p[sh.M] = run_ey > 0.f ? -run_s : run_s;
     p[2 * (int64_t)sh.M] = run_q;
     p[3 * (int64_t)sh.M] = ref_m;
     p[4 * (int64_t)sh.M] = ref_s;

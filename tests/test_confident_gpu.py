@@ -170,7 +170,8 @@ def test_confident_lp_keeps_one_minus_py(cuda_device, case, run):
     K1's slab sums leave the sampled token out and K2 takes lp = log1p(-S_{v != y} / S) (with
     z_y - lse, lse's absolute rounding ~1e-6 would swamp 1 - p_y ~ 1e-6). Checked for the
     forward (K2) and the lp recording (icepop_logprob), at K1 run lengths 1 / 2 / 16 (the
-    token's partial is flagged and merged at every level: slab, run, column half, K2), against
+    token's partial is flagged and merged at every level: slab, run, column half, K2), and for
+    the KL-to-ref forward (the reference loop's call, gamma = 0; dual-accumulator epilogue), against
     fp64 on the same bf16 inputs, down to 1 - p_y ~ 4e-13. Bound: median relative error of
     1 - p_y <= 2e-5 and 99th percentile <= 2e-4 on rows with p_y > 0.9 (fp32 logits from a bf16
     GEMM; measured 3.4e-6 / 1.9e-5, profiles/r02_confident_lp.log)."""
@@ -196,7 +197,10 @@ def test_confident_lp_keeps_one_minus_py(cuda_device, case, run):
         lp_rec, _, _ = icepop_logprob(H, W, b.tokens, layout=c["layout"])
     finally:
         _lib.check(lib.icepop_set_k1_run(0))
-    for name, lp in (("forward", f.lp_cur), ("recording", lp_rec)):
+    # the reference loop's own call (ref passed, gamma = 0): the dual-accumulator epilogue
+    W_ref = (W.float() * 1.01).to(torch.bfloat16)
+    fr = icepop_fwd(H, W, b, IcePopConfig(), layout=c["layout"], weight_ref=W_ref, store_probs=False)
+    for name, lp in (("forward", f.lp_cur), ("recording", lp_rec), ("forward with ref", fr.lp_cur)):
         g = -np.expm1(lp.cpu().numpy())
         rel = np.abs(g - q)[conf] / q[conf]
         med, p99 = float(np.median(rel)), float(np.quantile(rel, 0.99))
