@@ -387,6 +387,9 @@ int64_t k1_parts(int64_t n_tokens, int64_t V, int64_t d) {
   return (n_t + r - 1) / r;
 }
 
+// Vocabulary columns per K1 partial: the sampled token y's statistics are in partial y / this.
+int32_t k1_part_cols(int64_t n_tokens, int64_t V, int64_t d) { return k1_bn() * k1_run_len(n_tokens, V, d); }
+
 // A 512-wide tile does the work of two 256-wide ones ~5% cheaper (fewer operand bytes per
 // FLOP) but halves the tile count. On a small output (C1's dH: 32 wide tiles for 74 CTA
 // pairs) that leaves pairs idle, so the long-K GEMMs take wide tiles only when their wave
@@ -776,7 +779,7 @@ int run_k2(const icepop_shape* shape, const icepop_config* cfg, const icepop_bat
   if (!ref) a.kl_coeff = 0.0;  // no reference policy: kl_t = 0 (objective.py:254)
   a.part = w.part;
   a.n_parts = (int32_t)(ref ? (V + bn_of(EPI_LSE_REF) - 1) / bn_of(EPI_LSE_REF) : k1_parts(N, V, d));
-  a.part_rows = ref ? 6 : 3;
+  a.part_cols = ref ? bn_of(EPI_LSE_REF) : k1_part_cols(N, V, d);
   a.kl_f = ref ? out->kl : nullptr;
   a.lse_ref_f = ref ? out->lse_ref : nullptr;
   a.kl_w_f = ref ? out->kl_w : nullptr;
@@ -790,7 +793,8 @@ int run_k2(const icepop_shape* shape, const icepop_config* cfg, const icepop_bat
   a.coeff_f = out->coeff;
   a.block_stats = w.block_stats;
   const int grid = token_grid(N);
-  k2_icepop_tokens<0><<<grid, TOK_THREADS, 0, st>>>(a);
+  if (ref) k2_icepop_tokens<3><<<grid, TOK_THREADS, 0, st>>>(a);
+  else k2_icepop_tokens<0><<<grid, TOK_THREADS, 0, st>>>(a);
   ICP_CUDA(cudaGetLastError());
   k_finalize_stats<<<1, 32 * ICEPOP_NSTATS, 0, st>>>(w.block_stats, grid, out->stats);
   k_merge_err<<<1, 1, 0, st>>>(w.err, out->stats);
@@ -955,30 +959,17 @@ int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, con
   return ICEPOP_OK;
 }
 
-__global__ void k_logprob_finish(const float* part, int n_parts, const float* ztok, int64_t n, float* lse,
-                                 double* lp, float* entropy) {
+__global__ void k_logprob_finish(const float* part, int n_parts, int32_t part_cols, const int32_t* tokens,
+                                 const float* ztok, int64_t n, float* lse, double* lp, float* entropy) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const float zy = ztok[t], uy = zy * LOG2E_TOK;
-    float M = -1e30f, S = 0.f, Q = 0.f, Ey = 0.f;
-    for (int j = 0; j < n_parts; ++j) {  // one pass with a running maximum (k2_icepop_tokens)
-      const float* p = part + (int64_t)j * 3 * n + t;
-      const float mj = p[0], sr = p[n], sj = fabsf(sr), nm = fmaxf(M, mj);
-      const float eyj = signbit(sr) ? exp2f(uy - mj) : 0.f;  // the partial holding the token
-      const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
-      Q = fmaf(ca, fmaf(M - nm, S + Ey, Q), cb * fmaf(mj - nm, sj + eyj, p[2 * n]));
-      S = fmaf(ca, S, cb * sj);
-      Ey = fmaf(ca, Ey, cb * eyj);
-      M = nm;
-    }
-    // the partials leave the sampled token out (k2_icepop_tokens): add it back, log1p when confident
-    const float ey = exp2f(uy - M);
-    const float Sx = S;
-    S += ey;
-    const float l2s = log2f(S);
-    const float l = (M + l2s) * LN2_F;
+    PartMerge pm;  // one pass with a running maximum (k2_icepop_tokens)
+    merge_partials<3>(pm, part, n_parts, n, t);
+    float l, e;
+    double lpv;
+    pm.finish(ztok[t], part[token_part(tokens[t], part_cols, n_parts) * 3 * n + t], l, lpv, e);
     if (lse) lse[t] = l;
-    if (lp) lp[t] = ey > 0.5f * S ? (double)log1pf(-Sx / S) : (double)(zy - l);
-    if (entropy) entropy[t] = (l2s - Q / S) * LN2_F;
+    if (lp) lp[t] = lpv;
+    if (entropy) entropy[t] = e;
   }
 }
 
@@ -1002,8 +993,8 @@ int icepop_logprob_bf16(const icepop_shape* shape, double temperature, const voi
   ep.ztok = w.ztok;
   const bool b_mn = shape->weight_layout == ICEPOP_W_DV;
   ICP_TRY(run_umma(EPI_LSE, hidden, d, false, weight, b_mn ? V : d, b_mn, N, V, d, ep, st));
-  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)k1_parts(N, V, d), w.ztok, N, lse, lp,
-                                                          entropy);
+  k_logprob_finish<<<token_grid(N), TOK_THREADS, 0, st>>>(w.part, (int)k1_parts(N, V, d), k1_part_cols(N, V, d),
+                                                          tokens, w.ztok, N, lse, lp, entropy);
   ICP_CUDA(cudaGetLastError());
   return ICEPOP_OK;
 }
@@ -1729,6 +1720,7 @@ static int preload_kernels() {
   ICP_TRY(touch(k2_icepop_tokens<0>));
   ICP_TRY(touch(k2_icepop_tokens<1>));
   ICP_TRY(touch(k2_icepop_tokens<2>));
+  ICP_TRY(touch(k2_icepop_tokens<3>));
   ICP_TRY(touch(k_finalize_stats));
   ICP_TRY(touch(k_merge_err));
   ICP_TRY(touch(k_check_tokens));

@@ -84,9 +84,9 @@ struct TokenArgs {
   const double* adv;
   const double* calib_in;  // caller-computed c_t, or null (exp on the device)
   // bf16 mode inputs: K1 partials
-  const float* part;  // [n_parts][part_rows][n_tokens]
+  const float* part;  // [n_parts][3 or 6 rows][n_tokens] (MODE 0 / MODE 3)
   int32_t n_parts;
-  int32_t part_rows;  // 3, or 6 with the KL-to-ref terms (epi_lse_ref)
+  int32_t part_cols;  // vocabulary columns per partial (the token's partial is y / part_cols)
   const float* ztok;  // [n_tokens]
   // f64 mode inputs (already computed per token by the f64 row kernel)
   const double* lp_cur_in;
@@ -107,7 +107,7 @@ struct TokenArgs {
   double* surrogate;
   float* coeff_f;
   double* coeff_d;
-  float* kl_f;       // KL-to-ref outputs (part_rows == 6)
+  float* kl_f;       // KL-to-ref outputs (MODE 3)
   float* lse_ref_f;
   float* kl_w_f;     // w_t * gamma / T (backward coefficient of the KL gradient)
   double* block_stats;  // [gridDim.x][ICEPOP_NSTATS] (required)
@@ -164,66 +164,109 @@ __device__ __forceinline__ void block_reduce_stats(double (&st)[ICEPOP_NSTATS], 
   }
 }
 
-// MODE 0: bf16 path (merge K1 partials), MODE 1: fp64 path (lp_cur/entropy/kl given),
-// MODE 2: on-policy (theta == theta_old): lp_cur = lp_train_old, lse/entropy recorded.
+// The partial holding token y (clamped: an out-of-range token is reported by k_check_tokens).
+__device__ __forceinline__ int64_t token_part(int32_t y, int32_t part_cols, int32_t n_parts) {
+  return (int64_t)min(max(y, 0) / part_cols, n_parts - 1);
+}
+
+// Running merge of K1's split-V partials for one token (log2 units): (M, S, Q) over the z
+// partials (S leaves the sampled token out: K1 flags the partial holding it with the sign bit
+// of its s, which the merge drops), and for R == 6 the ref (Mr, Sr) and the cross term X.
+struct PartMerge {
+  float M = -1e30f, S = 0.f, Q = 0.f, Mr = -1e30f, Sr = 0.f, X = 0.f;
+  template <int R>
+  __device__ __forceinline__ void add(const float (&v)[R]) {
+    const float mj = v[0], sj = fabsf(v[1]), qj = v[2];
+    const float nm = fmaxf(M, mj);
+    const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
+    // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S before the rescale. With S
+    // leaving the token out, each rebase from the token's partial on misses (M_k - nm_k)
+    // 2^(u_y - nm_k); rescaled to the final M these telescope to (m_y - M) 2^(u_y - M), m_y
+    // that partial's maximum, added once in finish() (tracking the flag in this loop measured
+    // 1.5x slower: the partial is located from the token index instead)
+    Q = fmaf(ca, fmaf(M - nm, S, Q), cb * fmaf(mj - nm, sj, qj));
+    S = fmaf(ca, S, cb * sj);
+    if constexpr (R == 6) {
+      X = fmaf(ca, X, cb * v[5]);
+      const float nr = fmaxf(Mr, v[3]);
+      Sr = fmaf(exp2f(Mr - nr), Sr, exp2f(v[3] - nr) * v[4]);
+      Mr = nr;
+    }
+    M = nm;
+  }
+  // After the last partial, with zy = z_y / T (natural units) and my the maximum of the
+  // partial holding the token: the partials leave the sampled token out of S, so add
+  // 2^(u_y - M) back (and, to Q, its share of the rebasing) for the log-sum-exp and entropy,
+  // and take a confident token's log-prob as log1p(-S_{v != y} / S), which keeps 1 - p_y (the
+  // backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is to 1 (z_y - lse
+  // would keep only lse's absolute precision, ~1e-6 for |z| ~ 10). Returns the full sum S.
+  __device__ __forceinline__ float finish(float zy, float my, float& lse, double& lp, float& entropy) {
+    const float ey = exp2f(zy * LOG2E_TOK - M);
+    const float q = fmaf(my - M, ey, Q);
+    const float s = S + ey;
+    const float l2s = log2f(s);
+    lse = (M + l2s) * LN2_F;
+    entropy = (l2s - q / s) * LN2_F;
+    lp = ey > 0.5f * s ? (double)log1pf(-S / s) : (double)(zy - lse);
+    return s;
+  }
+};
+
+// One pass over a token's partials with a running maximum: each partial is read exactly once
+// (a max pass first would re-read the maxima from DRAM: they exceed L2 at C2's size). Loads
+// are issued UNROLL partials ahead of the dependent merge chain, for memory-level parallelism.
+template <int R>
+__device__ __forceinline__ void merge_partials(PartMerge& pm, const float* __restrict__ part, int n_parts, int64_t n,
+                                               int64_t t) {
+  constexpr int UNROLL = 4;
+  const float* p = part + t;
+  const int64_t stride = (int64_t)R * n;
+  int j = 0;
+  for (; j + UNROLL <= n_parts; j += UNROLL, p += UNROLL * stride) {
+    float v[UNROLL][R];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[u][r] = __ldg(p + u * stride + r * n);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) pm.add<R>(v[u]);
+  }
+  for (; j < n_parts; ++j, p += stride) {
+    float v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = __ldg(p + r * n);
+    pm.add<R>(v);
+  }
+}
+
+// MODE 0: bf16 path (merge K1's partials, 3 rows each), MODE 3: the same with the KL-to-ref
+// dual partials (6 rows), MODE 1: fp64 path (lp_cur/entropy/kl given), MODE 2: on-policy
+// (theta == theta_old): lp_cur = lp_train_old, lse/entropy recorded.
 template <int MODE>
 __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs a) {
+  constexpr bool MERGE = MODE == 0 || MODE == 3;
+  constexpr int R = MODE == 3 ? 6 : 3;
   double st[ICEPOP_NSTATS] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned err = 0;
   const double clip_lo = 1.0 - a.clip_eps, clip_hi = 1.0 + a.clip_eps;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.n_tokens;
        t += (int64_t)gridDim.x * blockDim.x) {
     double lp_cur, ent, kl = 0.0;
-    if (MODE == 0) {
-      // merge split-V partials (log2 units) -> lse, entropy; lp = z[y] - lse. One pass with a
-      // running maximum: each partial is read exactly once (a max pass first would re-read the
-      // partials' maxima from DRAM: they exceed L2 at C2's size)
-      const int64_t R = a.part_rows;
-      const float uy = a.ztok[t] * LOG2E_TOK;
-      float M = -1e30f, Mr = -1e30f;
-      float S = 0.f, Q = 0.f, Sr = 0.f, X = 0.f, Ey = 0.f;
-      for (int j = 0; j < a.n_parts; ++j) {
-        const float* p = a.part + (int64_t)j * R * a.n_tokens + t;
-        const float mj = p[0], sr = p[a.n_tokens], qj = p[2 * a.n_tokens];
-        // the partial holding the sampled token flags it in the sign bit of its s (which leaves
-        // the token out); its 2^(u_y - mj) joins the full sum Q is rebased with
-        const float sj = fabsf(sr);
-        const float eyj = signbit(sr) ? exp2f(uy - mj) : 0.f;
-        const float nm = fmaxf(M, mj);
-        const float ca = exp2f(M - nm), cb = exp2f(mj - nm);
-        // Q is sum 2^(u - M) (u - M): rebasing to nm adds (M - nm) S_full before the rescale
-        Q = fmaf(ca, fmaf(M - nm, S + Ey, Q), cb * fmaf(mj - nm, sj + eyj, qj));
-        S = fmaf(ca, S, cb * sj);
-        Ey = fmaf(ca, Ey, cb * eyj);
-        if (R == 6) {
-          X = fmaf(ca, X, cb * p[5 * a.n_tokens]);
-          const float mr = p[3 * a.n_tokens];
-          const float nr = fmaxf(Mr, mr);
-          Sr = fmaf(exp2f(Mr - nr), Sr, exp2f(mr - nr) * p[4 * a.n_tokens]);
-          Mr = nr;
-        }
-        M = nm;
-      }
-      // K1's partials leave the sampled token out of S: add 2^(u_y - M) back for the log-sum-exp,
-      // and take a confident token's log-prob as log1p(-S_{v != y} / S), which keeps 1 - p_y (the
-      // backward's -expm1(lp_cur)) to fp32 relative precision however close p_y is to 1;
-      // z_y - lse would leave only the absolute precision of lse (~1e-6 for |z| ~ 10)
-      const float zy = a.ztok[t];
-      const float ey = exp2f(uy - M);
-      const float Sx = S;
-      S += ey;
-      const float l2s = log2f(S);
-      const float lse = (M + l2s) * LN2_F;
-      const float entf = (l2s - Q / S) * LN2_F;
-      lp_cur = ey > 0.5f * S ? (double)log1pf(-Sx / S) : (double)(zy - lse);
+    if (MERGE) {
+      // merge split-V partials -> lse, entropy, lp_cur
+      PartMerge pm;
+      merge_partials<R>(pm, a.part, a.n_parts, a.n_tokens, t);
+      const float my = a.part[token_part(a.tokens[t], a.part_cols, a.n_parts) * R * a.n_tokens + t];
+      float lse, entf;
+      const float S = pm.finish(a.ztok[t], my, lse, lp_cur, entf);
       ent = (double)entf;
       if (a.lse_f) a.lse_f[t] = lse;
       if (a.entropy_f) a.entropy_f[t] = entf;
       if (!isfinite(lse) || !isfinite(entf) || !isfinite(a.ztok[t])) err |= ICEPOP_ERR_NONFINITE;
       if (R == 6) {
         // kl = sum_v p (logp - logp_ref) = sum_v p (z - z_ref) - lse + lse_ref  (objective.py:257-258)
-        const float lse_r = (Mr + log2f(Sr)) * LN2_F;
-        const float klf = (X / S) * LN2_F - lse + lse_r;
+        const float lse_r = (pm.Mr + log2f(pm.Sr)) * LN2_F;
+        const float klf = (pm.X / S) * LN2_F - lse + lse_r;
         kl = (double)klf;
         if (a.kl_f) a.kl_f[t] = klf;
         if (a.lse_ref_f) a.lse_ref_f[t] = lse_r;
