@@ -623,11 +623,14 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     gw = torch.zeros((V, d), dtype=torch.float32, device=dev)
     timed("K4_dhidden", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), W.data_ptr(), gh.data_ptr(), nc, d, V,
                                                                 0, 1, 0, 0, s)), 2.0 * nc * d * V)
-    # as in the step: a single (or first) chunk overwrites dW; recompute-mode later chunks accumulate
+    # as in the step: a single (or first) chunk overwrites dW; recompute-mode later chunks accumulate.
+    # The row-scaled stored-probabilities backward feeds K5 the scaled hidden transposed (K-major,
+    # written by its prep kernel); the recompute mode reads H as it is (MN-major)
     k5_acc = 0 if (sp or nc >= N) else 1
-    timed("K5_dweight", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, nc,
-                                                                1, 1, 1, k5_acc, s)), 2.0 * nc * d * V)
-    del dz, gh, gw
+    hk = H[:nc].t().contiguous() if sp else H
+    timed("K5_dweight", lambda: _lib.check(lib.icepop_gemm_bf16(dz.data_ptr(), hk.data_ptr(), gw.data_ptr(), V, d, nc,
+                                                                1, 0 if sp else 1, 1, k5_acc, s)), 2.0 * nc * d * V)
+    del dz, gh, gw, hk
     holder.clear()
     return res
 

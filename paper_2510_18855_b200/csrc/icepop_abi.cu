@@ -683,7 +683,8 @@ struct SparseWorkspace {
   float* rscale;    // [n] s_t
   float* ohc;       // [n] c_t
   uint8_t* exc;     // [n] exception rows (dZ formed in place)
-  __nv_bfloat16* hid_s;  // [n, d] s_t H[t]
+  __nv_bfloat16* hid_t;  // [d, ldt] s_t H[t] transposed (k_sp_prep), ldt = n rounded up to 64
+  int64_t ldt;
   int32_t* keys;    // [n] tokens sorted
   int32_t* iota;    // [n]
   int32_t* vals;    // [n] token indices sorted by token
@@ -711,7 +712,8 @@ SparseWorkspace carve_sparse(const icepop_shape* s, void* base) {
   w.rscale = c.take<float>((size_t)n);
   w.ohc = c.take<float>((size_t)n);
   w.exc = c.take<uint8_t>((size_t)n);
-  w.hid_s = c.take<__nv_bfloat16>((size_t)n * s->hidden);
+  w.ldt = (n + 63) / 64 * 64;
+  w.hid_t = c.take<__nv_bfloat16>((size_t)w.ldt * s->hidden);
   w.keys = c.take<int32_t>((size_t)n);
   w.iota = c.take<int32_t>((size_t)n);
   w.vals = c.take<int32_t>((size_t)n);
@@ -1133,10 +1135,11 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       }
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
       if (scaled) {
-        k_sp_prep<<<grid, SPP_THREADS, 0, st>>>(sv.tile_max, tm_ld, (int32_t)((V + 63) / 64), lse, coeff,
-                                                (float)grad_scale, sv.lp_cur, tokens, dzb, V,
-                                                reinterpret_cast<const uint4*>(hidden), d / 8, sw.rscale, sw.ohc,
-                                                sw.exc, reinterpret_cast<uint4*>(sw.hid_s), nc);
+        const int pgrid = (int)std::min<int64_t>((nc + SPP_TILE - 1) / SPP_TILE, (int64_t)num_sms() * 8);
+        k_sp_prep<<<pgrid, SPP_THREADS, 0, st>>>(sv.tile_max, tm_ld, (int32_t)((V + 63) / 64), lse, coeff,
+                                                 (float)grad_scale, sv.lp_cur, tokens, dzb, V,
+                                                 reinterpret_cast<const uint4*>(hidden), d / 8, sw.rscale, sw.ohc,
+                                                 sw.exc, reinterpret_cast<uint4*>(sw.hid_t), sw.ldt, nc);
       }
       k_dz_probs<<<grid, DZP_THREADS, 0, st>>>(reinterpret_cast<uint4*>(dzb), sv.tile_max, tm_ld, lse, coeff,
                                                (float)grad_scale, tokens, nc, V / 8, sv.lp_cur,
@@ -1218,7 +1221,6 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
         ew.out = nullptr;
         ext_k.dim = skip ? 2 : 0;
       }
-      if (scaled) h = sw.hid_s;
       // an empty K extent must still store (zeros, or the local partial to the peers) when
       // nothing else writes the result
       const bool keep_empty = ((skip || sparse) && !ew.accumulate) || (rs && last);
@@ -1229,12 +1231,17 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       }
       const void* ovec = rs && last ? (const void*)rs->slots[0] : (const void*)grad_weight;
       ew.vec_ok = ((reinterpret_cast<uintptr_t>(ovec) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
+      // H (MN-major: [nc, d]), or the row-scaled H' transposed by k_sp_prep (K-major: [d, ldt])
+      const void* hk = scaled ? (const void*)sw.hid_t : h;
+      const int64_t ldh = scaled ? sw.ldt : d;
       if (dv) {
-        ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc] (MN-major), B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, h, d, true, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
+        ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc], B = dZ [N=V, K=nc] (MN-major)
+        ICP_TRY(run_umma(EPI_STORE, hk, ldh, !scaled, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, keep_empty,
+                         sp5));
       } else {
-        ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, h, d, true, V, d, nc, ew, st, ext_k, nullptr, keep_empty, sp5));
+        ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc]
+        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, hk, ldh, !scaled, V, d, nc, ew, st, ext_k, nullptr, keep_empty,
+                         sp5));
       }
       // the one-hot part after K5 stored dW: into grad_weight, or (fused reduce-scatter) straight
       // into the owners' slots, sparse read-modify-writes of the rows the batch's tokens touch

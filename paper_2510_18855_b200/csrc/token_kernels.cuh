@@ -772,8 +772,14 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const int32_t* __res
 // it as c - c q_y 2^(-lse2) instead cancels: the bf16 q_y carries 2^-9 p_y of error against a
 // result of size 1 - p_y (12% on a token with p_y = 0.98, the common case in RL batches).
 // Exception rows get their dZ in place (k_dz_probs with `only`) and enter the GEMMs unscaled
-// (s = 1, c = 0). Writes s, c (1 - p_y), the exception flag and H'[t] = bf16(s H[t]).
-constexpr int SPP_THREADS = 128;
+// (s = 1, c = 0). Writes s, c (1 - p_y), the exception flag and H' = bf16(s H) TRANSPOSED,
+// hid_t[k][t] (d rows of ldt tokens; tokens >= n are zero): K5 then reads H' K-major. With
+// both of K5's operands MN-major (q^T and H') the long-K GEMM ran 1-2% slower
+// (profiles/major_ab.py). One block per 64-token tile: warps find the rows' scales, then the
+// tile's H rows pass through shared memory 64 hidden columns at a time.
+constexpr int SPP_THREADS = 256;
+constexpr int SPP_TILE = 64;
+constexpr int SPP_LD = SPP_TILE + 2;  // bf16 elements per smem row: 33 words, conflict-free stores
 __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict__ tile_max, int32_t tm_ld,
                                                          int32_t n_slabs, const float* __restrict__ lse,
                                                          const float* __restrict__ coeff, float gs,
@@ -782,32 +788,64 @@ __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict
                                                          __nv_bfloat16* __restrict__ probs, int64_t vocab,
                                                          const uint4* __restrict__ hid, int64_t d8,
                                                          float* __restrict__ rscale, float* __restrict__ ohc,
-                                                         uint8_t* __restrict__ exc, uint4* __restrict__ hid_s, int64_t n) {
-  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
-    const float* tm = tile_max + t * tm_ld;
-    int any = 0;
-    for (int j = threadIdx.x; j < n_slabs; j += SPP_THREADS) any |= tm[j] != 0.f;
-    const bool ex = __syncthreads_or(any) != 0;
-    const float cf = coeff[t] * gs;
-    const float sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
-    if (threadIdx.x == 0) {
-      rscale[t] = sc;
-      ohc[t] = (ex || cf == 0.f) ? 0.f : (float)((double)cf * -expm1(lp_cur[t]));
-      exc[t] = ex ? 1 : 0;
-      if (!ex) probs[t * vocab + tokens[t]] = __ushort_as_bfloat16((unsigned short)0);
-    }
-    const uint4* src = hid + t * d8;
-    uint4* dst = hid_s + t * d8;
-    for (int64_t k = threadIdx.x; k < d8; k += SPP_THREADS) {
-      uint4 x = src[k];
-      uint32_t* w = reinterpret_cast<uint32_t*>(&x);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
-        const __nv_bfloat162 o = __floats2bfloat162_rn(h.x * sc, h.y * sc);
-        w[i] = *reinterpret_cast<const uint32_t*>(&o);
+                                                         uint8_t* __restrict__ exc, uint4* __restrict__ hid_t,
+                                                         int64_t ldt, int64_t n) {
+  __shared__ float s_sc[SPP_TILE];
+  __shared__ uint32_t tile[SPP_TILE * SPP_LD / 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = (n + SPP_TILE - 1) / SPP_TILE;
+  for (int64_t tt = blockIdx.x; tt < n_tiles; tt += gridDim.x) {
+    const int64_t t0 = tt * SPP_TILE;
+    for (int r = warp; r < SPP_TILE; r += SPP_THREADS / 32) {
+      const int64_t t = t0 + r;
+      float sc = 0.f;
+      if (t < n) {
+        const float* tm = tile_max + t * tm_ld;
+        bool any = false;
+        for (int j = lane; j < n_slabs; j += 32) any |= tm[j] != 0.f;
+        const bool ex = __any_sync(0xffffffffu, any);
+        const float cf = coeff[t] * gs;
+        sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
+        if (lane == 0) {
+          rscale[t] = sc;
+          ohc[t] = (ex || cf == 0.f) ? 0.f : (float)((double)cf * -expm1(lp_cur[t]));
+          exc[t] = ex ? 1 : 0;
+          if (!ex) probs[t * vocab + tokens[t]] = __ushort_as_bfloat16((unsigned short)0);
+        }
       }
-      dst[k] = x;
+      if (lane == 0) s_sc[r] = sc;
+    }
+    __syncthreads();
+    const uint16_t* th = reinterpret_cast<const uint16_t*>(tile);
+    for (int64_t c8 = 0; c8 < d8; c8 += SPP_TILE / 8) {  // 64 hidden columns
+      // load + scale: thread -> (row, 8-column group), stored as four 32-bit words
+      for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
+        const int row = i >> 3, q = i & 7;
+        const int64_t t = t0 + row;
+        uint4 x = make_uint4(0u, 0u, 0u, 0u);
+        if (t < n && c8 + q < d8) x = hid[t * d8 + c8 + q];
+        uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+        const float sc = s_sc[row];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+          const __nv_bfloat162 o = __floats2bfloat162_rn(h.x * sc, h.y * sc);
+          tile[row * (SPP_LD / 2) + 4 * q + k] = *reinterpret_cast<const uint32_t*>(&o);
+        }
+      }
+      __syncthreads();
+      // transposed store: thread -> (hidden column, 8-token group), one 16-byte store
+      for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
+        const int c = i >> 3, q = i & 7;
+        if (c8 * 8 + c < d8 * 8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            w[k] = (uint32_t)th[(8 * q + 2 * k) * SPP_LD + c] | ((uint32_t)th[(8 * q + 2 * k + 1) * SPP_LD + c] << 16);
+          hid_t[((c8 * 8 + c) * ldt + t0) / 8 + q] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      __syncthreads();
     }
   }
 }
