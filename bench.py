@@ -233,7 +233,7 @@ def run_ours(args):
         dist.all_reduce(agree, op=dist.ReduceOp.MIN)
         sp = bool(agree[0].item())
         sp_chunk = 0 if sp else int(agree[1].item())
-    rows = _dz_chunk_bytes(dev) // (2 * V)
+    rows = _dz_chunk_bytes(dev) // (2 * (V + d))
     chunk = N if (sp or rows >= N) else max(128, rows // 128 * 128)
     if sp_chunk:
         chunk = sp_chunk
@@ -241,13 +241,13 @@ def run_ours(args):
     # fwd: K0, token check, K1, K2, finalize, err-merge; bwd: stored probabilities -> block
     # flags + lists, row prep, exception-row dZ, K4, K5, iota + one-hot scatter (CUB's radix
     # sort kernels are library code, not counted); per token chunk when chunked; recompute ->
-    # 4 compaction kernels + (K3, K4, K5) per dZ chunk
+    # 4 compaction kernels + (K3, K4, hidden transpose, K5) per dZ chunk
     if sp:
         launches_per_step = 6 + 8
     elif sp_chunk:
         launches_per_step = n_chunks * (6 + 8)
     else:
-        launches_per_step = 6 + 4 + 3 * n_chunks
+        launches_per_step = 6 + 4 + 4 * n_chunks
     dz_mode = "stored-probabilities" if sp else (
         f"stored-probabilities in {n_chunks} token chunks" if sp_chunk else "recompute")
 

@@ -623,6 +623,8 @@ struct BF16Workspace {
   float* coeff_act;
   double* lp_act;
   __nv_bfloat16* dz;
+  __nv_bfloat16* hid_t;  // [d, ldt] the dZ chunk's hidden rows transposed (K5's K-major operand)
+  int64_t ldt;
   int64_t chunk;
   size_t bytes;
 };
@@ -668,6 +670,10 @@ BF16Workspace carve_bf16(const icepop_shape* s, void* base, int64_t chunk, bool 
     w.lp_act = c.take<double>((size_t)n);
   }
   w.dz = c.take<__nv_bfloat16>((size_t)chunk * (size_t)s->vocab);
+  if (bwd && chunk > 0) {
+    w.ldt = (chunk + 63) / 64 * 64;
+    w.hid_t = c.take<__nv_bfloat16>((size_t)w.ldt * s->hidden);
+  }
   w.chunk = chunk;
   w.bytes = align_up(c.off, 256);
   return w;
@@ -1066,7 +1072,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
     if (!workspace || workspace_bytes < need_min)
       return fail(ICEPOP_EINVAL, "backward workspace too small: need >= %zu bytes", need_min);
     const size_t fixed = carve_bf16(shape, nullptr, 0, true).bytes;
-    chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)V * 2));
+    chunk = (int64_t)((workspace_bytes - fixed) / ((size_t)(V + d) * 2));  // dZ row + transposed H row
     if (chunk >= N) {
       chunk = N;
     } else {
@@ -1231,16 +1237,25 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       }
       const void* ovec = rs && last ? (const void*)rs->slots[0] : (const void*)grad_weight;
       ew.vec_ok = ((reinterpret_cast<uintptr_t>(ovec) & 15u) == 0) && (d % 8 == 0) && (V % 8 == 0);
-      // H (MN-major: [nc, d]), or the row-scaled H' transposed by k_sp_prep (K-major: [d, ldt])
-      const void* hk = scaled ? (const void*)sw.hid_t : h;
-      const int64_t ldh = scaled ? sw.ldt : d;
+      // K5's hidden operand K-major (one MN-major operand, not two: profiles/major_ab.py): the
+      // row-scaled H' transposed by k_sp_prep, or this chunk's rows transposed here (the
+      // recompute backward); H itself (MN-major, [nc, d]) only without either workspace
+      if (!scaled && w.hid_t) {
+        const int tg = (int)std::min<int64_t>((nc + SPP_TILE - 1) / SPP_TILE, (int64_t)num_sms() * 8);
+        k_transpose_rows<<<tg, SPP_THREADS, 0, st>>>(reinterpret_cast<const uint4*>(h), d / 8,
+                                                     reinterpret_cast<uint4*>(w.hid_t), w.ldt, nc);
+        ICP_CUDA(cudaGetLastError());
+      }
+      const bool h_kmajor = scaled || w.hid_t != nullptr;
+      const void* hk = scaled ? (const void*)sw.hid_t : (w.hid_t ? (const void*)w.hid_t : (const void*)h);
+      const int64_t ldh = scaled ? sw.ldt : (w.hid_t ? w.ldt : d);
       if (dv) {
         ew.ldo = V;  // dW[d,V]: A = H chunk viewed [M=d, K=nc], B = dZ [N=V, K=nc] (MN-major)
-        ICP_TRY(run_umma(EPI_STORE, hk, ldh, !scaled, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, keep_empty,
+        ICP_TRY(run_umma(EPI_STORE, hk, ldh, !h_kmajor, dzb, V, true, d, V, nc, ew, st, ext_k, nullptr, keep_empty,
                          sp5));
       } else {
         ew.ldo = d;  // dW[V,d]: A = dZ viewed [M=V, K=nc] (MN-major), B = H chunk [N=d, K=nc]
-        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, hk, ldh, !scaled, V, d, nc, ew, st, ext_k, nullptr, keep_empty,
+        ICP_TRY(run_umma(EPI_STORE, dzb, V, true, hk, ldh, !h_kmajor, V, d, nc, ew, st, ext_k, nullptr, keep_empty,
                          sp5));
       }
       // the one-hot part after K5 stored dW: into grad_weight, or (fused reduce-scatter) straight
@@ -1748,6 +1763,7 @@ static int preload_kernels() {
   ICP_TRY(touch(k_block_flags));
   ICP_TRY(touch(k_block_lists));
   ICP_TRY(touch(k_sp_prep));
+  ICP_TRY(touch(k_transpose_rows));
   ICP_TRY(touch(k_iota));
   ICP_TRY(touch(k_onehot_scatter));
   // CUB's radix sort (the one-hot scatter's order): run a small and a large sort once so that

@@ -780,6 +780,46 @@ __global__ void __launch_bounds__(BL_THREADS) k_block_lists(const int32_t* __res
 constexpr int SPP_THREADS = 256;
 constexpr int SPP_TILE = 64;
 constexpr int SPP_LD = SPP_TILE + 2;  // bf16 elements per smem row: 33 words, conflict-free stores
+// One 64-token tile of H (rows t0.., d8 16-byte groups per row), each row scaled by s_sc[row]
+// and rounded to bf16, written transposed: hid_t[k][t] (ldt tokens per row; rows >= n give zeros).
+// The rows pass through shared memory 64 hidden columns at a time: coalesced 128-byte reads of
+// H rows, 16-byte stores of 8 tokens of one hidden column.
+__device__ __forceinline__ void transpose_tile_scaled(const uint4* __restrict__ hid, int64_t d8, int64_t t0, int64_t n,
+                                                      const float* s_sc, uint32_t* tile, uint4* __restrict__ hid_t,
+                                                      int64_t ldt) {
+  const uint16_t* th = reinterpret_cast<const uint16_t*>(tile);
+  for (int64_t c8 = 0; c8 < d8; c8 += SPP_TILE / 8) {  // 64 hidden columns
+    // load + scale: thread -> (row, 8-column group), stored as four 32-bit words
+    for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
+      const int row = i >> 3, q = i & 7;
+      const int64_t t = t0 + row;
+      uint4 x = make_uint4(0u, 0u, 0u, 0u);
+      if (t < n && c8 + q < d8) x = hid[t * d8 + c8 + q];
+      uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+      const float sc = s_sc[row];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+        const __nv_bfloat162 o = __floats2bfloat162_rn(h.x * sc, h.y * sc);
+        tile[row * (SPP_LD / 2) + 4 * q + k] = *reinterpret_cast<const uint32_t*>(&o);
+      }
+    }
+    __syncthreads();
+    // transposed store: thread -> (hidden column, 8-token group), one 16-byte store
+    for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
+      const int c = i >> 3, q = i & 7;
+      if (c8 * 8 + c < d8 * 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = (uint32_t)th[(8 * q + 2 * k) * SPP_LD + c] | ((uint32_t)th[(8 * q + 2 * k + 1) * SPP_LD + c] << 16);
+        hid_t[((c8 * 8 + c) * ldt + t0) / 8 + q] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict__ tile_max, int32_t tm_ld,
                                                          int32_t n_slabs, const float* __restrict__ lse,
                                                          const float* __restrict__ coeff, float gs,
@@ -816,37 +856,20 @@ __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict
       if (lane == 0) s_sc[r] = sc;
     }
     __syncthreads();
-    const uint16_t* th = reinterpret_cast<const uint16_t*>(tile);
-    for (int64_t c8 = 0; c8 < d8; c8 += SPP_TILE / 8) {  // 64 hidden columns
-      // load + scale: thread -> (row, 8-column group), stored as four 32-bit words
-      for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
-        const int row = i >> 3, q = i & 7;
-        const int64_t t = t0 + row;
-        uint4 x = make_uint4(0u, 0u, 0u, 0u);
-        if (t < n && c8 + q < d8) x = hid[t * d8 + c8 + q];
-        uint32_t* w = reinterpret_cast<uint32_t*>(&x);
-        const float sc = s_sc[row];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
-          const __nv_bfloat162 o = __floats2bfloat162_rn(h.x * sc, h.y * sc);
-          tile[row * (SPP_LD / 2) + 4 * q + k] = *reinterpret_cast<const uint32_t*>(&o);
-        }
-      }
-      __syncthreads();
-      // transposed store: thread -> (hidden column, 8-token group), one 16-byte store
-      for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
-        const int c = i >> 3, q = i & 7;
-        if (c8 * 8 + c < d8 * 8) {
-          uint32_t w[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            w[k] = (uint32_t)th[(8 * q + 2 * k) * SPP_LD + c] | ((uint32_t)th[(8 * q + 2 * k + 1) * SPP_LD + c] << 16);
-          hid_t[((c8 * 8 + c) * ldt + t0) / 8 + q] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
-      __syncthreads();
-    }
+    transpose_tile_scaled(hid, d8, t0, n, s_sc, tile, hid_t, ldt);
+  }
+}
+
+// The plain H^T of K5's K-major operand in the recompute backward (rows of a dZ chunk, scale 1).
+__global__ void __launch_bounds__(SPP_THREADS) k_transpose_rows(const uint4* __restrict__ hid, int64_t d8,
+                                                                 uint4* __restrict__ hid_t, int64_t ldt, int64_t n) {
+  __shared__ float s_sc[SPP_TILE];
+  __shared__ uint32_t tile[SPP_TILE * SPP_LD / 2];
+  if (threadIdx.x < SPP_TILE) s_sc[threadIdx.x] = 1.f;
+  const int64_t n_tiles = (n + SPP_TILE - 1) / SPP_TILE;
+  for (int64_t tt = blockIdx.x; tt < n_tiles; tt += gridDim.x) {
+    __syncthreads();
+    transpose_tile_scaled(hid, d8, tt * SPP_TILE, n, s_sc, tile, hid_t, ldt);
   }
 }
 

@@ -90,9 +90,9 @@ def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
         try:
             return torch.empty(bwd_workspace_bytes(n, d, v, n_seqs, cb), dtype=torch.uint8, device=device)
         except torch.OutOfMemoryError:
-            if cb <= 128 * 2 * v:
+            if cb <= 128 * 2 * (v + d):
                 raise
-            cb = max(128 * 2 * v, cb // 2)
+            cb = max(128 * 2 * (v + d), cb // 2)
 
 
 SP_ROWSCALE = os.environ.get("ICEPOP_SP_ROWSCALE", "1") != "0"
@@ -576,7 +576,7 @@ def bwd_workspace_bytes(n_tokens: int, hidden: int, vocab: int, n_seqs: int, chu
     shape = _lib.Shape(n_tokens=n_tokens, token_offset=0, hidden=hidden, vocab=vocab, n_seqs=max(n_seqs, 1),
                        n_groups=1, weight_layout=_lib.W_VD)
     cb = DZ_CHUNK_BYTES if chunk_bytes is None else chunk_bytes
-    rows = cb // (2 * vocab)
+    rows = cb // (2 * (vocab + hidden))  # a bf16 dZ row and the row of H transposed for K5
     chunk = n_tokens if rows >= n_tokens else max(128, rows // 128 * 128)
     bwd_b = _lib._sz()
     _lib.check(lib.icepop_workspace_bytes(shape, chunk, 0, None, bwd_b))
@@ -698,7 +698,7 @@ def icepop_bwd_reduce_scatter(
     scratch = None
     if probs is None:
         ws = _bwd_workspace(n, d, v, shape.n_seqs, dev)
-        single_chunk = ws.numel() >= bwd_workspace_bytes(n, d, v, shape.n_seqs, 2 * n * v)
+        single_chunk = ws.numel() >= bwd_workspace_bytes(n, d, v, shape.n_seqs, 2 * n * (v + d))
         scratch = None if single_chunk else torch.empty(tuple(weight.shape), dtype=torch.float32, device=dev)
     else:  # stored probabilities: one chunk; the one-hot part of dW goes straight to the slots
         ws = _sp_workspace(n, d, v, shape.n_seqs, dev)

@@ -131,7 +131,7 @@ def test_backward_chunking_matches_single_chunk(cuda_device, monkeypatch):
     H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
     f = L.icepop_fwd(H, W, _batch(c, cuda_device), L.IcePopConfig(), store_probs=False)  # chunks: recompute mode
     gh1, gw1 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
-    monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * 1000 * 2)  # 256-row chunks
+    monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * (1000 + H.shape[1]) * 2)  # 256-row chunks (dZ + H^T rows)
     gh2, gw2 = L.icepop_bwd(H, W, _batch(c, cuda_device), f, L.IcePopConfig())
     assert torch.equal(gh1, gh2)
     assert _rel(gw2.cpu().numpy(), gw1.cpu().numpy()) < 1e-5  # fp32 partial sums per chunk
@@ -483,7 +483,7 @@ def test_fused_reduce_scatter_emulated_ranks(cuda_device, monkeypatch, layout, w
         shard_rows += 1
     slot_bufs = [torch.full((world * shard_rows * row_len,), float("nan"), device=cuda_device) for _ in range(world)]
     if chunked:
-        monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * V * 2)  # 256-row dZ chunks -> local scratch path
+        monkeypatch.setattr(L, "DZ_CHUNK_BYTES", 256 * (V + H.shape[1]) * 2)  # 256-row dZ chunks -> local scratch
     N = len(c["tokens"])
     for r in range(world):
         s, e = shard_range(N, world, r)

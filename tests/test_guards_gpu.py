@@ -76,7 +76,7 @@ def test_no_out_of_bounds_writes(cuda_device, cg, layout, ref):
                          stats=stats.data_ptr(), kl=kl.data_ptr(), lse_ref=lser.data_ptr(), kl_w=klw.data_ptr())
         _lib.check(lib.icepop_fwd_bf16(shape, cfg.to_c(), H.data_ptr(), W.data_ptr(), _lib.ptr(Wr), b.to_c(), fo,
                                        ws.data_ptr(), ws.numel(), st))
-        bw = bwd_workspace_bytes(N, d, V, 3, chunk_bytes=128 * V * 2)  # 128-row chunks: several tails
+        bw = bwd_workspace_bytes(N, d, V, 3, chunk_bytes=128 * (V + d) * 2)  # 128-row chunks: several tails
         bws_raw, bws = guarded(bw, cuda_device)
         bufs["bwd_ws"] = bws_raw
         gh_raw, ghv = guarded(N * d * 4, cuda_device)
