@@ -717,7 +717,7 @@ def run_e2e(H, W, batch, icfg, args, dev, world, sp=False, sp_chunk=0):
 
 
 # ----------------------------------------------------------------------------- reference-facing API
-def run_dropin_c1(dev, reps: int = 8) -> dict:
+def run_dropin_c1(dev, reps: int = 12) -> dict:
     """BASELINE configs[0] (8 x 512 tokens, 1,024 features, V = 32,768, one GRPO group of 8)
     through the drop-in ``objective_and_grad`` -- the call the reference's own loop makes
     (scheduler.py:540-542) -- with its Python records and host fp64 weights in, the fp64
@@ -767,8 +767,9 @@ def run_dropin_c1(dev, reps: int = 8) -> dict:
     out = {}
     with torch.cuda.device(dev):
         for name, kw in (("fresh_grad", {}), ("grad_out", {"grad_out": buf})):
-            for _ in range(2):
-                O.objective_and_grad(copy.deepcopy(groups), theta, theta, None, cfg, bounds, precision="bf16", **kw)
+            r = None
+            for _ in range(3):  # steady state: the caller holds the previous result (two gradient buffers)
+                r = O.objective_and_grad(copy.deepcopy(groups), theta, theta, None, cfg, bounds, precision="bf16", **kw)
             ts = []
             for _ in range(reps):
                 gs = copy.deepcopy(groups)

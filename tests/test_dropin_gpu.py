@@ -410,6 +410,40 @@ def test_grad_out_untouched_on_error_and_must_not_alias_parameters():
         O.objective_and_grad([g], theta, theta, None, cfg, b, grad_out=theta.weights)
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp64"])
+def test_fresh_gradients_never_alias_while_held(precision):
+    """Fresh gradients come back in pooled page-locked buffers: a buffer is reused only once the
+    array returned in it (and every view of it) is gone, so gradients the caller holds never
+    change under later calls."""
+    import gc
+
+    O = _obj()
+    cfg, b = O.ObjectiveConfig(group_size=2), O.MaskingBounds()
+    held, copies = [], []
+    for seed in range(4):
+        theta = rand_params(24, 16, 0.5, 40 + seed)  # the same shape every call: the same pool
+        g = manual_group(theta, [(1, 1.0, 1.0), (2, 1.0, 1.0)], [1.0, -1.0])
+        out = O.objective_and_grad([g], theta, theta, None, cfg, b, precision=precision)
+        held.append(out.grad[2:])  # a view keeps the buffer taken
+        copies.append(out.grad.copy())
+        del out
+    for i in range(len(held)):
+        for j in range(i):
+            assert not np.shares_memory(held[i], held[j])
+        assert np.array_equal(held[i], copies[i][2:])
+    # released buffers are handed out again (and hold the new call's gradient)
+    del held
+    gc.collect()
+    theta = rand_params(24, 16, 0.5, 50)
+    g = manual_group(theta, [(1, 1.0, 1.0), (2, 1.0, 1.0)], [1.0, -1.0])
+    out = O.objective_and_grad([g], theta, theta, None, cfg, b, precision=precision)
+    pooled = [slot[0].numpy() for slot in O._GRAD_POOL[theta.weights.shape]]
+    assert any(np.shares_memory(out.grad, p) for p in pooled)
+    ref = O.objective_and_grad([manual_group(theta, [(1, 1.0, 1.0), (2, 1.0, 1.0)], [1.0, -1.0])], theta, theta,
+                               None, cfg, b, precision=precision, grad_out=np.empty_like(theta.weights))
+    assert np.array_equal(out.grad, ref.grad)
+
+
 def test_mask_uses_numpys_calibration_bits():
     """per_token_calibration is numpy's exp(lp_old - lp_inf) itself, and the mask follows it even
     for a ratio sitting exactly on a bound (objective.py:227-232)."""
