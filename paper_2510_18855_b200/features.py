@@ -48,13 +48,46 @@ def feature_rows(prompt_id: int, prev: int, last: int, n_features: int) -> tuple
     )
 
 
+def _splitmix64_np(x: np.ndarray) -> np.ndarray:
+    """_splitmix64 over a uint64 array (numpy's uint64 arithmetic wraps mod 2^64, as the
+    reference's `& _MASK64` does)."""
+    x = x + np.uint64(_GOLDEN)
+    x ^= x >> np.uint64(30)
+    x *= np.uint64(0xBF58476D1CE4E5B9)
+    x ^= x >> np.uint64(27)
+    x *= np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def _mix_np(prefix: tuple, *arrays: np.ndarray) -> np.ndarray:
+    """_mix(*prefix, *arrays) per position: the scalar prefix is mixed once in Python, then each
+    int64 array (two's complement = the reference's `v & _MASK64`) over all positions."""
+    h0 = 0x8A5CD789635D2DFF
+    for v in prefix:
+        h0 = _splitmix64(h0 ^ (v & _MASK64))
+    h = np.full(arrays[0].shape, h0, dtype=np.uint64)
+    for v in arrays:
+        h = _splitmix64_np(h ^ v.astype(np.uint64))
+    return h
+
+
 def rollout_feats(prompt_id: int, token_ids, n_features: int) -> np.ndarray:
-    """(T, 4) feature rows for every position of a rollout (objective.py:162-169)."""
-    feats = np.empty((len(token_ids), 4), dtype=np.int64)
-    prev, last = -1, -1
-    for t, tok in enumerate(token_ids):
-        feats[t] = feature_rows(prompt_id, prev, last, n_features)
-        prev, last = last, int(tok)
+    """(T, 4) feature rows for every position of a rollout (objective.py:162-169): position t
+    hashes the window (prev, last) = (token t-2, token t-1), -1 before the start. Vectorised
+    over the positions (feature_rows is the scalar form, policy.py:229-260)."""
+    tok = np.asarray(token_ids, dtype=np.int64).reshape(-1)
+    T = tok.size
+    last = np.full(T, -1, dtype=np.int64)
+    prev = np.full(T, -1, dtype=np.int64)
+    last[1:] = tok[:-1]
+    prev[2:] = tok[:-2]
+    nf = np.uint64(n_features)
+    feats = np.empty((T, 4), dtype=np.int64)
+    with np.errstate(over="ignore"):
+        feats[:, 0] = int(_mix(1) % n_features)
+        feats[:, 1] = (_mix_np((3, prompt_id), last) % nf).astype(np.int64)
+        feats[:, 2] = (_mix_np((4, prompt_id), prev, last) % nf).astype(np.int64)
+        feats[:, 3] = (_mix_np((5, prompt_id), prev, last) % nf).astype(np.int64)
     return feats
 
 

@@ -95,6 +95,25 @@ def test_feature_hash_matches_reference_rows(name):
         assert np.array_equal(got, d["feats"][cu[i]:cu[i + 1]])
 
 
+def test_vectorised_feature_hash_equals_the_scalar_walk():
+    """rollout_feats (numpy uint64, all positions at once) equals the reference's per-position
+    walk of feature_rows (objective.py:162-169, policy.py:229-260) bit for bit, including
+    negative / 63-bit prompt ids, large token ids and 1- and 2-token rollouts."""
+    from paper_2510_18855_b200.features import feature_rows, rollout_feats
+
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        T = int(rng.integers(1, 40))
+        nf = int(rng.integers(1, 5000))
+        pid = int(rng.integers(-2 ** 62, 2 ** 62))
+        toks = [int(x) for x in rng.integers(0, 2 ** 31 - 1, T)]
+        ref, prev, last = [], -1, -1
+        for t in toks:
+            ref.append(feature_rows(pid, prev, last, nf))
+            prev, last = last, t
+        assert np.array_equal(rollout_feats(pid, toks, nf), np.array(ref, dtype=np.int64).reshape(-1, 4))
+
+
 def test_multihot_counts_duplicates():
     from paper_2510_18855_b200.features import multihot
 
