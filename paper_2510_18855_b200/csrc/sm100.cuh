@@ -180,27 +180,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
-// 2^x for two lanes on the FMA pipe (x <= 0; NaN is not propagated, callers handle it):
-// x = n + f with n = rint(x) (the 1.5 * 2^23 shifter), 2^f by a degree-5 polynomial fitted for
-// relative error on [-1/2, 1/2] (2.3e-7 max, the same as ex2.approx), 2^n added to the exponent
-// field. Used for a third of K1's softmax exponentials so the MUFU pipe (16 results/clk/SM) is
-// not the epilogue's only bottleneck.
-__device__ __forceinline__ float2 exp2_fma2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), x);
-  float2 p = __ffma2_rn(make_float2(1.3276469e-3f, 1.3276469e-3f), f, make_float2(9.6755410e-3f, 9.6755410e-3f));
-  p = __ffma2_rn(p, f, make_float2(5.5507135e-2f, 5.5507135e-2f));
-  p = __ffma2_rn(p, f, make_float2(2.4022120e-1f, 2.4022120e-1f));
-  p = __ffma2_rn(p, f, make_float2(6.9314694e-1f, 6.9314694e-1f));
-  p = __ffma2_rn(p, f, make_float2(1.0000001f, 1.0000001f));
-  // low bits of t hold n (two's complement); << 23 moves them into the exponent field
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits (=1 at bit 46).
 //   K-major  operand: LBO unused (16 B), SBO = 1024 B (8 rows x 128 B swizzle atom).
 //   MN-major operand: LBO = byte stride between 64-element MN blocks,

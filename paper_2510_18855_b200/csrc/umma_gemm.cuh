@@ -392,10 +392,11 @@ __device__ __forceinline__ void lse_slab(float (&v)[64], int valid, float scale_
   ey = 0.f;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    // masked columns: d ~ -1e30 -> e = 0 and e * d = -0
+    // masked columns: d ~ -1e30 -> e = 0 and e * d = -0. All exponentials on the MUFU (6% busy
+    // at this tile rate): moving every third pair to an FMA-pipe polynomial measured 0.2% slower
+    // under the power cap, every other pair 0.3% (profiles/r02_ab_exp_mix.log)
     const float2 d = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nmx);
-    // every third pair of a full slab on the FMA pipe (masked columns need the MUFU's exact 0)
-    const float2 e = (FULL && j % 3 == 2) ? exp2_fma2(d) : make_float2(fast_exp2(d.x), fast_exp2(d.y));
+    const float2 e = make_float2(fast_exp2(d.x), fast_exp2(d.y));
     const float2 es = EXCL ? make_float2(2 * j == rel ? 0.f : e.x, 2 * j + 1 == rel ? 0.f : e.y) : e;
     if (EXCL) ey = 2 * j == rel ? e.x : (2 * j + 1 == rel ? e.y : ey);
     if (j & 1) {
