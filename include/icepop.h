@@ -133,9 +133,11 @@ int icepop_group_advantages(const double* rewards, const int32_t* group_offsets,
 /* hidden: [n_tokens, d] bf16 row-major. weight (and weight_ref): bf16 in `weight_layout`.
  * Workspace sizes (bytes) for icepop_fwd_bf16 / icepop_bwd_bf16 (with_ref: a weight_ref
  * will be passed). The backward materialises bf16 dZ chunks of at most `max_chunk_tokens`
- * rows (0 = all rows); a smaller workspace than recommended shrinks the chunk (>= 128 rows).
- * max_chunk_tokens < 0: the stored-probabilities backward's workspace (row-compaction
- * buffers only; without it that backward runs every row through the GEMMs). */
+ * rows (0 = all rows) and each chunk's hidden rows transposed (dW's GEMM reads them K-major):
+ * 2 (V + d) bytes per chunk row; a smaller workspace than recommended shrinks the chunk
+ * (>= 128 rows). max_chunk_tokens < 0: the stored-probabilities backward's workspace (block
+ * lists, row scales, s H transposed, the one-hot sort: ~2 n_tokens d bytes; without it that
+ * backward forms dZ in place for every row). */
 int icepop_workspace_bytes(const icepop_shape* shape, int64_t max_chunk_tokens, int32_t with_ref,
                            size_t* fwd_bytes, size_t* bwd_bytes);
 
