@@ -357,7 +357,9 @@ def run_ours(args):
         r.update(extra)
         return r
 
-    n_var = max(2, min(args.steps, 4))
+    # sub-record steps: a few at the headline's size; more when a step is short (C1: ~1 ms, where
+    # one host hiccup would dominate a 4-step average)
+    n_var = max(2, min(args.steps, 4)) if ms > 50.0 else max(10, min(args.steps, 20))
 
     # ---------------- on-policy variant (extra line item; the headline is the general case)
     onp_res = None

@@ -387,6 +387,16 @@ int64_t k1_parts(int64_t n_tokens, int64_t V, int64_t d) {
   return (n_t + r - 1) / r;
 }
 
+// Grid of the transposing kernels (k_sp_prep, k_transpose_rows): 64-token tiles along x and,
+// when the tiles alone would not give each SM two blocks (C1: 64 tiles), 64-column groups of
+// the hidden dimension along y.
+dim3 spp_grid(int64_t n, int64_t d) {
+  const int64_t tiles = std::max<int64_t>((n + SPP_TILE - 1) / SPP_TILE, 1);
+  const int64_t groups = std::max<int64_t>((d + SPP_TILE - 1) / SPP_TILE, 1);
+  const int64_t want = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
+  return dim3((unsigned)std::min<int64_t>(tiles, (int64_t)num_sms() * 8), (unsigned)std::max<int64_t>(1, std::min(groups, want)));
+}
+
 // Vocabulary columns per K1 partial: the sampled token y's statistics are in partial y / this.
 int32_t k1_part_cols(int64_t n_tokens, int64_t V, int64_t d) { return k1_bn() * k1_run_len(n_tokens, V, d); }
 
@@ -1141,7 +1151,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       }
       const int grid = (int)std::min<int64_t>(nc, (int64_t)num_sms() * 8);
       if (scaled) {
-        const int pgrid = (int)std::min<int64_t>((nc + SPP_TILE - 1) / SPP_TILE, (int64_t)num_sms() * 8);
+        const dim3 pgrid = spp_grid(nc, d);
         k_sp_prep<<<pgrid, SPP_THREADS, 0, st>>>(sv.tile_max, tm_ld, (int32_t)((V + 63) / 64), lse, coeff,
                                                  (float)grad_scale, sv.lp_cur, tokens, dzb, V,
                                                  reinterpret_cast<const uint4*>(hidden), d / 8, sw.rscale, sw.ohc,
@@ -1241,8 +1251,7 @@ static int bwd_impl(const icepop_shape* shape, const icepop_config* cfg, const v
       // row-scaled H' transposed by k_sp_prep, or this chunk's rows transposed here (the
       // recompute backward); H itself (MN-major, [nc, d]) only without either workspace
       if (!scaled && w.hid_t) {
-        const int tg = (int)std::min<int64_t>((nc + SPP_TILE - 1) / SPP_TILE, (int64_t)num_sms() * 8);
-        k_transpose_rows<<<tg, SPP_THREADS, 0, st>>>(reinterpret_cast<const uint4*>(h), d / 8,
+        k_transpose_rows<<<spp_grid(nc, d), SPP_THREADS, 0, st>>>(reinterpret_cast<const uint4*>(h), d / 8,
                                                      reinterpret_cast<uint4*>(w.hid_t), w.ldt, nc);
         ICP_CUDA(cudaGetLastError());
       }

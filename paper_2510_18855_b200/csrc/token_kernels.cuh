@@ -783,12 +783,13 @@ constexpr int SPP_LD = SPP_TILE + 2;  // bf16 elements per smem row: 33 words, c
 // One 64-token tile of H (rows t0.., d8 16-byte groups per row), each row scaled by s_sc[row]
 // and rounded to bf16, written transposed: hid_t[k][t] (ldt tokens per row; rows >= n give zeros).
 // The rows pass through shared memory 64 hidden columns at a time: coalesced 128-byte reads of
-// H rows, 16-byte stores of 8 tokens of one hidden column.
+// H rows, 16-byte stores of 8 tokens of one hidden column. Blocks along gridDim.y take
+// interleaved 64-column groups (small token counts still fill the GPU).
 __device__ __forceinline__ void transpose_tile_scaled(const uint4* __restrict__ hid, int64_t d8, int64_t t0, int64_t n,
                                                       const float* s_sc, uint32_t* tile, uint4* __restrict__ hid_t,
                                                       int64_t ldt) {
   const uint16_t* th = reinterpret_cast<const uint16_t*>(tile);
-  for (int64_t c8 = 0; c8 < d8; c8 += SPP_TILE / 8) {  // 64 hidden columns
+  for (int64_t c8 = (int64_t)blockIdx.y * (SPP_TILE / 8); c8 < d8; c8 += (int64_t)gridDim.y * (SPP_TILE / 8)) {
     // load + scale: thread -> (row, 8-column group), stored as four 32-bit words
     for (int i = threadIdx.x; i < SPP_TILE * 8; i += SPP_THREADS) {
       const int row = i >> 3, q = i & 7;
@@ -846,7 +847,7 @@ __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict
         const bool ex = __any_sync(0xffffffffu, any);
         const float cf = coeff[t] * gs;
         sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
-        if (lane == 0) {
+        if (lane == 0 && blockIdx.y == 0) {  // the column-group blocks of a tile share the scales
           rscale[t] = sc;
           ohc[t] = (ex || cf == 0.f) ? 0.f : (float)((double)cf * -expm1(lp_cur[t]));
           exc[t] = ex ? 1 : 0;

@@ -547,6 +547,23 @@ __device__ __forceinline__ float dz_entry(float cf, float p, bool is_y, float dz
   return is_y ? (dzy == dzy ? dzy : fmaf(-cf, p, cf)) : -cf * p;
 }
 
+// bf16 dZ of 32 columns (v: their logits), packed in pairs: -cf p, and for the lane whose
+// sampled token sits at column `rel` of them its exact entry. Y (warp-uniform: some lane's token
+// is in these columns, rare) selects the variant with the per-column compare; the common one
+// has none (it measured 45% of K3's time at C1's short K, where the epilogue is exposed).
+template <bool Y>
+__device__ __forceinline__ void dz_pack32(const float* v, float scale_log2, float lse2, float cf, int rel,
+                                          float dzy, bool live, uint32_t* pk) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float p0 = fast_exp2(fmaf(v[2 * j], scale_log2, -lse2));
+    const float p1 = fast_exp2(fmaf(v[2 * j + 1], scale_log2, -lse2));
+    const float d0 = Y ? dz_entry(cf, p0, 2 * j == rel, dzy) : -cf * p0;
+    const float d1 = Y ? dz_entry(cf, p1, 2 * j + 1 == rel, dzy) : -cf * p1;
+    pk[j] = live ? pack_bf16x2(d0, d1) : 0u;
+  }
+}
+
 // dZ = coeff_scale * c_t * (e_{y_t} - softmax(z_t)) for this tile -> bf16.
 template <int BN>
 __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep, int m0, int n0,
@@ -565,16 +582,12 @@ __device__ __forceinline__ void epi_dz(const GemmShape& sh, const EpiParams& ep,
     float v[32];
     tmem_ld32(taddr + c * 32, v);
     const int col0 = n0 + c * 32;
+    const int rel = y - col0;
+    const bool y_here = __any_sync(0xffffffffu, (unsigned)rel < 32u);  // warp-uniform, before lanes part
     if (!row_ok || col0 >= sh.N) continue;
     uint32_t pk[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float p0 = fast_exp2(fmaf(v[2 * j], ep.scale_log2, -lse2));
-      const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
-      const float d0 = dz_entry(cf, p0, col0 + 2 * j == y, dzy);
-      const float d1 = dz_entry(cf, p1, col0 + 2 * j + 1 == y, dzy);
-      pk[j] = live ? pack_bf16x2(d0, d1) : 0u;
-    }
+    if (y_here) dz_pack32<true>(v, ep.scale_log2, lse2, cf, rel, dzy, live, pk);
+    else dz_pack32<false>(v, ep.scale_log2, lse2, cf, rel, dzy, live, pk);
     __nv_bfloat16* dst = ep.dz + (int64_t)m * ep.ldz + col0;
     if (col0 + 32 <= sh.N && ep.vec_ok) {
 #pragma unroll
@@ -616,17 +629,13 @@ __device__ __forceinline__ void epi_dz_tma(const GemmShape& sh, const EpiParams&
     const int col0 = n0 + c * 64;
     if (!warp_rows || col0 >= sh.N) continue;  // warp-uniform
     uint32_t pk[32];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float p0 = fast_exp2(fmaf(v[2 * j], ep.scale_log2, -lse2));
-      const float p1 = fast_exp2(fmaf(v[2 * j + 1], ep.scale_log2, -lse2));
-      const float q0 = fast_exp2(fmaf(w[2 * j], ep.scale_log2, -lse2));
-      const float q1 = fast_exp2(fmaf(w[2 * j + 1], ep.scale_log2, -lse2));
-      pk[j] = live ? pack_bf16x2(dz_entry(cf, p0, col0 + 2 * j == y, dzy),
-                                 dz_entry(cf, p1, col0 + 2 * j + 1 == y, dzy)) : 0u;
-      pk[16 + j] = live ? pack_bf16x2(dz_entry(cf, q0, col0 + 32 + 2 * j == y, dzy),
-                                      dz_entry(cf, q1, col0 + 32 + 2 * j + 1 == y, dzy)) : 0u;
-    }
+    const int rel = y - col0;
+    if (__any_sync(0xffffffffu, (unsigned)rel < 32u)) dz_pack32<true>(v, ep.scale_log2, lse2, cf, rel, dzy, live, pk);
+    else dz_pack32<false>(v, ep.scale_log2, lse2, cf, rel, dzy, live, pk);
+    if (__any_sync(0xffffffffu, (unsigned)(rel - 32) < 32u))
+      dz_pack32<true>(w, ep.scale_log2, lse2, cf, rel - 32, dzy, live, pk + 16);
+    else
+      dz_pack32<false>(w, ep.scale_log2, lse2, cf, rel - 32, dzy, live, pk + 16);
     stage_store_slab(tmC, stage2, ebuf, pk, col0, row0, lane);
   }
 }

@@ -108,7 +108,7 @@ def _bwd_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor:
     """The recompute-mode backward workspace with the largest dZ chunk that allocates: the
     free-memory estimate counts torch's cached blocks, which fragmentation can make unusable
     for one large block, so an out-of-memory halves the chunk (down to 128 rows)."""
-    cb = _dz_chunk_bytes(device)
+    cb = _dz_chunk_bytes(device, 2 * n * (v + d))
     while True:
         try:
             return torch.empty(bwd_workspace_bytes(n, d, v, n_seqs, cb), dtype=torch.uint8, device=device)
@@ -143,8 +143,11 @@ def _sp_workspace(n: int, d: int, v: int, n_seqs: int, device) -> torch.Tensor |
         return None
 
 
-def _dz_chunk_bytes(device) -> int:
-    free = _free_bytes(device)
+def _dz_chunk_bytes(device, need: int | None = None) -> int:
+    """Bytes for the recompute backward's dZ chunk (+ transposed hidden rows): the cap, or 60%
+    of the free device memory. `need` (the whole batch's bytes) lets a recent free-memory reading
+    stand in when it is small against it (_free_bytes)."""
+    free = _free_bytes(device, need)
     if free is None:
         return DZ_CHUNK_BYTES
     return max(1, min(DZ_CHUNK_BYTES, int(0.6 * free)))
