@@ -10,7 +10,7 @@ h.th_hold_sms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_
                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 h.th_set_flag.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 dev = torch.device('cuda', 0)
-M, N, K = 2048, 4096, 32768
+M, N, K = 4096, 4096, 32768
 A = torch.randn((M, K), device=dev).to(torch.bfloat16)
 B = torch.randn((K, N), device=dev).to(torch.bfloat16)
 C = torch.empty((M, N), dtype=torch.float32, device=dev)

@@ -38,7 +38,7 @@ def test_long_k_gemm_completes_while_sms_are_held(cuda_device, a_mn, b_mn):
 
     lib = _lib.ensure_device(0)
     h = _helpers()
-    M, N, K = 2048, 4096, 32768  # 512 k-blocks: a long-K (waves) GEMM of 64 wide pair tiles
+    M, N, K = 4096, 4096, 32768  # 512 k-blocks: a long-K GEMM of 128 wide pair tiles (two waves: barriers)
     g = torch.Generator(device=cuda_device).manual_seed(5)
     A = torch.randn((K, M) if a_mn else (M, K), device=cuda_device, generator=g).to(torch.bfloat16)
     B = torch.randn((K, N) if b_mn else (N, K), device=cuda_device, generator=g).to(torch.bfloat16)

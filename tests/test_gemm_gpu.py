@@ -71,11 +71,12 @@ def wide_tiles():
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(600, 1304, 16448), (256, 512, 16384), (136, 2104, 20000)])
+@pytest.mark.parametrize("M,N,K", [(600, 1304, 16448), (256, 512, 16384), (136, 2104, 20000), (4096, 4096, 16448)])
 def test_gemm_long_k_wide_tiles(cuda_device, wide_tiles, a_mn, b_mn, M, N, K):
-    """K >= 16384 runs the static-wave schedule; on CTA pairs the 256 x 512 tiles (two N = 256
-    MMAs into one accumulator, pair-interleaved B rows). Same per-element k order as the
-    256 x 256 tiles, so the two agree bit for bit; both vs fp64."""
+    """K >= 16384 is the long-K path: static waves with the k-chunk barrier when the tiles take
+    more than one wave (the 4096 x 4096 case), the dynamic schedule otherwise; on CTA pairs the
+    256 x 512 tiles (two N = 256 MMAs into one accumulator, pair-interleaved B rows). Same
+    per-element k order as the 256 x 256 tiles, so the two agree bit for bit; both vs fp64."""
     g = torch.Generator(device="cpu").manual_seed(M + N + K)
     A = torch.randn(M, K, generator=g).to(torch.bfloat16).to(cuda_device)
     B = torch.randn(N, K, generator=g).to(torch.bfloat16).to(cuda_device)
