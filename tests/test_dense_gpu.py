@@ -600,3 +600,25 @@ def test_custom_ops_pass_opcheck(cuda_device, store_probs):
              b.lp_infer_old, b.cu_seqlens, b.group_offsets, b.advantages, lse, lp_cur, coeff, kl, lse_ref, kl_w,
              probs, tile_max, 0.5, 5.0, 0.2, 2.0, 1.0, 0.0, 0, _lib.W_VD, 0, True, True)
     torch.library.opcheck(_icepop_loss_backward_op, bargs, test_utils=("test_schema", "test_faketensor"))
+
+
+@pytest.mark.parametrize("mode", ["probs", "recompute", "ref"])
+def test_out_of_range_tokens_raise_without_faulting(cuda_device, mode):
+    """A token id outside [0, V) (here -1 and V) is reported as the reference's ValueError by the
+    forward's error word; the kernels that index by token (K1's gather, K2's lookup of the
+    token's partial, the lp recording) clamp and never read or write out of bounds."""
+    from paper_2510_18855_b200.loss import IcePopConfig, finish, icepop_fwd, icepop_logprob
+
+    c = _case(seed=41, V=1000, n_seqs=4, lens=[100, 90, 80, 70])
+    c["tokens"][5] = -1
+    c["tokens"][200] = 1000
+    H, W = c["H"].to(cuda_device), c["W"].to(cuda_device)
+    Wr = W if mode == "ref" else None
+    f = icepop_fwd(H, W, _batch(c, cuda_device), IcePopConfig(), weight_ref=Wr, store_probs=(mode == "probs"))
+    with pytest.raises(ValueError, match="outside the vocabulary"):
+        finish(f.stats)
+    lp, lse, _ = icepop_logprob(H, W, torch.from_numpy(c["tokens"]).to(cuda_device))
+    torch.cuda.synchronize()  # a fault would surface here
+    ok = np.ones(len(c["tokens"]), bool)
+    ok[[5, 200]] = False
+    assert torch.isfinite(lse).all() and np.isfinite(lp.cpu().numpy()[ok]).all()
