@@ -76,8 +76,12 @@ def main():
     def k4():
         _lib.check(lib.icepop_gemm_bf16(zbuf().data_ptr(), W.data_ptr(), gh.data_ptr(), N, d, V, 0, 1, 0, 0, st))
 
+    # K5 as in the step: the stored-probabilities backward reads the hidden rows transposed
+    # (K-major, written by its prep kernel); the recompute mode transposes each dZ chunk's rows
+    HT = H.t().contiguous()
+
     def k5():
-        _lib.check(lib.icepop_gemm_bf16(zbuf().data_ptr(), H.data_ptr(), gw.data_ptr(), V, d, N, 1, 1, 1, 1, st))
+        _lib.check(lib.icepop_gemm_bf16(zbuf().data_ptr(), HT.data_ptr(), gw.data_ptr(), V, d, N, 1, 0, 1, 1, st))
 
     kernels = (("K1", k1), ("dZ" if sp else "K3", k3), ("K4", k4), ("K5", k5))
     for _, fn in kernels:  # warm-ups first, so `ncu -s 4 -c 4` sees K1, K3, K4, K5 in order
