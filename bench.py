@@ -556,12 +556,13 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
         N = chunk
     res = {}
 
-    def timed(name, fn, flop, reps=2, nbytes=None):
+    def timed(name, fn, flop, reps=2, nbytes=None, spin=8_000_000):
         fn()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # a ~5 ms device spin ahead of the start event lets the host enqueue every rep first, so
-        # a short kernel (K2: ~0.25 ms) is timed without the Python call overhead between reps
-        torch.cuda._sleep(8_000_000)
+        # a device spin ahead of the start event lets the host enqueue every rep first, so a
+        # short kernel (K2: ~0.2 ms, less than one Python call's host time) is timed without the
+        # host's call overhead between reps
+        torch.cuda._sleep(spin)
         a.record(st)
         for _ in range(reps):
             fn()
@@ -586,7 +587,7 @@ def kernel_times(H, W, batch, icfg, meta, cfg, chunk, dev, sp=False):
     from paper_2510_18855_b200.loss import icepop_epilogue
 
     n_parts = _k1_parts(N, V, d)
-    timed("K2_epilogue", lambda: icepop_epilogue(batch, f, icfg), 0.0, reps=10,
+    timed("K2_epilogue", lambda: icepop_epilogue(batch, f, icfg), 0.0, reps=10, spin=60_000_000,
           nbytes=N * (12 * n_parts + 24 + 37))
     res["K2_epilogue"]["n_partials_per_token"] = n_parts
     s = st.cuda_stream
