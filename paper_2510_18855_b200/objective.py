@@ -265,6 +265,7 @@ def _page_lock(arr: np.ndarray) -> None:
 # views keep it alive). Returning pinned memory spares the D2H a staging copy, and reusing it
 # spares a fresh 8 * n_features * V-byte page-locked allocation per call (~50-150 ms at C1).
 _GRAD_POOL: dict = {}
+_GRAD_POOL_MAX_BYTES = 2 << 30  # larger gradients are not pooled (2 x 2 shapes would pin > 8 GB)
 
 
 def _fresh_grad(shape) -> tuple["torch.Tensor", np.ndarray]:
@@ -281,7 +282,7 @@ def _fresh_grad(shape) -> tuple["torch.Tensor", np.ndarray]:
             return slot[0], arr
     t = torch.empty(shape, dtype=torch.float64, pin_memory=True)
     arr = t.numpy()
-    if len(pool) < 2:
+    if len(pool) < 2 and t.nbytes <= _GRAD_POOL_MAX_BYTES:  # bounded page-locked host memory
         pool.append([t, weakref.ref(arr)])
     return t, arr
 
