@@ -984,11 +984,12 @@ int icepop_fwd_onpolicy(const icepop_shape* shape, const icepop_config* cfg, con
 __global__ void k_logprob_finish(const float* part, int n_parts, int32_t part_cols, const int32_t* tokens,
                                  const float* ztok, int64_t n, float* lse, double* lp, float* entropy) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const float my = __ldg(part + token_part(__ldg(tokens + t), part_cols, n_parts) * 3 * n + t);
     PartMerge pm;  // one pass with a running maximum (k2_icepop_tokens)
     merge_partials<3>(pm, part, n_parts, n, t);
     float l, e;
     double lpv;
-    pm.finish(ztok[t], part[token_part(tokens[t], part_cols, n_parts) * 3 * n + t], l, lpv, e);
+    pm.finish(ztok[t], my, l, lpv, e);
     if (lse) lse[t] = l;
     if (lp) lp[t] = lpv;
     if (entropy) entropy[t] = e;

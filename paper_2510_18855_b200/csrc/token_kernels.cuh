@@ -214,11 +214,12 @@ struct PartMerge {
 
 // One pass over a token's partials with a running maximum: each partial is read exactly once
 // (a max pass first would re-read the maxima from DRAM: they exceed L2 at C2's size). Loads
-// are issued UNROLL partials ahead of the dependent merge chain, for memory-level parallelism.
+// are issued UNROLL partials ahead of the dependent merge chain, for memory-level parallelism
+// (profiles/k2_ab.py A/B).
 template <int R>
 __device__ __forceinline__ void merge_partials(PartMerge& pm, const float* __restrict__ part, int n_parts, int64_t n,
                                                int64_t t) {
-  constexpr int UNROLL = 4;
+  constexpr int UNROLL = 16;  // 16 partials in flight per thread: 0.257 -> 0.200 ms at C2 (4: 0.28 with the prefetch)
   const float* p = part + t;
   const int64_t stride = (int64_t)R * n;
   int j = 0;
@@ -254,9 +255,10 @@ __global__ void __launch_bounds__(TOK_THREADS) k2_icepop_tokens(const TokenArgs 
     double lp_cur, ent, kl = 0.0;
     if (MERGE) {
       // merge split-V partials -> lse, entropy, lp_cur
+      // the token's partial maximum first: its (uncoalesced) load overlaps the merge loop
+      const float my = __ldg(a.part + token_part(__ldg(a.tokens + t), a.part_cols, a.n_parts) * R * a.n_tokens + t);
       PartMerge pm;
       merge_partials<R>(pm, a.part, a.n_parts, a.n_tokens, t);
-      const float my = a.part[token_part(a.tokens[t], a.part_cols, a.n_parts) * R * a.n_tokens + t];
       float lse, entf;
       const float S = pm.finish(a.ztok[t], my, lse, lp_cur, entf);
       ent = (double)entf;
