@@ -843,9 +843,16 @@ __global__ void __launch_bounds__(SPP_THREADS) k_sp_prep(const float* __restrict
       const int64_t t = t0 + r;
       float sc = 0.f;
       if (t < n) {
-        const float* tm = tile_max + t * tm_ld;
+        // any slab reference != 0 (an exception row): 16-byte loads, several in flight per lane
+        // (tm_ld is a multiple of 4 and its padding entries are 0)
+        const float4* tm4 = reinterpret_cast<const float4*>(tile_max + t * tm_ld);
+        const int n4 = (n_slabs + 3) >> 2;
         bool any = false;
-        for (int j = lane; j < n_slabs; j += 32) any |= tm[j] != 0.f;
+#pragma unroll 4
+        for (int j = lane; j < n4; j += 32) {
+          const float4 r = __ldg(tm4 + j);
+          any |= (r.x != 0.f) | (r.y != 0.f) | (r.z != 0.f) | (r.w != 0.f);
+        }
         const bool ex = __any_sync(0xffffffffu, any);
         const float cf = coeff[t] * gs;
         sc = ex ? 1.f : (cf == 0.f ? 0.f : -cf * exp2f(-lse[t] * 1.4426950408889634f));
