@@ -207,3 +207,38 @@ def test_confident_lp_keeps_one_minus_py(cuda_device, case, run):
         print(f"{case} run={run} {name}: {int(conf.sum())} confident rows, min 1-p_y {q[conf].min():.2e}, "
               f"rel err of 1-p_y median {med:.2e} p99 {p99:.2e}")
         assert med <= 2e-5 and p99 <= 2e-4, (name, med, p99)
+
+
+def test_confident_tokens_with_kl_gradient(cuda_device):
+    """The KL-to-ref gradient (gamma > 0: the recompute backward K3r, objective.py:254-263) on
+    peaked on-policy logits: the sampled token's IcePop entry comes from lp_cur (dz_entry), so
+    the per-row dH error on confident rows has a bf16-level median (<= 5e-3) against fp64. Its
+    tail is set by the KL term itself: -(w gamma / T) p_y (log p_y - log p_ref,y - kl) is a
+    difference of nearly equal log-probabilities, and with fp32 logits from the GEMM (absolute
+    error ~1e-5) the rows whose difference is ~1e-4 keep only a few % of it (measured p95 7.5%,
+    the dW Frobenius error 1.6e-3); an fp64 GEMM would be needed to do better."""
+    from oracle.icepop_oracle import icepop_dense
+    from paper_2510_18855_b200.loss import IcePopConfig, PackedBatch, finish, icepop_bwd, icepop_fwd
+
+    c = _peaked_case(seed=77, N=1024, d=256, V=1000, layout="vd", sigma_logit=12.0)
+    rng = np.random.default_rng(78)
+    W_ref = (c["W"].float() + torch.from_numpy(rng.normal(0, 0.02, tuple(c["W"].shape))).float()).to(torch.bfloat16)
+    dev = cuda_device
+    b = PackedBatch(torch.from_numpy(c["tokens"]).to(dev), torch.from_numpy(c["lp_old"]).to(dev),
+                    torch.from_numpy(c["lp_inf"]).to(dev), torch.from_numpy(c["cu"]).to(dev),
+                    torch.from_numpy(c["go"]).to(dev), torch.from_numpy(c["adv"]).to(dev))
+    H, W, Wr = c["H"].to(dev), c["W"].to(dev), W_ref.to(dev)
+    cfg = IcePopConfig(kl_coeff=0.4)
+    f = icepop_fwd(H, W, b, cfg, layout="vd", weight_ref=Wr)
+    gh, gw = icepop_bwd(H, W, b, f, cfg, layout="vd", weight_ref=Wr, grad_hidden_dtype=torch.float32)
+    finish(f.stats)
+    o = icepop_dense(c["H"].double().numpy(), c["W"].double().numpy(), c["tokens"], c["lp_old"], c["lp_inf"],
+                     c["cu"], c["go"], c["adv"], layout="vd", kl_coeff=0.4, weight_ref=W_ref.double().numpy())
+    conf = (c["py"] > 0.9) & (o["coeff"] != 0)
+    assert conf.sum() >= 20
+    eh = _row_err(gh.double().cpu().numpy(), o["grad_hidden"])[conf]
+    gref = o["grad_weight"]
+    ew = np.linalg.norm(gw.double().cpu().numpy() - gref) / np.linalg.norm(gref)
+    print(f"KL gradient, {int(conf.sum())} confident rows: dH median {np.median(eh):.2e} p95 "
+          f"{np.quantile(eh, 0.95):.2e}; dW rel {ew:.2e}")
+    assert np.median(eh) <= 5e-3 and ew <= 1e-2
