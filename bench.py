@@ -202,7 +202,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_18855_b200 import _lib  # noqa: F401
+    from paper_2510_18855_b200 import _lib
     from paper_2510_18855_b200.distributed import allreduce_grad, allreduce_stats, wait_grad
     from paper_2510_18855_b200.loss import (Diagnostics, IcePopConfig, _dz_chunk_bytes, _resolve_store_probs, finish,
                                             icepop_bwd, icepop_fwd, icepop_fwd_bwd, probs_chunk_tokens)
@@ -444,6 +444,10 @@ def run_ours(args):
                    "hidden": d, "vocab": V, "group_size": cfg["group"], "parallelism": f"dp{world} token-sharded",
                    "weight_layout": "[V,d]", "dz_chunk_tokens": chunk,
                    "dz_mode": dz_mode,
+                   # HBM the stored-probabilities mode holds between forward and backward: bf16 q
+                   # [N, V] + the fp32 slab references (0 in the recompute mode)
+                   "stored_probs_bytes": (int(min(N, sp_chunk or N) * (2 * V + 4 * _lib.tile_max_ld(V)))
+                                          if (sp or sp_chunk) else 0),
                    "l2": "inputs larger than L2 (H %.1f GB, W %.1f GB vs 126 MB)" % (N * d * 2 / 1e9, V * d * 2 / 1e9),
                    "popped_fraction": round(diag.clipped_fraction, 6), "dw_collective": collective,
                    "zero_adv_group_frac": args.zero_adv_frac},
